@@ -1,0 +1,264 @@
+/*
+ * mlck_b200.h -- C ABI of the B200-native MoEtion checkpoint data path.
+ *
+ * The reference (/root/reference/proj/include/moelab) is a header-only C++20
+ * API.  This ABI is what a drop-in replacement of its checkpoint path binds:
+ * plain pointers and sizes, opaque handles, int status + thread-local message.
+ * include/moelab_b200/*.hpp wraps it back into the reference's C++ signatures
+ * (same names, same exception types and texts); INTEGRATION.md shows the
+ * binding.  Every entry below cites the reference function it replaces.
+ *
+ * Status codes: 0 ok; 1 = the reference would throw std::invalid_argument;
+ * 2 = std::runtime_error (integrity / state errors); 3 = CUDA failure.
+ * mlck_last_error() returns the message of the last failing call on this
+ * thread, with the reference's exception text where one exists.
+ *
+ * Threading: one host thread per mlck_ctx; calls on one ctx are ordered on
+ * its stream.  Contexts on different devices are independent.
+ */
+#ifndef MLCK_B200_H
+#define MLCK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MLCK_OK 0
+#define MLCK_EINVAL 1
+#define MLCK_ERUNTIME 2
+#define MLCK_ECUDA 3
+
+typedef struct mlck_ctx mlck_ctx;
+typedef struct mlck_state mlck_state;
+typedef struct mlck_blob mlck_blob;
+typedef struct mlck_gradlog mlck_gradlog;
+typedef struct mlck_log mlck_log;
+
+/* OptimizerConfig (engine.hpp:21-28). kind 0 = Adam, 1 = SGD. */
+typedef struct {
+  int32_t kind;
+  float lr, beta1, beta2, eps;
+} mlck_optimizer;
+
+/* Header fields of an MLCK record (snapshot.hpp:61-70). */
+typedef struct {
+  uint8_t kind;
+  uint64_t iteration;
+  uint64_t window_start;
+  uint32_t wsparse;
+  uint32_t slot;
+  uint64_t data_seed;
+  uint32_t op_count;
+} mlck_record_info;
+
+/* One decoded entry (ParsedRecord entries, snapshot.hpp:182-195); payloads
+ * stay on the device at payload_offset inside the blob. */
+typedef struct {
+  uint32_t id;
+  uint8_t mode; /* 0 Full, 1 ComputeOnly */
+  uint64_t param_count;
+  uint64_t step;
+  uint64_t payload_offset;
+} mlck_entry_info;
+
+/* ---- errors / context -------------------------------------------------- */
+const char* mlck_last_error(void);
+int mlck_ctx_create(int device, mlck_ctx** out);
+int mlck_ctx_destroy(mlck_ctx* ctx);
+/* Launch all work of this ctx on `stream` (a cudaStream_t; NULL = the
+ * context's own non-blocking stream). */
+int mlck_ctx_set_stream(mlck_ctx* ctx, void* stream);
+int mlck_ctx_synchronize(mlck_ctx* ctx);
+/* Number of kernels this ctx launched so far (bench gpu_launches). */
+uint64_t mlck_ctx_kernel_launches(mlck_ctx* ctx);
+/* Per-kernel timing with CUDA events on the launch stream (pack, fnv,
+ * fnv_verify, walk, replay).  mlck_ctx_timings synchronizes, returns the
+ * labels as CSV and the durations (ms) recorded since the last read. */
+int mlck_ctx_set_timing(mlck_ctx* ctx, int on);
+int mlck_ctx_timings(mlck_ctx* ctx, char* labels_csv, uint64_t labels_cap, float* ms,
+                     uint32_t cap, uint32_t* n);
+
+/* ---- device state arena: TrainState / OperatorState (engine.hpp:33-51) -- */
+/* Each operator's master|m|v is one contiguous 12P-byte span (the Full
+ * payload body); compute weights are kept in their wire encoding (fp16 bits,
+ * 1-byte E4M3-240 codes or fp32) -- OperatorState::compute is the decoded
+ * image of exactly these codes. */
+int mlck_state_create(mlck_ctx* ctx, uint32_t n_ops, const uint64_t* param_counts,
+                      int compute_bytes, mlck_state** out);
+int mlck_state_destroy(mlck_state* st);
+int mlck_state_set_meta(mlck_state* st, uint64_t iteration, uint64_t data_seed);
+int mlck_state_get_meta(mlck_state* st, uint64_t* iteration, uint64_t* data_seed);
+/* Host arrays in; compute = quantize(master) on the device
+ * (OperatorState::refresh_compute, engine.hpp:41-44). */
+int mlck_state_upload_op(mlck_state* st, uint32_t id, const float* master, const float* m,
+                         const float* v, uint64_t step, int has_full_state);
+/* Host arrays out (any pointer may be NULL); compute decoded to float. */
+int mlck_state_download_op(mlck_state* st, uint32_t id, float* master, float* m, float* v,
+                           uint64_t* step, float* compute, int* has_full_state);
+int mlck_state_set_step(mlck_state* st, uint32_t id, uint64_t step, int has_full_state);
+/* Device pointers of an operator (compute: its code array). */
+int mlck_state_op_ptrs(mlck_state* st, uint32_t id, float** master, float** m, float** v,
+                       void** compute);
+/* Counter-based synthetic state (benchmark inputs; oracle mlo_synth_value):
+ * master U(-.25,.25), m U(-1e-3,1e-3), v U(0,1e-6), step = `step`. */
+int mlck_state_fill_synthetic(mlck_state* st, uint64_t seed, uint64_t step);
+/* Engine::serialize_state "MLST" (engine.hpp:246-261): size query with
+ * host_out = NULL; else packs on the device and copies to host_out. */
+int mlck_state_serialize(mlck_state* st, uint8_t* host_out, uint64_t cap, uint64_t* size);
+/* Same bytes into a device blob. */
+int mlck_state_serialize_blob(mlck_state* st, mlck_blob* out);
+
+/* ---- device blobs (SparseCheckpoint::blobs element, snapshot.hpp:304) --- */
+int mlck_blob_create(mlck_ctx* ctx, uint64_t capacity, mlck_blob** out);
+int mlck_blob_destroy(mlck_blob* b);
+int mlck_blob_from_host(mlck_ctx* ctx, const uint8_t* bytes, uint64_t n, mlck_blob** out);
+uint64_t mlck_blob_size(const mlck_blob* b);
+void* mlck_blob_device_ptr(const mlck_blob* b);
+int mlck_blob_to_host(const mlck_blob* b, uint8_t* host, uint64_t cap);
+/* Replica targets written by the same pack kernel as the local copy: a
+ * device pointer of >= capacity bytes (local HBM, or a peer buffer opened
+ * with mlck_ipc_open / peer access).  Up to 3 replicas. */
+int mlck_blob_add_replica(mlck_blob* b, void* device_ptr, uint64_t capacity);
+int mlck_blob_clear_replicas(mlck_blob* b);
+
+/* ---- K1+K2: snapshot pack ----------------------------------------------
+ * serialize_record(take_sparse_snapshot(engine, slot, slot_index), plan,
+ * kind, window_start, wsparse)  (snapshot.hpp:204-241 + 115-144):
+ * validates the slot ("snapshot slot references unknown operator N",
+ * "snapshot: operator N in active set has no full state"), orders entries by
+ * id, packs the byte-exact MLCK record (+ FNV-1a-64 trailer) into `out` and
+ * every replica of `out`. */
+int mlck_snapshot_record(mlck_state* st, const uint32_t* active, uint32_t n_active,
+                         const uint32_t* compute_only, uint32_t n_compute_only,
+                         uint32_t slot_index, uint8_t kind, uint64_t window_start,
+                         uint32_t wsparse, mlck_blob* out);
+/* The same call with the record delivered to host memory (the reference's
+ * std::vector<uint8_t> return): device pack + one D2H copy. */
+int mlck_snapshot_record_host(mlck_state* st, const uint32_t* active, uint32_t n_active,
+                              const uint32_t* compute_only, uint32_t n_compute_only,
+                              uint32_t slot_index, uint8_t kind, uint64_t window_start,
+                              uint32_t wsparse, mlck_blob* scratch, uint8_t* host_out,
+                              uint64_t cap, uint64_t* size);
+/* take_dense_checkpoint(engine).serialize(plan) (snapshot.hpp:245-295):
+ * "dense checkpoint: operator N is frozen" when an op lacks full state. */
+int mlck_dense_checkpoint(mlck_state* st, mlck_blob* out);
+
+/* fnv1a64 (digest.hpp:18-25) over n device bytes. */
+int mlck_fnv1a64(mlck_ctx* ctx, const void* device_ptr, uint64_t n, uint64_t seed, uint64_t* out);
+
+/* ---- parse / coverage ----------------------------------------------------
+ * parse_record (snapshot.hpp:153-197): verifies the trailer on the device
+ * ("container checksum mismatch"), then magic/version ("container: bad
+ * magic", "container: unsupported version N"), walks the entry table
+ * ("container truncated").  Entry metadata out; payloads stay on device. */
+int mlck_parse_record(mlck_blob* b, int compute_bytes, mlck_record_info* info,
+                      mlck_entry_info* entries, uint32_t cap, uint32_t* n_entries);
+/* Decode one entry's payload to host floats (read_compute, snapshot.hpp:95-111). */
+int mlck_read_entry(mlck_blob* b, const mlck_entry_info* e, int compute_bytes, float* master,
+                    float* m, float* v, float* compute);
+/* SparseCheckpoint::check_coverage (snapshot.hpp:322-334). */
+int mlck_check_coverage(mlck_blob* const* blobs, uint32_t n_blobs, uint64_t op_count,
+                        int compute_bytes);
+
+/* ---- gradient log (inputs of Adam replay) --------------------------------
+ * Per-iteration, per-operator fp32 gradients, device resident.  The reference
+ * re-derives them by re-running the toy model (engine.hpp:214-222); the GPU
+ * path logs them once and replays Adam from the log (bit-identical, SURVEY.md
+ * 8(c)).  Iterations are absolute; capacity counts iterations kept. */
+int mlck_gradlog_create(mlck_ctx* ctx, uint32_t n_ops, const uint64_t* param_counts,
+                        uint32_t capacity_iterations, mlck_gradlog** out);
+int mlck_gradlog_destroy(mlck_gradlog* g);
+/* Host floats in (P of the op). */
+int mlck_gradlog_put(mlck_gradlog* g, uint64_t iteration, uint32_t op_id, const float* host);
+/* Device pointer of the slot for (iteration, op) -- allocates the slot. */
+int mlck_gradlog_slot(mlck_gradlog* g, uint64_t iteration, uint32_t op_id, float** device_ptr);
+int mlck_gradlog_fill_synthetic(mlck_gradlog* g, uint64_t first_iteration, uint32_t n_iterations,
+                                uint64_t seed);
+
+/* ---- Adam ----------------------------------------------------------------
+ * optimizer_step_adam (engine.hpp:738-753) on device arrays; *step is the
+ * host-side counter (incremented before the bias corrections, as the
+ * reference does). */
+int mlck_optimizer_step_adam(mlck_ctx* ctx, float* master, float* m, float* v, uint64_t* step,
+                             const float* grad, uint64_t n, const mlck_optimizer* opt);
+/* Engine::apply_updates (engine.hpp:699-728) for the listed operators with
+ * the gradients of `iteration` from `g`: Adam or SGD, then refresh_compute. */
+int mlck_state_apply_updates(mlck_state* st, const uint32_t* ids, uint32_t n_ids,
+                             mlck_gradlog* g, uint64_t iteration, const mlck_optimizer* opt);
+
+/* ---- K3: sparse-to-dense conversion --------------------------------------
+ * sparse_to_dense_convert (recovery.hpp:180-227) with Adam replay from the
+ * gradient log: verifies every record (FNV trailer), takes each operator's
+ * unique Full payload (slot k) and applies W-k optimizer steps from the
+ * gradients of iterations window_start+k+1 .. window_start+W in one fused
+ * pass, writing master/m/v + compute codes into `out` (sized like the model)
+ * and setting its iteration (window_start+W; the record's for W == 1) and
+ * data_seed.  Errors: "sparse checkpoint incomplete: n of W records",
+ * "sparse checkpoint record (slot k): <parse error>",
+ * "conversion finished with frozen operator N". */
+int mlck_sparse_to_dense_convert(mlck_state* out, mlck_blob* const* blobs, uint32_t n_blobs,
+                                 uint64_t window_start, uint32_t wsparse, uint64_t data_seed,
+                                 mlck_gradlog* g, const mlck_optimizer* opt);
+
+/* ---- K4: upstream boundary log (LogKey/UpstreamLog, engine.hpp:55-94) ----
+ * kind 0: pinned host ring (copy engine, side stream); kind 1: device ring
+ * on `device` (peer HBM over NVLink when device != ctx device). */
+int mlck_log_create(mlck_ctx* ctx, int kind, int device, uint64_t capacity_bytes,
+                    mlck_log** out);
+int mlck_log_destroy(mlck_log* l);
+/* Records the sender-side copy of a boundary tensor (engine.hpp:383-385,
+ * 407-409); src is device memory produced on the ctx stream. Overwrites an
+ * existing key like the reference's map assignment. */
+int mlck_log_put(mlck_log* l, uint64_t iteration, uint32_t micro_batch, uint32_t boundary,
+                 uint8_t direction, const float* device_src, uint64_t n_floats);
+/* UpstreamLog::at (engine.hpp:71-79): "upstream log missing entry: ..." */
+int mlck_log_get(mlck_log* l, uint64_t iteration, uint32_t micro_batch, uint32_t boundary,
+                 uint8_t direction, float* host_out, uint64_t cap_floats, uint64_t* n_floats);
+/* Device-side copy of an entry into dst (replay input). */
+int mlck_log_get_device(mlck_log* l, uint64_t iteration, uint32_t micro_batch, uint32_t boundary,
+                        uint8_t direction, float* device_dst, uint64_t cap_floats,
+                        uint64_t* n_floats);
+uint64_t mlck_log_count(mlck_log* l);
+uint64_t mlck_log_bytes(mlck_log* l);
+/* i-th entry in LogKey order (std::map order of the reference). */
+int mlck_log_entry(mlck_log* l, uint64_t index, uint64_t* iteration, uint32_t* micro_batch,
+                   uint32_t* boundary, uint8_t* direction, float* host_out, uint64_t cap_floats,
+                   uint64_t* n_floats);
+/* gc_logs (engine.hpp:90-94): drop iteration < persisted_window_start. */
+int mlck_gc_logs(mlck_log* l, uint64_t persisted_window_start);
+/* Wait until every put() has landed. */
+int mlck_log_sync(mlck_log* l);
+
+/* ---- codecs (tensor.hpp:99-183), bulk on device --------------------------- */
+int mlck_quantize(mlck_ctx* ctx, const float* device_in, float* device_out, uint64_t n,
+                  int compute_bytes);
+int mlck_encode_compute(mlck_ctx* ctx, const float* device_in, void* device_codes, uint64_t n,
+                        int compute_bytes);
+int mlck_decode_compute(mlck_ctx* ctx, const void* device_codes, float* device_out, uint64_t n,
+                        int compute_bytes);
+
+/* ---- multi-GPU replica placement (CUDA IPC over NVLink) ------------------ */
+int mlck_ipc_export(mlck_ctx* ctx, void* device_ptr, uint8_t handle[64]);
+int mlck_ipc_open(mlck_ctx* ctx, const uint8_t handle[64], void** device_ptr);
+int mlck_ipc_close(mlck_ctx* ctx, void* device_ptr);
+int mlck_enable_peer_access(mlck_ctx* ctx, int peer_device);
+
+/* ---- timing helpers for the benchmark (events on the ctx stream) --------- */
+int mlck_event_record(mlck_ctx* ctx, int slot);
+int mlck_event_elapsed_ms(mlck_ctx* ctx, int slot_a, int slot_b, float* ms);
+/* Raw device allocation helpers (L2 flush buffer, synthetic inputs). */
+int mlck_device_alloc(mlck_ctx* ctx, uint64_t bytes, void** ptr);
+int mlck_device_free(mlck_ctx* ctx, void* ptr);
+int mlck_device_memset(mlck_ctx* ctx, void* ptr, int value, uint64_t bytes);
+int mlck_host_alloc_pinned(mlck_ctx* ctx, uint64_t bytes, void** ptr);
+int mlck_host_free_pinned(mlck_ctx* ctx, void* ptr);
+int mlck_memcpy_h2d(mlck_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+int mlck_memcpy_d2h(mlck_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -75,6 +75,12 @@ int mlo_quantize_value(float x, int compute_bytes, float* out) {
   }
 }
 
+int mlo_quantize_array(const float* in, size_t n, int compute_bytes, float* out) {
+  for (size_t i = 0; i < n; ++i)
+    if (mlo_quantize_value(in[i], compute_bytes, out + i) != 0) return -1;
+  return 0;
+}
+
 /* ---- tensor.hpp:127-151 pack_reduced ---------------------------------- */
 uint16_t mlo_pack_reduced(float x, int ebits, int mbits) {
   uint32_t bits;

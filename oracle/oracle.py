@@ -97,6 +97,7 @@ class Oracle:
         L.mlo_fnv1a64.restype = C.c_uint64
         L.mlo_fnv1a64.argtypes = [u8p, C.c_size_t, C.c_uint64]
         L.mlo_quantize_value.argtypes = [C.c_float, C.c_int, f32p]
+        L.mlo_quantize_array.argtypes = [f32p, C.c_size_t, C.c_int, f32p]
         L.mlo_pack_reduced.restype = C.c_uint16
         L.mlo_pack_reduced.argtypes = [C.c_float, C.c_int, C.c_int]
         L.mlo_unpack_reduced.restype = C.c_float
@@ -141,14 +142,11 @@ class Oracle:
         return out.value
 
     def quantize(self, vals: np.ndarray, compute_bytes: int) -> np.ndarray:
-        """Vectorised quantize via encode->decode (exact: the codecs are
-        lossless on grid values and quantize is RNE to the grid)."""
+        """quantize_inplace (tensor.hpp:433-436) over an array."""
         vals = np.ascontiguousarray(vals, dtype=np.float32)
-        if compute_bytes == 4:
-            return vals.copy()
         out = np.empty_like(vals)
-        for i, x in enumerate(vals):
-            out[i] = self.quantize_value(float(x), compute_bytes)
+        if self.lib.mlo_quantize_array(_ptr(vals, f32p), vals.size, compute_bytes, _ptr(out, f32p)) != 0:
+            raise ValueError(f"quantize: unsupported width {compute_bytes}")
         return out
 
     def pack_reduced(self, x: float, e: int, m: int) -> int:
@@ -410,7 +408,7 @@ class RefEngine:
 
     def run_iteration(self, log=None):
         err = self.ref._err()
-        self.ref._check(self.ref.lib.mlr_engine_run_iteration(self.h, log.h if log else None, err, 1024), err)
+        self.ref._check(self.ref.lib.mlr_engine_run_iteration(self.h, log.h if log is not None else None, err, 1024), err)
 
     def get_op(self, i: int) -> OpState:
         n = int(self.ref.lib.mlr_engine_op_size(self.h, i))

@@ -1,0 +1,1231 @@
+// capi.cu -- host runtime behind include/mlck_b200.h.
+//
+// Owns the device arenas, blobs, gradient log and boundary log, builds the
+// per-call segment tables and launches the sm_100a kernels of kernels.cu.
+// Error texts follow the reference exceptions they replace (file:line at
+// each site) so the C++ shim (include/moelab_b200) can rethrow them verbatim.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/mlck_b200.h"
+#include "kernels.cuh"
+
+using namespace mlck;
+
+namespace mlck {
+std::string& last_error() {
+  thread_local std::string e;
+  return e;
+}
+}  // namespace mlck
+
+namespace {
+
+template <typename F>
+int api(F&& f) {
+  return api_call(static_cast<F&&>(f));
+}
+
+constexpr uint64_t kAlign = 256;
+constexpr uint32_t kMagic = 0x4b434c4du;
+
+}  // namespace
+
+// =========================================================================
+// context
+// =========================================================================
+struct mlck_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  uint64_t launches = 0;
+  struct Stage {
+    uint8_t* host = nullptr;
+    uint8_t* dev = nullptr;
+    size_t cap = 0;
+    cudaEvent_t done = nullptr;
+    bool used = false;
+  } stage[2];
+  int cur = 0;
+  uint32_t* fnv_scratch = nullptr;
+  size_t fnv_words = 0;
+  unsigned long long* results = nullptr;  // device [64]
+  unsigned long long* host_results = nullptr;  // pinned [64]
+  cudaEvent_t ev[16] = {};
+  // Optional per-kernel timing (CUDA events on the launch stream), read back
+  // with mlck_ctx_timings() -- the benchmark's roofline denominator.
+  bool timing = false;
+  struct Timed {
+    const char* label;
+    cudaEvent_t a, b;
+  };
+  std::vector<Timed> timed;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+
+  void activate() const { MLCK_CUDA(cudaSetDevice(device)); }
+
+  cudaEvent_t next_event() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      MLCK_CUDA(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
+  // Brackets one launch; returns -1 when timing is off.
+  int tbegin(const char* label) {
+    if (!timing) return -1;
+    Timed t{label, next_event(), next_event()};
+    MLCK_CUDA(cudaEventRecord(t.a, stream));
+    timed.push_back(t);
+    return static_cast<int>(timed.size()) - 1;
+  }
+  void tend(int idx) {
+    if (idx >= 0) MLCK_CUDA(cudaEventRecord(timed[idx].b, stream));
+  }
+
+  // Pinned staging + device mirror for one call's metadata.
+  Stage& stage_for(size_t bytes) {
+    cur ^= 1;
+    Stage& s = stage[cur];
+    if (s.used) MLCK_CUDA(cudaEventSynchronize(s.done));
+    if (bytes > s.cap) {
+      // the device copy may still be read by an in-flight kernel
+      MLCK_CUDA(cudaStreamSynchronize(stream));
+      if (s.host) MLCK_CUDA(cudaFreeHost(s.host));
+      if (s.dev) MLCK_CUDA(cudaFree(s.dev));
+      s.cap = align_up(std::max<size_t>(bytes, 1 << 16), 4096);
+      MLCK_CUDA(cudaMallocHost(&s.host, s.cap));
+      MLCK_CUDA(cudaMalloc(&s.dev, s.cap));
+    }
+    return s;
+  }
+  void stage_upload(Stage& s, size_t bytes) {
+    MLCK_CUDA(cudaMemcpyAsync(s.dev, s.host, bytes, cudaMemcpyHostToDevice, stream));
+    MLCK_CUDA(cudaEventRecord(s.done, stream));
+    s.used = true;
+  }
+  uint32_t* fnv_scratch_for(uint64_t n) {
+    const size_t need = fnv_scratch_words(n);
+    if (need > fnv_words) {
+      MLCK_CUDA(cudaStreamSynchronize(stream));
+      if (fnv_scratch) MLCK_CUDA(cudaFree(fnv_scratch));
+      fnv_words = align_up(std::max<size_t>(need, 4096), 1024);
+      MLCK_CUDA(cudaMalloc(&fnv_scratch, fnv_words * 4));
+    }
+    return fnv_scratch;
+  }
+};
+
+// =========================================================================
+// state arena
+// =========================================================================
+struct mlck_state {
+  mlck_ctx* ctx = nullptr;
+  uint32_t n_ops = 0;
+  int cb = 2;
+  std::vector<uint64_t> P, step, full_off, code_off;
+  std::vector<uint8_t> has_full, present;
+  uint8_t* arena = nullptr;
+  uint64_t arena_bytes = 0;
+  uint64_t iteration = 0, data_seed = 0;
+
+  float* master(uint32_t i) const { return reinterpret_cast<float*>(arena + full_off[i]); }
+  void* codes(uint32_t i) const { return arena + code_off[i]; }
+  void check_id(uint32_t id) const {
+    if (id >= n_ops) throw_invalid("operator id " + std::to_string(id) + " out of range");
+  }
+};
+
+struct mlck_blob {
+  mlck_ctx* ctx = nullptr;
+  uint8_t* dev = nullptr;
+  uint64_t cap = 0, size = 0;
+  std::vector<std::pair<uint8_t*, uint64_t>> replicas;
+
+  void reserve(uint64_t n) {
+    if (n <= cap) return;
+    MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (dev) MLCK_CUDA(cudaFree(dev));
+    cap = align_up(n, kAlign);
+    MLCK_CUDA(cudaMalloc(&dev, cap));
+  }
+};
+
+struct mlck_gradlog {
+  mlck_ctx* ctx = nullptr;
+  uint32_t n_ops = 0;
+  std::vector<uint64_t> P, off;  // float offsets inside one iteration slot
+  uint64_t per_iter = 0;
+  uint32_t cap = 0;
+  float* pool = nullptr;
+  std::vector<int64_t> ring_iter;
+  std::vector<std::vector<uint8_t>> present;
+
+  float* slot(uint64_t it, uint32_t op) {
+    if (op >= n_ops) throw_invalid("gradient log: operator " + std::to_string(op) + " out of range");
+    const uint32_t r = static_cast<uint32_t>(it % cap);
+    if (ring_iter[r] != static_cast<int64_t>(it)) {
+      ring_iter[r] = static_cast<int64_t>(it);
+      std::fill(present[r].begin(), present[r].end(), 0);
+    }
+    present[r][op] = 1;
+    return pool + r * per_iter + off[op];
+  }
+  const float* lookup(uint64_t it, uint32_t op) const {
+    const uint32_t r = static_cast<uint32_t>(it % cap);
+    if (op < n_ops && ring_iter[r] == static_cast<int64_t>(it) && present[r][op])
+      return pool + r * per_iter + off[op];
+    throw_runtime("gradient log missing iteration " + std::to_string(it) + " operator " +
+                  std::to_string(op));
+  }
+};
+
+namespace {
+
+uint64_t state_mlst_size(const mlck_state* st) {
+  uint64_t s = 28;
+  for (uint32_t i = 0; i < st->n_ops; ++i) s += 16 + (st->present[i] ? 12 * st->P[i] : 0);
+  return s;
+}
+
+template <typename T>
+void put_le(std::vector<uint8_t>& b, T v) {
+  const size_t o = b.size();
+  b.resize(o + sizeof(T));
+  std::memcpy(b.data() + o, &v, sizeof(T));
+}
+
+// Assembles a byte image as segments: inline bytes (headers) live in the
+// staging buffer's meta region, payload spans point into device memory.
+struct SegmentBuilder {
+  std::vector<pack::Segment> segs;  // src of inline segments = meta offset (patched)
+  std::vector<uint8_t> is_meta;
+  std::vector<uint8_t> meta;
+  uint64_t pos = 0;
+
+  void begin_meta() {}
+  template <typename T>
+  void value(T v) {
+    const uint64_t moff = meta.size();
+    put_le(meta, v);
+    if (!segs.empty() && is_meta.back() && segs.back().dst + segs.back().len == pos &&
+        reinterpret_cast<uint64_t>(segs.back().src) + segs.back().len == moff) {
+      segs.back().len += sizeof(T);
+    } else {
+      segs.push_back({pos, sizeof(T), reinterpret_cast<const uint8_t*>(moff)});
+      is_meta.push_back(1);
+    }
+    pos += sizeof(T);
+  }
+  void span(const void* dev, uint64_t len) {
+    if (!len) return;
+    segs.push_back({pos, len, static_cast<const uint8_t*>(dev)});
+    is_meta.push_back(0);
+    pos += len;
+  }
+};
+
+// Uploads the segment table + meta, launches pack (and the FNV trailer when
+// `trailer`): the blob body is [0, builder.pos), the trailer at pos.
+void run_pack(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
+  const uint64_t body = b.pos;
+  const uint64_t total = body + (trailer ? 8 : 0);
+  out->reserve(total);
+  for (auto& r : out->replicas)
+    if (r.second < total)
+      throw_invalid("replica capacity " + std::to_string(r.second) + " < record size " +
+                    std::to_string(total));
+  out->size = total;
+  const size_t seg_bytes = b.segs.size() * sizeof(pack::Segment);
+  const size_t meta_off = align_up(seg_bytes, 16);
+  auto& s = ctx->stage_for(meta_off + b.meta.size());
+  for (size_t i = 0; i < b.segs.size(); ++i)
+    if (b.is_meta[i])
+      b.segs[i].src = s.dev + meta_off + reinterpret_cast<uint64_t>(b.segs[i].src);
+  std::memcpy(s.host, b.segs.data(), seg_bytes);
+  std::memcpy(s.host + meta_off, b.meta.data(), b.meta.size());
+  ctx->stage_upload(s, meta_off + b.meta.size());
+  pack::Dsts d{};
+  d.p[0] = out->dev;
+  d.n = 1;
+  for (auto& r : out->replicas) d.p[d.n++] = r.first;
+  const int tp = ctx->tbegin("pack");
+  launch_pack(reinterpret_cast<const pack::Segment*>(s.dev), static_cast<int>(b.segs.size()), body,
+              d, ctx->stream);
+  ctx->tend(tp);
+  ctx->launches += body ? 1 : 0;
+  if (trailer) {
+    TrailerDsts t{};
+    for (int r = 0; r < d.n; ++r) t.p[r] = d.p[r] + body;
+    t.n = d.n;
+    uint32_t* scratch = ctx->fnv_scratch_for(body);
+    const int tf = ctx->tbegin("fnv");
+    launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->results, t, ctx->stream);
+    ctx->tend(tf);
+    ctx->launches += 1;
+  }
+}
+
+void build_state_image(const mlck_state* st, SegmentBuilder& b) {
+  b.value<uint32_t>(0x4d4c5354u);  // "MLST"
+  b.value<uint32_t>(1u);
+  b.value<uint64_t>(st->iteration);
+  b.value<uint64_t>(st->data_seed);
+  b.value<uint32_t>(st->n_ops);
+  for (uint32_t i = 0; i < st->n_ops; ++i) {
+    const bool pr = st->present[i];
+    b.value<uint64_t>(pr ? st->step[i] : 0);
+    b.value<uint64_t>(pr ? st->P[i] : 0);
+    if (pr) b.span(st->master(i), 12 * st->P[i]);
+  }
+}
+
+struct SlotEntry {
+  uint32_t id;
+  uint8_t mode;
+};
+
+void build_record(const mlck_state* st, const std::vector<SlotEntry>& ents, uint8_t kind,
+                  uint64_t iteration, uint64_t window_start, uint32_t wsparse, uint32_t slot,
+                  uint64_t data_seed, SegmentBuilder& b) {
+  // snapshot.hpp:120-141
+  b.value<uint32_t>(kMagic);
+  b.value<uint32_t>(1u);
+  b.value<uint8_t>(kind);
+  b.value<uint64_t>(iteration);
+  b.value<uint64_t>(window_start);
+  b.value<uint32_t>(wsparse);
+  b.value<uint32_t>(slot);
+  b.value<uint64_t>(data_seed);
+  b.value<uint32_t>(static_cast<uint32_t>(ents.size()));
+  for (const auto& e : ents) {
+    const uint64_t P = st->P[e.id];
+    b.value<uint32_t>(e.id);
+    b.value<uint8_t>(e.mode);
+    b.value<uint64_t>(P);
+    if (e.mode == 0) {
+      b.value<uint64_t>(st->step[e.id]);
+      b.span(st->master(e.id), 12 * P);
+    } else {
+      b.span(st->codes(e.id), static_cast<uint64_t>(st->cb) * P);
+    }
+  }
+}
+
+std::vector<SlotEntry> slot_entries(const mlck_state* st, const uint32_t* active, uint32_t na,
+                                    const uint32_t* co, uint32_t nc) {
+  std::vector<SlotEntry> ents;
+  ents.reserve(na + nc);
+  for (uint32_t k = 0; k < na; ++k) {
+    const uint32_t id = active[k];
+    if (id >= st->n_ops)  // snapshot.hpp:212-216
+      throw_invalid("snapshot slot references unknown operator " + std::to_string(id));
+    if (!st->has_full[id])  // snapshot.hpp:220-222
+      throw_runtime("snapshot: operator " + std::to_string(id) + " in active set has no full state");
+    ents.push_back({id, 0});
+  }
+  for (uint32_t k = 0; k < nc; ++k) {
+    const uint32_t id = co[k];
+    if (id >= st->n_ops)
+      throw_invalid("snapshot slot references unknown operator " + std::to_string(id));
+    ents.push_back({id, 1});
+  }
+  std::stable_sort(ents.begin(), ents.end(),
+                   [](const SlotEntry& a, const SlotEntry& b) { return a.id < b.id; });
+  return ents;
+}
+
+adam::Opt to_opt(const mlck_optimizer* o) {
+  adam::Opt r;
+  r.kind = o ? o->kind : 0;
+  r.lr = o ? o->lr : 1e-3f;
+  r.b1 = o ? o->beta1 : 0.9f;
+  r.b2 = o ? o->beta2 : 0.999f;
+  r.eps = o ? o->eps : 1e-8f;
+  r.omb1 = 1.0f - r.b1;
+  r.omb2 = 1.0f - r.b2;
+  return r;
+}
+
+// host libm, exactly the reference's std::pow(float, float) (engine.hpp:716-717)
+float bias_correction(float beta, uint64_t step) {
+  return 1.0f - std::pow(beta, static_cast<float>(step));
+}
+
+// Parsed view of a device record (parse_record): checksum, header, entries.
+struct Parsed {
+  WalkResult hdr;
+  std::vector<WalkEntry> entries;
+};
+
+std::string walk_error(const WalkResult& r) {
+  switch (r.status) {
+    case kWalkTruncated: return "container truncated";
+    case kWalkMagic: return "container: bad magic";
+    case kWalkVersion: return "container: unsupported version " + std::to_string(r.version);
+    case kWalkWidth: return "container: unsupported compute width";
+    default: return "container: parse error";
+  }
+}
+
+// Verifies and walks n blobs with one FNV launch per blob and one walk
+// launch, one synchronization.  errors[k] empty when blob k parsed.
+std::vector<Parsed> parse_blobs(mlck_ctx* ctx, mlck_blob* const* blobs, uint32_t n, int cb,
+                                std::vector<std::string>& errors) {
+  errors.assign(n, std::string());
+  std::vector<Parsed> out(n);
+  if (n == 0) return out;
+  if (n > 32) throw_invalid("parse: at most 32 records per call");
+  // device scratch: results + per-blob walk outputs + entry tables
+  const uint32_t cap_entries = 1u << 16;
+  // entry tables live in a per-call device allocation
+  std::vector<uint8_t> checksum_ok(n, 0);
+  std::vector<unsigned long long> computed(n), stored(n);
+  for (uint32_t k = 0; k < n; ++k) {
+    const mlck_blob* b = blobs[k];
+    if (b->size < 8) {
+      errors[k] = "container truncated";
+      continue;
+    }
+    TrailerDsts none{};
+    uint32_t* scratch = ctx->fnv_scratch_for(b->size - 8);
+    const int tf = ctx->tbegin("fnv_verify");
+    launch_fnv(b->dev, b->size - 8, kFnvOffset, scratch, ctx->results + k, none, ctx->stream);
+    ctx->tend(tf);
+    ctx->launches += 1;
+    MLCK_CUDA(cudaMemcpyAsync(ctx->results + 32 + k, b->dev + b->size - 8, 8,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  MLCK_CUDA(cudaMemcpyAsync(ctx->host_results, ctx->results, 64 * 8, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::vector<WalkJob> jobs;
+  std::vector<uint32_t> job_blob;
+  for (uint32_t k = 0; k < n; ++k) {
+    if (!errors[k].empty()) continue;
+    if (ctx->host_results[k] != ctx->host_results[32 + k]) {  // snapshot.hpp:158-163
+      errors[k] = "container checksum mismatch";
+      continue;
+    }
+    job_blob.push_back(k);
+  }
+  if (job_blob.empty()) return out;
+  const size_t nj = job_blob.size();
+  const size_t res_bytes = align_up(nj * sizeof(WalkResult), 256);
+  const size_t ent_bytes = static_cast<size_t>(cap_entries) * sizeof(WalkEntry);
+  uint8_t* dscratch = nullptr;
+  MLCK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dscratch), res_bytes + nj * ent_bytes, ctx->stream));
+  for (size_t j = 0; j < nj; ++j) {
+    const mlck_blob* b = blobs[job_blob[j]];
+    WalkJob w;
+    w.blob = b->dev;
+    w.n = b->size;
+    w.compute_bytes = cb;
+    w.cap = cap_entries;
+    w.result = reinterpret_cast<WalkResult*>(dscratch) + j;
+    w.entries = reinterpret_cast<WalkEntry*>(dscratch + res_bytes + j * ent_bytes);
+    jobs.push_back(w);
+  }
+  auto& s = ctx->stage_for(nj * sizeof(WalkJob));
+  std::memcpy(s.host, jobs.data(), nj * sizeof(WalkJob));
+  ctx->stage_upload(s, nj * sizeof(WalkJob));
+  const int tw = ctx->tbegin("walk");
+  launch_walk(reinterpret_cast<const WalkJob*>(s.dev), static_cast<int>(nj), ctx->stream);
+  ctx->tend(tw);
+  ctx->launches += 1;
+  std::vector<WalkResult> res(nj);
+  MLCK_CUDA(cudaMemcpyAsync(res.data(), dscratch, nj * sizeof(WalkResult), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (size_t j = 0; j < nj; ++j) {
+    const uint32_t k = job_blob[j];
+    out[k].hdr = res[j];
+    if (res[j].status != kWalkOk) {
+      errors[k] = walk_error(res[j]);
+      continue;
+    }
+    out[k].entries.resize(std::min(res[j].n_entries, cap_entries));
+    MLCK_CUDA(cudaMemcpyAsync(out[k].entries.data(), dscratch + res_bytes + j * ent_bytes,
+                              out[k].entries.size() * sizeof(WalkEntry), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+  }
+  MLCK_CUDA(cudaFreeAsync(dscratch, ctx->stream));
+  MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mlck_last_error(void) { return last_error().c_str(); }
+
+// internal: used by log.cu
+int mlck_ctx_device_stream_(mlck_ctx* c, int* device, void** stream) {
+  *device = c->device;
+  *stream = c->stream;
+  return 0;
+}
+
+int mlck_ctx_create(int device, mlck_ctx** out) {
+  return api([&] {
+    auto* c = new mlck_ctx();
+    c->device = device;
+    c->activate();
+    MLCK_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    c->stream = c->own;
+    for (auto& s : c->stage) MLCK_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+    for (auto& e : c->ev) MLCK_CUDA(cudaEventCreate(&e));
+    MLCK_CUDA(cudaMalloc(&c->results, 64 * 8));
+    MLCK_CUDA(cudaMallocHost(&c->host_results, 64 * 8));
+    init_constants();
+    *out = c;
+  });
+}
+
+int mlck_ctx_destroy(mlck_ctx* c) {
+  return api([&] {
+    if (!c) return;
+    c->activate();
+    cudaStreamSynchronize(c->stream);
+    for (auto& s : c->stage) {
+      if (s.host) cudaFreeHost(s.host);
+      if (s.dev) cudaFree(s.dev);
+      cudaEventDestroy(s.done);
+    }
+    for (auto& e : c->ev) cudaEventDestroy(e);
+    if (c->fnv_scratch) cudaFree(c->fnv_scratch);
+    cudaFree(c->results);
+    cudaFreeHost(c->host_results);
+    cudaStreamDestroy(c->own);
+    delete c;
+  });
+}
+
+int mlck_ctx_set_stream(mlck_ctx* c, void* stream) {
+  return api([&] {
+    MLCK_CUDA(cudaStreamSynchronize(c->stream));
+    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own;
+  });
+}
+int mlck_ctx_synchronize(mlck_ctx* c) {
+  return api([&] {
+    c->activate();
+    MLCK_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+uint64_t mlck_ctx_kernel_launches(mlck_ctx* c) { return c ? c->launches : 0; }
+
+int mlck_ctx_set_timing(mlck_ctx* c, int on) {
+  return api([&] {
+    c->timing = on != 0;
+    c->timed.clear();
+    c->ev_used = 0;
+  });
+}
+
+int mlck_ctx_timings(mlck_ctx* c, char* labels, uint64_t labels_cap, float* ms, uint32_t cap,
+                     uint32_t* n) {
+  return api([&] {
+    c->activate();
+    MLCK_CUDA(cudaStreamSynchronize(c->stream));
+    std::string csv;
+    const uint32_t cnt = static_cast<uint32_t>(c->timed.size());
+    for (uint32_t i = 0; i < cnt; ++i) {
+      if (i < cap) MLCK_CUDA(cudaEventElapsedTime(ms + i, c->timed[i].a, c->timed[i].b));
+      if (i) csv += ",";
+      csv += c->timed[i].label;
+    }
+    if (labels && labels_cap) std::snprintf(labels, labels_cap, "%s", csv.c_str());
+    if (n) *n = cnt;
+    c->timed.clear();
+    c->ev_used = 0;
+  });
+}
+
+// ------------------------------------------------------------------ state
+int mlck_state_create(mlck_ctx* ctx, uint32_t n_ops, const uint64_t* pc, int cb, mlck_state** out) {
+  return api([&] {
+    if (cb != 1 && cb != 2 && cb != 4)  // tensor.hpp:107-109
+      throw_invalid("quantize: unsupported width " + std::to_string(cb));
+    ctx->activate();
+    auto* st = new mlck_state();
+    st->ctx = ctx;
+    st->n_ops = n_ops;
+    st->cb = cb;
+    st->P.assign(pc, pc + n_ops);
+    st->step.assign(n_ops, 0);
+    st->has_full.assign(n_ops, 1);
+    st->present.assign(n_ops, 1);
+    uint64_t off = 0;
+    for (uint32_t i = 0; i < n_ops; ++i) {
+      st->full_off.push_back(off);
+      off += align_up(12 * st->P[i] + 16, kAlign);
+    }
+    for (uint32_t i = 0; i < n_ops; ++i) {
+      st->code_off.push_back(off);
+      off += align_up(static_cast<uint64_t>(cb) * st->P[i] + 16, kAlign);
+    }
+    st->arena_bytes = std::max<uint64_t>(off, kAlign);
+    MLCK_CUDA(cudaMalloc(&st->arena, st->arena_bytes));
+    MLCK_CUDA(cudaMemsetAsync(st->arena, 0, st->arena_bytes, ctx->stream));
+    *out = st;
+  });
+}
+
+int mlck_state_destroy(mlck_state* st) {
+  return api([&] {
+    if (!st) return;
+    st->ctx->activate();
+    cudaStreamSynchronize(st->ctx->stream);
+    cudaFree(st->arena);
+    delete st;
+  });
+}
+
+int mlck_state_set_meta(mlck_state* st, uint64_t it, uint64_t seed) {
+  return api([&] {
+    st->iteration = it;
+    st->data_seed = seed;
+  });
+}
+int mlck_state_get_meta(mlck_state* st, uint64_t* it, uint64_t* seed) {
+  return api([&] {
+    if (it) *it = st->iteration;
+    if (seed) *seed = st->data_seed;
+  });
+}
+
+int mlck_state_upload_op(mlck_state* st, uint32_t id, const float* master, const float* m,
+                         const float* v, uint64_t step, int has_full) {
+  return api([&] {
+    st->check_id(id);
+    st->ctx->activate();
+    const uint64_t P = st->P[id];
+    float* d = st->master(id);
+    cudaStream_t s = st->ctx->stream;
+    if (P) {
+      MLCK_CUDA(cudaMemcpyAsync(d, master, 4 * P, cudaMemcpyHostToDevice, s));
+      MLCK_CUDA(cudaMemcpyAsync(d + P, m, 4 * P, cudaMemcpyHostToDevice, s));
+      MLCK_CUDA(cudaMemcpyAsync(d + 2 * P, v, 4 * P, cudaMemcpyHostToDevice, s));
+      launch_encode(d, st->codes(id), P, st->cb, s);  // refresh_compute
+      st->ctx->launches += 1;
+    }
+    MLCK_CUDA(cudaStreamSynchronize(s));  // host arrays are caller-owned
+    st->step[id] = step;
+    st->has_full[id] = has_full ? 1 : 0;
+    st->present[id] = 1;
+  });
+}
+
+int mlck_state_download_op(mlck_state* st, uint32_t id, float* master, float* m, float* v,
+                           uint64_t* step, float* compute, int* has_full) {
+  return api([&] {
+    st->check_id(id);
+    st->ctx->activate();
+    const uint64_t P = st->P[id];
+    float* d = st->master(id);
+    cudaStream_t s = st->ctx->stream;
+    if (P) {
+      if (master) MLCK_CUDA(cudaMemcpyAsync(master, d, 4 * P, cudaMemcpyDeviceToHost, s));
+      if (m) MLCK_CUDA(cudaMemcpyAsync(m, d + P, 4 * P, cudaMemcpyDeviceToHost, s));
+      if (v) MLCK_CUDA(cudaMemcpyAsync(v, d + 2 * P, 4 * P, cudaMemcpyDeviceToHost, s));
+      if (compute) {
+        float* tmp = nullptr;
+        MLCK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), 4 * P, s));
+        launch_decode(st->codes(id), tmp, P, st->cb, s);
+        st->ctx->launches += 1;
+        MLCK_CUDA(cudaMemcpyAsync(compute, tmp, 4 * P, cudaMemcpyDeviceToHost, s));
+        MLCK_CUDA(cudaFreeAsync(tmp, s));
+      }
+    }
+    MLCK_CUDA(cudaStreamSynchronize(s));
+    if (step) *step = st->step[id];
+    if (has_full) *has_full = st->has_full[id];
+  });
+}
+
+int mlck_state_set_step(mlck_state* st, uint32_t id, uint64_t step, int has_full) {
+  return api([&] {
+    st->check_id(id);
+    st->step[id] = step;
+    st->has_full[id] = has_full ? 1 : 0;
+  });
+}
+
+int mlck_state_op_ptrs(mlck_state* st, uint32_t id, float** master, float** m, float** v,
+                       void** compute) {
+  return api([&] {
+    st->check_id(id);
+    float* d = st->master(id);
+    if (master) *master = d;
+    if (m) *m = d + st->P[id];
+    if (v) *v = d + 2 * st->P[id];
+    if (compute) *compute = st->codes(id);
+  });
+}
+
+int mlck_state_fill_synthetic(mlck_state* st, uint64_t seed, uint64_t step) {
+  return api([&] {
+    st->ctx->activate();
+    cudaStream_t s = st->ctx->stream;
+    for (uint32_t i = 0; i < st->n_ops; ++i) {
+      const uint64_t P = st->P[i];
+      float* d = st->master(i);
+      launch_synth(d, P, seed, 3ull * i + 0, -0.25f, 0.25f, s);
+      launch_synth(d + P, P, seed, 3ull * i + 1, -1e-3f, 1e-3f, s);
+      launch_synth(d + 2 * P, P, seed, 3ull * i + 2, 0.0f, 1e-6f, s);
+      launch_encode(d, st->codes(i), P, st->cb, s);
+      st->ctx->launches += P ? 4 : 0;
+      st->step[i] = step;
+      st->has_full[i] = 1;
+      st->present[i] = 1;
+    }
+  });
+}
+
+int mlck_state_serialize_blob(mlck_state* st, mlck_blob* out) {
+  return api([&] {
+    st->ctx->activate();
+    SegmentBuilder b;
+    build_state_image(st, b);
+    run_pack(st->ctx, b, out, /*trailer=*/false);
+  });
+}
+
+int mlck_state_serialize(mlck_state* st, uint8_t* host_out, uint64_t cap, uint64_t* size) {
+  return api([&] {
+    const uint64_t n = state_mlst_size(st);
+    if (size) *size = n;
+    if (!host_out) return;
+    if (cap < n) throw_invalid("serialize_state: buffer too small");
+    st->ctx->activate();
+    mlck_blob tmp;
+    tmp.ctx = st->ctx;
+    SegmentBuilder b;
+    build_state_image(st, b);
+    run_pack(st->ctx, b, &tmp, false);
+    MLCK_CUDA(cudaMemcpyAsync(host_out, tmp.dev, n, cudaMemcpyDeviceToHost, st->ctx->stream));
+    MLCK_CUDA(cudaStreamSynchronize(st->ctx->stream));
+    MLCK_CUDA(cudaFree(tmp.dev));
+  });
+}
+
+// ------------------------------------------------------------------ blobs
+int mlck_blob_create(mlck_ctx* ctx, uint64_t capacity, mlck_blob** out) {
+  return api([&] {
+    ctx->activate();
+    auto* b = new mlck_blob();
+    b->ctx = ctx;
+    b->reserve(std::max<uint64_t>(capacity, kAlign));
+    *out = b;
+  });
+}
+int mlck_blob_destroy(mlck_blob* b) {
+  return api([&] {
+    if (!b) return;
+    b->ctx->activate();
+    cudaStreamSynchronize(b->ctx->stream);
+    if (b->dev) cudaFree(b->dev);
+    delete b;
+  });
+}
+int mlck_blob_from_host(mlck_ctx* ctx, const uint8_t* bytes, uint64_t n, mlck_blob** out) {
+  return api([&] {
+    ctx->activate();
+    auto* b = new mlck_blob();
+    b->ctx = ctx;
+    b->reserve(std::max<uint64_t>(n, kAlign));
+    if (n) MLCK_CUDA(cudaMemcpyAsync(b->dev, bytes, n, cudaMemcpyHostToDevice, ctx->stream));
+    MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+    b->size = n;
+    *out = b;
+  });
+}
+uint64_t mlck_blob_size(const mlck_blob* b) { return b ? b->size : 0; }
+void* mlck_blob_device_ptr(const mlck_blob* b) { return b ? b->dev : nullptr; }
+int mlck_blob_to_host(const mlck_blob* b, uint8_t* host, uint64_t cap) {
+  return api([&] {
+    if (cap < b->size) throw_invalid("blob_to_host: buffer too small");
+    b->ctx->activate();
+    if (b->size)
+      MLCK_CUDA(cudaMemcpyAsync(host, b->dev, b->size, cudaMemcpyDeviceToHost, b->ctx->stream));
+    MLCK_CUDA(cudaStreamSynchronize(b->ctx->stream));
+  });
+}
+int mlck_blob_add_replica(mlck_blob* b, void* ptr, uint64_t capacity) {
+  return api([&] {
+    if (b->replicas.size() + 1 >= static_cast<size_t>(pack::kMaxDst))
+      throw_invalid("at most " + std::to_string(pack::kMaxDst - 1) + " replicas per blob");
+    if (reinterpret_cast<uintptr_t>(ptr) % 16)
+      throw_invalid("replica buffers must be 16-byte aligned");
+    b->replicas.push_back({static_cast<uint8_t*>(ptr), capacity});
+  });
+}
+int mlck_blob_clear_replicas(mlck_blob* b) {
+  return api([&] { b->replicas.clear(); });
+}
+
+// ------------------------------------------------------------------ snapshot
+int mlck_snapshot_record(mlck_state* st, const uint32_t* active, uint32_t na, const uint32_t* co,
+                         uint32_t nc, uint32_t slot_index, uint8_t kind, uint64_t window_start,
+                         uint32_t wsparse, mlck_blob* out) {
+  return api([&] {
+    st->ctx->activate();
+    const auto ents = slot_entries(st, active, na, co, nc);
+    SegmentBuilder b;
+    build_record(st, ents, kind, st->iteration, window_start, wsparse, slot_index, st->data_seed, b);
+    run_pack(st->ctx, b, out, true);
+  });
+}
+
+int mlck_snapshot_record_host(mlck_state* st, const uint32_t* active, uint32_t na,
+                              const uint32_t* co, uint32_t nc, uint32_t slot_index, uint8_t kind,
+                              uint64_t window_start, uint32_t wsparse, mlck_blob* scratch,
+                              uint8_t* host_out, uint64_t cap, uint64_t* size) {
+  return api([&] {
+    st->ctx->activate();
+    const auto ents = slot_entries(st, active, na, co, nc);
+    SegmentBuilder b;
+    build_record(st, ents, kind, st->iteration, window_start, wsparse, slot_index, st->data_seed, b);
+    const uint64_t n = b.pos + 8;
+    if (size) *size = n;
+    if (!host_out) return;
+    if (cap < n) throw_invalid("snapshot: host buffer too small");
+    run_pack(st->ctx, b, scratch, true);
+    MLCK_CUDA(cudaMemcpyAsync(host_out, scratch->dev, n, cudaMemcpyDeviceToHost, st->ctx->stream));
+    MLCK_CUDA(cudaStreamSynchronize(st->ctx->stream));
+  });
+}
+
+int mlck_dense_checkpoint(mlck_state* st, mlck_blob* out) {
+  return api([&] {
+    std::vector<SlotEntry> ents;
+    for (uint32_t id = 0; id < st->n_ops; ++id) {
+      if (!st->has_full[id])  // snapshot.hpp:283-285
+        throw_runtime("dense checkpoint: operator " + std::to_string(id) + " is frozen");
+      ents.push_back({id, 0});
+    }
+    st->ctx->activate();
+    SegmentBuilder b;
+    build_record(st, ents, 0, st->iteration, st->iteration, 1, 0, st->data_seed, b);
+    run_pack(st->ctx, b, out, true);
+  });
+}
+
+int mlck_fnv1a64(mlck_ctx* ctx, const void* ptr, uint64_t n, uint64_t seed, uint64_t* out) {
+  return api([&] {
+    ctx->activate();
+    TrailerDsts none{};
+    launch_fnv(static_cast<const uint8_t*>(ptr), n, seed, ctx->fnv_scratch_for(n), ctx->results,
+               none, ctx->stream);
+    ctx->launches += 1;
+    MLCK_CUDA(cudaMemcpyAsync(ctx->host_results, ctx->results, 8, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = ctx->host_results[0];
+  });
+}
+
+// ------------------------------------------------------------------ parse
+int mlck_parse_record(mlck_blob* b, int cb, mlck_record_info* info, mlck_entry_info* entries,
+                      uint32_t cap, uint32_t* n_entries) {
+  return api([&] {
+    b->ctx->activate();
+    std::vector<std::string> errs;
+    auto p = parse_blobs(b->ctx, &b, 1, cb, errs);
+    if (!errs[0].empty()) throw_runtime(errs[0]);
+    const auto& h = p[0].hdr;
+    if (info) *info = {h.kind, h.iteration, h.window_start, h.wsparse, h.slot, h.data_seed, h.op_count};
+    if (n_entries) *n_entries = static_cast<uint32_t>(p[0].entries.size());
+    for (uint32_t i = 0; i < std::min<uint32_t>(cap, p[0].entries.size()); ++i) {
+      const auto& e = p[0].entries[i];
+      entries[i] = {e.id, e.mode, e.param_count, e.step, e.payload_offset};
+    }
+  });
+}
+
+int mlck_read_entry(mlck_blob* b, const mlck_entry_info* e, int cb, float* master, float* m,
+                    float* v, float* compute) {
+  return api([&] {
+    mlck_ctx* ctx = b->ctx;
+    ctx->activate();
+    const uint64_t P = e->param_count;
+    const uint8_t* src = b->dev + e->payload_offset;
+    if (e->mode == 0) {
+      if (master) MLCK_CUDA(cudaMemcpyAsync(master, src, 4 * P, cudaMemcpyDeviceToHost, ctx->stream));
+      if (m) MLCK_CUDA(cudaMemcpyAsync(m, src + 4 * P, 4 * P, cudaMemcpyDeviceToHost, ctx->stream));
+      if (v) MLCK_CUDA(cudaMemcpyAsync(v, src + 8 * P, 4 * P, cudaMemcpyDeviceToHost, ctx->stream));
+    } else if (compute && P) {
+      // codes at an arbitrary offset: stage aligned, decode on device
+      void* codes = nullptr;
+      float* tmp = nullptr;
+      MLCK_CUDA(cudaMallocAsync(&codes, cb * P, ctx->stream));
+      MLCK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), 4 * P, ctx->stream));
+      MLCK_CUDA(cudaMemcpyAsync(codes, src, cb * P, cudaMemcpyDeviceToDevice, ctx->stream));
+      launch_decode(codes, tmp, P, cb, ctx->stream);
+      ctx->launches += 1;
+      MLCK_CUDA(cudaMemcpyAsync(compute, tmp, 4 * P, cudaMemcpyDeviceToHost, ctx->stream));
+      MLCK_CUDA(cudaFreeAsync(codes, ctx->stream));
+      MLCK_CUDA(cudaFreeAsync(tmp, ctx->stream));
+    }
+    MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int mlck_check_coverage(mlck_blob* const* blobs, uint32_t n, uint64_t op_count, int cb) {
+  return api([&] {
+    if (n == 0) {
+      if (op_count) throw_runtime("window coverage violated for operator 0: 0 full payloads");
+      return;
+    }
+    mlck_ctx* ctx = blobs[0]->ctx;
+    ctx->activate();
+    std::vector<std::string> errs;
+    auto p = parse_blobs(ctx, blobs, n, cb, errs);
+    std::vector<int> seen(op_count, 0);
+    for (uint32_t k = 0; k < n; ++k) {
+      if (!errs[k].empty()) throw_runtime(errs[k]);
+      for (const auto& e : p[k].entries)
+        if (e.mode == 0) {
+          if (e.id >= op_count) throw_runtime("window coverage: operator id out of range");
+          seen[e.id] += 1;
+        }
+    }
+    for (uint64_t id = 0; id < op_count; ++id)  // snapshot.hpp:329-333
+      if (seen[id] != 1)
+        throw_runtime("window coverage violated for operator " + std::to_string(id) + ": " +
+                      std::to_string(seen[id]) + " full payloads");
+  });
+}
+
+// ------------------------------------------------------------------ gradients
+int mlck_gradlog_create(mlck_ctx* ctx, uint32_t n_ops, const uint64_t* pc, uint32_t cap,
+                        mlck_gradlog** out) {
+  return api([&] {
+    if (cap == 0) throw_invalid("gradient log: capacity must be >= 1");
+    ctx->activate();
+    auto* g = new mlck_gradlog();
+    g->ctx = ctx;
+    g->n_ops = n_ops;
+    g->P.assign(pc, pc + n_ops);
+    for (uint32_t i = 0; i < n_ops; ++i) {
+      g->off.push_back(g->per_iter);
+      g->per_iter += align_up(g->P[i], 64);  // 256-byte aligned slots
+    }
+    g->per_iter = std::max<uint64_t>(g->per_iter, 64);
+    g->cap = cap;
+    MLCK_CUDA(cudaMalloc(&g->pool, 4 * g->per_iter * cap));
+    g->ring_iter.assign(cap, -1);
+    g->present.assign(cap, std::vector<uint8_t>(n_ops, 0));
+    *out = g;
+  });
+}
+int mlck_gradlog_destroy(mlck_gradlog* g) {
+  return api([&] {
+    if (!g) return;
+    g->ctx->activate();
+    cudaStreamSynchronize(g->ctx->stream);
+    cudaFree(g->pool);
+    delete g;
+  });
+}
+int mlck_gradlog_put(mlck_gradlog* g, uint64_t it, uint32_t op, const float* host) {
+  return api([&] {
+    g->ctx->activate();
+    float* d = g->slot(it, op);
+    if (g->P[op])
+      MLCK_CUDA(cudaMemcpyAsync(d, host, 4 * g->P[op], cudaMemcpyHostToDevice, g->ctx->stream));
+    MLCK_CUDA(cudaStreamSynchronize(g->ctx->stream));
+  });
+}
+int mlck_gradlog_slot(mlck_gradlog* g, uint64_t it, uint32_t op, float** ptr) {
+  return api([&] { *ptr = g->slot(it, op); });
+}
+int mlck_gradlog_fill_synthetic(mlck_gradlog* g, uint64_t first, uint32_t n_it, uint64_t seed) {
+  return api([&] {
+    g->ctx->activate();
+    for (uint32_t k = 0; k < n_it; ++k)
+      for (uint32_t op = 0; op < g->n_ops; ++op) {
+        const uint64_t it = first + k;
+        launch_synth(g->slot(it, op), g->P[op], seed, 1000000ull + it * g->n_ops + op, -1e-2f,
+                     1e-2f, g->ctx->stream);
+        g->ctx->launches += g->P[op] ? 1 : 0;
+      }
+  });
+}
+
+// ------------------------------------------------------------------ Adam
+int mlck_optimizer_step_adam(mlck_ctx* ctx, float* w, float* m, float* v, uint64_t* step,
+                             const float* g, uint64_t n, const mlck_optimizer* opt) {
+  return api([&] {
+    ctx->activate();
+    const adam::Opt o = to_opt(opt);
+    *step += 1;  // engine.hpp:745
+    launch_adam_arrays(w, m, v, g, n, o, bias_correction(o.b1, *step), bias_correction(o.b2, *step),
+                       ctx->stream);
+    ctx->launches += n ? 1 : 0;
+  });
+}
+
+namespace {
+// Launch the fused replay over `ops` (host vectors) with their gradient
+// pointers and bias corrections.
+void run_replay(mlck_ctx* ctx, std::vector<adam::ConvOp>& ops, const std::vector<const float*>& gptr,
+                const std::vector<float2>& bc, const adam::Opt& o, int cb) {
+  uint64_t units = 0;
+  for (auto& op : ops) {
+    op.unit_begin = units;
+    units += div_up(op.P, 4);
+  }
+  const size_t ob = ops.size() * sizeof(adam::ConvOp);
+  const size_t go = align_up(ob, 16), gb = gptr.size() * sizeof(float*);
+  const size_t bo = align_up(go + gb, 16), bb = bc.size() * sizeof(float2);
+  auto& s = ctx->stage_for(bo + bb + 16);
+  std::memcpy(s.host, ops.data(), ob);
+  std::memcpy(s.host + go, gptr.data(), gb);
+  std::memcpy(s.host + bo, bc.data(), bb);
+  ctx->stage_upload(s, bo + bb);
+  const int tr = ctx->tbegin("replay");
+  launch_replay(reinterpret_cast<const adam::ConvOp*>(s.dev), static_cast<int>(ops.size()),
+                reinterpret_cast<const float* const*>(s.dev + go),
+                reinterpret_cast<const float2*>(s.dev + bo), o, cb, units, ctx->stream);
+  ctx->tend(tr);
+  ctx->launches += units ? 1 : 0;
+}
+}  // namespace
+
+int mlck_state_apply_updates(mlck_state* st, const uint32_t* ids, uint32_t n_ids, mlck_gradlog* g,
+                             uint64_t iteration, const mlck_optimizer* opt) {
+  return api([&] {
+    st->ctx->activate();
+    const adam::Opt o = to_opt(opt);
+    std::vector<adam::ConvOp> ops;
+    std::vector<const float*> gptr;
+    std::vector<float2> bc;
+    for (uint32_t k = 0; k < n_ids; ++k) {
+      const uint32_t id = ids[k];
+      st->check_id(id);
+      adam::ConvOp c{};
+      c.src = reinterpret_cast<const uint8_t*>(st->master(id));
+      c.dst = st->master(id);
+      c.codes = st->codes(id);
+      c.P = st->P[id];
+      c.n_steps = 1;
+      c.grad_base = static_cast<uint32_t>(gptr.size());
+      c.bc_base = static_cast<uint32_t>(bc.size());
+      gptr.push_back(g->lookup(iteration, id));
+      const uint64_t s1 = st->step[id] + 1;  // engine.hpp:713/715
+      bc.push_back(make_float2(bias_correction(o.b1, s1), bias_correction(o.b2, s1)));
+      st->step[id] = s1;
+      ops.push_back(c);
+    }
+    run_replay(st->ctx, ops, gptr, bc, o, st->cb);
+  });
+}
+
+// ------------------------------------------------------------------ K3
+int mlck_sparse_to_dense_convert(mlck_state* out, mlck_blob* const* blobs, uint32_t n_blobs,
+                                 uint64_t window_start, uint32_t W, uint64_t data_seed,
+                                 mlck_gradlog* g, const mlck_optimizer* opt) {
+  return api([&] {
+    if (n_blobs != W)  // recovery.hpp:184-187
+      throw_runtime("sparse checkpoint incomplete: " + std::to_string(n_blobs) + " of " +
+                    std::to_string(W) + " records");
+    mlck_ctx* ctx = out->ctx;
+    ctx->activate();
+    std::vector<std::string> errs;
+    const uint32_t n_parse = (W == 1) ? 1 : W;
+    auto parsed = parse_blobs(ctx, blobs, n_parse, out->cb, errs);
+    for (uint32_t k = 0; k < n_parse; ++k)  // recovery.hpp:163-171
+      if (!errs[k].empty())
+        throw_runtime("sparse checkpoint record (slot " + std::to_string(k) + "): " + errs[k]);
+    // each operator's last Full payload in slot order (load_record overwrites)
+    struct Src {
+      int slot = -1;
+      const WalkEntry* e = nullptr;
+    };
+    std::vector<Src> src(out->n_ops);
+    for (uint32_t k = 0; k < n_parse; ++k)
+      for (const auto& e : parsed[k].entries) {
+        if (e.id >= out->n_ops) throw_runtime("conversion: record operator id out of range");
+        if (e.mode == 0) {
+          if (e.param_count != out->P[e.id])
+            throw_invalid("conversion: operator " + std::to_string(e.id) + " size mismatch");
+          src[e.id] = {static_cast<int>(k), &e};
+        }
+      }
+    const adam::Opt o = to_opt(opt);
+    std::vector<adam::ConvOp> ops;
+    std::vector<const float*> gptr;
+    std::vector<float2> bc;
+    if (W > 1) {
+      for (uint32_t id = 0; id < out->n_ops; ++id)  // recovery.hpp:222-225
+        if (src[id].slot < 0)
+          throw_runtime("conversion finished with frozen operator " + std::to_string(id));
+    }
+    std::vector<uint64_t> new_step(out->n_ops, 0);
+    for (uint32_t id = 0; id < out->n_ops; ++id) {
+      out->present[id] = src[id].slot >= 0 ? 1 : 0;
+      out->has_full[id] = out->present[id];
+      if (src[id].slot < 0) continue;
+      const int k = src[id].slot;
+      const WalkEntry& e = *src[id].e;
+      adam::ConvOp c{};
+      c.src = blobs[k]->dev + e.payload_offset;
+      c.dst = out->master(id);
+      c.codes = out->codes(id);
+      c.P = e.param_count;
+      c.n_steps = W > 1 ? W - static_cast<uint32_t>(k) : 0;
+      c.grad_base = static_cast<uint32_t>(gptr.size());
+      c.bc_base = static_cast<uint32_t>(bc.size());
+      uint64_t stp = e.step;
+      for (uint32_t s = 0; s < c.n_steps; ++s) {
+        const uint64_t it = window_start + static_cast<uint64_t>(k) + 1 + s;
+        if (!g) throw_invalid("conversion: gradient log required for W > 1");
+        gptr.push_back(g->lookup(it, id));
+        stp += 1;
+        bc.push_back(make_float2(bias_correction(o.b1, stp), bias_correction(o.b2, stp)));
+      }
+      new_step[id] = stp;
+      ops.push_back(c);
+    }
+    run_replay(ctx, ops, gptr, bc, o, out->cb);
+    for (uint32_t id = 0; id < out->n_ops; ++id) out->step[id] = new_step[id];
+    if (W == 1) {
+      out->iteration = parsed[0].hdr.iteration;
+      out->data_seed = parsed[0].hdr.data_seed;
+    } else {
+      out->iteration = window_start + W;
+      out->data_seed = data_seed;
+    }
+  });
+}
+
+// ------------------------------------------------------------------ codecs
+int mlck_quantize(mlck_ctx* ctx, const float* in, float* out, uint64_t n, int cb) {
+  return api([&] {
+    if (cb != 1 && cb != 2 && cb != 4) throw_invalid("quantize: unsupported width " + std::to_string(cb));
+    ctx->activate();
+    launch_quantize(in, out, n, cb, ctx->stream);
+    ctx->launches += n ? 1 : 0;
+  });
+}
+int mlck_encode_compute(mlck_ctx* ctx, const float* in, void* codes, uint64_t n, int cb) {
+  return api([&] {
+    if (cb != 1 && cb != 2 && cb != 4) throw_invalid("container: unsupported compute width");
+    ctx->activate();
+    launch_encode(in, codes, n, cb, ctx->stream);
+    ctx->launches += n ? 1 : 0;
+  });
+}
+int mlck_decode_compute(mlck_ctx* ctx, const void* codes, float* out, uint64_t n, int cb) {
+  return api([&] {
+    if (cb != 1 && cb != 2 && cb != 4) throw_invalid("container: unsupported compute width");
+    ctx->activate();
+    launch_decode(codes, out, n, cb, ctx->stream);
+    ctx->launches += n ? 1 : 0;
+  });
+}
+
+// ------------------------------------------------------------------ IPC / peers
+int mlck_ipc_export(mlck_ctx* ctx, void* ptr, uint8_t handle[64]) {
+  return api([&] {
+    ctx->activate();
+    cudaIpcMemHandle_t h;
+    MLCK_CUDA(cudaIpcGetMemHandle(&h, ptr));
+    static_assert(sizeof(h) == 64, "ipc handle size");
+    std::memcpy(handle, &h, 64);
+  });
+}
+int mlck_ipc_open(mlck_ctx* ctx, const uint8_t handle[64], void** ptr) {
+  return api([&] {
+    ctx->activate();
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    MLCK_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+int mlck_ipc_close(mlck_ctx* ctx, void* ptr) {
+  return api([&] {
+    ctx->activate();
+    MLCK_CUDA(cudaIpcCloseMemHandle(ptr));
+  });
+}
+int mlck_enable_peer_access(mlck_ctx* ctx, int peer) {
+  return api([&] {
+    ctx->activate();
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+      cudaGetLastError();
+      return;
+    }
+    MLCK_CUDA(e);
+  });
+}
+
+// ------------------------------------------------------------------ timing / memory
+int mlck_event_record(mlck_ctx* ctx, int slot) {
+  return api([&] {
+    if (slot < 0 || slot >= 16) throw_invalid("event slot out of range");
+    MLCK_CUDA(cudaEventRecord(ctx->ev[slot], ctx->stream));
+  });
+}
+int mlck_event_elapsed_ms(mlck_ctx* ctx, int a, int b, float* ms) {
+  return api([&] {
+    MLCK_CUDA(cudaEventSynchronize(ctx->ev[b]));
+    MLCK_CUDA(cudaEventElapsedTime(ms, ctx->ev[a], ctx->ev[b]));
+  });
+}
+int mlck_device_alloc(mlck_ctx* ctx, uint64_t bytes, void** ptr) {
+  return api([&] {
+    ctx->activate();
+    MLCK_CUDA(cudaMalloc(ptr, std::max<uint64_t>(bytes, 16)));
+  });
+}
+int mlck_device_free(mlck_ctx* ctx, void* ptr) {
+  return api([&] {
+    ctx->activate();
+    MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+    MLCK_CUDA(cudaFree(ptr));
+  });
+}
+int mlck_device_memset(mlck_ctx* ctx, void* ptr, int value, uint64_t bytes) {
+  return api([&] {
+    ctx->activate();
+    MLCK_CUDA(cudaMemsetAsync(ptr, value, bytes, ctx->stream));
+  });
+}
+int mlck_host_alloc_pinned(mlck_ctx* ctx, uint64_t bytes, void** ptr) {
+  return api([&] {
+    ctx->activate();
+    MLCK_CUDA(cudaMallocHost(ptr, std::max<uint64_t>(bytes, 16)));
+  });
+}
+int mlck_host_free_pinned(mlck_ctx* ctx, void* ptr) {
+  return api([&] {
+    ctx->activate();
+    MLCK_CUDA(cudaFreeHost(ptr));
+  });
+}
+int mlck_memcpy_h2d(mlck_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+  return api([&] {
+    ctx->activate();
+    MLCK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  });
+}
+int mlck_memcpy_d2h(mlck_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+  return api([&] {
+    ctx->activate();
+    MLCK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  });
+}
+
+}  // extern "C"

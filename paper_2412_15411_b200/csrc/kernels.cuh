@@ -1,0 +1,63 @@
+// kernels.cuh -- host launchers for the kernels in kernels.cu.
+#pragma once
+
+#include "adam.cuh"
+#include "mlck_common.cuh"
+#include "pack.cuh"
+
+namespace mlck {
+
+constexpr uint64_t kFnvOffset = 0xcbf29ce484222325ull;  // digest.hpp:18
+
+struct TrailerDsts {
+  uint8_t* p[pack::kMaxDst];
+  int n;
+};
+
+// ---- record walk (parse_record after the checksum)
+enum WalkStatus : uint32_t { kWalkOk = 0, kWalkTruncated = 1, kWalkMagic = 3, kWalkVersion = 4, kWalkWidth = 5 };
+struct WalkEntry {
+  uint32_t id;
+  uint8_t mode;
+  uint64_t param_count;
+  uint64_t step;
+  uint64_t payload_offset;
+};
+struct WalkResult {
+  uint32_t status, version, op_count, n_entries;
+  uint8_t kind;
+  uint64_t iteration, window_start, data_seed;
+  uint32_t wsparse, slot;
+};
+struct WalkJob {
+  const uint8_t* blob;
+  uint64_t n;
+  int compute_bytes;
+  uint32_t cap;
+  WalkEntry* entries;
+  WalkResult* result;
+};
+
+void init_constants();
+uint64_t fnv_chunks(uint64_t n);
+size_t fnv_scratch_words(uint64_t n);
+void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch,
+                unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream);
+void launch_fnv_empty(uint64_t seed, unsigned long long* result, const TrailerDsts& trailer,
+                      cudaStream_t stream);
+void launch_pack(const pack::Segment* segs, int n_segs, uint64_t total, const pack::Dsts& d,
+                 cudaStream_t stream);
+void launch_walk(const WalkJob* jobs, int n_jobs, cudaStream_t stream);
+void launch_replay(const adam::ConvOp* ops, int n_ops, const float* const* gptr, const float2* bc,
+                   const adam::Opt& o, int cb, uint64_t total_units, cudaStream_t stream);
+void launch_adam_arrays(float* w, float* m, float* v, const float* g, uint64_t n,
+                        const adam::Opt& o, float bc1, float bc2, cudaStream_t stream);
+void launch_quantize(const float* in, float* out, uint64_t n, int cb, cudaStream_t stream);
+void launch_encode(const float* in, void* codes, uint64_t n, int cb, cudaStream_t stream);
+void launch_decode(const void* codes, float* out, uint64_t n, int cb, cudaStream_t stream);
+uint64_t synth_key(uint64_t seed, uint64_t stream);
+void launch_synth(float* out, uint64_t n, uint64_t seed, uint64_t stream_id, float lo, float hi,
+                  cudaStream_t stream);
+void launch_copy16(void* dst, const void* src, uint64_t bytes, cudaStream_t stream);
+
+}  // namespace mlck

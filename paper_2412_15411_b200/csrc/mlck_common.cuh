@@ -1,0 +1,79 @@
+// mlck_common.cuh -- shared helpers for the sm_100a checkpoint data path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace mlck {
+
+// Error kinds carried across the C ABI (include/mlck_b200.h): the C++ shim
+// rethrows kInvalid as std::invalid_argument and kRuntime / kCuda as
+// std::runtime_error with the same text the reference uses.
+enum Status : int { kOk = 0, kInvalid = 1, kRuntime = 2, kCuda = 3 };
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void throw_invalid(const std::string& m) { throw Error(kInvalid, m); }
+[[noreturn]] inline void throw_runtime(const std::string& m) { throw Error(kRuntime, m); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(kCuda, std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
+}
+#define MLCK_CUDA(call) ::mlck::cuda_check((call), #call)
+
+// Thread-local message of the last failing C-ABI call (defined in capi.cu).
+std::string& last_error();
+
+// Runs f, mapping exceptions to the C-ABI status codes.
+template <typename F>
+int api_call(F&& f) {
+  try {
+    f();
+    return kOk;
+  } catch (const Error& e) {
+    last_error() = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    last_error() = e.what();
+    return kRuntime;
+  }
+}
+
+__host__ __device__ constexpr uint64_t div_up(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+__host__ __device__ constexpr uint64_t align_up(uint64_t a, uint64_t b) { return div_up(a, b) * b; }
+
+constexpr int kSmCount = 148;  // B200: 2 dies x 74 SMs
+
+// ---- memory-model helpers (inline PTX, sm_100a) -------------------------
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Streaming 128-bit load that does not allocate in L1 (each byte of the
+// state arena is read exactly once per pack).
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_v4(void* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+}  // namespace mlck

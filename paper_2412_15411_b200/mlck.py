@@ -1,0 +1,624 @@
+"""Python binding of the C ABI (include/mlck_b200.h) -- the host-side mirror
+of the reference's moelab checkpoint API used by the tests and bench.py.
+
+The reference is C++ (proj/include/moelab); its drop-in is the C++ shim in
+include/moelab_b200/.  This module binds the same ABI with ctypes so pytest
+and the benchmark can drive the sm_100a kernels.  It loads ONLY the in-tree
+libmlck_b200.so and raises if it is missing: there is no CPU fallback.
+
+Error mapping mirrors the reference: status 1 -> ValueError
+(std::invalid_argument), 2/3 -> RuntimeError (std::runtime_error), with the
+reference's message text.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_build", "libmlck_b200.so")
+
+u8p = C.POINTER(C.c_uint8)
+f32p = C.POINTER(C.c_float)
+u32p = C.POINTER(C.c_uint32)
+u64p = C.POINTER(C.c_uint64)
+vp = C.c_void_p
+
+
+class MlckInvalid(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class MlckRuntime(RuntimeError):
+    """std::runtime_error in the reference (integrity / state errors)."""
+
+
+class Optimizer(C.Structure):
+    """OptimizerConfig (engine.hpp:21-28)."""
+    _fields_ = [("kind", C.c_int32), ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
+                ("eps", C.c_float)]
+
+    @classmethod
+    def adam(cls, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8):
+        return cls(0, lr, beta1, beta2, eps)
+
+    @classmethod
+    def sgd(cls, lr=1e-3):
+        return cls(1, lr, 0.9, 0.999, 1e-8)
+
+
+class RecordInfo(C.Structure):
+    _fields_ = [("kind", C.c_uint8), ("iteration", C.c_uint64), ("window_start", C.c_uint64),
+                ("wsparse", C.c_uint32), ("slot", C.c_uint32), ("data_seed", C.c_uint64),
+                ("op_count", C.c_uint32)]
+
+
+class EntryInfo(C.Structure):
+    _fields_ = [("id", C.c_uint32), ("mode", C.c_uint8), ("param_count", C.c_uint64),
+                ("step", C.c_uint64), ("payload_offset", C.c_uint64)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `make -C paper_2412_15411_b200` "
+                              "(the CUDA path has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        sig = {
+            "mlck_last_error": (C.c_char_p, []),
+            "mlck_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+            "mlck_ctx_destroy": (C.c_int, [vp]),
+            "mlck_ctx_set_stream": (C.c_int, [vp, vp]),
+            "mlck_ctx_synchronize": (C.c_int, [vp]),
+            "mlck_ctx_kernel_launches": (C.c_uint64, [vp]),
+            "mlck_ctx_set_timing": (C.c_int, [vp, C.c_int]),
+            "mlck_ctx_timings": (C.c_int, [vp, C.c_char_p, C.c_uint64, f32p, C.c_uint32, u32p]),
+            "mlck_state_create": (C.c_int, [vp, C.c_uint32, u64p, C.c_int, C.POINTER(vp)]),
+            "mlck_state_destroy": (C.c_int, [vp]),
+            "mlck_state_set_meta": (C.c_int, [vp, C.c_uint64, C.c_uint64]),
+            "mlck_state_get_meta": (C.c_int, [vp, u64p, u64p]),
+            "mlck_state_upload_op": (C.c_int, [vp, C.c_uint32, f32p, f32p, f32p, C.c_uint64, C.c_int]),
+            "mlck_state_download_op": (C.c_int, [vp, C.c_uint32, f32p, f32p, f32p, u64p, f32p,
+                                                 C.POINTER(C.c_int)]),
+            "mlck_state_set_step": (C.c_int, [vp, C.c_uint32, C.c_uint64, C.c_int]),
+            "mlck_state_op_ptrs": (C.c_int, [vp, C.c_uint32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                                             C.POINTER(vp)]),
+            "mlck_state_fill_synthetic": (C.c_int, [vp, C.c_uint64, C.c_uint64]),
+            "mlck_state_serialize": (C.c_int, [vp, u8p, C.c_uint64, u64p]),
+            "mlck_state_serialize_blob": (C.c_int, [vp, vp]),
+            "mlck_blob_create": (C.c_int, [vp, C.c_uint64, C.POINTER(vp)]),
+            "mlck_blob_destroy": (C.c_int, [vp]),
+            "mlck_blob_from_host": (C.c_int, [vp, u8p, C.c_uint64, C.POINTER(vp)]),
+            "mlck_blob_size": (C.c_uint64, [vp]),
+            "mlck_blob_device_ptr": (vp, [vp]),
+            "mlck_blob_to_host": (C.c_int, [vp, u8p, C.c_uint64]),
+            "mlck_blob_add_replica": (C.c_int, [vp, vp, C.c_uint64]),
+            "mlck_blob_clear_replicas": (C.c_int, [vp]),
+            "mlck_snapshot_record": (C.c_int, [vp, u32p, C.c_uint32, u32p, C.c_uint32, C.c_uint32, C.c_uint8,
+                                               C.c_uint64, C.c_uint32, vp]),
+            "mlck_snapshot_record_host": (C.c_int, [vp, u32p, C.c_uint32, u32p, C.c_uint32, C.c_uint32,
+                                                    C.c_uint8, C.c_uint64, C.c_uint32, vp, vp, C.c_uint64,
+                                                    u64p]),
+            "mlck_dense_checkpoint": (C.c_int, [vp, vp]),
+            "mlck_fnv1a64": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, u64p]),
+            "mlck_parse_record": (C.c_int, [vp, C.c_int, C.POINTER(RecordInfo), C.POINTER(EntryInfo),
+                                            C.c_uint32, u32p]),
+            "mlck_read_entry": (C.c_int, [vp, C.POINTER(EntryInfo), C.c_int, f32p, f32p, f32p, f32p]),
+            "mlck_check_coverage": (C.c_int, [C.POINTER(vp), C.c_uint32, C.c_uint64, C.c_int]),
+            "mlck_gradlog_create": (C.c_int, [vp, C.c_uint32, u64p, C.c_uint32, C.POINTER(vp)]),
+            "mlck_gradlog_destroy": (C.c_int, [vp]),
+            "mlck_gradlog_put": (C.c_int, [vp, C.c_uint64, C.c_uint32, f32p]),
+            "mlck_gradlog_slot": (C.c_int, [vp, C.c_uint64, C.c_uint32, C.POINTER(vp)]),
+            "mlck_gradlog_fill_synthetic": (C.c_int, [vp, C.c_uint64, C.c_uint32, C.c_uint64]),
+            "mlck_optimizer_step_adam": (C.c_int, [vp, vp, vp, vp, u64p, vp, C.c_uint64,
+                                                   C.POINTER(Optimizer)]),
+            "mlck_state_apply_updates": (C.c_int, [vp, u32p, C.c_uint32, vp, C.c_uint64,
+                                                   C.POINTER(Optimizer)]),
+            "mlck_sparse_to_dense_convert": (C.c_int, [vp, C.POINTER(vp), C.c_uint32, C.c_uint64, C.c_uint32,
+                                                       C.c_uint64, vp, C.POINTER(Optimizer)]),
+            "mlck_log_create": (C.c_int, [vp, C.c_int, C.c_int, C.c_uint64, C.POINTER(vp)]),
+            "mlck_log_destroy": (C.c_int, [vp]),
+            "mlck_log_put": (C.c_int, [vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint8, vp, C.c_uint64]),
+            "mlck_log_get": (C.c_int, [vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint8, f32p, C.c_uint64,
+                                       u64p]),
+            "mlck_log_get_device": (C.c_int, [vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint8, vp,
+                                              C.c_uint64, u64p]),
+            "mlck_log_count": (C.c_uint64, [vp]),
+            "mlck_log_bytes": (C.c_uint64, [vp]),
+            "mlck_log_entry": (C.c_int, [vp, C.c_uint64, u64p, u32p, u32p, u8p, f32p, C.c_uint64, u64p]),
+            "mlck_gc_logs": (C.c_int, [vp, C.c_uint64]),
+            "mlck_log_sync": (C.c_int, [vp]),
+            "mlck_quantize": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_int]),
+            "mlck_encode_compute": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_int]),
+            "mlck_decode_compute": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_int]),
+            "mlck_ipc_export": (C.c_int, [vp, vp, u8p]),
+            "mlck_ipc_open": (C.c_int, [vp, u8p, C.POINTER(vp)]),
+            "mlck_ipc_close": (C.c_int, [vp, vp]),
+            "mlck_enable_peer_access": (C.c_int, [vp, C.c_int]),
+            "mlck_event_record": (C.c_int, [vp, C.c_int]),
+            "mlck_event_elapsed_ms": (C.c_int, [vp, C.c_int, C.c_int, f32p]),
+            "mlck_device_alloc": (C.c_int, [vp, C.c_uint64, C.POINTER(vp)]),
+            "mlck_device_free": (C.c_int, [vp, vp]),
+            "mlck_device_memset": (C.c_int, [vp, vp, C.c_int, C.c_uint64]),
+            "mlck_host_alloc_pinned": (C.c_int, [vp, C.c_uint64, C.POINTER(vp)]),
+            "mlck_host_free_pinned": (C.c_int, [vp, vp]),
+            "mlck_memcpy_h2d": (C.c_int, [vp, vp, vp, C.c_uint64]),
+            "mlck_memcpy_d2h": (C.c_int, [vp, vp, vp, C.c_uint64]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def check(rc: int):
+    if rc == 0:
+        return
+    msg = lib().mlck_last_error().decode()
+    if rc == 1:
+        raise MlckInvalid(msg)
+    raise MlckRuntime(msg)
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _ptr(a, t):
+    return a.ctypes.data_as(t)
+
+
+def _u32(ids):
+    return np.ascontiguousarray(np.asarray(list(ids), dtype=np.uint32))
+
+
+# --------------------------------------------------------------------------
+class Context:
+    """One device context (stream, staging, scratch)."""
+
+    def __init__(self, device: int = 0):
+        self.h = vp()
+        check(lib().mlck_ctx_create(device, C.byref(self.h)))
+        self.device = device
+
+    def close(self):
+        if self.h:
+            lib().mlck_ctx_destroy(self.h)
+            self.h = vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_handle: int | None):
+        check(lib().mlck_ctx_set_stream(self.h, stream_handle or None))
+
+    def synchronize(self):
+        check(lib().mlck_ctx_synchronize(self.h))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(lib().mlck_ctx_kernel_launches(self.h))
+
+    def set_timing(self, on: bool):
+        check(lib().mlck_ctx_set_timing(self.h, int(on)))
+
+    def timings(self):
+        """[(label, ms)] of the kernels launched since the last call."""
+        labels = C.create_string_buffer(1 << 16)
+        cap = 4096
+        ms = (C.c_float * cap)()
+        n = C.c_uint32()
+        check(lib().mlck_ctx_timings(self.h, labels, 1 << 16, ms, cap, C.byref(n)))
+        names = labels.value.decode().split(",") if n.value else []
+        return [(names[i], float(ms[i])) for i in range(min(n.value, cap))]
+
+    # raw memory helpers
+    def alloc(self, nbytes: int) -> int:
+        p = vp()
+        check(lib().mlck_device_alloc(self.h, nbytes, C.byref(p)))
+        return p.value
+
+    def free(self, ptr: int):
+        check(lib().mlck_device_free(self.h, ptr))
+
+    def memset(self, ptr: int, value: int, nbytes: int):
+        check(lib().mlck_device_memset(self.h, ptr, value, nbytes))
+
+    def alloc_pinned(self, nbytes: int) -> int:
+        p = vp()
+        check(lib().mlck_host_alloc_pinned(self.h, nbytes, C.byref(p)))
+        return p.value
+
+    def free_pinned(self, ptr: int):
+        check(lib().mlck_host_free_pinned(self.h, ptr))
+
+    def h2d(self, dst: int, src: int, nbytes: int):
+        check(lib().mlck_memcpy_h2d(self.h, dst, src, nbytes))
+
+    def d2h(self, dst: int, src: int, nbytes: int):
+        check(lib().mlck_memcpy_d2h(self.h, dst, src, nbytes))
+
+    def upload(self, arr: np.ndarray) -> int:
+        arr = np.ascontiguousarray(arr)
+        p = self.alloc(arr.nbytes)
+        self.h2d(p, arr.ctypes.data, arr.nbytes)
+        self.synchronize()
+        return p
+
+    def download(self, ptr: int, nbytes: int) -> bytes:
+        out = np.empty(nbytes, dtype=np.uint8)
+        self.d2h(out.ctypes.data, ptr, nbytes)
+        self.synchronize()
+        return out.tobytes()
+
+    def event_record(self, slot: int):
+        check(lib().mlck_event_record(self.h, slot))
+
+    def event_ms(self, a: int, b: int) -> float:
+        ms = C.c_float()
+        check(lib().mlck_event_elapsed_ms(self.h, a, b, C.byref(ms)))
+        return ms.value
+
+    def fnv1a64(self, device_ptr: int, n: int, seed: int = 0xcbf29ce484222325) -> int:
+        """fnv1a64 (digest.hpp:18-25) over device bytes."""
+        out = C.c_uint64()
+        check(lib().mlck_fnv1a64(self.h, device_ptr, n, seed, C.byref(out)))
+        return out.value
+
+    def enable_peer_access(self, peer: int):
+        check(lib().mlck_enable_peer_access(self.h, peer))
+
+    def ipc_export(self, ptr: int) -> bytes:
+        h = (C.c_uint8 * 64)()
+        check(lib().mlck_ipc_export(self.h, ptr, h))
+        return bytes(h)
+
+    def ipc_open(self, handle: bytes) -> int:
+        h = (C.c_uint8 * 64).from_buffer_copy(handle)
+        p = vp()
+        check(lib().mlck_ipc_open(self.h, h, C.byref(p)))
+        return p.value
+
+    def ipc_close(self, ptr: int):
+        check(lib().mlck_ipc_close(self.h, ptr))
+
+    # codecs
+    def quantize(self, dev_in: int, dev_out: int, n: int, cb: int):
+        check(lib().mlck_quantize(self.h, dev_in, dev_out, n, cb))
+
+    def encode_compute(self, dev_in: int, dev_codes: int, n: int, cb: int):
+        check(lib().mlck_encode_compute(self.h, dev_in, dev_codes, n, cb))
+
+    def decode_compute(self, dev_codes: int, dev_out: int, n: int, cb: int):
+        check(lib().mlck_decode_compute(self.h, dev_codes, dev_out, n, cb))
+
+
+@dataclass
+class OpHost:
+    master: np.ndarray
+    m: np.ndarray
+    v: np.ndarray
+    step: int
+    compute: np.ndarray
+    has_full_state: bool
+
+
+class DeviceState:
+    """Device-resident TrainState (engine.hpp:47-51)."""
+
+    def __init__(self, ctx: Context, param_counts, compute_bytes: int = 2):
+        self.ctx = ctx
+        self.param_counts = [int(p) for p in param_counts]
+        self.compute_bytes = compute_bytes
+        pc = np.ascontiguousarray(self.param_counts, dtype=np.uint64)
+        self.h = vp()
+        check(lib().mlck_state_create(ctx.h, len(pc), _ptr(pc, u64p), compute_bytes, C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            lib().mlck_state_destroy(self.h)
+            self.h = vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def n_ops(self):
+        return len(self.param_counts)
+
+    def set_meta(self, iteration: int, data_seed: int):
+        check(lib().mlck_state_set_meta(self.h, iteration, data_seed))
+
+    def meta(self):
+        it, seed = C.c_uint64(), C.c_uint64()
+        check(lib().mlck_state_get_meta(self.h, C.byref(it), C.byref(seed)))
+        return it.value, seed.value
+
+    def upload_op(self, i, master, m, v, step, has_full_state=True):
+        master, m, v = _f32(master), _f32(m), _f32(v)
+        assert master.size == self.param_counts[i]
+        check(lib().mlck_state_upload_op(self.h, i, _ptr(master, f32p), _ptr(m, f32p), _ptr(v, f32p), step,
+                                         int(has_full_state)))
+
+    def download_op(self, i) -> OpHost:
+        n = self.param_counts[i]
+        a = [np.empty(n, dtype=np.float32) for _ in range(4)]
+        st, hf = C.c_uint64(), C.c_int()
+        check(lib().mlck_state_download_op(self.h, i, *(_ptr(x, f32p) for x in a[:3]), C.byref(st),
+                                           _ptr(a[3], f32p), C.byref(hf)))
+        return OpHost(a[0], a[1], a[2], st.value, a[3], bool(hf.value))
+
+    def set_step(self, i, step, has_full_state=True):
+        check(lib().mlck_state_set_step(self.h, i, step, int(has_full_state)))
+
+    def op_ptrs(self, i):
+        ps = [vp() for _ in range(4)]
+        check(lib().mlck_state_op_ptrs(self.h, i, *(C.byref(p) for p in ps)))
+        return tuple(p.value for p in ps)
+
+    def fill_synthetic(self, seed: int, step: int = 10):
+        check(lib().mlck_state_fill_synthetic(self.h, seed, step))
+
+    def serialize_state(self) -> bytes:
+        """Engine::serialize_state (engine.hpp:246-261)."""
+        n = C.c_uint64()
+        check(lib().mlck_state_serialize(self.h, None, 0, C.byref(n)))
+        out = np.empty(n.value, dtype=np.uint8)
+        check(lib().mlck_state_serialize(self.h, _ptr(out, u8p), n.value, C.byref(n)))
+        return out.tobytes()
+
+    def serialize_state_blob(self, out: "Blob"):
+        check(lib().mlck_state_serialize_blob(self.h, out.h))
+
+    def apply_updates(self, ids, gradlog: "GradLog", iteration: int, opt: Optimizer | None = None):
+        """Engine::apply_updates (engine.hpp:699-728) for the listed ops."""
+        ids = _u32(ids)
+        opt = opt or Optimizer.adam()
+        check(lib().mlck_state_apply_updates(self.h, _ptr(ids, u32p), ids.size, gradlog.h, iteration,
+                                             C.byref(opt)))
+
+
+class Blob:
+    """A serialized record in device memory (+ replicas)."""
+
+    def __init__(self, ctx: Context, capacity: int = 256, _h=None):
+        self.ctx = ctx
+        self.h = vp()
+        if _h is not None:
+            self.h = _h
+        else:
+            check(lib().mlck_blob_create(ctx.h, capacity, C.byref(self.h)))
+
+    @classmethod
+    def from_host(cls, ctx: Context, data: bytes) -> "Blob":
+        a = np.frombuffer(bytes(data), dtype=np.uint8)
+        h = vp()
+        check(lib().mlck_blob_from_host(ctx.h, _ptr(a, u8p) if a.size else None, a.size, C.byref(h)))
+        return cls(ctx, _h=h)
+
+    def close(self):
+        if self.h:
+            lib().mlck_blob_destroy(self.h)
+            self.h = vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def size(self) -> int:
+        return int(lib().mlck_blob_size(self.h))
+
+    @property
+    def device_ptr(self) -> int:
+        return int(lib().mlck_blob_device_ptr(self.h) or 0)
+
+    def to_host(self) -> bytes:
+        out = np.empty(self.size, dtype=np.uint8)
+        check(lib().mlck_blob_to_host(self.h, _ptr(out, u8p), out.size))
+        return out.tobytes()
+
+    def add_replica(self, device_ptr: int, capacity: int):
+        check(lib().mlck_blob_add_replica(self.h, device_ptr, capacity))
+
+    def clear_replicas(self):
+        check(lib().mlck_blob_clear_replicas(self.h))
+
+
+def snapshot_record(state: DeviceState, active, compute_only, slot_index: int, kind: int = 1,
+                    window_start: int = 0, wsparse: int = 1, out: Blob | None = None) -> Blob:
+    """serialize_record(take_sparse_snapshot(engine, slot, slot_index), plan,
+    kind, window_start, wsparse) (snapshot.hpp:204-241, 115-144)."""
+    a, c = _u32(active), _u32(compute_only)
+    out = out or Blob(state.ctx)
+    check(lib().mlck_snapshot_record(state.h, _ptr(a, u32p), a.size, _ptr(c, u32p), c.size, slot_index, kind,
+                                     window_start, wsparse, out.h))
+    return out
+
+
+def snapshot_record_host(state: DeviceState, active, compute_only, slot_index: int, kind=1, window_start=0,
+                         wsparse=1, scratch: Blob | None = None, host_buf: int | None = None,
+                         cap: int = 0) -> int | bytes:
+    """Same record delivered to host memory (pinned host_buf when given)."""
+    a, c = _u32(active), _u32(compute_only)
+    scratch = scratch or Blob(state.ctx)
+    n = C.c_uint64()
+    args = (state.h, _ptr(a, u32p), a.size, _ptr(c, u32p), c.size, slot_index, kind, window_start, wsparse,
+            scratch.h)
+    if host_buf is not None:
+        check(lib().mlck_snapshot_record_host(*args, host_buf, cap, C.byref(n)))
+        return n.value
+    check(lib().mlck_snapshot_record_host(*args, None, 0, C.byref(n)))
+    out = np.empty(n.value, dtype=np.uint8)
+    check(lib().mlck_snapshot_record_host(*args, out.ctypes.data, out.size, C.byref(n)))
+    return out.tobytes()
+
+
+def dense_checkpoint(state: DeviceState, out: Blob | None = None) -> Blob:
+    """take_dense_checkpoint(engine).serialize(plan) (snapshot.hpp:245-295)."""
+    out = out or Blob(state.ctx)
+    check(lib().mlck_dense_checkpoint(state.h, out.h))
+    return out
+
+
+def parse_record(blob: Blob, compute_bytes: int):
+    """parse_record (snapshot.hpp:153-197): (header dict, entry dicts)."""
+    info = RecordInfo()
+    cap = 1 << 16
+    ents = (EntryInfo * cap)()
+    n = C.c_uint32()
+    check(lib().mlck_parse_record(blob.h, compute_bytes, C.byref(info), ents, cap, C.byref(n)))
+    header = dict(kind=info.kind, iteration=info.iteration, window_start=info.window_start,
+                  wsparse=info.wsparse, slot=info.slot, data_seed=info.data_seed)
+    entries = [dict(id=ents[i].id, mode=ents[i].mode, param_count=ents[i].param_count, step=ents[i].step,
+                    payload_offset=ents[i].payload_offset) for i in range(n.value)]
+    return header, entries
+
+
+def read_entry(blob: Blob, entry: dict, compute_bytes: int) -> dict:
+    e = EntryInfo(entry["id"], entry["mode"], entry["param_count"], entry["step"], entry["payload_offset"])
+    P = entry["param_count"]
+    if entry["mode"] == 0:
+        a = [np.empty(P, dtype=np.float32) for _ in range(3)]
+        check(lib().mlck_read_entry(blob.h, C.byref(e), compute_bytes, *(_ptr(x, f32p) for x in a), None))
+        return dict(master=a[0], m=a[1], v=a[2], step=entry["step"])
+    c = np.empty(P, dtype=np.float32)
+    check(lib().mlck_read_entry(blob.h, C.byref(e), compute_bytes, None, None, None, _ptr(c, f32p)))
+    return dict(compute=c)
+
+
+def check_coverage(blobs, op_count: int, compute_bytes: int):
+    """SparseCheckpoint::check_coverage (snapshot.hpp:322-334)."""
+    arr = (vp * max(1, len(blobs)))(*[b.h for b in blobs])
+    check(lib().mlck_check_coverage(arr, len(blobs), op_count, compute_bytes))
+
+
+class GradLog:
+    """Per-iteration operator gradients on the device (Adam-replay input)."""
+
+    def __init__(self, ctx: Context, param_counts, capacity_iterations: int):
+        self.ctx = ctx
+        self.param_counts = [int(p) for p in param_counts]
+        pc = np.ascontiguousarray(self.param_counts, dtype=np.uint64)
+        self.h = vp()
+        check(lib().mlck_gradlog_create(ctx.h, len(pc), _ptr(pc, u64p), capacity_iterations, C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            lib().mlck_gradlog_destroy(self.h)
+            self.h = vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def put(self, iteration: int, op: int, grad):
+        g = _f32(grad)
+        check(lib().mlck_gradlog_put(self.h, iteration, op, _ptr(g, f32p)))
+
+    def slot(self, iteration: int, op: int) -> int:
+        p = vp()
+        check(lib().mlck_gradlog_slot(self.h, iteration, op, C.byref(p)))
+        return p.value
+
+    def fill_synthetic(self, first_iteration: int, n_iterations: int, seed: int):
+        check(lib().mlck_gradlog_fill_synthetic(self.h, first_iteration, n_iterations, seed))
+
+
+def sparse_to_dense_convert(out: DeviceState, blobs, window_start: int, wsparse: int, data_seed: int,
+                            gradlog: GradLog | None, opt: Optimizer | None = None):
+    """sparse_to_dense_convert (recovery.hpp:180-227) with logged-gradient replay."""
+    arr = (vp * max(1, len(blobs)))(*[b.h for b in blobs])
+    opt = opt or Optimizer.adam()
+    check(lib().mlck_sparse_to_dense_convert(out.h, arr, len(blobs), window_start, wsparse, data_seed,
+                                             gradlog.h if gradlog else None, C.byref(opt)))
+
+
+def optimizer_step_adam(ctx: Context, master: int, m: int, v: int, step: int, grad: int, n: int,
+                        opt: Optimizer | None = None) -> int:
+    """optimizer_step_adam (engine.hpp:738-753) on device pointers; returns step."""
+    st = C.c_uint64(step)
+    opt = opt or Optimizer.adam()
+    check(lib().mlck_optimizer_step_adam(ctx.h, master, m, v, C.byref(st), grad, n, C.byref(opt)))
+    return st.value
+
+
+class UpstreamLog:
+    """Boundary log (LogKey/UpstreamLog, engine.hpp:55-94) on a side stream.
+    kind 0 = pinned host ring, 1 = device ring on `device`."""
+
+    def __init__(self, ctx: Context, capacity_bytes: int, kind: int = 0, device: int = 0):
+        self.ctx = ctx
+        self.h = vp()
+        check(lib().mlck_log_create(ctx.h, kind, device, capacity_bytes, C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            lib().mlck_log_destroy(self.h)
+            self.h = vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def put(self, iteration, micro_batch, boundary, direction, device_src: int, n_floats: int):
+        check(lib().mlck_log_put(self.h, iteration, micro_batch, boundary, direction, device_src, n_floats))
+
+    def at(self, iteration, micro_batch, boundary, direction) -> np.ndarray:
+        n = C.c_uint64()
+        check(lib().mlck_log_get(self.h, iteration, micro_batch, boundary, direction, None, 0, C.byref(n)))
+        out = np.empty(n.value, dtype=np.float32)
+        check(lib().mlck_log_get(self.h, iteration, micro_batch, boundary, direction, _ptr(out, f32p), out.size,
+                                 C.byref(n)))
+        return out
+
+    def get_device(self, iteration, micro_batch, boundary, direction, dst: int, cap: int) -> int:
+        n = C.c_uint64()
+        check(lib().mlck_log_get_device(self.h, iteration, micro_batch, boundary, direction, dst, cap,
+                                        C.byref(n)))
+        return n.value
+
+    def __len__(self):
+        return int(lib().mlck_log_count(self.h))
+
+    def bytes(self) -> int:
+        return int(lib().mlck_log_bytes(self.h))
+
+    def entries(self):
+        out = []
+        for i in range(len(self)):
+            it, mb, b, d, n = C.c_uint64(), C.c_uint32(), C.c_uint32(), C.c_uint8(), C.c_uint64()
+            check(lib().mlck_log_entry(self.h, i, C.byref(it), C.byref(mb), C.byref(b), C.byref(d), None, 0,
+                                       C.byref(n)))
+            data = np.empty(n.value, dtype=np.float32)
+            check(lib().mlck_log_entry(self.h, i, C.byref(it), C.byref(mb), C.byref(b), C.byref(d),
+                                       _ptr(data, f32p), data.size, C.byref(n)))
+            out.append(((it.value, mb.value, b.value, d.value), data))
+        return out
+
+    def gc(self, persisted_window_start: int):
+        """gc_logs (engine.hpp:90-94)."""
+        check(lib().mlck_gc_logs(self.h, persisted_window_start))
+
+    def sync(self):
+        check(lib().mlck_log_sync(self.h))

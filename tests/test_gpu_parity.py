@@ -1,0 +1,358 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden vectors and the CPU oracle.  Bit-exact everywhere (Adam tolerance: 0
+ulp, asserted on raw bits)."""
+import numpy as np
+import pytest
+
+from golden_cases import CASE_NAMES, load_case, load_npz
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mk():
+    from paper_2412_15411_b200 import mlck
+    return mlck
+
+
+@pytest.fixture(scope="module")
+def ctx(mk):
+    c = mk.Context(0)
+    yield c
+    c.close()
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+
+
+def upload_state(mk, ctx, c, s):
+    st = mk.DeviceState(ctx, c.meta["param_counts"], c.compute_bytes)
+    for i in range(c.n_ops):
+        o = c.op(s, i)
+        st.upload_op(i, o["master"], o["m"], o["v"], o["step"])
+    st.set_meta(s, c.data_seed)
+    return st
+
+
+# ---------------------------------------------------------------- FNV (K2)
+def test_fnv_goldens(mk, ctx):
+    g = load_npz("fnv")
+    i = 0
+    while f"data{i}" in g:
+        data = g[f"data{i}"]
+        ptr = ctx.upload(data) if data.size else ctx.alloc(16)
+        assert ctx.fnv1a64(ptr, data.size) == int(g[f"hash{i}"][0]), data.size
+        ctx.free(ptr)
+        i += 1
+
+
+@pytest.mark.parametrize("n", [16383, 16384, 16385, 1 << 20, 5 * (1 << 20) + 77, 64 * (1 << 20) + 13])
+def test_fnv_large_vs_oracle(mk, ctx, oracle, n):
+    rng = np.random.default_rng(n)
+    data = rng.integers(0, 256, n, dtype=np.uint8)
+    # long runs of equal bytes exercise the carry chain differently
+    data[n // 3: n // 3 + 5000] = 0xff
+    data[n // 2: n // 2 + 5000] = 0
+    ptr = ctx.upload(data)
+    try:
+        assert ctx.fnv1a64(ptr, n) == oracle.fnv1a64(data)
+        # unaligned start (parse of a sub-range)
+        assert ctx.fnv1a64(ptr + 3, n - 3) == oracle.fnv1a64(data[3:])
+        assert ctx.fnv1a64(ptr, n, seed=12345) == oracle.fnv1a64(data, seed=12345)
+    finally:
+        ctx.free(ptr)
+
+
+# ---------------------------------------------------------------- codecs
+def test_codec_goldens(mk, ctx):
+    g = load_npz("codec")
+    x = np.ascontiguousarray(g["x"], dtype=np.float32)
+    dx = ctx.upload(x)
+    out = ctx.alloc(x.nbytes)
+    try:
+        for cb in (1, 2, 4):
+            ctx.quantize(dx, out, x.size, cb)
+            q = np.frombuffer(ctx.download(out, x.nbytes), dtype=np.float32)
+            assert np.array_equal(bits(q), bits(g[f"q{cb}"])), cb
+        dq = ctx.upload(np.ascontiguousarray(g["q2"]))
+        ctx.encode_compute(dq, out, x.size, 2)
+        codes = np.frombuffer(ctx.download(out, 2 * x.size), dtype=np.uint16)
+        assert np.array_equal(codes, g["pack16"])
+        dq1 = ctx.upload(np.ascontiguousarray(g["q1"]))
+        ctx.encode_compute(dq1, out, x.size, 1)
+        codes = np.frombuffer(ctx.download(out, x.size), dtype=np.uint8)
+        assert np.array_equal(codes.astype(np.uint16), g["pack8"])
+        allc = ctx.upload(np.arange(65536, dtype=np.uint16))
+        dec = ctx.alloc(65536 * 4)
+        ctx.decode_compute(allc, dec, 65536, 2)
+        assert np.array_equal(bits(np.frombuffer(ctx.download(dec, 65536 * 4), np.float32)),
+                              bits(g["unpack16"]))
+        c8 = ctx.upload(np.arange(256, dtype=np.uint8))
+        ctx.decode_compute(c8, dec, 256, 1)
+        assert np.array_equal(bits(np.frombuffer(ctx.download(dec, 256 * 4), np.float32)), bits(g["unpack8"]))
+        for p in (dq, dq1, allc, dec, c8):
+            ctx.free(p)
+    finally:
+        ctx.free(dx)
+        ctx.free(out)
+    with pytest.raises(ValueError, match="unsupported width"):
+        ctx.quantize(0, 0, 1, 3)
+
+
+# ---------------------------------------------------------------- Adam
+def test_adam_goldens(mk, ctx):
+    g = load_npz("adam")
+    w, m, v = (ctx.upload(g[k]) for k in ("w0", "m0", "v0"))
+    step = int(g["step0"][0])
+    n = g["w0"].size
+    for s in range(5):
+        gp = ctx.upload(g[f"g{s}"])
+        step = mk.optimizer_step_adam(ctx, w, m, v, step, gp, n)
+        ctx.synchronize()
+        ctx.free(gp)
+        for ptr, key in ((w, "w"), (m, "m"), (v, "v")):
+            got = np.frombuffer(ctx.download(ptr, 4 * n), dtype=np.float32)
+            assert np.array_equal(bits(got), bits(g[f"{key}{s + 1}"])), (s, key)
+    assert step == 8
+    for p in (w, m, v):
+        ctx.free(p)
+
+
+# ---------------------------------------------------------------- K1 snapshot
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_snapshot_matches_reference_bytes(mk, ctx, name):
+    c = load_case(name)
+    for s in range(c.T + 1):
+        st = upload_state(mk, ctx, c, s)
+        active, co = c.slot(s % c.W)
+        blob = mk.snapshot_record(st, active, co, s % c.W, 1, s // c.W * c.W, c.W)
+        assert blob.to_host() == c.blob(s), (name, s)
+        # the same record through the host-buffer entry point (e2e path)
+        assert mk.snapshot_record_host(st, active, co, s % c.W, 1, s // c.W * c.W, c.W) == c.blob(s)
+        assert st.serialize_state() == c.mlst(s)
+
+
+@pytest.mark.parametrize("name", ["verify_toy", "six_op_cb1", "six_op_cb4"])
+def test_dense_checkpoint_matches_reference(mk, ctx, name):
+    c = load_case(name)
+    for s in (0, c.T):
+        st = upload_state(mk, ctx, c, s)
+        assert mk.dense_checkpoint(st).to_host() == c.d[f"dense_s{s}"].tobytes()
+
+
+def test_snapshot_replicas_identical(mk, ctx):
+    c = load_case("verify_toy")
+    st = upload_state(mk, ctx, c, 4)
+    out = mk.Blob(ctx, 1 << 16)
+    r1, r2 = ctx.alloc(1 << 16), ctx.alloc(1 << 16)
+    out.add_replica(r1, 1 << 16)
+    out.add_replica(r2, 1 << 16)
+    active, co = c.slot(1)
+    mk.snapshot_record(st, active, co, 1, 1, 3, 3, out)
+    ref = c.blob(4)
+    assert out.to_host() == ref
+    assert ctx.download(r1, len(ref)) == ref
+    assert ctx.download(r2, len(ref)) == ref
+    with pytest.raises(ValueError, match="replica capacity"):
+        small = mk.Blob(ctx, 1 << 16)
+        small.add_replica(r1, 64)
+        mk.snapshot_record(st, active, co, 1, 1, 3, 3, small)
+    ctx.free(r1)
+    ctx.free(r2)
+
+
+def test_snapshot_errors(mk, ctx):
+    c = load_case("six_op_cb4")
+    st = upload_state(mk, ctx, c, 1)
+    with pytest.raises(ValueError, match="unknown operator 42"):  # test_snapshot.cpp:198-204
+        mk.snapshot_record(st, [42], [], 0)
+    st.set_step(3, 0, has_full_state=False)
+    with pytest.raises(RuntimeError, match="has no full state"):
+        mk.snapshot_record(st, [3], [], 0)
+    with pytest.raises(RuntimeError, match="is frozen"):  # test_snapshot.cpp:154-160
+        mk.dense_checkpoint(st)
+
+
+def test_snapshot_large_synthetic_vs_oracle(mk, ctx, oracle):
+    """Odd sizes and every compute width at MB scale against the oracle."""
+    rng = np.random.default_rng(2)
+    for cb in (1, 2, 4):
+        pcs = [int(x) for x in rng.integers(100_000, 700_000, 7)] + [1, 3, 5]
+        st = mk.DeviceState(ctx, pcs, cb)
+        st.fill_synthetic(seed=99 + cb, step=17)
+        st.set_meta(123, 7)
+        active, co = [0, 3, 8], [1, 2, 4, 5, 6, 7, 9]
+        blob = mk.snapshot_record(st, active, co, 2, 1, 120, 6)
+        ents = []
+        for i in sorted(active + co):
+            P = pcs[i]
+            master = oracle.synth(99 + cb, 3 * i, -0.25, 0.25, P)
+            if i in active:
+                ents.append(dict(id=i, mode=0, param_count=P, step=17, master=master,
+                                 m=oracle.synth(99 + cb, 3 * i + 1, -1e-3, 1e-3, P),
+                                 v=oracle.synth(99 + cb, 3 * i + 2, 0.0, 1e-6, P)))
+            else:
+                ents.append(dict(id=i, mode=1, param_count=P, compute=oracle.quantize(master, cb)))
+        ref = oracle.serialize_record(dict(kind=1, iteration=123, window_start=120, wsparse=6, slot=2,
+                                           data_seed=7), ents, cb)
+        got = blob.to_host()
+        assert len(got) == len(ref)
+        assert got == ref, cb
+
+
+# ---------------------------------------------------------------- parse
+@pytest.mark.parametrize("name", ["verify_toy", "six_op_cb1", "six_op_cb4"])
+def test_parse_record_matches_oracle(mk, ctx, oracle, name):
+    c = load_case(name)
+    for s in range(c.T + 1):
+        b = mk.Blob.from_host(ctx, c.blob(s))
+        h, ents = mk.parse_record(b, c.compute_bytes)
+        oh, oents = oracle.parse_record(c.blob(s), c.compute_bytes)
+        assert h == oh and ents == oents
+        for e in ents[:3]:
+            got = mk.read_entry(b, e, c.compute_bytes)
+            o = c.op(s, e["id"])
+            if e["mode"] == 0:
+                assert np.array_equal(bits(got["master"]), bits(o["master"]))
+            else:
+                assert np.array_equal(bits(got["compute"]), bits(o["compute"]))
+
+
+def test_parse_errors(mk, ctx, oracle):
+    c = load_case("six_op_cb4")
+    blob = bytearray(c.blob(1))
+    blob[len(blob) // 2] ^= 0x40
+    with pytest.raises(RuntimeError, match="container checksum mismatch"):
+        mk.parse_record(mk.Blob.from_host(ctx, bytes(blob)), 4)
+    with pytest.raises(RuntimeError, match="container truncated"):
+        mk.parse_record(mk.Blob.from_host(ctx, b"\x01\x02\x03"), 4)
+    body = b"XXXX" + c.blob(1)[4:-8]
+    bad = body + oracle.fnv1a64(body).to_bytes(8, "little")
+    with pytest.raises(RuntimeError, match="bad magic"):
+        mk.parse_record(mk.Blob.from_host(ctx, bad), 4)
+    body = c.blob(1)[:4] + (7).to_bytes(4, "little") + c.blob(1)[8:-8]
+    bad = body + oracle.fnv1a64(body).to_bytes(8, "little")
+    with pytest.raises(RuntimeError, match="unsupported version 7"):
+        mk.parse_record(mk.Blob.from_host(ctx, bad), 4)
+    body = c.blob(1)[:-100]
+    bad = body + oracle.fnv1a64(body).to_bytes(8, "little")
+    with pytest.raises(RuntimeError, match="container truncated"):
+        mk.parse_record(mk.Blob.from_host(ctx, bad), 4)
+
+
+def test_check_coverage(mk, ctx):
+    c = load_case("six_op_cb4")  # test_snapshot.cpp:170-196
+    blobs = [mk.Blob.from_host(ctx, c.blob(k)) for k in range(3)]
+    mk.check_coverage(blobs, c.n_ops, 4)
+    bad = [blobs[0], blobs[1], blobs[1]]
+    with pytest.raises(RuntimeError, match="window coverage violated for operator 2: 2 full payloads"):
+        mk.check_coverage(bad, c.n_ops, 4)
+
+
+# ---------------------------------------------------------------- K3 conversion
+def gradlog_for(mk, ctx, c, w):
+    g = mk.GradLog(ctx, c.meta["param_counts"], max(c.W, 1))
+    for it in range(w + 1, w + c.W + 1):
+        for i in range(c.n_ops):
+            g.put(it, i, c.grads(it, i))
+    return g
+
+
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_conversion_matches_reference(mk, ctx, name):
+    c = load_case(name)
+    opt = c.optimizer
+    o = mk.Optimizer(opt["kind"], opt["lr"], opt["beta1"], opt["beta2"], opt["eps"])
+    for w in c.meta["converted_windows"]:
+        blobs = [mk.Blob.from_host(ctx, b) for b in c.window_blobs(w)]
+        g = gradlog_for(mk, ctx, c, w) if c.W > 1 else None
+        out = mk.DeviceState(ctx, c.meta["param_counts"], c.compute_bytes)
+        mk.sparse_to_dense_convert(out, blobs, w, c.W, c.data_seed, g, o)
+        assert out.serialize_state() == c.converted(w), (name, w)
+        # compute weights are refreshed from the converted masters
+        it = w + c.W if c.W > 1 else w
+        for i in range(c.n_ops):
+            assert np.array_equal(bits(out.download_op(i).compute), bits(c.op(it, i)["compute"]))
+
+
+def test_conversion_from_device_snapshots(mk, ctx):
+    """Snapshot on the GPU, convert on the GPU: end-to-end window."""
+    c = load_case("verify_toy")
+    w = 3
+    blobs = []
+    for k in range(c.W):
+        st = upload_state(mk, ctx, c, w + k)
+        a, co = c.slot(k)
+        blobs.append(mk.snapshot_record(st, a, co, k, 1, w, c.W))
+    g = gradlog_for(mk, ctx, c, w)
+    out = mk.DeviceState(ctx, c.meta["param_counts"], c.compute_bytes)
+    mk.sparse_to_dense_convert(out, blobs, w, c.W, c.data_seed, g)
+    assert out.serialize_state() == c.mlst(w + c.W)
+
+
+def test_conversion_errors(mk, ctx):
+    c = load_case("six_op_cb4")
+    blobs = [mk.Blob.from_host(ctx, b) for b in c.window_blobs(0)]
+    g = gradlog_for(mk, ctx, c, 0)
+    out = mk.DeviceState(ctx, c.meta["param_counts"], 4)
+    with pytest.raises(RuntimeError, match="sparse checkpoint incomplete: 2 of 3 records"):
+        mk.sparse_to_dense_convert(out, blobs[:2], 0, 3, c.data_seed, g)
+    raw = bytearray(c.blob(1))
+    raw[len(raw) // 3] ^= 0x10  # test_recovery.cpp:129-139
+    bad = [blobs[0], mk.Blob.from_host(ctx, bytes(raw)), blobs[2]]
+    with pytest.raises(RuntimeError, match=r"slot 1.*checksum"):
+        mk.sparse_to_dense_convert(out, bad, 0, 3, c.data_seed, g)
+    with pytest.raises(RuntimeError, match="conversion finished with frozen operator 4"):
+        mk.sparse_to_dense_convert(out, [blobs[0], blobs[1], blobs[1]], 0, 3, c.data_seed, g)
+
+
+# ---------------------------------------------------------------- training step
+@pytest.mark.parametrize("name", ["verify_toy", "toy_sgd", "six_op_cb1"])
+def test_apply_updates_matches_engine(mk, ctx, name):
+    """Engine::apply_updates on device == the reference's next state."""
+    c = load_case(name)
+    opt = c.optimizer
+    o = mk.Optimizer(opt["kind"], opt["lr"], opt["beta1"], opt["beta2"], opt["eps"])
+    g = mk.GradLog(ctx, c.meta["param_counts"], 2)
+    for s in range(c.T):
+        st = upload_state(mk, ctx, c, s)
+        for i in range(c.n_ops):
+            g.put(s + 1, i, c.grads(s + 1, i))
+        st.apply_updates(range(c.n_ops), g, s + 1, o)
+        st.set_meta(s + 1, c.data_seed)
+        assert st.serialize_state() == c.mlst(s + 1), (name, s)
+
+
+# ---------------------------------------------------------------- K4 logging
+@pytest.mark.parametrize("name", ["verify_toy", "dp2_pp2"])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_upstream_log_matches_reference(mk, ctx, name, kind):
+    c = load_case(name)
+    ref = c.log_entries()
+    log = mk.UpstreamLog(ctx, 1 << 22, kind=kind, device=0)
+    # producers write in execution order; the reference map orders by key
+    order = np.random.default_rng(1).permutation(len(ref))
+    bufs = []
+    for j in order:
+        key, data = ref[j]
+        p = ctx.upload(data)
+        bufs.append(p)
+        log.put(*key, p, data.size)
+    log.sync()
+    got = log.entries()
+    assert [k for k, _ in got] == [k for k, _ in ref]
+    for (_, a), (_, b) in zip(got, ref):
+        assert np.array_equal(bits(a), bits(b))
+    assert log.bytes() == sum(d.size * 4 for _, d in ref)
+    k0 = ref[-1][0]
+    assert np.array_equal(bits(log.at(*k0)), bits(ref[-1][1]))
+    # gc_logs keeps iteration >= window start (engine.hpp:90-94)
+    log.gc(3)
+    assert all(k[0] >= 3 for k, _ in log.entries())
+    log.gc(100)
+    assert len(log) == 0
+    with pytest.raises(RuntimeError, match="upstream log missing entry: iteration 1 micro-batch 0 boundary 0 fwd"):
+        log.at(1, 0, 0, 0)
+    for p in bufs:
+        ctx.free(p)
