@@ -352,6 +352,7 @@ class Reference:
         L.mlr_fnv1a64.restype = C.c_uint64
         L.mlr_fnv1a64.argtypes = [u8p, C.c_size_t, C.c_uint64]
         L.mlr_quantize_value.argtypes = [C.c_float, C.c_int, f32p, C.c_char_p, C.c_size_t]
+        L.mlr_quantize_array.argtypes = [f32p, C.c_size_t, C.c_int, f32p, C.c_char_p, C.c_size_t]
         L.mlr_pack_reduced.restype = C.c_uint16
         L.mlr_pack_reduced.argtypes = [C.c_float, C.c_int, C.c_int]
         L.mlr_unpack_reduced.restype = C.c_float

@@ -333,6 +333,14 @@ uint64_t mlr_fnv1a64(const uint8_t* data, size_t n, uint64_t seed) {
 int mlr_quantize_value(float x, int compute_bytes, float* out, char* err, size_t ecap) {
   return guarded(err, ecap, [&] { *out = quantize_value(x, compute_bytes); });
 }
+// Array form (no float->double round trip through the caller: keeps
+// signalling-NaN payloads exactly as quantize_value returns them).
+int mlr_quantize_array(const float* in, size_t n, int compute_bytes, float* out, char* err,
+                       size_t ecap) {
+  return guarded(err, ecap, [&] {
+    for (size_t i = 0; i < n; ++i) out[i] = quantize_value(in[i], compute_bytes);
+  });
+}
 uint16_t mlr_pack_reduced(float x, int ebits, int mbits) { return pack_reduced(x, ebits, mbits); }
 float mlr_unpack_reduced(uint16_t c, int ebits, int mbits) { return unpack_reduced(c, ebits, mbits); }
 

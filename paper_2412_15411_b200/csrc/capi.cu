@@ -834,6 +834,39 @@ int mlck_fnv1a64(mlck_ctx* ctx, const void* ptr, uint64_t n, uint64_t seed, uint
   });
 }
 
+// FNV with the kernel's profile counters (development aid): counters =
+// [look-back probes, spin re-reads, cycles before look-backs, cycles in
+// look-backs, cycles in phase B, chunks], cycles summed over chunks (thread 0).
+int mlck_fnv1a64_profile(mlck_ctx* ctx, const void* ptr, uint64_t n, uint64_t seed, uint64_t* out,
+                         uint64_t* counters, uint64_t* trace_host) {
+  return api([&] {
+    ctx->activate();
+    unsigned long long* prof = nullptr;
+    MLCK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&prof), 8 * 8, ctx->stream));
+    MLCK_CUDA(cudaMemsetAsync(prof, 0, 8 * 8, ctx->stream));
+    TrailerDsts none{};
+    unsigned long long* trace = nullptr;
+    const uint64_t tb = fnv_chunks(n) * 12 * 8;
+    if (trace_host) {
+      MLCK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&trace), tb, ctx->stream));
+      MLCK_CUDA(cudaMemsetAsync(trace, 0, tb, ctx->stream));
+    }
+    launch_fnv(static_cast<const uint8_t*>(ptr), n, seed, ctx->fnv_scratch_for(n), ctx->results,
+               none, ctx->stream, prof, trace);
+    ctx->launches += 1;
+    if (trace_host) {
+      MLCK_CUDA(cudaMemcpyAsync(trace_host, trace, tb, cudaMemcpyDeviceToHost, ctx->stream));
+      MLCK_CUDA(cudaFreeAsync(trace, ctx->stream));
+    }
+    MLCK_CUDA(cudaMemcpyAsync(ctx->host_results, ctx->results, 8, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    MLCK_CUDA(cudaMemcpyAsync(counters, prof, 6 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    MLCK_CUDA(cudaFreeAsync(prof, ctx->stream));
+    MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = ctx->host_results[0];
+  });
+}
+
 // ------------------------------------------------------------------ parse
 int mlck_parse_record(mlck_blob* b, int cb, mlck_record_info* info, mlck_entry_info* entries,
                       uint32_t cap, uint32_t* n_entries) {

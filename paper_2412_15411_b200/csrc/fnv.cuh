@@ -38,7 +38,26 @@ struct Scratch {
   unsigned long long* accum;   // sum of chunk terms
   uint32_t* finished;          // completed-chunk counter
   unsigned long long* result;  // final 64-bit hash
+  // optional profile counters (null = off): [0] look-back probes,
+  // [1] spin re-reads, [2] cycles before look-backs, [3] cycles in
+  // look-backs, [4] cycles in phase B, [5] chunks
+  unsigned long long* prof;
+  // optional per-chunk trace (null = off): 12 words per chunk, %globaltimer
+  // ns at [0] start, [1+2r] map published, [2+2r] round resolved, [9] end,
+  // [10] smid
+  unsigned long long* trace;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
 
 // P^(64 k) for k = 0..kThreads-1, written by init_constants() (kernels.cu).
 __constant__ unsigned long long c_pow64[kThreads];
@@ -156,123 +175,317 @@ __device__ __forceinline__ void level_carry(int j, const uint32_t y[8], Carries&
   }
 }
 
-// Look-back over predecessor chunks for bit level j.  Executed by one full
-// warp; returns the start bit (state bit j before the chunk's first byte).
-__device__ __forceinline__ uint32_t look_back(const uint32_t* status, int64_t chunk, int j,
-                                              uint32_t seed_bit) {
+// Two bit levels (2r, 2r+1) are resolved per look-back round.  A chunk's
+// effect on those two state bits, given its true lower start bits, is the map
+//   s0' = s0 ^ a,   s1' = s1 ^ (s0 ? b1 : b0)
+// packed as bits {a, b0, b1}; the family is closed under composition.
+__device__ __forceinline__ uint32_t map_compose(uint32_t g, uint32_t f) {  // g o f
+  const uint32_t af = f & 1u, b0f = (f >> 1) & 1u, b1f = (f >> 2) & 1u;
+  const uint32_t ag = g & 1u, b0g = (g >> 1) & 1u, b1g = (g >> 2) & 1u;
+  const uint32_t b0 = b0f ^ (af ? b1g : b0g);
+  const uint32_t b1 = b1f ^ (af ? b0g : b1g);
+  return (af ^ ag) | (b0 << 1) | (b1 << 2);
+}
+__device__ __forceinline__ uint32_t map_apply(uint32_t m, uint32_t s) {
+  const uint32_t s0 = s & 1u, s1 = (s >> 1) & 1u;
+  return (s0 ^ (m & 1u)) | ((s1 ^ ((m >> (1 + s0)) & 1u)) << 1);
+}
+
+// Status word of a chunk: bits [3r,3r+3) the round-r map, [12+2r,14+2r) the
+// round-r inclusive end bits, [20,23) rounds with map published, [24,27)
+// rounds with inclusive published.
+constexpr int kRounds = 4;
+__device__ __forceinline__ uint32_t st_nagg(uint32_t s) { return (s >> 20) & 7u; }
+__device__ __forceinline__ uint32_t st_nincl(uint32_t s) { return (s >> 24) & 7u; }
+
+// Warp-level look-back for round r: composes predecessor maps back to the
+// nearest chunk whose inclusive state for round r is known; returns the two
+// start bits of this chunk.  `seed2` = the 2 seed bits (virtual chunk -1).
+__device__ __forceinline__ uint32_t look_back2(const uint32_t* status, int64_t chunk, int r,
+                                               uint32_t seed2) {
   const int lane = threadIdx.x & 31;
-  uint32_t acc = 0;
+  uint32_t acc = 0;  // identity map
   int64_t base = chunk - 1;
   while (true) {
     const int64_t k = base - lane;
     bool incl;
-    uint32_t bit;
+    uint32_t val;
     if (k < 0) {
       incl = true;
-      bit = seed_bit;
+      val = seed2;
     } else {
       uint32_t s;
       do {
         s = ld_relaxed_gpu(status + k);
-      } while (((s >> 16) & 0xf) <= static_cast<uint32_t>(j));
-      incl = ((s >> 20) & 0xf) > static_cast<uint32_t>(j);
-      bit = incl ? (s >> (8 + j)) & 1u : (s >> j) & 1u;
+      } while (st_nagg(s) <= static_cast<uint32_t>(r));
+      incl = st_nincl(s) > static_cast<uint32_t>(r);
+      val = incl ? (s >> (12 + 2 * r)) & 3u : (s >> (3 * r)) & 7u;
     }
     const uint32_t incl_mask = __ballot_sync(0xffffffffu, incl);
-    if (incl_mask) {
-      const int first = __ffs(incl_mask) - 1;
-      const uint32_t bits = __ballot_sync(0xffffffffu, bit && lane <= first);
-      return acc ^ (__popc(bits) & 1u);
+    const int first = incl_mask ? __ffs(incl_mask) - 1 : 32;
+    // m_0 o m_1 o ... o m_{first-1}: lane 0 is the nearest predecessor
+    uint32_t m = lane < first ? val : 0u;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t o = __shfl_down_sync(0xffffffffu, m, off);
+      if (lane + off < 32) m = map_compose(m, o);
     }
-    acc ^= __popc(__ballot_sync(0xffffffffu, bit)) & 1u;
+    m = __shfl_sync(0xffffffffu, m, 0);
+    acc = map_compose(acc, m);
+    if (incl_mask) {
+      const uint32_t inc = __shfl_sync(0xffffffffu, val, first);
+      return map_apply(acc, inc);
+    }
     base -= 32;
   }
 }
 
-// Block-level FNV contribution of one kChunk-byte chunk.  Every thread
-// passes its 64 bytes (16 little-endian words, positions thread*64 ..),
-// already zero-padded past `n`.  The chunk's term P^(N-end) * H is
-// atomically accumulated into scr.accum; the last chunk to finish writes the
-// final hash into scr.result (and sh.pc) and returns true in thread 0.
 struct SharedState {
-  uint32_t warp_par[kWarps];
-  uint32_t start_bit;
-  unsigned long long pc;  // P^(N - chunk_end) for the chunk
+  uint32_t sa[kWarps];      // level-2r thread-parity scan
+  uint32_t sb[2][kWarps];   // level-2r+1 scan, per variant
+  uint32_t start;           // resolved start bits of the round
+  uint32_t lb_first[kWarps];  // block look-back: nearest inclusive per warp
+  uint32_t lb_map[kWarps];    // block look-back: composed map per warp
+  uint32_t lb_incl;           // inclusive value of the nearest inclusive chunk
+  unsigned long long pc;    // P^(N - chunk_end); final hash in the last block
   unsigned long long red[kWarps];
 };
 
-__device__ inline bool chunk_contribution(const uint32_t (&w)[16], int64_t chunk, uint64_t n,
+// Block-wide look-back for round r: every thread probes one predecessor, so
+// one probe covers kThreads chunks (the whole in-flight window at full
+// occupancy).  Returns the chunk's two start bits in every thread.
+__device__ __forceinline__ uint32_t look_back2_block(const uint32_t* status, int64_t chunk, int r,
+                                                     uint32_t seed2, SharedState& sh,
+                                                     unsigned long long* prof) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t acc = 0;  // identity map
+  int64_t base = chunk - 1;
+  while (true) {
+    if (prof && tid == 0) atomicAdd(prof + 0, 1ull);
+    const int64_t k = base - tid;
+    bool incl;
+    uint32_t val;
+    if (k < 0) {
+      incl = true;
+      val = seed2;
+    } else {
+      uint32_t s;
+      uint32_t spins = 0, backoff = 32;
+      // back off while the predecessor is behind: ~150K polling threads
+      // would otherwise saturate L2 and delay the very stores they wait for
+      while (st_nagg(s = ld_relaxed_gpu(status + k)) <= static_cast<uint32_t>(r)) {
+        __nanosleep(backoff);
+        backoff = backoff < 256 ? 2 * backoff : 256;
+        ++spins;
+      }
+      ++spins;
+      if (prof && spins > 1) atomicAdd(prof + 1, static_cast<unsigned long long>(spins - 1));
+      incl = st_nincl(s) > static_cast<uint32_t>(r);
+      val = incl ? (s >> (12 + 2 * r)) & 3u : (s >> (3 * r)) & 7u;
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, incl);
+    if (lane == 0) sh.lb_first[warp] = bal ? warp * 32 + __ffs(bal) - 1 : 0xffffffffu;
+    __syncthreads();
+    uint32_t first = 0xffffffffu;
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) first = min(first, sh.lb_first[q]);
+    if (static_cast<uint32_t>(tid) == first) sh.lb_incl = val;
+    // m_0 o m_1 o ... o m_{first-1}, thread 0 = nearest predecessor
+    uint32_t m = static_cast<uint32_t>(tid) < first ? val : 0u;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t o = __shfl_down_sync(0xffffffffu, m, off);
+      if (lane + off < 32) m = map_compose(m, o);
+    }
+    if (lane == 0) sh.lb_map[warp] = m;
+    __syncthreads();
+    uint32_t M = 0;
+#pragma unroll
+    for (int q = kWarps - 1; q >= 0; --q) M = map_compose(sh.lb_map[q], M);
+    acc = map_compose(acc, M);
+    if (first != 0xffffffffu) {
+      const uint32_t inc = sh.lb_incl;
+      __syncthreads();  // lb_* reused by the next round
+      return map_apply(acc, inc);
+    }
+    __syncthreads();
+    base -= kThreads;
+  }
+}
+
+constexpr int kGroups = kBytesPerThread / 32;
+
+// 64 bytes at pos0 as 16 little-endian words, zero past n.
+__device__ __forceinline__ void load_words64(const uint8_t* data, uint64_t n, uint64_t pos0,
+                                             uint32_t (&w)[16]) {
+  if (pos0 + 64 <= n && (reinterpret_cast<uintptr_t>(data) & 15u) == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 v = *reinterpret_cast<const uint4*>(data + pos0 + 16 * q);
+      w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      uint32_t x = 0;
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t p = pos0 + 4 * q + k;
+        if (p < n) x |= static_cast<uint32_t>(data[p]) << (8 * k);
+      }
+      w[q] = x;
+    }
+  }
+}
+
+// Block-level FNV contribution of one kChunk-byte chunk of `data`; thread t
+// owns bytes [chunk*kChunk + 64t, +64).  The chunk's term P^(N-end) * H is
+// atomically accumulated into scr.accum; the last chunk to finish writes the
+// final hash into scr.result (and sh.pc) and returns true in thread 0.
+__device__ inline bool chunk_contribution(const uint8_t* data, int64_t chunk, uint64_t n,
                                           uint64_t seed, const Scratch& scr, uint64_t n_chunks,
                                           SharedState& sh) {
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint64_t pos0 = static_cast<uint64_t>(chunk) * kChunk + static_cast<uint64_t>(tid) * kBytesPerThread;
 
-  uint32_t B[2][8], Y[2][8];
-  Carries car[2];
-  to_planes(w, B[0]);
-  to_planes(w + 8, B[1]);
-  // Positions past n must not toggle: their bytes are zero, so B=0 there; the
-  // automaton runs on but d_i is forced to zero below and nothing later reads
-  // these states (only the final chunk is padded).
+  uint32_t B[kGroups][8], Y[kGroups][8];
+  Carries car[kGroups];
+  {
+    uint32_t w[16];
+    load_words64(data, n, pos0, w);
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g) to_planes(w + 8 * g, B[g]);
+  }
+  // Positions past n are zero bytes; d_i is forced to zero for them below and
+  // only the final chunk is padded, so its trailing states are never used.
 
+  __syncthreads();  // previous chunk's readers of sh are done
   uint32_t status = 0;  // owner's view (thread 0)
+  long long t_mark = scr.prof ? clock64() : 0;
+  if (scr.trace && tid == 0) {
+    scr.trace[chunk * 12 + 0] = gtimer();
+    scr.trace[chunk * 12 + 10] = smid();
+  }
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    uint32_t T[2], I[2];
+  for (int r = 0; r < kRounds; ++r) {
+    const int j0 = 2 * r, j1 = 2 * r + 1;
+    // ---- level j0 (all lower start bits known): toggles and their prefix
+    uint32_t T0[kGroups], I0[kGroups];
 #pragma unroll
-    for (int g = 0; g < 2; ++g) {
-      T[g] = B[g][j] ^ level_r(j, Y[g], car[g]);
-      I[g] = prefix_xor(T[g]);
+    for (int g = 0; g < kGroups; ++g) {
+      T0[g] = B[g][j0] ^ level_r(j0, Y[g], car[g]);
+      I0[g] = prefix_xor(T0[g]);
+      if (g) I0[g] ^= bcast(I0[g - 1] >> 31);
     }
-    I[1] ^= bcast(I[0] >> 31);
-    const uint32_t par = I[1] >> 31;
-    const uint32_t ballot = __ballot_sync(0xffffffffu, par);
-    const uint32_t lane_excl = __popc(ballot & ((1u << lane) - 1u)) & 1u;
-    if (lane == 0) sh.warp_par[warp] = __popc(ballot) & 1u;
-    __syncthreads();
-    uint32_t warp_excl = 0, agg = 0;
+    {
+      const uint32_t bal = __ballot_sync(0xffffffffu, I0[kGroups - 1] >> 31);
+      if (lane == 0) sh.sa[warp] = __popc(bal) & 1u;
+      __syncthreads();
+      uint32_t wx = 0, agg = 0;
 #pragma unroll
-    for (int q = 0; q < kWarps; ++q) {
-      const uint32_t p = sh.warp_par[q];
-      warp_excl ^= (q < warp) ? p : 0u;
-      agg ^= p;
-    }
-    if (warp == 0) {
-      const uint32_t seed_bit = static_cast<uint32_t>(seed >> j) & 1u;
-      // status word: [7:0] aggregate bits, [15:8] inclusive bits,
-      // [19:16] levels with aggregate published, [23:20] levels inclusive
-      if (lane == 0) {
-        status = (status & ~(0xfu << 16)) | (agg << j) | (static_cast<uint32_t>(j + 1) << 16);
-        st_relaxed_gpu(scr.status + chunk, status);
+      for (int q = 0; q < kWarps; ++q) {
+        wx ^= q < warp ? sh.sa[q] : 0u;
+        agg ^= sh.sa[q];
       }
-      const uint32_t start = look_back(scr.status, chunk, j, seed_bit);
-      if (lane == 0) {
-        status = (status & ~(0xfu << 20)) | ((start ^ agg) << (8 + j)) |
-                 (static_cast<uint32_t>(j + 1) << 20);
-        st_relaxed_gpu(scr.status + chunk, status);
-        sh.start_bit = start;
-      }
-    }
-    __syncthreads();
-    const uint32_t ts = bcast(sh.start_bit ^ warp_excl ^ lane_excl);
+      const uint32_t e0 = wx ^ (__popc(bal & lt) & 1u);
+      // ---- level j1 for both values v of the chunk's start bit j0
+      uint32_t T1[2][kGroups];
+      uint32_t pv[2];
 #pragma unroll
-    for (int g = 0; g < 2; ++g) {
-      const uint32_t U = I[g] ^ T[g] ^ ts;  // state bit j before each position
-      Y[g][j] = U ^ B[g][j];
-      level_carry(j, Y[g], car[g]);
+      for (int v = 0; v < 2; ++v) {
+        uint32_t x = 0;
+#pragma unroll
+        for (int g = 0; g < kGroups; ++g) {
+          uint32_t yv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) yv[q] = Y[g][q];
+          yv[j0] = I0[g] ^ T0[g] ^ bcast(e0 ^ static_cast<uint32_t>(v)) ^ B[g][j0];
+          Carries cv = car[g];
+          level_carry(j0, yv, cv);
+          T1[v][g] = B[g][j1] ^ level_r(j1, yv, cv);
+          x ^= T1[v][g];
+        }
+        pv[v] = __popc(x) & 1u;
+      }
+      const uint32_t bal0 = __ballot_sync(0xffffffffu, pv[0]);
+      const uint32_t bal1 = __ballot_sync(0xffffffffu, pv[1]);
+      if (lane == 0) {
+        sh.sb[0][warp] = __popc(bal0) & 1u;
+        sh.sb[1][warp] = __popc(bal1) & 1u;
+      }
+      __syncthreads();
+      uint32_t wx1[2] = {0, 0}, tot[2] = {0, 0};
+#pragma unroll
+      for (int q = 0; q < kWarps; ++q) {
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          wx1[v] ^= q < warp ? sh.sb[v][q] : 0u;
+          tot[v] ^= sh.sb[v][q];
+        }
+      }
+      const uint32_t map = agg | (tot[0] << 1) | (tot[1] << 2);
+      if (tid == 0) {
+        status = (status & ~(7u << 20)) | (map << (3 * r)) | (static_cast<uint32_t>(r + 1) << 20);
+        atomicExch(scr.status + chunk, status);  // performed at L2: visible to pollers now
+        if (scr.trace) scr.trace[chunk * 12 + 1 + 2 * r] = gtimer();
+      }
+      const uint32_t seed2 = static_cast<uint32_t>(seed >> j0) & 3u;
+      if (scr.prof && tid == 0) {
+        const long long t = clock64();
+        atomicAdd(scr.prof + 2, static_cast<unsigned long long>(t - t_mark));
+        t_mark = t;
+      }
+      const uint32_t start = look_back2_block(scr.status, chunk, r, seed2, sh, scr.prof);
+      if (scr.prof && tid == 0) {
+        const long long t = clock64();
+        atomicAdd(scr.prof + 3, static_cast<unsigned long long>(t - t_mark));
+        t_mark = t;
+      }
+      if (tid == 0) {
+        status = (status & ~(7u << 24)) | (map_apply(map, start) << (12 + 2 * r)) |
+                 (static_cast<uint32_t>(r + 1) << 24);
+        atomicExch(scr.status + chunk, status);
+        if (scr.trace) scr.trace[chunk * 12 + 2 + 2 * r] = gtimer();
+      }
+      const uint32_t s0 = start & 1u, s1 = (start >> 1) & 1u;
+      // ---- finalize level j0 with the true start bit
+#pragma unroll
+      for (int g = 0; g < kGroups; ++g) {
+        Y[g][j0] = I0[g] ^ T0[g] ^ bcast(e0 ^ s0) ^ B[g][j0];
+        level_carry(j0, Y[g], car[g]);
+      }
+      // ---- finalize level j1 (variant s0)
+      const uint32_t e1 = (s0 ? wx1[1] : wx1[0]) ^ (__popc((s0 ? bal1 : bal0) & lt) & 1u);
+      uint32_t Iprev = 0;
+#pragma unroll
+      for (int g = 0; g < kGroups; ++g) {
+        const uint32_t T = s0 ? T1[1][g] : T1[0][g];
+        uint32_t I = prefix_xor(T);
+        if (g) I ^= bcast(Iprev >> 31);
+        Iprev = I;
+        Y[g][j1] = I ^ T ^ bcast(e1 ^ s1) ^ B[g][j1];
+        level_carry(j1, Y[g], car[g]);
+      }
     }
   }
 
+  if (scr.prof && tid == 0) {
+    const long long t = clock64();
+    atomicAdd(scr.prof + 2, static_cast<unsigned long long>(t - t_mark));
+    t_mark = t;
+  }
   // ---- phase B: d_i = b_i - 2 (u_i & b_i); z = u & b = b & ~y
   uint32_t zw[16];
 #pragma unroll
-  for (int g = 0; g < 2; ++g) {
+  for (int g = 0; g < kGroups; ++g) {
     uint32_t Z[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) Z[j] = B[g][j] & ~Y[g][j];
     from_planes(Z, zw + 8 * g);
   }
-  const uint64_t pos0 = static_cast<uint64_t>(chunk) * kChunk + static_cast<uint64_t>(tid) * kBytesPerThread;
+  uint32_t w[16];  // reloaded (L1/L2 hit) instead of held live across the levels
+  load_words64(data, n, pos0, w);
   uint64_t acc = 0;
   uint64_t seg_end = pos0 + kBytesPerThread;
   if (pos0 + kBytesPerThread <= n) {
@@ -305,6 +518,11 @@ __device__ inline bool chunk_contribution(const uint32_t (&w)[16], int64_t chunk
   } else {
     term = acc * pow_p(n - seg_end);
   }
+  if (scr.prof && tid == 0) {
+    atomicAdd(scr.prof + 4, static_cast<unsigned long long>(clock64() - t_mark));
+    atomicAdd(scr.prof + 5, 1ull);
+  }
+  if (scr.trace && tid == 0) scr.trace[chunk * 12 + 9] = gtimer();
   // block reduction (mod 2^64, order-independent)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) term += __shfl_xor_sync(0xffffffffu, term, o);

@@ -7,50 +7,35 @@
 #include "kernels.cuh"
 #include "pack.cuh"
 
+#include <algorithm>
+
 namespace mlck {
 
 // ---------------------------------------------------------------- FNV (K2)
 namespace {
 
-__device__ __forceinline__ void load_words64(const uint8_t* data, uint64_t n, uint64_t pos0,
-                                             uint32_t (&w)[16]) {
-  if (pos0 + 64 <= n && (reinterpret_cast<uintptr_t>(data) & 15u) == 0) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint4 v = *reinterpret_cast<const uint4*>(data + pos0 + 16 * q);
-      w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      uint32_t x = 0;
-      for (int k = 0; k < 4; ++k) {
-        const uint64_t p = pos0 + 4 * q + k;
-        if (p < n) x |= static_cast<uint32_t>(data[p]) << (8 * k);
-      }
-      w[q] = x;
-    }
-  }
-}
-
-__global__ void __launch_bounds__(fnv::kThreads) fnv_kernel(const uint8_t* __restrict__ data,
+__global__ void __launch_bounds__(fnv::kThreads, 4) fnv_kernel(const uint8_t* __restrict__ data,
                                                              uint64_t n, uint64_t seed,
                                                              fnv::Scratch scr, uint64_t n_chunks,
                                                              TrailerDsts trailer) {
   __shared__ fnv::SharedState sh;
   __shared__ int64_t s_chunk;
-  if (threadIdx.x == 0) s_chunk = atomicAdd(scr.ticket, 1u);
-  __syncthreads();
-  const int64_t chunk = s_chunk;
-  uint32_t w[16];
-  load_words64(data, n, static_cast<uint64_t>(chunk) * fnv::kChunk + threadIdx.x * 64ull, w);
-  const bool last = fnv::chunk_contribution(w, chunk, n, seed, scr, n_chunks, sh);
-  // the block that finished last also writes the trailer bytes
-  // (serialize_record appends the checksum, snapshot.hpp:142)
-  if (last) {
-    const unsigned long long h = sh.pc;
-    for (int r = 0; r < trailer.n; ++r)
-      for (int b = 0; b < 8; ++b) trailer.p[r][b] = static_cast<uint8_t>(h >> (8 * b));
+  // Persistent CTAs take chunks in ticket order, so every predecessor of a
+  // chunk is resident or finished when its look-back spins on it.
+  while (true) {
+    if (threadIdx.x == 0) s_chunk = atomicAdd(scr.ticket, 1u);
+    __syncthreads();
+    const int64_t chunk = s_chunk;
+    if (chunk >= static_cast<int64_t>(n_chunks)) return;
+    const bool last = fnv::chunk_contribution(data, chunk, n, seed, scr, n_chunks, sh);
+    // the block that finished last also writes the trailer bytes
+    // (serialize_record appends the checksum, snapshot.hpp:142)
+    if (last) {
+      const unsigned long long h = sh.pc;
+      for (int r = 0; r < trailer.n; ++r)
+        for (int b = 0; b < 8; ++b) trailer.p[r][b] = static_cast<uint8_t>(h >> (8 * b));
+    }
+    __syncthreads();  // s_chunk is rewritten next iteration
   }
 }
 
@@ -71,7 +56,8 @@ uint64_t fnv_chunks(uint64_t n) { return div_up(n, fnv::kChunk); }
 size_t fnv_scratch_words(uint64_t n) { return fnv_chunks(n) + 16; }
 
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch,
-                unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream) {
+                unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
+                unsigned long long* prof, unsigned long long* trace) {
   const uint64_t n_chunks = fnv_chunks(n);
   // layout: [ticket, flag, finished, pad][accum u64][pad..] [status n_chunks]
   fnv::Scratch scr;
@@ -80,14 +66,28 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
   scr.accum = reinterpret_cast<unsigned long long*>(scratch + 4);
   scr.result = result;
   scr.status = scratch + 16;
+  scr.prof = prof;
+  scr.trace = trace;
   MLCK_CUDA(cudaMemsetAsync(scratch, 0, fnv_scratch_words(n) * 4, stream));
   if (n_chunks == 0) {
     // empty input: h = seed
     launch_fnv_empty(seed, result, trailer, stream);
     return;
   }
-  fnv_kernel<<<static_cast<unsigned>(n_chunks), fnv::kThreads, 0, stream>>>(data, n, seed, scr,
-                                                                            n_chunks, trailer);
+  static int resident = 0;  // CTAs per SM at full occupancy
+  if (resident == 0) {
+    MLCK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, fnv_kernel, fnv::kThreads, 0));
+    if (resident < 1) resident = 1;
+  }
+  int sms = kSmCount;
+  {
+    int dev = 0;
+    MLCK_CUDA(cudaGetDevice(&dev));
+    MLCK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const uint64_t grid = std::min<uint64_t>(n_chunks, static_cast<uint64_t>(resident) * sms);
+  fnv_kernel<<<static_cast<unsigned>(grid), fnv::kThreads, 0, stream>>>(data, n, seed, scr,
+                                                                         n_chunks, trailer);
   MLCK_CUDA(cudaGetLastError());
 }
 

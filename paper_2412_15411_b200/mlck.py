@@ -108,6 +108,7 @@ def lib():
                                                     u64p]),
             "mlck_dense_checkpoint": (C.c_int, [vp, vp]),
             "mlck_fnv1a64": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, u64p]),
+            "mlck_fnv1a64_profile": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, u64p, u64p, vp]),
             "mlck_parse_record": (C.c_int, [vp, C.c_int, C.POINTER(RecordInfo), C.POINTER(EntryInfo),
                                             C.c_uint32, u32p]),
             "mlck_read_entry": (C.c_int, [vp, C.POINTER(EntryInfo), C.c_int, f32p, f32p, f32p, f32p]),
@@ -275,6 +276,14 @@ class Context:
         out = C.c_uint64()
         check(lib().mlck_fnv1a64(self.h, device_ptr, n, seed, C.byref(out)))
         return out.value
+
+    def fnv1a64_profile(self, device_ptr: int, n: int, seed: int = 0xcbf29ce484222325, trace=None):
+        out = C.c_uint64()
+        cnt = (C.c_uint64 * 6)()
+        check(lib().mlck_fnv1a64_profile(self.h, device_ptr, n, seed, C.byref(out), cnt,
+                                         trace.ctypes.data if trace is not None else None))
+        keys = ["lookback_probes", "spin_rereads", "cycles_compute", "cycles_lookback", "cycles_phaseB", "chunks"]
+        return out.value, dict(zip(keys, [int(x) for x in cnt]))
 
     def enable_peer_access(self, peer: int):
         check(lib().mlck_enable_peer_access(self.h, peer))

@@ -1,0 +1,52 @@
+"""Development probe: FNV kernel throughput and its profile counters."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+from paper_2412_15411_b200 import mlck
+
+ctx = mlck.Context(0)
+for mb in (16, 256, 1024):
+    n = mb << 20
+    st = mlck.DeviceState(ctx, [n // 12], 4)
+    st.fill_synthetic(1, 1)
+    ptr = st.op_ptrs(0)[0]
+    ctx.synchronize()
+    h0 = ctx.fnv1a64(ptr, n)
+    ctx.event_record(0)
+    reps = 3
+    for _ in range(reps):
+        ctx.fnv1a64(ptr, n)
+    ctx.event_record(1)
+    ms = ctx.event_ms(0, 1) / reps
+    h1, prof = ctx.fnv1a64_profile(ptr, n)
+    ch = max(1, prof["chunks"])
+    print(f"{mb} MB: {ms:.3f} ms  {n / ms / 1e6:.1f} GB/s  same={h0 == h1}  per-chunk: "
+          f"probes {prof['lookback_probes'] / ch:.2f} spins {prof['spin_rereads'] / ch:.1f} "
+          f"cyc compute {prof['cycles_compute'] / ch:.0f} lookback {prof['cycles_lookback'] / ch:.0f} "
+          f"phaseB {prof['cycles_phaseB'] / ch:.0f}")
+    st.close()
+
+# per-chunk trace on 64 MB
+n = 64 << 20
+st = mlck.DeviceState(ctx, [n // 12], 4)
+st.fill_synthetic(1, 1)
+ptr = st.op_ptrs(0)[0]
+chunks = (n + 16383) // 16384
+tr = np.zeros(chunks * 12, dtype=np.uint64)
+ctx.fnv1a64_profile(ptr, n, trace=tr)
+tr = tr.reshape(chunks, 12).astype(np.int64)
+t0 = tr[:, 0].min()
+np.set_printoptions(linewidth=200)
+print("columns: start, agg0, res0, agg1, res1, agg2, res2, agg3, res3, end (us rel. to first start), sm")
+for c in list(range(0, 8)) + list(range(1000, 1008)) + list(range(3000, 3004)):
+    row = tr[c]
+    print(c, [(int(x - t0) // 100) / 10 for x in row[:10]], int(row[10]))
+dur = (tr[:, 9] - tr[:, 0]) / 1000
+print("chunk lifetime us: median %.1f p90 %.1f max %.1f" % (np.median(dur), np.percentile(dur, 90), dur.max()))
+for r in range(4):
+    w = (tr[:, 2 + 2 * r] - tr[:, 1 + 2 * r]) / 1000
+    c = (tr[:, 1 + 2 * r] - (tr[:, 2 * r] if r else tr[:, 0])) / 1000
+    print(f"round {r}: compute-to-publish median {np.median(c):.2f} us, lookback wait median {np.median(w):.2f} us p90 {np.percentile(w, 90):.2f}")
+# dependency: time res(c, r) vs agg(c-1, r)
+lag = (tr[1:, 2] - tr[:-1, 1]) / 1000
+print("res0(c) - agg0(c-1) median %.2f us" % np.median(lag))
