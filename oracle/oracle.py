@@ -163,6 +163,14 @@ class Oracle:
             raise ValueError("container: unsupported compute width")
         return out.tobytes()
 
+    def decode_compute(self, codes: bytes, n: int, compute_bytes: int) -> np.ndarray:
+        """read_compute (snapshot.hpp:95-111) over an array of codes."""
+        a = np.frombuffer(codes, dtype=np.uint8)
+        out = np.empty(n, dtype=np.float32)
+        if self.lib.mlo_decode_compute(_ptr(a, u8p), n, compute_bytes, _ptr(out, f32p)) < 0:
+            raise ValueError("container: unsupported compute width")
+        return out
+
     # ---- container
     def _entries(self, entries, keep):
         arr = (MloEntry * max(1, len(entries)))()

@@ -341,6 +341,9 @@ int mlr_quantize_array(const float* in, size_t n, int compute_bytes, float* out,
     for (size_t i = 0; i < n; ++i) out[i] = quantize_value(in[i], compute_bytes);
   });
 }
+void mlr_unpack_array(const uint16_t* codes, size_t n, int ebits, int mbits, float* out) {
+  for (size_t i = 0; i < n; ++i) out[i] = unpack_reduced(codes[i], ebits, mbits);
+}
 uint16_t mlr_pack_reduced(float x, int ebits, int mbits) { return pack_reduced(x, ebits, mbits); }
 float mlr_unpack_reduced(uint16_t c, int ebits, int mbits) { return unpack_reduced(c, ebits, mbits); }
 

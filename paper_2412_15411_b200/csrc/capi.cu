@@ -111,6 +111,7 @@ struct mlck_ctx {
     MLCK_CUDA(cudaEventRecord(s.done, stream));
     s.used = true;
   }
+  uint32_t fnv_epoch = 0;
   uint32_t* fnv_scratch_for(uint64_t n) {
     const size_t need = fnv_scratch_words(n);
     if (need > fnv_words) {
@@ -118,8 +119,17 @@ struct mlck_ctx {
       if (fnv_scratch) MLCK_CUDA(cudaFree(fnv_scratch));
       fnv_words = align_up(std::max<size_t>(need, 4096), 1024);
       MLCK_CUDA(cudaMalloc(&fnv_scratch, fnv_words * 4));
+      // epoch 0 never matches a launch: a zeroed array reads as "unpublished"
+      MLCK_CUDA(cudaMemsetAsync(fnv_scratch, 0, fnv_words * 4, stream));
     }
     return fnv_scratch;
+  }
+  uint32_t next_epoch() {
+    if (++fnv_epoch == 0) {  // wrapped: clear stale tags once
+      MLCK_CUDA(cudaMemsetAsync(fnv_scratch, 0, fnv_words * 4, stream));
+      fnv_epoch = 1;
+    }
+    return fnv_epoch;
   }
 };
 
@@ -267,7 +277,7 @@ void run_pack(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
     t.n = d.n;
     uint32_t* scratch = ctx->fnv_scratch_for(body);
     const int tf = ctx->tbegin("fnv");
-    launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->results, t, ctx->stream);
+    launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream);
     ctx->tend(tf);
     ctx->launches += 1;
   }
@@ -397,7 +407,8 @@ std::vector<Parsed> parse_blobs(mlck_ctx* ctx, mlck_blob* const* blobs, uint32_t
     TrailerDsts none{};
     uint32_t* scratch = ctx->fnv_scratch_for(b->size - 8);
     const int tf = ctx->tbegin("fnv_verify");
-    launch_fnv(b->dev, b->size - 8, kFnvOffset, scratch, ctx->results + k, none, ctx->stream);
+    launch_fnv(b->dev, b->size - 8, kFnvOffset, scratch, ctx->next_epoch(), ctx->results + k, none,
+               ctx->stream);
     ctx->tend(tf);
     ctx->launches += 1;
     MLCK_CUDA(cudaMemcpyAsync(ctx->results + 32 + k, b->dev + b->size - 8, 8,
@@ -485,6 +496,12 @@ int mlck_ctx_create(int device, mlck_ctx** out) {
     for (auto& e : c->ev) MLCK_CUDA(cudaEventCreate(&e));
     MLCK_CUDA(cudaMalloc(&c->results, 64 * 8));
     MLCK_CUDA(cudaMallocHost(&c->host_results, 64 * 8));
+    // stream-ordered scratch (parse tables, staging) stays in the pool across
+    // synchronizations instead of being returned to the OS every call
+    cudaMemPool_t pool;
+    MLCK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    MLCK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     init_constants();
     *out = c;
   });
@@ -824,7 +841,8 @@ int mlck_fnv1a64(mlck_ctx* ctx, const void* ptr, uint64_t n, uint64_t seed, uint
   return api([&] {
     ctx->activate();
     TrailerDsts none{};
-    launch_fnv(static_cast<const uint8_t*>(ptr), n, seed, ctx->fnv_scratch_for(n), ctx->results,
+    uint32_t* scratch = ctx->fnv_scratch_for(n);
+    launch_fnv(static_cast<const uint8_t*>(ptr), n, seed, scratch, ctx->next_epoch(), ctx->results,
                none, ctx->stream);
     ctx->launches += 1;
     MLCK_CUDA(cudaMemcpyAsync(ctx->host_results, ctx->results, 8, cudaMemcpyDeviceToHost,
@@ -851,7 +869,8 @@ int mlck_fnv1a64_profile(mlck_ctx* ctx, const void* ptr, uint64_t n, uint64_t se
       MLCK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&trace), tb, ctx->stream));
       MLCK_CUDA(cudaMemsetAsync(trace, 0, tb, ctx->stream));
     }
-    launch_fnv(static_cast<const uint8_t*>(ptr), n, seed, ctx->fnv_scratch_for(n), ctx->results,
+    uint32_t* scratch = ctx->fnv_scratch_for(n);
+    launch_fnv(static_cast<const uint8_t*>(ptr), n, seed, scratch, ctx->next_epoch(), ctx->results,
                none, ctx->stream, prof, trace);
     ctx->launches += 1;
     if (trace_host) {

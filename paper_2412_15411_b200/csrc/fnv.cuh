@@ -27,13 +27,24 @@ namespace fnv {
 
 constexpr uint64_t kPrime = 0x100000001b3ull;
 constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
-constexpr int kThreads = 256;
+#ifndef MLCK_FNV_THREADS
+#define MLCK_FNV_THREADS 1024
+#endif
+constexpr int kThreads = MLCK_FNV_THREADS;  // one CTA per SM at 64 regs/thread
 constexpr int kBytesPerThread = 64;  // two 32-position groups
 constexpr int kChunk = kThreads * kBytesPerThread;
 constexpr int kWarps = kThreads / 32;
 
+// One 64-bit look-back word per chunk, kStatusStride words apart (256 B): the
+// ~600 in-flight chunks' words land in different L2 slices instead of a
+// handful of hot lines.  The high half is the launch epoch, so the array is
+// never cleared between launches (a word from an older launch reads as
+// "nothing published").
+constexpr int kStatusStride = 32;
+
 struct Scratch {
-  uint32_t* status;            // [n_chunks] look-back words (zeroed per launch)
+  unsigned long long* status;  // [n_chunks * kStatusStride] epoch-tagged words
+  uint32_t epoch;              // this launch's tag (>= 1)
   uint32_t* ticket;            // chunk dispatch counter (zeroed per launch)
   unsigned long long* accum;   // sum of chunk terms
   uint32_t* finished;          // completed-chunk counter
@@ -61,7 +72,6 @@ __device__ __forceinline__ uint32_t smid() {
 
 // P^(64 k) for k = 0..kThreads-1, written by init_constants() (kernels.cu).
 __constant__ unsigned long long c_pow64[kThreads];
-
 __host__ __device__ inline uint64_t mul_p(uint64_t x) { return x * kPrime; }
 
 __host__ __device__ inline uint64_t pow_p(uint64_t e) {
@@ -198,118 +208,76 @@ constexpr int kRounds = 4;
 __device__ __forceinline__ uint32_t st_nagg(uint32_t s) { return (s >> 20) & 7u; }
 __device__ __forceinline__ uint32_t st_nincl(uint32_t s) { return (s >> 24) & 7u; }
 
-// Warp-level look-back for round r: composes predecessor maps back to the
-// nearest chunk whose inclusive state for round r is known; returns the two
-// start bits of this chunk.  `seed2` = the 2 seed bits (virtual chunk -1).
-__device__ __forceinline__ uint32_t look_back2(const uint32_t* status, int64_t chunk, int r,
-                                               uint32_t seed2) {
-  const int lane = threadIdx.x & 31;
-  uint32_t acc = 0;  // identity map
-  int64_t base = chunk - 1;
-  while (true) {
-    const int64_t k = base - lane;
-    bool incl;
-    uint32_t val;
-    if (k < 0) {
-      incl = true;
-      val = seed2;
-    } else {
-      uint32_t s;
-      do {
-        s = ld_relaxed_gpu(status + k);
-      } while (st_nagg(s) <= static_cast<uint32_t>(r));
-      incl = st_nincl(s) > static_cast<uint32_t>(r);
-      val = incl ? (s >> (12 + 2 * r)) & 3u : (s >> (3 * r)) & 7u;
-    }
-    const uint32_t incl_mask = __ballot_sync(0xffffffffu, incl);
-    const int first = incl_mask ? __ffs(incl_mask) - 1 : 32;
-    // m_0 o m_1 o ... o m_{first-1}: lane 0 is the nearest predecessor
-    uint32_t m = lane < first ? val : 0u;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t o = __shfl_down_sync(0xffffffffu, m, off);
-      if (lane + off < 32) m = map_compose(m, o);
-    }
-    m = __shfl_sync(0xffffffffu, m, 0);
-    acc = map_compose(acc, m);
-    if (incl_mask) {
-      const uint32_t inc = __shfl_sync(0xffffffffu, val, first);
-      return map_apply(acc, inc);
-    }
-    base -= 32;
-  }
-}
-
 struct SharedState {
   uint32_t sa[kWarps];      // level-2r thread-parity scan
   uint32_t sb[2][kWarps];   // level-2r+1 scan, per variant
   uint32_t start;           // resolved start bits of the round
-  uint32_t lb_first[kWarps];  // block look-back: nearest inclusive per warp
-  uint32_t lb_map[kWarps];    // block look-back: composed map per warp
-  uint32_t lb_incl;           // inclusive value of the nearest inclusive chunk
   unsigned long long pc;    // P^(N - chunk_end); final hash in the last block
   unsigned long long red[kWarps];
 };
 
-// Block-wide look-back for round r: every thread probes one predecessor, so
-// one probe covers kThreads chunks (the whole in-flight window at full
-// occupancy).  Returns the chunk's two start bits in every thread.
-__device__ __forceinline__ uint32_t look_back2_block(const uint32_t* status, int64_t chunk, int r,
-                                                     uint32_t seed2, SharedState& sh,
-                                                     unsigned long long* prof) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// Look-back for round r, run by warp 0 alone: lane l probes the 8
+// predecessors base-8l .. base-8l-7 with all 8 loads in flight, so one probe
+// covers 256 chunks (more than the in-flight window) at one load latency.
+// Returns the chunk's two start bits (in warp 0).
+constexpr int kProbePerLane = 8;
+__device__ __forceinline__ uint32_t look_back2_warp(const unsigned long long* status,
+                                                    uint32_t epoch, int64_t chunk, int r,
+                                                    uint32_t seed2, unsigned long long* prof) {
+  const int lane = threadIdx.x & 31;
   uint32_t acc = 0;  // identity map
   int64_t base = chunk - 1;
   while (true) {
-    if (prof && tid == 0) atomicAdd(prof + 0, 1ull);
-    const int64_t k = base - tid;
-    bool incl;
-    uint32_t val;
-    if (k < 0) {
-      incl = true;
-      val = seed2;
-    } else {
+    if (prof && lane == 0) atomicAdd(prof + 0, 1ull);
+    unsigned long long v[kProbePerLane];
+#pragma unroll
+    for (int q = 0; q < kProbePerLane; ++q) {
+      const int64_t k = base - kProbePerLane * lane - q;
+      v[q] = k < 0 ? 0ull : ld_relaxed_gpu_u64(status + k * kStatusStride);
+    }
+    // lane-local: nearest-first composition up to the first inclusive
+    uint32_t m = 0, incl_val = 0;
+    bool has_incl = false;
+#pragma unroll
+    for (int q = 0; q < kProbePerLane; ++q) {
+      if (has_incl) continue;
+      const int64_t k = base - kProbePerLane * lane - q;
+      if (k < 0) {
+        has_incl = true;
+        incl_val = seed2;
+        continue;
+      }
       uint32_t s;
-      uint32_t spins = 0, backoff = 32;
-      // back off while the predecessor is behind: ~150K polling threads
-      // would otherwise saturate L2 and delay the very stores they wait for
-      while (st_nagg(s = ld_relaxed_gpu(status + k)) <= static_cast<uint32_t>(r)) {
+      uint32_t backoff = 32, spins = 0;
+      // back off while the predecessor is behind (keeps pollers off L2)
+      while (static_cast<uint32_t>(v[q] >> 32) != epoch ||
+             st_nagg(s = static_cast<uint32_t>(v[q])) <= static_cast<uint32_t>(r)) {
         __nanosleep(backoff);
         backoff = backoff < 256 ? 2 * backoff : 256;
+        v[q] = ld_relaxed_gpu_u64(status + k * kStatusStride);
         ++spins;
       }
-      ++spins;
-      if (prof && spins > 1) atomicAdd(prof + 1, static_cast<unsigned long long>(spins - 1));
-      incl = st_nincl(s) > static_cast<uint32_t>(r);
-      val = incl ? (s >> (12 + 2 * r)) & 3u : (s >> (3 * r)) & 7u;
+      if (prof && spins) atomicAdd(prof + 1, static_cast<unsigned long long>(spins));
+      if (st_nincl(s) > static_cast<uint32_t>(r)) {
+        has_incl = true;
+        incl_val = (s >> (12 + 2 * r)) & 3u;
+      } else {
+        m = map_compose(m, (s >> (3 * r)) & 7u);  // apply the farther map first
+      }
     }
-    const uint32_t bal = __ballot_sync(0xffffffffu, incl);
-    if (lane == 0) sh.lb_first[warp] = bal ? warp * 32 + __ffs(bal) - 1 : 0xffffffffu;
-    __syncthreads();
-    uint32_t first = 0xffffffffu;
-#pragma unroll
-    for (int q = 0; q < kWarps; ++q) first = min(first, sh.lb_first[q]);
-    if (static_cast<uint32_t>(tid) == first) sh.lb_incl = val;
-    // m_0 o m_1 o ... o m_{first-1}, thread 0 = nearest predecessor
-    uint32_t m = static_cast<uint32_t>(tid) < first ? val : 0u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, has_incl);
+    const int first = bal ? __ffs(bal) - 1 : 32;
+    // L_0 o L_1 o ... o L_first (lanes past the nearest inclusive: identity)
+    uint32_t t = lane <= first ? m : 0u;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t o = __shfl_down_sync(0xffffffffu, m, off);
-      if (lane + off < 32) m = map_compose(m, o);
+      const uint32_t o = __shfl_down_sync(0xffffffffu, t, off);
+      if (lane + off < 32) t = map_compose(t, o);
     }
-    if (lane == 0) sh.lb_map[warp] = m;
-    __syncthreads();
-    uint32_t M = 0;
-#pragma unroll
-    for (int q = kWarps - 1; q >= 0; --q) M = map_compose(sh.lb_map[q], M);
-    acc = map_compose(acc, M);
-    if (first != 0xffffffffu) {
-      const uint32_t inc = sh.lb_incl;
-      __syncthreads();  // lb_* reused by the next round
-      return map_apply(acc, inc);
-    }
-    __syncthreads();
-    base -= kThreads;
+    t = __shfl_sync(0xffffffffu, t, 0);
+    acc = map_compose(acc, t);
+    if (bal) return map_apply(acc, __shfl_sync(0xffffffffu, incl_val, first));
+    base -= 32 * kProbePerLane;
   }
 }
 
@@ -382,13 +350,11 @@ __device__ inline bool chunk_contribution(const uint8_t* data, int64_t chunk, ui
       const uint32_t bal = __ballot_sync(0xffffffffu, I0[kGroups - 1] >> 31);
       if (lane == 0) sh.sa[warp] = __popc(bal) & 1u;
       __syncthreads();
-      uint32_t wx = 0, agg = 0;
-#pragma unroll
-      for (int q = 0; q < kWarps; ++q) {
-        wx ^= q < warp ? sh.sa[q] : 0u;
-        agg ^= sh.sa[q];
-      }
-      const uint32_t e0 = wx ^ (__popc(bal & lt) & 1u);
+      // warp-parity bits of all warps in one ballot (lane q reads warp q)
+      const uint32_t wb = __ballot_sync(0xffffffffu, lane < kWarps ? sh.sa[lane] : 0u);
+      const uint32_t lt_w = (1u << warp) - 1u;
+      const uint32_t agg = __popc(wb) & 1u;
+      const uint32_t e0 = (__popc(wb & lt_w) ^ __popc(bal & lt)) & 1u;
       // ---- level j1 for both values v of the chunk's start bit j0
       uint32_t T1[2][kGroups];
       uint32_t pv[2];
@@ -415,19 +381,19 @@ __device__ inline bool chunk_contribution(const uint8_t* data, int64_t chunk, ui
         sh.sb[1][warp] = __popc(bal1) & 1u;
       }
       __syncthreads();
-      uint32_t wx1[2] = {0, 0}, tot[2] = {0, 0};
+      uint32_t wx1[2], tot[2];
 #pragma unroll
-      for (int q = 0; q < kWarps; ++q) {
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          wx1[v] ^= q < warp ? sh.sb[v][q] : 0u;
-          tot[v] ^= sh.sb[v][q];
-        }
+      for (int v = 0; v < 2; ++v) {
+        const uint32_t w1 = __ballot_sync(0xffffffffu, lane < kWarps ? sh.sb[v][lane] : 0u);
+        wx1[v] = __popc(w1 & lt_w) & 1u;
+        tot[v] = __popc(w1) & 1u;
       }
       const uint32_t map = agg | (tot[0] << 1) | (tot[1] << 2);
       if (tid == 0) {
         status = (status & ~(7u << 20)) | (map << (3 * r)) | (static_cast<uint32_t>(r + 1) << 20);
-        atomicExch(scr.status + chunk, status);  // performed at L2: visible to pollers now
+        // atomic: performed at L2, visible to pollers immediately
+        atomicExch(scr.status + chunk * kStatusStride,
+                   (static_cast<unsigned long long>(scr.epoch) << 32) | status);
         if (scr.trace) scr.trace[chunk * 12 + 1 + 2 * r] = gtimer();
       }
       const uint32_t seed2 = static_cast<uint32_t>(seed >> j0) & 3u;
@@ -436,18 +402,24 @@ __device__ inline bool chunk_contribution(const uint8_t* data, int64_t chunk, ui
         atomicAdd(scr.prof + 2, static_cast<unsigned long long>(t - t_mark));
         t_mark = t;
       }
-      const uint32_t start = look_back2_block(scr.status, chunk, r, seed2, sh, scr.prof);
+      if (warp == 0) {
+        const uint32_t start = look_back2_warp(scr.status, scr.epoch, chunk, r, seed2, scr.prof);
+        if (lane == 0) {
+          status = (status & ~(7u << 24)) | (map_apply(map, start) << (12 + 2 * r)) |
+                   (static_cast<uint32_t>(r + 1) << 24);
+          atomicExch(scr.status + chunk * kStatusStride,
+                     (static_cast<unsigned long long>(scr.epoch) << 32) | status);
+          sh.start = start;
+          if (scr.trace) scr.trace[chunk * 12 + 2 + 2 * r] = gtimer();
+        }
+      }
+      __syncthreads();
       if (scr.prof && tid == 0) {
         const long long t = clock64();
         atomicAdd(scr.prof + 3, static_cast<unsigned long long>(t - t_mark));
         t_mark = t;
       }
-      if (tid == 0) {
-        status = (status & ~(7u << 24)) | (map_apply(map, start) << (12 + 2 * r)) |
-                 (static_cast<uint32_t>(r + 1) << 24);
-        atomicExch(scr.status + chunk, status);
-        if (scr.trace) scr.trace[chunk * 12 + 2 + 2 * r] = gtimer();
-      }
+      const uint32_t start = sh.start;
       const uint32_t s0 = start & 1u, s1 = (start >> 1) & 1u;
       // ---- finalize level j0 with the true start bit
 #pragma unroll
@@ -484,39 +456,41 @@ __device__ inline bool chunk_contribution(const uint8_t* data, int64_t chunk, ui
     for (int j = 0; j < 8; ++j) Z[j] = B[g][j] & ~Y[g][j];
     from_planes(Z, zw + 8 * g);
   }
-  uint32_t w[16];  // reloaded (L1/L2 hit) instead of held live across the levels
-  load_words64(data, n, pos0, w);
-  uint64_t acc = 0;
-  uint64_t seg_end = pos0 + kBytesPerThread;
-  if (pos0 + kBytesPerThread <= n) {
+  const uint64_t chunk_end = static_cast<uint64_t>(chunk + 1) * kChunk;
+  uint64_t term = 0;
+  {
+    uint32_t w[16];  // reloaded (L1/L2 hit) instead of held live across the levels
+    load_words64(data, n, pos0, w);
+    uint64_t acc = 0;
+    uint64_t seg_end = pos0 + kBytesPerThread;
+    if (pos0 + kBytesPerThread <= n) {
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
+      for (int q = 0; q < 16; ++q) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int32_t b = (w[q] >> (8 * k)) & 0xff;
-        const int32_t z = (zw[q] >> (8 * k)) & 0xff;
-        acc = (acc + static_cast<uint64_t>(static_cast<int64_t>(b - 2 * z))) * kPrime;
-      }
-    }
-  } else {
-    seg_end = pos0 < n ? n : pos0;
-    for (int q = 0; q < 16; ++q)
-      for (int k = 0; k < 4; ++k)
-        if (pos0 + 4 * q + k < n) {
+        for (int k = 0; k < 4; ++k) {
           const int32_t b = (w[q] >> (8 * k)) & 0xff;
           const int32_t z = (zw[q] >> (8 * k)) & 0xff;
           acc = (acc + static_cast<uint64_t>(static_cast<int64_t>(b - 2 * z))) * kPrime;
         }
-  }
-  // term = acc * P^(N - seg_end)
-  const uint64_t chunk_end = static_cast<uint64_t>(chunk + 1) * kChunk;
-  uint64_t term;
-  if (chunk_end <= n) {
-    if (tid == 0) sh.pc = pow_p(n - chunk_end);
-    __syncthreads();
-    term = acc * sh.pc * c_pow64[kThreads - 1 - tid];
-  } else {
-    term = acc * pow_p(n - seg_end);
+      }
+    } else {
+      seg_end = pos0 < n ? n : pos0;
+      for (int q = 0; q < 16; ++q)
+        for (int k = 0; k < 4; ++k)
+          if (pos0 + 4 * q + k < n) {
+            const int32_t b = (w[q] >> (8 * k)) & 0xff;
+            const int32_t z = (zw[q] >> (8 * k)) & 0xff;
+            acc = (acc + static_cast<uint64_t>(static_cast<int64_t>(b - 2 * z))) * kPrime;
+          }
+    }
+    // term = acc * P^(N - seg_end)
+    if (chunk_end <= n) {
+      if (tid == 0) sh.pc = pow_p(n - chunk_end);
+      __syncthreads();
+      term = acc * sh.pc * c_pow64[kThreads - 1 - tid];
+    } else {
+      term = acc * pow_p(n - seg_end);
+    }
   }
   if (scr.prof && tid == 0) {
     atomicAdd(scr.prof + 4, static_cast<unsigned long long>(clock64() - t_mark));

@@ -14,7 +14,7 @@ namespace mlck {
 // ---------------------------------------------------------------- FNV (K2)
 namespace {
 
-__global__ void __launch_bounds__(fnv::kThreads, 4) fnv_kernel(const uint8_t* __restrict__ data,
+__global__ void __launch_bounds__(fnv::kThreads, 65536 / (64 * fnv::kThreads)) fnv_kernel(const uint8_t* __restrict__ data,
                                                              uint64_t n, uint64_t seed,
                                                              fnv::Scratch scr, uint64_t n_chunks,
                                                              TrailerDsts trailer) {
@@ -53,22 +53,24 @@ void init_constants() {
 }
 
 uint64_t fnv_chunks(uint64_t n) { return div_up(n, fnv::kChunk); }
-size_t fnv_scratch_words(uint64_t n) { return fnv_chunks(n) + 16; }
+// [256 B header: ticket u32 @0, finished u32 @8, accum u64 @16]
+// [status: n_chunks words of 8 B at a 256 B stride]
+size_t fnv_scratch_words(uint64_t n) { return (256 + fnv_chunks(n) * fnv::kStatusStride * 8) / 4; }
 
-void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch,
+void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
                 unsigned long long* prof, unsigned long long* trace) {
   const uint64_t n_chunks = fnv_chunks(n);
-  // layout: [ticket, flag, finished, pad][accum u64][pad..] [status n_chunks]
   fnv::Scratch scr;
   scr.ticket = scratch;
   scr.finished = scratch + 2;
   scr.accum = reinterpret_cast<unsigned long long*>(scratch + 4);
   scr.result = result;
-  scr.status = scratch + 16;
+  scr.status = reinterpret_cast<unsigned long long*>(scratch + 64);
+  scr.epoch = epoch;
   scr.prof = prof;
   scr.trace = trace;
-  MLCK_CUDA(cudaMemsetAsync(scratch, 0, fnv_scratch_words(n) * 4, stream));
+  MLCK_CUDA(cudaMemsetAsync(scratch, 0, 256, stream));  // header only: status is epoch-tagged
   if (n_chunks == 0) {
     // empty input: h = seed
     launch_fnv_empty(seed, result, trailer, stream);

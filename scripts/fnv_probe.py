@@ -28,10 +28,11 @@ for mb in (16, 256, 1024):
 
 # per-chunk trace on 64 MB
 n = 64 << 20
+CH = int(os.environ.get("FNV_CHUNK", "65536"))
 st = mlck.DeviceState(ctx, [n // 12], 4)
 st.fill_synthetic(1, 1)
 ptr = st.op_ptrs(0)[0]
-chunks = (n + 16383) // 16384
+chunks = (n + CH - 1) // CH
 tr = np.zeros(chunks * 12, dtype=np.uint64)
 ctx.fnv1a64_profile(ptr, n, trace=tr)
 tr = tr.reshape(chunks, 12).astype(np.int64)

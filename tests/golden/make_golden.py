@@ -128,9 +128,13 @@ def codec_vectors(ref: Reference) -> dict:
         out[f"q{cb}"] = q
     out["pack16"] = np.array([ref.lib.mlr_pack_reduced(C.c_float(v), 5, 10) for v in out["q2"]], dtype=np.uint16)
     out["pack8"] = np.array([ref.lib.mlr_pack_reduced(C.c_float(v), 4, 3) for v in out["q1"]], dtype=np.uint16)
-    codes16 = np.arange(65536, dtype=np.uint32)
-    out["unpack16"] = np.array([ref.lib.mlr_unpack_reduced(int(c), 5, 10) for c in codes16], dtype=np.float32)
-    out["unpack8"] = np.array([ref.lib.mlr_unpack_reduced(int(c), 4, 3) for c in range(256)], dtype=np.float32)
+    up = ref.lib.mlr_unpack_array
+    up.argtypes = [C.POINTER(C.c_uint16), C.c_size_t, C.c_int, C.c_int, C.POINTER(C.c_float)]
+    for name, n, e, m in (("unpack16", 65536, 5, 10), ("unpack8", 256, 4, 3)):
+        codes = np.arange(n, dtype=np.uint16)
+        vals = np.empty(n, dtype=np.float32)
+        up(codes.ctypes.data_as(C.POINTER(C.c_uint16)), n, e, m, fp(vals))  # sNaN-exact
+        out[name] = vals
     return out
 
 
