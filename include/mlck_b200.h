@@ -4,7 +4,7 @@
  * The reference (/root/reference/proj/include/moelab) is a header-only C++20
  * API.  This ABI is what a drop-in replacement of its checkpoint path binds:
  * plain pointers and sizes, opaque handles, int status + thread-local message.
- * include/moelab_b200/*.hpp wraps it back into the reference's C++ signatures
+ * include/moelab_b200/checkpoint.hpp wraps it back into the reference's C++ signatures
  * (same names, same exception types and texts); INTEGRATION.md shows the
  * binding.  Every entry below cites the reference function it replaces.
  *
@@ -78,6 +78,13 @@ uint64_t mlck_ctx_kernel_launches(mlck_ctx* ctx);
  * fnv_verify, walk, replay).  mlck_ctx_timings synchronizes, returns the
  * labels as CSV and the durations (ms) recorded since the last read. */
 int mlck_ctx_set_timing(mlck_ctx* ctx, int on);
+/* 1 (default): a record is gathered, written (local + replicas) and hashed
+ * by one kernel; 0: separate pack and FNV kernels (for ablation). */
+int mlck_ctx_set_fused_pack(mlck_ctx* ctx, int on);
+/* Replica transport: 1 (default) copy engines on a side stream, overlapped
+ * with the FNV kernel (peer replicas go over NVLink); 0 remote/local stores
+ * issued by the pack kernel. */
+int mlck_ctx_set_replica_mode(mlck_ctx* ctx, int mode);
 int mlck_ctx_timings(mlck_ctx* ctx, char* labels_csv, uint64_t labels_cap, float* ms,
                      uint32_t cap, uint32_t* n);
 

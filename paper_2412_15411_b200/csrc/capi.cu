@@ -112,6 +112,12 @@ struct mlck_ctx {
     s.used = true;
   }
   uint32_t fnv_epoch = 0;
+  bool fused_pack = false;  // pack + FNV trailer in one kernel (mlck_ctx_set_fused_pack)
+  // Replica transport: 1 = copy engines on a side stream, overlapping the FNV
+  // kernel (default); 0 = remote stores issued by the pack kernel itself.
+  int replica_mode = 1;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_packed = nullptr, ev_hashed = nullptr, ev_pushed = nullptr;
   uint32_t* fnv_scratch_for(uint64_t n) {
     const size_t need = fnv_scratch_words(n);
     if (need > fnv_words) {
@@ -266,9 +272,54 @@ void run_pack(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
   d.p[0] = out->dev;
   d.n = 1;
   for (auto& r : out->replicas) d.p[d.n++] = r.first;
+  const auto* segs = reinterpret_cast<const pack::Segment*>(s.dev);
+  const int n_segs = static_cast<int>(b.segs.size());
+  if (trailer && ctx->fused_pack && body) {
+    // one pass: gather + local/peer stores + FNV trailer
+    TrailerDsts t{};
+    for (int r = 0; r < d.n; ++r) t.p[r] = d.p[r] + body;
+    t.n = d.n;
+    uint32_t* scratch = ctx->fnv_scratch_for(body);
+    const int tf = ctx->tbegin("pack_fnv");
+    launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream,
+               nullptr, nullptr, segs, n_segs, &d);
+    ctx->tend(tf);
+    ctx->launches += 1;
+    return;
+  }
+  if (trailer && ctx->replica_mode == 1 && !out->replicas.empty() && body) {
+    // pack the local record; push it to every replica with the copy engines
+    // (NVLink for peers) on the side stream while the FNV kernel hashes it;
+    // the 8-byte trailer follows the hash.
+    pack::Dsts local{};
+    local.p[0] = out->dev;
+    local.n = 1;
+    const int tp = ctx->tbegin("pack");
+    launch_pack(segs, n_segs, body, local, ctx->stream);
+    ctx->tend(tp);
+    ctx->launches += 1;
+    MLCK_CUDA(cudaEventRecord(ctx->ev_packed, ctx->stream));
+    MLCK_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_packed, 0));
+    for (auto& r : out->replicas)
+      MLCK_CUDA(cudaMemcpyAsync(r.first, out->dev, body, cudaMemcpyDefault, ctx->side));
+    TrailerDsts t{};
+    t.p[0] = out->dev + body;
+    t.n = 1;
+    uint32_t* scratch = ctx->fnv_scratch_for(body);
+    const int tf = ctx->tbegin("fnv");
+    launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream);
+    ctx->tend(tf);
+    ctx->launches += 1;
+    MLCK_CUDA(cudaEventRecord(ctx->ev_hashed, ctx->stream));
+    MLCK_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_hashed, 0));
+    for (auto& r : out->replicas)
+      MLCK_CUDA(cudaMemcpyAsync(r.first + body, out->dev + body, 8, cudaMemcpyDefault, ctx->side));
+    MLCK_CUDA(cudaEventRecord(ctx->ev_pushed, ctx->side));
+    MLCK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_pushed, 0));  // record complete everywhere
+    return;
+  }
   const int tp = ctx->tbegin("pack");
-  launch_pack(reinterpret_cast<const pack::Segment*>(s.dev), static_cast<int>(b.segs.size()), body,
-              d, ctx->stream);
+  launch_pack(segs, n_segs, body, d, ctx->stream);
   ctx->tend(tp);
   ctx->launches += body ? 1 : 0;
   if (trailer) {
@@ -493,6 +544,9 @@ int mlck_ctx_create(int device, mlck_ctx** out) {
     MLCK_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
     c->stream = c->own;
     for (auto& s : c->stage) MLCK_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+    MLCK_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&c->ev_packed, &c->ev_hashed, &c->ev_pushed})
+      MLCK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (auto& e : c->ev) MLCK_CUDA(cudaEventCreate(&e));
     MLCK_CUDA(cudaMalloc(&c->results, 64 * 8));
     MLCK_CUDA(cudaMallocHost(&c->host_results, 64 * 8));
@@ -539,6 +593,17 @@ int mlck_ctx_synchronize(mlck_ctx* c) {
   });
 }
 uint64_t mlck_ctx_kernel_launches(mlck_ctx* c) { return c ? c->launches : 0; }
+
+int mlck_ctx_set_fused_pack(mlck_ctx* c, int on) {
+  return api([&] { c->fused_pack = on != 0; });
+}
+
+int mlck_ctx_set_replica_mode(mlck_ctx* c, int mode) {
+  return api([&] {
+    if (mode != 0 && mode != 1) throw_invalid("replica mode must be 0 (SM stores) or 1 (copy engines)");
+    c->replica_mode = mode;
+  });
+}
 
 int mlck_ctx_set_timing(mlck_ctx* c, int on) {
   return api([&] {

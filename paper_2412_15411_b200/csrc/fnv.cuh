@@ -72,6 +72,11 @@ __device__ __forceinline__ uint32_t smid() {
 
 // P^(64 k) for k = 0..kThreads-1, written by init_constants() (kernels.cu).
 __constant__ unsigned long long c_pow64[kThreads];
+// Q_k = P^(64-k) for a thread segment, split into 32-bit halves, and
+// 512 * sum_k Q_k (the bias of the unsigned per-byte terms).
+__constant__ uint32_t c_qlo[kBytesPerThread];
+__constant__ uint32_t c_qhi[kBytesPerThread];
+__constant__ unsigned long long c_qbias;
 __host__ __device__ inline uint64_t mul_p(uint64_t x) { return x * kPrime; }
 
 __host__ __device__ inline uint64_t pow_p(uint64_t e) {
@@ -464,15 +469,23 @@ __device__ inline bool chunk_contribution(const uint8_t* data, int64_t chunk, ui
     uint64_t acc = 0;
     uint64_t seg_end = pos0 + kBytesPerThread;
     if (pos0 + kBytesPerThread <= n) {
+      // acc = sum_k d_k P^(64-k) as independent products (no serial Horner):
+      // with db = d + 512 >= 0, sum db*Q mod 2^64 = sum mad.wide(db, Q_lo)
+      // + 2^32 sum mad.lo(db, Q_hi); the bias is removed once (c_qbias).
+      uint64_t lo = 0;
+      uint32_t hi = 0;
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const int32_t b = (w[q] >> (8 * k)) & 0xff;
-          const int32_t z = (zw[q] >> (8 * k)) & 0xff;
-          acc = (acc + static_cast<uint64_t>(static_cast<int64_t>(b - 2 * z))) * kPrime;
+          const uint32_t b = __byte_perm(w[q], 0, 0x4440 + k);
+          const uint32_t z = __byte_perm(zw[q], 0, 0x4440 + k);
+          const uint32_t db = b + 512u - 2u * z;
+          lo += static_cast<uint64_t>(db) * c_qlo[4 * q + k];  // mad.wide.u32
+          hi += db * c_qhi[4 * q + k];
         }
       }
+      acc = lo + (static_cast<uint64_t>(hi) << 32) - c_qbias;
     } else {
       seg_end = pos0 < n ? n : pos0;
       for (int q = 0; q < 16; ++q)

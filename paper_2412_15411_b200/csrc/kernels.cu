@@ -14,10 +14,52 @@ namespace mlck {
 // ---------------------------------------------------------------- FNV (K2)
 namespace {
 
-__global__ void __launch_bounds__(fnv::kThreads, 65536 / (64 * fnv::kThreads)) fnv_kernel(const uint8_t* __restrict__ data,
+// K1 fused into K2: the thread's 64 output bytes gathered from the record's
+// segment table (header bytes + arena spans at arbitrary alignment) with
+// aligned 128-bit loads and a funnel shift, written to the local record and
+// every replica (peer pointers: NVLink stores), then hashed from registers'
+// worth of data the thread just wrote.
+__device__ __forceinline__ void gather_write64(const pack::Segment* __restrict__ segs, int n_segs,
+                                               uint64_t pos0, uint64_t n, const pack::Dsts& d) {
+  if (pos0 >= n) return;
+  const int s = pack::find_segment(segs, n_segs, pos0);
+  const pack::Segment seg = segs[s];
+  if (pos0 + 64 <= n && seg.dst + seg.len >= pos0 + 64) {
+    const uint8_t* src = seg.src + (pos0 - seg.dst);
+    const uint32_t sh = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(src) & 15u);
+    const uint8_t* base = src - sh;
+    uint4 a[5];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = ld_stream(base + 16 * i);
+    a[4] = sh ? ld_stream(base + 64) : a[3];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 o = sh ? pack::funnel16(a[i], a[i + 1], sh) : a[i];
+#pragma unroll
+      for (int r = 0; r < pack::kMaxDst; ++r)
+        if (r < d.n) st_v4(d.p[r] + pos0 + 16 * i, o);
+    }
+    return;
+  }
+  int k = s;  // straddles segments (headers) or the record end: byte path
+  const uint64_t end = pos0 + 64 < n ? pos0 + 64 : n;
+  for (uint64_t p = pos0; p < end; ++p) {
+    while (k + 1 < n_segs && segs[k + 1].dst <= p) ++k;
+    const uint8_t b = segs[k].src[p - segs[k].dst];
+#pragma unroll
+    for (int r = 0; r < pack::kMaxDst; ++r)
+      if (r < d.n) d.p[r][p] = b;
+  }
+}
+
+// `data` is not __restrict__: in the fused mode it is the local record the
+// same kernel just wrote (no read-only / non-coherent cache path allowed).
+__global__ void __launch_bounds__(fnv::kThreads, 65536 / (64 * fnv::kThreads)) fnv_kernel(const uint8_t* data,
                                                              uint64_t n, uint64_t seed,
                                                              fnv::Scratch scr, uint64_t n_chunks,
-                                                             TrailerDsts trailer) {
+                                                             TrailerDsts trailer,
+                                                             const pack::Segment* __restrict__ segs,
+                                                             int n_segs, pack::Dsts dsts) {
   __shared__ fnv::SharedState sh;
   __shared__ int64_t s_chunk;
   // Persistent CTAs take chunks in ticket order, so every predecessor of a
@@ -27,6 +69,9 @@ __global__ void __launch_bounds__(fnv::kThreads, 65536 / (64 * fnv::kThreads)) f
     __syncthreads();
     const int64_t chunk = s_chunk;
     if (chunk >= static_cast<int64_t>(n_chunks)) return;
+    if (n_segs > 0)  // fused pack: write this thread's bytes, then hash them
+      gather_write64(segs, n_segs,
+                     static_cast<uint64_t>(chunk) * fnv::kChunk + threadIdx.x * 64ull, n, dsts);
     const bool last = fnv::chunk_contribution(data, chunk, n, seed, scr, n_chunks, sh);
     // the block that finished last also writes the trailer bytes
     // (serialize_record appends the checksum, snapshot.hpp:142)
@@ -50,6 +95,18 @@ void init_constants() {
     x *= p64;
   }
   MLCK_CUDA(cudaMemcpyToSymbol(fnv::c_pow64, t, sizeof(t)));
+  uint32_t qlo[fnv::kBytesPerThread], qhi[fnv::kBytesPerThread];
+  unsigned long long qsum = 0;
+  for (int k = 0; k < fnv::kBytesPerThread; ++k) {
+    const uint64_t q = fnv::pow_p(static_cast<uint64_t>(fnv::kBytesPerThread - k));
+    qlo[k] = static_cast<uint32_t>(q);
+    qhi[k] = static_cast<uint32_t>(q >> 32);
+    qsum += q;
+  }
+  const unsigned long long qbias = 512ull * qsum;
+  MLCK_CUDA(cudaMemcpyToSymbol(fnv::c_qlo, qlo, sizeof(qlo)));
+  MLCK_CUDA(cudaMemcpyToSymbol(fnv::c_qhi, qhi, sizeof(qhi)));
+  MLCK_CUDA(cudaMemcpyToSymbol(fnv::c_qbias, &qbias, sizeof(qbias)));
 }
 
 uint64_t fnv_chunks(uint64_t n) { return div_up(n, fnv::kChunk); }
@@ -59,7 +116,8 @@ size_t fnv_scratch_words(uint64_t n) { return (256 + fnv_chunks(n) * fnv::kStatu
 
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
-                unsigned long long* prof, unsigned long long* trace) {
+                unsigned long long* prof, unsigned long long* trace, const pack::Segment* segs,
+                int n_segs, const pack::Dsts* dsts) {
   const uint64_t n_chunks = fnv_chunks(n);
   fnv::Scratch scr;
   scr.ticket = scratch;
@@ -88,8 +146,10 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
     MLCK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   const uint64_t grid = std::min<uint64_t>(n_chunks, static_cast<uint64_t>(resident) * sms);
-  fnv_kernel<<<static_cast<unsigned>(grid), fnv::kThreads, 0, stream>>>(data, n, seed, scr,
-                                                                         n_chunks, trailer);
+  pack::Dsts d{};
+  if (dsts) d = *dsts;
+  fnv_kernel<<<static_cast<unsigned>(grid), fnv::kThreads, 0, stream>>>(
+      data, n, seed, scr, n_chunks, trailer, segs, segs ? n_segs : 0, d);
   MLCK_CUDA(cudaGetLastError());
 }
 

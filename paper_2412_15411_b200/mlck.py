@@ -79,6 +79,8 @@ def lib():
             "mlck_ctx_synchronize": (C.c_int, [vp]),
             "mlck_ctx_kernel_launches": (C.c_uint64, [vp]),
             "mlck_ctx_set_timing": (C.c_int, [vp, C.c_int]),
+            "mlck_ctx_set_fused_pack": (C.c_int, [vp, C.c_int]),
+            "mlck_ctx_set_replica_mode": (C.c_int, [vp, C.c_int]),
             "mlck_ctx_timings": (C.c_int, [vp, C.c_char_p, C.c_uint64, f32p, C.c_uint32, u32p]),
             "mlck_state_create": (C.c_int, [vp, C.c_uint32, u64p, C.c_int, C.POINTER(vp)]),
             "mlck_state_destroy": (C.c_int, [vp]),
@@ -210,6 +212,13 @@ class Context:
     @property
     def kernel_launches(self) -> int:
         return int(lib().mlck_ctx_kernel_launches(self.h))
+
+    def set_fused_pack(self, on: bool):
+        check(lib().mlck_ctx_set_fused_pack(self.h, int(on)))
+
+    def set_replica_mode(self, mode: int):
+        """1: copy engines overlapped with the hash (default); 0: SM stores."""
+        check(lib().mlck_ctx_set_replica_mode(self.h, mode))
 
     def set_timing(self, on: bool):
         check(lib().mlck_ctx_set_timing(self.h, int(on)))

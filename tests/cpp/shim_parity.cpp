@@ -1,0 +1,135 @@
+// shim_parity.cpp -- drives the C++ drop-in (include/moelab_b200) the way the
+// reference's own harness drives moelab (TrainRun, test_recovery.cpp:34-67):
+// one window of sparse snapshots, coverage check, sparse-to-dense conversion.
+// Inputs come from tests/test_cpp_shim.py (golden states/grads of the real
+// reference); outputs are written for byte comparison, plus the reference's
+// error texts for the failure paths.
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <iostream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "moelab_b200/checkpoint.hpp"
+
+using namespace moelab_b200;
+
+namespace {
+struct Reader {
+  std::vector<uint8_t> buf;
+  size_t pos = 0;
+  template <typename T>
+  T get() {
+    T v;
+    std::memcpy(&v, buf.data() + pos, sizeof(T));
+    pos += sizeof(T);
+    return v;
+  }
+  void floats(std::vector<float>& v, size_t n) {
+    v.resize(n);
+    std::memcpy(v.data(), buf.data() + pos, 4 * n);
+    pos += 4 * n;
+  }
+};
+
+void write(const std::string& path, const std::vector<uint8_t>& b) {
+  std::ofstream(path, std::ios::binary).write(reinterpret_cast<const char*>(b.data()), b.size());
+}
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc != 3) {
+    std::fprintf(stderr, "usage: shim_parity <case.bin> <outdir>\n");
+    return 2;
+  }
+  Reader r;
+  {
+    std::ifstream f(argv[1], std::ios::binary);
+    r.buf.assign(std::istreambuf_iterator<char>(f), {});
+  }
+  const std::string out = argv[2];
+  const uint32_t n_ops = r.get<uint32_t>(), cb = r.get<uint32_t>(), W = r.get<uint32_t>();
+  const uint64_t data_seed = r.get<uint64_t>(), ws = r.get<uint64_t>();
+  OptimizerConfig oc;
+  oc.kind = r.get<int32_t>() == 0 ? OptimizerConfig::Kind::Adam : OptimizerConfig::Kind::Sgd;
+  oc.lr = r.get<float>();
+  oc.beta1 = r.get<float>();
+  oc.beta2 = r.get<float>();
+  oc.eps = r.get<float>();
+  std::vector<uint64_t> P(n_ops);
+  for (auto& p : P) p = r.get<uint64_t>();
+  PrecisionPlan plan;
+  plan.compute_bytes = cb;
+
+  Context ctx(0);
+  SparseCheckpoint ckpt;
+  ckpt.window_start = ws;
+  ckpt.wsparse = W;
+  std::vector<ScheduleSlot> slots(W);
+  for (uint32_t k = 0; k < W; ++k) {
+    DeviceState st(ctx, P, static_cast<int>(cb));
+    const uint64_t it = r.get<uint64_t>();
+    for (uint32_t i = 0; i < n_ops; ++i) {
+      OperatorState op;
+      op.step = r.get<uint64_t>();
+      r.floats(op.master, P[i]);
+      r.floats(op.m, P[i]);
+      r.floats(op.v, P[i]);
+      op.has_full_state = true;
+      st.set_op(i, op);
+    }
+    st.set_meta(it, data_seed);
+    auto& sl = slots[k];
+    sl.active.resize(r.get<uint32_t>());
+    for (auto& id : sl.active) id = r.get<uint32_t>();
+    sl.compute_only.resize(r.get<uint32_t>());
+    for (auto& id : sl.compute_only) id = r.get<uint32_t>();
+    // capture_windows (verify.hpp:75-76)
+    ckpt.add_record(take_sparse_snapshot(st, sl, k), plan);
+    write(out + "/blob_" + std::to_string(k) + ".bin",
+          serialize_record(take_sparse_snapshot(st, sl, k), plan, 1, ws, W));
+    if (k == 0) {
+      // reference error paths (test_snapshot.cpp:198-204, 133-143)
+      try {
+        ScheduleSlot bad;
+        bad.active = {n_ops + 7};
+        (void)take_sparse_snapshot(st, bad, 0);
+      } catch (const std::invalid_argument& e) {
+        std::cout << "ERR invalid_argument: " << e.what() << "\n";
+      }
+      auto bytes = ckpt.blobs[0].bytes();
+      bytes[bytes.size() / 2] ^= 0x40;
+      try {
+        (void)parse_record(ctx, bytes, plan);
+      } catch (const std::runtime_error& e) {
+        std::cout << "ERR runtime_error: " << e.what() << "\n";
+      }
+      const ParsedRecord pr = parse_record(ctx, ckpt.blobs[0].bytes(), plan);
+      std::cout << "PARSED iteration " << pr.iteration << " entries " << pr.entries.size() << "\n";
+    }
+  }
+  ckpt.check_coverage(n_ops, plan);
+  std::cout << "complete " << ckpt.complete() << " persisted " << ckpt.persisted() << "\n";
+
+  GradientLog g(ctx, P, W);
+  for (uint32_t s = 1; s <= W; ++s)
+    for (uint32_t i = 0; i < n_ops; ++i) {
+      std::vector<float> gr;
+      r.floats(gr, P[i]);
+      g.put(ws + s, i, gr);
+    }
+  DeviceState conv(ctx, P, static_cast<int>(cb));
+  sparse_to_dense_convert(conv, ckpt, &g, data_seed, oc);
+  write(out + "/conv.bin", conv.serialize_state());
+  try {
+    SparseCheckpoint partial;
+    partial.wsparse = W + 1;
+    sparse_to_dense_convert(conv, partial, &g, data_seed, oc);
+  } catch (const std::runtime_error& e) {
+    std::cout << "ERR runtime_error: " << e.what() << "\n";
+  }
+  std::cout << "OK\n";
+  return 0;
+}
