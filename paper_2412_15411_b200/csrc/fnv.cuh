@@ -394,7 +394,11 @@ __device__ inline bool chunk_contribution(const uint8_t* data, int64_t chunk, ui
         tot[v] = __popc(w1) & 1u;
       }
       const uint32_t map = agg | (tot[0] << 1) | (tot[1] << 2);
-      if (tid == 0) {
+      // The last warp owns the status word and runs the look-back: the
+      // scheduler issues highest-warp-id first, so the critical-path warp is
+      // not starved by compute warps of co-resident work.
+      const bool lb_warp = warp == kWarps - 1;
+      if (lb_warp && lane == 0) {
         status = (status & ~(7u << 20)) | (map << (3 * r)) | (static_cast<uint32_t>(r + 1) << 20);
         // atomic: performed at L2, visible to pollers immediately
         atomicExch(scr.status + chunk * kStatusStride,
@@ -407,7 +411,7 @@ __device__ inline bool chunk_contribution(const uint8_t* data, int64_t chunk, ui
         atomicAdd(scr.prof + 2, static_cast<unsigned long long>(t - t_mark));
         t_mark = t;
       }
-      if (warp == 0) {
+      if (lb_warp) {
         const uint32_t start = look_back2_warp(scr.status, scr.epoch, chunk, r, seed2, scr.prof);
         if (lane == 0) {
           status = (status & ~(7u << 24)) | (map_apply(map, start) << (12 + 2 * r)) |
@@ -472,8 +476,8 @@ __device__ inline bool chunk_contribution(const uint8_t* data, int64_t chunk, ui
       // acc = sum_k d_k P^(64-k) as independent products (no serial Horner):
       // with db = d + 512 >= 0, sum db*Q mod 2^64 = sum mad.wide(db, Q_lo)
       // + 2^32 sum mad.lo(db, Q_hi); the bias is removed once (c_qbias).
-      uint64_t lo = 0;
-      uint32_t hi = 0;
+      uint64_t lo[4] = {0, 0, 0, 0};  // independent chains for ILP
+      uint32_t hi[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
 #pragma unroll
@@ -481,11 +485,12 @@ __device__ inline bool chunk_contribution(const uint8_t* data, int64_t chunk, ui
           const uint32_t b = __byte_perm(w[q], 0, 0x4440 + k);
           const uint32_t z = __byte_perm(zw[q], 0, 0x4440 + k);
           const uint32_t db = b + 512u - 2u * z;
-          lo += static_cast<uint64_t>(db) * c_qlo[4 * q + k];  // mad.wide.u32
-          hi += db * c_qhi[4 * q + k];
+          lo[k] += static_cast<uint64_t>(db) * c_qlo[4 * q + k];  // mad.wide.u32
+          hi[k] += db * c_qhi[4 * q + k];
         }
       }
-      acc = lo + (static_cast<uint64_t>(hi) << 32) - c_qbias;
+      acc = (lo[0] + lo[1]) + (lo[2] + lo[3]) +
+            (static_cast<uint64_t>((hi[0] + hi[1]) + (hi[2] + hi[3])) << 32) - c_qbias;
     } else {
       seg_end = pos0 < n ? n : pos0;
       for (int q = 0; q < 16; ++q)
