@@ -138,6 +138,19 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(kernel):
+    """dram read+write bytes of one launch of `kernel` from the newest committed
+    `ncu --set full` summary (profiles/rNN_ncu_summary.json, scripts/profile.sh)."""
+    pdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+    try:
+        names = sorted(n for n in os.listdir(pdir) if n.endswith("_ncu_summary.json"))
+        with open(os.path.join(pdir, names[-1])) as fh:
+            s = json.load(fh)
+        return float(s["full_captures"][kernel]["traffic_bytes"]), f"profiles/{names[-1]} (one launch)"
+    except (OSError, IndexError, KeyError, ValueError):
+        return None, None
+
+
 # --------------------------------------------------------------------------
 # distributed plumbing
 # --------------------------------------------------------------------------
@@ -355,8 +368,10 @@ def run_ours(args, d: Dist):
     dom = max(("pack", "fnv"), key=lambda k: kernels[k]["ms_avg"])
     kd = kernels[dom]
     ach = kd["bytes_per_launch"] / (kd["ms_avg"] / 1000) / GB
+    traffic, traffic_src = ncu_traffic(dom + "_kernel")
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                "frac": ach / hbm_peak, "peak_kind": peak_kind, "traffic": None,
+                "frac": ach / hbm_peak, "peak_kind": peak_kind, "traffic": traffic,
+                "traffic_source": traffic_src,
                 "per_launch_bytes": kd["bytes_per_launch"],
                 "note": "dominant kernel of the step; the pack kernel alone: kernels['pack']"}
     if d.world > 1:
