@@ -78,10 +78,6 @@ uint64_t mlck_ctx_kernel_launches(mlck_ctx* ctx);
  * fnv_verify, walk, replay).  mlck_ctx_timings synchronizes, returns the
  * labels as CSV and the durations (ms) recorded since the last read. */
 int mlck_ctx_set_timing(mlck_ctx* ctx, int on);
-/* 0 (default): separate pack and FNV kernels; 1: the FNV kernel gathers the
- * record itself and writes it while hashing (one pass, slower today because
- * the hash is latency-bound; kept for ablation). */
-int mlck_ctx_set_fused_pack(mlck_ctx* ctx, int on);
 /* Replica transport: 1 (default) copy engines on a side stream, overlapped
  * with the FNV kernel (peer replicas go over NVLink); 0 remote/local stores
  * issued by the pack kernel. */

@@ -112,7 +112,6 @@ struct mlck_ctx {
     s.used = true;
   }
   uint32_t fnv_epoch = 0;
-  bool fused_pack = false;  // pack + FNV trailer in one kernel (mlck_ctx_set_fused_pack)
   // Replica transport: 1 = copy engines on a side stream, overlapping the FNV
   // kernel (default); 0 = remote stores issued by the pack kernel itself.
   int replica_mode = 1;
@@ -274,19 +273,6 @@ void run_pack(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
   for (auto& r : out->replicas) d.p[d.n++] = r.first;
   const auto* segs = reinterpret_cast<const pack::Segment*>(s.dev);
   const int n_segs = static_cast<int>(b.segs.size());
-  if (trailer && ctx->fused_pack && body) {
-    // one pass: gather + local/peer stores + FNV trailer
-    TrailerDsts t{};
-    for (int r = 0; r < d.n; ++r) t.p[r] = d.p[r] + body;
-    t.n = d.n;
-    uint32_t* scratch = ctx->fnv_scratch_for(body);
-    const int tf = ctx->tbegin("pack_fnv");
-    launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream,
-               nullptr, nullptr, segs, n_segs, &d);
-    ctx->tend(tf);
-    ctx->launches += 1;
-    return;
-  }
   if (trailer && ctx->replica_mode == 1 && !out->replicas.empty() && body) {
     // pack the local record; push it to every replica with the copy engines
     // (NVLink for peers) on the side stream while the FNV kernel hashes it;
@@ -594,9 +580,6 @@ int mlck_ctx_synchronize(mlck_ctx* c) {
 }
 uint64_t mlck_ctx_kernel_launches(mlck_ctx* c) { return c ? c->launches : 0; }
 
-int mlck_ctx_set_fused_pack(mlck_ctx* c, int on) {
-  return api([&] { c->fused_pack = on != 0; });
-}
 
 int mlck_ctx_set_replica_mode(mlck_ctx* c, int mode) {
   return api([&] {
@@ -917,16 +900,15 @@ int mlck_fnv1a64(mlck_ctx* ctx, const void* ptr, uint64_t n, uint64_t seed, uint
   });
 }
 
-// FNV with the kernel's profile counters (development aid): counters =
-// [look-back probes, spin re-reads, cycles before look-backs, cycles in
-// look-backs, cycles in phase B, chunks], cycles summed over chunks (thread 0).
+// FNV with the kernel's profile counters (development aid): 16 counters, see
+// fnv::Scratch::prof (fnv.cuh).
 int mlck_fnv1a64_profile(mlck_ctx* ctx, const void* ptr, uint64_t n, uint64_t seed, uint64_t* out,
                          uint64_t* counters, uint64_t* trace_host) {
   return api([&] {
     ctx->activate();
     unsigned long long* prof = nullptr;
-    MLCK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&prof), 8 * 8, ctx->stream));
-    MLCK_CUDA(cudaMemsetAsync(prof, 0, 8 * 8, ctx->stream));
+    MLCK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&prof), 16 * 8, ctx->stream));
+    MLCK_CUDA(cudaMemsetAsync(prof, 0, 16 * 8, ctx->stream));
     TrailerDsts none{};
     unsigned long long* trace = nullptr;
     const uint64_t tb = fnv_chunks(n) * 12 * 8;
@@ -944,7 +926,7 @@ int mlck_fnv1a64_profile(mlck_ctx* ctx, const void* ptr, uint64_t n, uint64_t se
     }
     MLCK_CUDA(cudaMemcpyAsync(ctx->host_results, ctx->results, 8, cudaMemcpyDeviceToHost,
                               ctx->stream));
-    MLCK_CUDA(cudaMemcpyAsync(counters, prof, 6 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    MLCK_CUDA(cudaMemcpyAsync(counters, prof, 16 * 8, cudaMemcpyDeviceToHost, ctx->stream));
     MLCK_CUDA(cudaFreeAsync(prof, ctx->stream));
     MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
     *out = ctx->host_results[0];

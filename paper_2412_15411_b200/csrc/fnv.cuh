@@ -4,20 +4,39 @@
 // both the pack path (serialize_record trailer, snapshot.hpp:142) and the
 // verify path (parse_record, snapshot.hpp:156-163).
 //
-// Decomposition (verified in tests/test_fnv_model.py):
-//   h_{i+1} = (h_i ^ b_i) * P  ==  (h_i + d_i) * P,  d_i = (u_i ^ b_i) - u_i,
-//   u_i = low byte of h_i, so  h_N = P^N h_0 + sum_i d_i P^(N-i)  (mod 2^64).
-// The only sequential part is the 8-bit automaton u' = ((u ^ b) * 0xb3) & 255.
-// It is a T-function: bit j of u' depends on bits <= j only, and
-//   u'_j = u_j ^ b_j ^ R_j(y_0..y_{j-1}),   y = u ^ b,
-// where R_j is the carry/sum of the lower columns of y*0xb3 (0xb3 = shifts
-// {0,1,4,5,7}).  So each bit level is a prefix-XOR over positions once the
-// lower levels are known.  Positions are bit-sliced 32 per word (an 8x8 bit
-// transpose per byte lane), every level is a word-parallel prefix-XOR, and the
-// chunk-to-chunk carry of each level is resolved with a decoupled look-back
-// (one status word per chunk carries 8 aggregate bits and 8 inclusive bits).
-// After the 8 levels every position knows u_i; d_i = b_i - 2 (u_i & b_i) and
-// the polynomial sum is a per-thread Horner combined with precomputed powers.
+// Algebra.  h_{i+1} = (h_i ^ b_i) * P with P = 2^40 + 0x1b3.  Since b_i < 256
+// the xor only touches the low byte u_i of h_i, so over a segment of L bytes
+//   FNV_seg(H) = FNV_seg(u) + P^L (H - u),      u = H & 0xff,
+// i.e. once every segment knows the low byte of the hash at its start, the
+// segments hash independently (the real recurrence, started from h = u) and
+// combine linearly:  h_N = P^N (H_0 & ~0xff) + sum_s P^(N - end_s) (g_s & ~0xff)
+// + u_N.  The only sequential part is the 8-bit automaton
+//   u' = ((u ^ b) * 0xb3) & 0xff,
+// a T-function (bit j of u' depends on bits <= j of u only).
+//
+// Resolving the automaton.  Four look-back rounds resolve two state bits
+// each.  In round r every 32-byte segment already knows its start bits
+// < 2r and runs the automaton itself -- byte-serial, several start variants
+// packed in SIMD lanes of one register -- from start bit 2r = 0 and 1.  Its
+// effect on bits (2r, 2r+1) is the map
+//   s0' = s0 ^ a,   s1' = s1 ^ (s0 ? b1 : b0)            ({a,b0,b1}, 3 bits)
+// a family closed under composition.  Maps are scanned across the segments
+// of a chunk with three ballots per warp (a is xor-linear; the b toggles are
+// xor-linear once the prefix of a is known), across the warps of the CTA by a
+// dedicated look-back warp, and across chunks by a decoupled look-back over
+// one status word per chunk.  Rounds 0-1 need only the low 2/4 bits (the
+// multiplier is 3 mod 16), so four variants share one register in 8-bit
+// lanes; rounds 2-3 use 16-bit lanes (two variants per register).  Cost:
+// 1.5 + 1.5 + 2.5 + 2.5 integer ops per byte, then ~4.5 for the final pass,
+// split between the ALU and FMA pipes.
+//
+// Latency.  Each CTA keeps kSlots chunks in flight (their bytes in shared
+// memory, refilled with cp.async) and its compute warps visit them
+// round-robin; each compute thread owns kSegs consecutive 32-byte segments of
+// a chunk, so the per-round scan and hand-off amortise over 128 bytes.  Every slot has its own look-back warp, which folds the warp
+// maps of the slot's round, publishes it and looks back while the compute
+// warps work on the other slots: a look-back has kSlots-1 slot turns to
+// complete before its result is needed.
 #pragma once
 
 #include "mlck_common.cuh"
@@ -27,35 +46,47 @@ namespace fnv {
 
 constexpr uint64_t kPrime = 0x100000001b3ull;
 constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
-#ifndef MLCK_FNV_THREADS
-#define MLCK_FNV_THREADS 1024
+#ifndef MLCK_FNV_SLOTS
+#define MLCK_FNV_SLOTS 3
 #endif
-constexpr int kThreads = MLCK_FNV_THREADS;  // one CTA per SM at 64 regs/thread
-constexpr int kBytesPerThread = 64;  // two 32-position groups
-constexpr int kChunk = kThreads * kBytesPerThread;
-constexpr int kWarps = kThreads / 32;
-
-// One 64-bit look-back word per chunk, kStatusStride words apart (256 B): the
-// ~600 in-flight chunks' words land in different L2 slices instead of a
-// handful of hot lines.  The high half is the launch epoch, so the array is
-// never cleared between launches (a word from an older launch reads as
-// "nothing published").
+#ifndef MLCK_FNV_WARPS
+#define MLCK_FNV_WARPS 14
+#endif
+constexpr int kSlots = MLCK_FNV_SLOTS;         // chunks in flight per CTA
+constexpr int kComputeWarps = MLCK_FNV_WARPS;  // + one look-back warp per slot
+constexpr int kWarps = kComputeWarps + kSlots;
+constexpr int kThreads = 32 * kWarps;
+constexpr int kComputeThreads = 32 * kComputeWarps;
+constexpr int kBarThreads = kComputeThreads + 32;  // named barriers: compute warps + one look-back warp
+constexpr int kSegs = 4;                           // 32-byte segments per thread
+constexpr int kThreadBytes = 32 * kSegs;
+constexpr int kThreadWords = kThreadBytes / 4;
+constexpr int kChunk = kComputeThreads * kThreadBytes;  // 57,344 bytes by default
+constexpr int kRounds = 4;
+static_assert(kSegs % 2 == 0, "segments are processed in pairs");
+// One 64-bit look-back word per chunk, kStatusStride words apart (256 B) so
+// the in-flight chunks' words land in different L2 slices.  The high half is
+// the launch epoch, so the array is never cleared between launches.
 constexpr int kStatusStride = 32;
+constexpr uint32_t kSpinLimit = 1u << 24;  // watchdog: never hang the GPU
 
 struct Scratch {
   unsigned long long* status;  // [n_chunks * kStatusStride] epoch-tagged words
   uint32_t epoch;              // this launch's tag (>= 1)
-  uint32_t* ticket;            // chunk dispatch counter (zeroed per launch)
-  unsigned long long* accum;   // sum of chunk terms
-  uint32_t* finished;          // completed-chunk counter
+  unsigned long long* accum;   // sum of chunk terms (inverse-power frame)
+  uint32_t* finished;          // completed-CTA counter
+  uint32_t* ulast;             // low byte of the final hash
+  uint32_t* error;             // watchdog tripped (look-back never resolved)
   unsigned long long* result;  // final 64-bit hash
-  // optional profile counters (null = off): [0] look-back probes,
-  // [1] spin re-reads, [2] cycles before look-backs, [3] cycles in
-  // look-backs, [4] cycles in phase B, [5] chunks
+  // optional profile counters (null = off): [0] look-back probes, [1] spin
+  // re-reads, compute thread 0 of each CTA: [2] cycles in rounds, [3] cycles
+  // waiting for look-back results, [4] final passes + refills, [6] other;
+  // [5] chunks; look-back warps (lane 0): [8] idle at PUB, [9] probe loads,
+  // [10] spins, [11] compose, [12] publish + hand-off, [13] total
   unsigned long long* prof;
   // optional per-chunk trace (null = off): 12 words per chunk, %globaltimer
-  // ns at [0] start, [1+2r] map published, [2+2r] round resolved, [9] end,
-  // [10] smid
+  // ns at [0] round-0 start, [1+2r] map published, [2+2r] round resolved,
+  // [9] final pass done, [10] smid
   unsigned long long* trace;
 };
 
@@ -70,17 +101,8 @@ __device__ __forceinline__ uint32_t smid() {
   return r;
 }
 
-// P^(64 k) for k = 0..kThreads-1, written by init_constants() (kernels.cu).
-__constant__ unsigned long long c_pow64[kThreads];
-// Q_k = P^(64-k) for a thread segment, split into 32-bit halves, and
-// 512 * sum_k Q_k (the bias of the unsigned per-byte terms).
-__constant__ uint32_t c_qlo[kBytesPerThread];
-__constant__ uint32_t c_qhi[kBytesPerThread];
-__constant__ unsigned long long c_qbias;
-__host__ __device__ inline uint64_t mul_p(uint64_t x) { return x * kPrime; }
-
-__host__ __device__ inline uint64_t pow_p(uint64_t e) {
-  uint64_t r = 1, b = kPrime;
+__host__ __device__ constexpr uint64_t pow_u64(uint64_t b, uint64_t e) {
+  uint64_t r = 1;
   while (e) {
     if (e & 1) r *= b;
     b *= b;
@@ -88,112 +110,40 @@ __host__ __device__ inline uint64_t pow_p(uint64_t e) {
   }
   return r;
 }
+__host__ __device__ constexpr uint64_t pow_p(uint64_t e) { return pow_u64(kPrime, e); }
+// P is odd, so it is a unit mod 2^64 (Newton: x <- x (2 - P x), 5 doublings).
+__host__ __device__ constexpr uint64_t inv_odd(uint64_t a) {
+  uint64_t x = a;  // correct to 3 bits
+  for (int i = 0; i < 5; ++i) x *= 2 - a * x;
+  return x;
+}
+constexpr uint64_t kPrimeInv = inv_odd(kPrime);
+static_assert(kPrime * kPrimeInv == 1ull, "P^-1 mod 2^64");
+constexpr uint64_t kPow32 = pow_p(32);
 
-// ---- bit-slice transposes ----------------------------------------------
-__device__ __forceinline__ void swapmove(uint32_t& a, uint32_t& b, uint32_t mask, int n) {
-  const uint32_t t = ((a >> n) ^ b) & mask;
-  b ^= t;
-  a ^= t << n;
-}
-__device__ __forceinline__ void bit_transpose8(uint32_t x[8]) {
-#pragma unroll
-  for (int i = 0; i < 8; i += 2) swapmove(x[i], x[i + 1], 0x55555555u, 1);
-#pragma unroll
-  for (int i : {0, 1, 4, 5}) swapmove(x[i], x[i + 2], 0x33333333u, 2);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) swapmove(x[i], x[i + 4], 0x0f0f0f0fu, 4);
-}
-// 32 bytes (word q byte k = position 4q+k) -> 8 planes (bit p = position p).
-__device__ __forceinline__ void to_planes(const uint32_t w[8], uint32_t x[8]) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int a = i >> 2, k = i & 3;
-    const uint32_t sel = k | ((k + 4) << 4);
-    const uint32_t lo = __byte_perm(w[a], w[a + 2], sel);
-    const uint32_t hi = __byte_perm(w[a + 4], w[a + 6], sel);
-    x[i] = __byte_perm(lo, hi, 0x5410);
-  }
-  bit_transpose8(x);
-}
-// inverse of to_planes
-__device__ __forceinline__ void from_planes(uint32_t x[8], uint32_t w[8]) {
-  bit_transpose8(x);
-  // w[q] byte k = position 4q+k = x[(4q+k)&7] byte ((4q+k)>>3)
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int lane = q >> 1;            // (4q+k)>>3 for k=0..3
-    const int i0 = (4 * q) & 7;         // x index of k=0
-    const uint32_t s = lane | ((lane + 4) << 4);
-    const uint32_t lo = __byte_perm(x[i0], x[i0 + 1], s);
-    const uint32_t hi = __byte_perm(x[i0 + 2], x[i0 + 3], s);
-    w[q] = __byte_perm(lo, hi, 0x5410);
-  }
+static_assert(kWarps <= 32, "one look-back warp per slot");
+__host__ __device__ constexpr int lookback_warp(int s) { return kComputeWarps + s; }
+// index of a compute warp among the compute warps, -1 for a look-back warp
+__host__ __device__ constexpr int compute_warp(int warp) { return warp < kComputeWarps ? warp : -1; }
+
+// P^-(c * kChunk) as a product of three table entries (init_constants)
+__constant__ unsigned long long c_wchunk[3][1024];
+__device__ __forceinline__ uint64_t chunk_weight(int64_t c) {
+  return c_wchunk[0][c & 1023] * c_wchunk[1][(c >> 10) & 1023] * c_wchunk[2][(c >> 20) & 1023];
 }
 
-__device__ __forceinline__ uint32_t prefix_xor(uint32_t t) {
-  t ^= t << 1;
-  t ^= t << 2;
-  t ^= t << 4;
-  t ^= t << 8;
-  t ^= t << 16;
-  return t;
-}
-__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) {
-  return (a & b) | (c & (a | b));
-}
-__device__ __forceinline__ uint32_t bcast(uint32_t bit) { return 0u - bit; }
-
-// Column-carry state of y*0xb3 for one 32-position group.
-struct Carries {
-  uint32_t c1, c2, c3, c4a, c4b, k5a, k5b, k5c, m6a, m6b, m6c;
-};
-
-// R_j: contribution of y_0..y_{j-1} (and lower carries) to bit j of y*0xb3.
-__device__ __forceinline__ uint32_t level_r(int j, const uint32_t y[8], const Carries& c) {
-  switch (j) {
-    case 0: return 0u;
-    case 1: return y[0];
-    case 2: return y[1] ^ c.c1;
-    case 3: return y[2] ^ c.c2;
-    case 4: return y[3] ^ y[0] ^ c.c3;
-    case 5: return y[4] ^ y[1] ^ y[0] ^ c.c4a ^ c.c4b;
-    case 6: return y[5] ^ y[2] ^ y[1] ^ c.k5a ^ c.k5b ^ c.k5c;
-    default: return y[6] ^ y[3] ^ y[2] ^ y[0] ^ c.m6a ^ c.m6b ^ c.m6c;
-  }
-}
-// After y_j is known: compress column j of y*0xb3 into carries for j+1.
-__device__ __forceinline__ void level_carry(int j, const uint32_t y[8], Carries& c) {
-  switch (j) {
-    case 1: c.c1 = y[1] & y[0]; break;
-    case 2: c.c2 = maj3(y[2], y[1], c.c1); break;
-    case 3: c.c3 = maj3(y[3], y[2], c.c2); break;
-    case 4: {
-      const uint32_t s = y[4] ^ y[3] ^ y[0];
-      c.c4a = maj3(y[4], y[3], y[0]);
-      c.c4b = s & c.c3;
-    } break;
-    case 5: {
-      const uint32_t s5a = y[5] ^ y[4] ^ y[1];
-      const uint32_t s5b = y[0] ^ c.c4a ^ c.c4b;
-      c.k5a = maj3(y[5], y[4], y[1]);
-      c.k5b = maj3(y[0], c.c4a, c.c4b);
-      c.k5c = s5a & s5b;
-    } break;
-    case 6: {
-      const uint32_t s6a = y[6] ^ y[5] ^ y[2];
-      const uint32_t s6b = y[1] ^ c.k5a ^ c.k5b;
-      c.m6a = maj3(y[6], y[5], y[2]);
-      c.m6b = maj3(y[1], c.k5a, c.k5b);
-      c.m6c = maj3(s6a, s6b, c.k5c);
-    } break;
-    default: break;
-  }
+// One step of the real recurrence on h = hi:lo (b < 256):
+// lo' = lo*0x1b3, hi' = hi*0x1b3 + carry + (lo << 8).
+__device__ __forceinline__ void fnv_byte(uint32_t& lo, uint32_t& hi, uint32_t b) {
+  lo ^= b;
+  const uint64_t t = static_cast<uint64_t>(lo) * 0x1b3u;
+  uint32_t f;
+  asm("mad.lo.u32 %0, %1, 256, %2;" : "=r"(f) : "r"(lo), "r"(static_cast<uint32_t>(t >> 32)));
+  asm("mad.lo.u32 %0, %1, 0x1b3, %2;" : "=r"(hi) : "r"(hi), "r"(f));
+  lo = static_cast<uint32_t>(t);
 }
 
-// Two bit levels (2r, 2r+1) are resolved per look-back round.  A chunk's
-// effect on those two state bits, given its true lower start bits, is the map
-//   s0' = s0 ^ a,   s1' = s1 ^ (s0 ? b1 : b0)
-// packed as bits {a, b0, b1}; the family is closed under composition.
+// ---- 2-bit maps {a, b0, b1} -----------------------------------------------
 __device__ __forceinline__ uint32_t map_compose(uint32_t g, uint32_t f) {  // g o f
   const uint32_t af = f & 1u, b0f = (f >> 1) & 1u, b1f = (f >> 2) & 1u;
   const uint32_t ag = g & 1u, b0g = (g >> 1) & 1u, b1g = (g >> 2) & 1u;
@@ -205,73 +155,150 @@ __device__ __forceinline__ uint32_t map_apply(uint32_t m, uint32_t s) {
   const uint32_t s0 = s & 1u, s1 = (s >> 1) & 1u;
   return (s0 ^ (m & 1u)) | ((s1 ^ ((m >> (1 + s0)) & 1u)) << 1);
 }
+// Warp-wide exclusive scan of per-lane maps (lane 0 first).  Returns the
+// lane's exclusive prefix map; *total = the composition of all 32.
+__device__ __forceinline__ uint32_t map_scan_warp(uint32_t m, uint32_t* total) {
+  const uint32_t lt = (1u << (threadIdx.x & 31)) - 1u;
+  const uint32_t bal_a = __ballot_sync(0xffffffffu, m & 1u);
+  const uint32_t ea = __popc(bal_a & lt) & 1u;
+  const uint32_t b0 = (m >> 1) & 1u, b1 = (m >> 2) & 1u;
+  // toggle of state bit 1 here, for chunk-start s0 = 0 and s0 = 1
+  const uint32_t bal0 = __ballot_sync(0xffffffffu, ea ? b1 : b0);
+  const uint32_t bal1 = __ballot_sync(0xffffffffu, ea ? b0 : b1);
+  *total = (__popc(bal_a) & 1u) | ((__popc(bal0) & 1u) << 1) | ((__popc(bal1) & 1u) << 2);
+  return ea | ((__popc(bal0 & lt) & 1u) << 1) | ((__popc(bal1 & lt) & 1u) << 2);
+}
 
-// Status word of a chunk: bits [3r,3r+3) the round-r map, [12+2r,14+2r) the
-// round-r inclusive end bits, [20,23) rounds with map published, [24,27)
-// rounds with inclusive published.
-constexpr int kRounds = 4;
-__device__ __forceinline__ uint32_t st_nagg(uint32_t s) { return (s >> 20) & 7u; }
-__device__ __forceinline__ uint32_t st_nincl(uint32_t s) { return (s >> 24) & 7u; }
+// ---- round r of one thread: the maps of its kSegs segments (segment i =
+// words w[8i..8i+7]) on state bits (2r, 2r+1), given their start bits < 2r
+// (st byte i).  Segments are processed in pairs sharing one byte-select.
+// Rounds 0-1 track the state mod 4 / mod 16 only (0xb3 = 3 mod 16) in 8-bit
+// lanes {S2p v0, S2p+1 v0, S2p v1, S2p+1 v1} (each < 46 after the multiply);
+// rounds 2-3 track the full byte in 16-bit lanes {S2p, S2p+1}, one register
+// per start variant.
+__device__ __forceinline__ void round_maps_low(const uint32_t (&w)[kThreadWords], uint32_t st, int r,
+                                               uint32_t (&map)[kSegs]) {
+  const uint32_t bit = 1u << (2 * r);
+  const uint32_t M = r == 0 ? 0x03030303u : 0x0f0f0f0fu;
+  uint32_t x[kSegs / 2];
+#pragma unroll
+  for (int p = 0; p < kSegs / 2; ++p) {
+    const uint32_t a = (st >> (16 * p)) & (bit - 1u), b = (st >> (16 * p + 8)) & (bit - 1u);
+    x[p] = a | (b << 8) | ((a | bit) << 16) | ((b | bit) << 24);
+  }
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t sel = (k & 3) | ((4 + (k & 3)) << 4) | ((k & 3) << 8) | ((4 + (k & 3)) << 12);
+#pragma unroll
+    for (int p = 0; p < kSegs / 2; ++p) {
+      const uint32_t y = __byte_perm(w[16 * p + (k >> 2)], w[16 * p + 8 + (k >> 2)], sel);
+      x[p] = ((x[p] ^ y) & M) * 3u;
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < kSegs / 2; ++p) {
+    const uint32_t e = x[p] >> (2 * r);  // lane bytes: bit0 = a, bit1 = b (of each variant)
+    map[2 * p] = (e & 3u) | (((e >> 16) & 2u) << 1);
+    map[2 * p + 1] = ((e >> 8) & 3u) | (((e >> 24) & 2u) << 1);
+  }
+}
+__device__ __forceinline__ void round_maps_high(const uint32_t (&w)[kThreadWords], uint32_t st, int r,
+                                                uint32_t (&map)[kSegs]) {
+  const uint32_t bit = 1u << (2 * r);
+  constexpr uint32_t M = 0x00ff00ffu;
+  uint32_t x0[kSegs / 2], x1[kSegs / 2];
+#pragma unroll
+  for (int p = 0; p < kSegs / 2; ++p) {
+    const uint32_t a = (st >> (16 * p)) & (bit - 1u), b = (st >> (16 * p + 8)) & (bit - 1u);
+    x0[p] = a | (b << 16);
+    x1[p] = x0[p] | bit | (bit << 16);
+  }
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t sel = (k & 3) | ((4 + (k & 3)) << 8);
+#pragma unroll
+    for (int p = 0; p < kSegs / 2; ++p) {
+      const uint32_t y = __byte_perm(w[16 * p + (k >> 2)], w[16 * p + 8 + (k >> 2)], sel);
+      x0[p] = ((x0[p] ^ y) & M) * 0xb3u;
+      x1[p] = ((x1[p] ^ y) & M) * 0xb3u;
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < kSegs / 2; ++p) {
+    const uint32_t e0 = x0[p] >> (2 * r), e1 = x1[p] >> (2 * r);
+    map[2 * p] = (e0 & 3u) | ((e1 & 2u) << 1);
+    map[2 * p + 1] = ((e0 >> 16) & 3u) | (((e1 >> 16) & 2u) << 1);
+  }
+}
 
-struct SharedState {
-  uint32_t sa[kWarps];      // level-2r thread-parity scan
-  uint32_t sb[2][kWarps];   // level-2r+1 scan, per variant
-  uint32_t start;           // resolved start bits of the round
-  unsigned long long pc;    // P^(N - chunk_end); final hash in the last block
-  unsigned long long red[kWarps];
-};
-
-// Look-back for round r, run by warp 0 alone: lane l probes the 8
-// predecessors base-8l .. base-8l-7 with all 8 loads in flight, so one probe
-// covers 256 chunks (more than the in-flight window) at one load latency.
-// Returns the chunk's two start bits (in warp 0).
+// Look-back for round r of `chunk` (one warp): lane l reads the 8
+// predecessors base-8l .. base-8l-7 with all loads in flight.  If an entry
+// nearer than the nearest inclusive one is not published yet, the whole
+// window is re-read (one round trip per retry, not one per stale entry).
+// Returns the chunk's two start bits.
 constexpr int kProbePerLane = 8;
-__device__ __forceinline__ uint32_t look_back2_warp(const unsigned long long* status,
-                                                    uint32_t epoch, int64_t chunk, int r,
-                                                    uint32_t seed2, unsigned long long* prof) {
+__device__ __forceinline__ uint32_t look_back2_warp(const Scratch& scr, int64_t chunk, int r,
+                                                    uint32_t seed2, long long* lap = nullptr) {
   const int lane = threadIdx.x & 31;
+  auto mark = [&](int bucket) {
+    if (lap) {
+      const long long now = clock64();
+      lap[bucket] += now - lap[0];
+      lap[0] = now;
+    }
+  };
   uint32_t acc = 0;  // identity map
   int64_t base = chunk - 1;
+  uint32_t retries = 0;
   while (true) {
-    if (prof && lane == 0) atomicAdd(prof + 0, 1ull);
+    if (scr.prof && lane == 0) atomicAdd(scr.prof + 0, 1ull);
     unsigned long long v[kProbePerLane];
+    uint32_t m, incl_val;
+    int first;
+    while (true) {
 #pragma unroll
-    for (int q = 0; q < kProbePerLane; ++q) {
-      const int64_t k = base - kProbePerLane * lane - q;
-      v[q] = k < 0 ? 0ull : ld_relaxed_gpu_u64(status + k * kStatusStride);
-    }
-    // lane-local: nearest-first composition up to the first inclusive
-    uint32_t m = 0, incl_val = 0;
-    bool has_incl = false;
+      for (int q = 0; q < kProbePerLane; ++q) {
+        const int64_t k = base - kProbePerLane * lane - q;
+        v[q] = k < 0 ? 0ull : ld_relaxed_gpu_u64(scr.status + k * kStatusStride);
+      }
+      // nearest-first: compose aggregates up to the first inclusive entry,
+      // stop at the first unpublished one
+      m = 0;
+      incl_val = 0;
+      bool has_incl = false, blocked = false;
 #pragma unroll
-    for (int q = 0; q < kProbePerLane; ++q) {
-      if (has_incl) continue;
-      const int64_t k = base - kProbePerLane * lane - q;
-      if (k < 0) {
-        has_incl = true;
-        incl_val = seed2;
-        continue;
+      for (int q = 0; q < kProbePerLane; ++q) {
+        if (has_incl || blocked) continue;
+        const int64_t k = base - kProbePerLane * lane - q;
+        if (k < 0) {
+          has_incl = true;
+          incl_val = seed2;
+          continue;
+        }
+        const uint32_t s = static_cast<uint32_t>(v[q]);
+        if (static_cast<uint32_t>(v[q] >> 32) != scr.epoch || ((s >> 20) & 7u) <= static_cast<uint32_t>(r)) {
+          blocked = true;
+        } else if (((s >> 24) & 7u) > static_cast<uint32_t>(r)) {
+          has_incl = true;
+          incl_val = (s >> (12 + 2 * r)) & 3u;
+        } else {
+          m = map_compose(m, (s >> (3 * r)) & 7u);  // the farther map applies first
+        }
       }
-      uint32_t s;
-      uint32_t backoff = 32, spins = 0;
-      // back off while the predecessor is behind (keeps pollers off L2)
-      while (static_cast<uint32_t>(v[q] >> 32) != epoch ||
-             st_nagg(s = static_cast<uint32_t>(v[q])) <= static_cast<uint32_t>(r)) {
-        __nanosleep(backoff);
-        backoff = backoff < 256 ? 2 * backoff : 256;
-        v[q] = ld_relaxed_gpu_u64(status + k * kStatusStride);
-        ++spins;
+      const uint32_t bal = __ballot_sync(0xffffffffu, has_incl);
+      const uint32_t blk = __ballot_sync(0xffffffffu, blocked);
+      first = bal ? __ffs(bal) - 1 : 32;
+      const int first_blk = blk ? __ffs(blk) - 1 : 32;
+      if (first_blk >= first) break;  // everything up to the inclusive entry is published
+      if (++retries > kSpinLimit) {   // never resolves: flag it and stop waiting
+        if (lane == 0) atomicExch(scr.error, 1u);
+        first = 0;
+        break;
       }
-      if (prof && spins) atomicAdd(prof + 1, static_cast<unsigned long long>(spins));
-      if (st_nincl(s) > static_cast<uint32_t>(r)) {
-        has_incl = true;
-        incl_val = (s >> (12 + 2 * r)) & 3u;
-      } else {
-        m = map_compose(m, (s >> (3 * r)) & 7u);  // apply the farther map first
-      }
+      __nanosleep(32);
     }
-    const uint32_t bal = __ballot_sync(0xffffffffu, has_incl);
-    const int first = bal ? __ffs(bal) - 1 : 32;
+    mark(3);
+    if (scr.prof && lane == 0 && retries) atomicAdd(scr.prof + 1, static_cast<unsigned long long>(retries));
     // L_0 o L_1 o ... o L_first (lanes past the nearest inclusive: identity)
     uint32_t t = lane <= first ? m : 0u;
 #pragma unroll
@@ -281,260 +308,96 @@ __device__ __forceinline__ uint32_t look_back2_warp(const unsigned long long* st
     }
     t = __shfl_sync(0xffffffffu, t, 0);
     acc = map_compose(acc, t);
-    if (bal) return map_apply(acc, __shfl_sync(0xffffffffu, incl_val, first));
+    if (first < 32) {
+      const uint32_t res = map_apply(acc, __shfl_sync(0xffffffffu, incl_val, first));
+      mark(4);
+      return res;
+    }
     base -= 32 * kProbePerLane;
+    retries = 0;
   }
 }
 
-constexpr int kGroups = kBytesPerThread / 32;
+// ---- shared memory ----------------------------------------------------------
+struct alignas(16) Shared {
+  uint4 data[kSlots][kComputeThreads * kThreadBytes / 16];  // thread t: 8 swizzled granules
+  unsigned long long mbar[kSlots];                          // slot data landed (cp.async)
+  uint32_t wmap[kSlots][32];    // warp maps of the round (compute -> look-back)
+  uint32_t wstart[kSlots][32];  // warp start bits (look-back -> compute)
+  unsigned long long red[32];
+};
+constexpr size_t kSmemBytes = sizeof(Shared);
+static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
 
-// 64 bytes at pos0 as 16 little-endian words, zero past n.
-__device__ __forceinline__ void load_words64(const uint8_t* data, uint64_t n, uint64_t pos0,
-                                             uint32_t (&w)[16]) {
-  if (pos0 + 64 <= n && (reinterpret_cast<uintptr_t>(data) & 15u) == 0) {
+// conflict-free 128-bit reads: lanes 8m..8m+7 hit 8 distinct granules mod 8
+constexpr int kGranules = kThreadBytes / 16;
+__device__ __forceinline__ int granule(int t, int q) { return kGranules * t + ((q + t) & (kGranules - 1)); }
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* m, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_addr(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* m) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.shared.b64 st, [%0]; }" ::"r"(smem_addr(m)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, uint32_t parity) {
+  asm volatile(
+      "{ .reg .pred p; W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1; @!p bra W; }" ::"r"(
+          smem_addr(m)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(unsigned long long* m) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_addr(m)) : "memory");
+}
+
+// Thread t's bytes of `chunk` into its slot granules, zero past n; one
+// arrival on the slot's mbarrier when they have landed.
+__device__ __forceinline__ void load_thread(Shared& sh, int slot, int t, const uint8_t* data,
+                                            uint64_t n, int64_t chunk) {
+  const uint64_t p = static_cast<uint64_t>(chunk) * kChunk + static_cast<uint64_t>(t) * kThreadBytes;
+  uint4* dst = sh.data[slot];
+  if (p + kThreadBytes <= n && (reinterpret_cast<uintptr_t>(data) & 15u) == 0) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint4 v = *reinterpret_cast<const uint4*>(data + pos0 + 16 * q);
-      w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
-    }
+    for (int q = 0; q < kGranules; ++q) cp_async16(dst + granule(t, q), data + p + 16 * q);
+    cp_async_arrive(&sh.mbar[slot]);
   } else {
+    for (int q = 0; q < kGranules; ++q) {
+      uint32_t v[4];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      uint32_t x = 0;
-      for (int k = 0; k < 4; ++k) {
-        const uint64_t p = pos0 + 4 * q + k;
-        if (p < n) x |= static_cast<uint32_t>(data[p]) << (8 * k);
+      for (int i = 0; i < 4; ++i) {
+        uint32_t x = 0;
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t b = p + 16 * q + 4 * i + k;
+          if (b < n) x |= static_cast<uint32_t>(data[b]) << (8 * k);
+        }
+        v[i] = x;
       }
-      w[q] = x;
+      dst[granule(t, q)] = make_uint4(v[0], v[1], v[2], v[3]);
     }
+    mbar_arrive(&sh.mbar[slot]);
   }
 }
-
-// Block-level FNV contribution of one kChunk-byte chunk of `data`; thread t
-// owns bytes [chunk*kChunk + 64t, +64).  The chunk's term P^(N-end) * H is
-// atomically accumulated into scr.accum; the last chunk to finish writes the
-// final hash into scr.result (and sh.pc) and returns true in thread 0.
-__device__ inline bool chunk_contribution(const uint8_t* data, int64_t chunk, uint64_t n,
-                                          uint64_t seed, const Scratch& scr, uint64_t n_chunks,
-                                          SharedState& sh) {
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const uint32_t lt = (1u << lane) - 1u;
-  const uint64_t pos0 = static_cast<uint64_t>(chunk) * kChunk + static_cast<uint64_t>(tid) * kBytesPerThread;
-
-  uint32_t B[kGroups][8], Y[kGroups][8];
-  Carries car[kGroups];
-  {
-    uint32_t w[16];
-    load_words64(data, n, pos0, w);
+__device__ __forceinline__ void read_thread(const Shared& sh, int slot, int t, uint32_t (&w)[kThreadWords]) {
 #pragma unroll
-    for (int g = 0; g < kGroups; ++g) to_planes(w + 8 * g, B[g]);
+  for (int q = 0; q < kGranules; ++q) {
+    const uint4 v = sh.data[slot][granule(t, q)];
+    w[4 * q] = v.x;
+    w[4 * q + 1] = v.y;
+    w[4 * q + 2] = v.z;
+    w[4 * q + 3] = v.w;
   }
-  // Positions past n are zero bytes; d_i is forced to zero for them below and
-  // only the final chunk is padded, so its trailing states are never used.
-
-  __syncthreads();  // previous chunk's readers of sh are done
-  uint32_t status = 0;  // owner's view (thread 0)
-  long long t_mark = scr.prof ? clock64() : 0;
-  if (scr.trace && tid == 0) {
-    scr.trace[chunk * 12 + 0] = gtimer();
-    scr.trace[chunk * 12 + 10] = smid();
-  }
-#pragma unroll
-  for (int r = 0; r < kRounds; ++r) {
-    const int j0 = 2 * r, j1 = 2 * r + 1;
-    // ---- level j0 (all lower start bits known): toggles and their prefix
-    uint32_t T0[kGroups], I0[kGroups];
-#pragma unroll
-    for (int g = 0; g < kGroups; ++g) {
-      T0[g] = B[g][j0] ^ level_r(j0, Y[g], car[g]);
-      I0[g] = prefix_xor(T0[g]);
-      if (g) I0[g] ^= bcast(I0[g - 1] >> 31);
-    }
-    {
-      const uint32_t bal = __ballot_sync(0xffffffffu, I0[kGroups - 1] >> 31);
-      if (lane == 0) sh.sa[warp] = __popc(bal) & 1u;
-      __syncthreads();
-      // warp-parity bits of all warps in one ballot (lane q reads warp q)
-      const uint32_t wb = __ballot_sync(0xffffffffu, lane < kWarps ? sh.sa[lane] : 0u);
-      const uint32_t lt_w = (1u << warp) - 1u;
-      const uint32_t agg = __popc(wb) & 1u;
-      const uint32_t e0 = (__popc(wb & lt_w) ^ __popc(bal & lt)) & 1u;
-      // ---- level j1 for both values v of the chunk's start bit j0
-      uint32_t T1[2][kGroups];
-      uint32_t pv[2];
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        uint32_t x = 0;
-#pragma unroll
-        for (int g = 0; g < kGroups; ++g) {
-          uint32_t yv[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) yv[q] = Y[g][q];
-          yv[j0] = I0[g] ^ T0[g] ^ bcast(e0 ^ static_cast<uint32_t>(v)) ^ B[g][j0];
-          Carries cv = car[g];
-          level_carry(j0, yv, cv);
-          T1[v][g] = B[g][j1] ^ level_r(j1, yv, cv);
-          x ^= T1[v][g];
-        }
-        pv[v] = __popc(x) & 1u;
-      }
-      const uint32_t bal0 = __ballot_sync(0xffffffffu, pv[0]);
-      const uint32_t bal1 = __ballot_sync(0xffffffffu, pv[1]);
-      if (lane == 0) {
-        sh.sb[0][warp] = __popc(bal0) & 1u;
-        sh.sb[1][warp] = __popc(bal1) & 1u;
-      }
-      __syncthreads();
-      uint32_t wx1[2], tot[2];
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const uint32_t w1 = __ballot_sync(0xffffffffu, lane < kWarps ? sh.sb[v][lane] : 0u);
-        wx1[v] = __popc(w1 & lt_w) & 1u;
-        tot[v] = __popc(w1) & 1u;
-      }
-      const uint32_t map = agg | (tot[0] << 1) | (tot[1] << 2);
-      // The last warp owns the status word and runs the look-back: the
-      // scheduler issues highest-warp-id first, so the critical-path warp is
-      // not starved by compute warps of co-resident work.
-      const bool lb_warp = warp == kWarps - 1;
-      if (lb_warp && lane == 0) {
-        status = (status & ~(7u << 20)) | (map << (3 * r)) | (static_cast<uint32_t>(r + 1) << 20);
-        // atomic: performed at L2, visible to pollers immediately
-        atomicExch(scr.status + chunk * kStatusStride,
-                   (static_cast<unsigned long long>(scr.epoch) << 32) | status);
-        if (scr.trace) scr.trace[chunk * 12 + 1 + 2 * r] = gtimer();
-      }
-      const uint32_t seed2 = static_cast<uint32_t>(seed >> j0) & 3u;
-      if (scr.prof && tid == 0) {
-        const long long t = clock64();
-        atomicAdd(scr.prof + 2, static_cast<unsigned long long>(t - t_mark));
-        t_mark = t;
-      }
-      if (lb_warp) {
-        const uint32_t start = look_back2_warp(scr.status, scr.epoch, chunk, r, seed2, scr.prof);
-        if (lane == 0) {
-          status = (status & ~(7u << 24)) | (map_apply(map, start) << (12 + 2 * r)) |
-                   (static_cast<uint32_t>(r + 1) << 24);
-          atomicExch(scr.status + chunk * kStatusStride,
-                     (static_cast<unsigned long long>(scr.epoch) << 32) | status);
-          sh.start = start;
-          if (scr.trace) scr.trace[chunk * 12 + 2 + 2 * r] = gtimer();
-        }
-      }
-      __syncthreads();
-      if (scr.prof && tid == 0) {
-        const long long t = clock64();
-        atomicAdd(scr.prof + 3, static_cast<unsigned long long>(t - t_mark));
-        t_mark = t;
-      }
-      const uint32_t start = sh.start;
-      const uint32_t s0 = start & 1u, s1 = (start >> 1) & 1u;
-      // ---- finalize level j0 with the true start bit
-#pragma unroll
-      for (int g = 0; g < kGroups; ++g) {
-        Y[g][j0] = I0[g] ^ T0[g] ^ bcast(e0 ^ s0) ^ B[g][j0];
-        level_carry(j0, Y[g], car[g]);
-      }
-      // ---- finalize level j1 (variant s0)
-      const uint32_t e1 = (s0 ? wx1[1] : wx1[0]) ^ (__popc((s0 ? bal1 : bal0) & lt) & 1u);
-      uint32_t Iprev = 0;
-#pragma unroll
-      for (int g = 0; g < kGroups; ++g) {
-        const uint32_t T = s0 ? T1[1][g] : T1[0][g];
-        uint32_t I = prefix_xor(T);
-        if (g) I ^= bcast(Iprev >> 31);
-        Iprev = I;
-        Y[g][j1] = I ^ T ^ bcast(e1 ^ s1) ^ B[g][j1];
-        level_carry(j1, Y[g], car[g]);
-      }
-    }
-  }
-
-  if (scr.prof && tid == 0) {
-    const long long t = clock64();
-    atomicAdd(scr.prof + 2, static_cast<unsigned long long>(t - t_mark));
-    t_mark = t;
-  }
-  // ---- phase B: d_i = b_i - 2 (u_i & b_i); z = u & b = b & ~y
-  uint32_t zw[16];
-#pragma unroll
-  for (int g = 0; g < kGroups; ++g) {
-    uint32_t Z[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) Z[j] = B[g][j] & ~Y[g][j];
-    from_planes(Z, zw + 8 * g);
-  }
-  const uint64_t chunk_end = static_cast<uint64_t>(chunk + 1) * kChunk;
-  uint64_t term = 0;
-  {
-    uint32_t w[16];  // reloaded (L1/L2 hit) instead of held live across the levels
-    load_words64(data, n, pos0, w);
-    uint64_t acc = 0;
-    uint64_t seg_end = pos0 + kBytesPerThread;
-    if (pos0 + kBytesPerThread <= n) {
-      // acc = sum_k d_k P^(64-k) as independent products (no serial Horner):
-      // with db = d + 512 >= 0, sum db*Q mod 2^64 = sum mad.wide(db, Q_lo)
-      // + 2^32 sum mad.lo(db, Q_hi); the bias is removed once (c_qbias).
-      uint64_t lo[4] = {0, 0, 0, 0};  // independent chains for ILP
-      uint32_t hi[4] = {0, 0, 0, 0};
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t b = __byte_perm(w[q], 0, 0x4440 + k);
-          const uint32_t z = __byte_perm(zw[q], 0, 0x4440 + k);
-          const uint32_t db = b + 512u - 2u * z;
-          lo[k] += static_cast<uint64_t>(db) * c_qlo[4 * q + k];  // mad.wide.u32
-          hi[k] += db * c_qhi[4 * q + k];
-        }
-      }
-      acc = (lo[0] + lo[1]) + (lo[2] + lo[3]) +
-            (static_cast<uint64_t>((hi[0] + hi[1]) + (hi[2] + hi[3])) << 32) - c_qbias;
-    } else {
-      seg_end = pos0 < n ? n : pos0;
-      for (int q = 0; q < 16; ++q)
-        for (int k = 0; k < 4; ++k)
-          if (pos0 + 4 * q + k < n) {
-            const int32_t b = (w[q] >> (8 * k)) & 0xff;
-            const int32_t z = (zw[q] >> (8 * k)) & 0xff;
-            acc = (acc + static_cast<uint64_t>(static_cast<int64_t>(b - 2 * z))) * kPrime;
-          }
-    }
-    // term = acc * P^(N - seg_end)
-    if (chunk_end <= n) {
-      if (tid == 0) sh.pc = pow_p(n - chunk_end);
-      __syncthreads();
-      term = acc * sh.pc * c_pow64[kThreads - 1 - tid];
-    } else {
-      term = acc * pow_p(n - seg_end);
-    }
-  }
-  if (scr.prof && tid == 0) {
-    atomicAdd(scr.prof + 4, static_cast<unsigned long long>(clock64() - t_mark));
-    atomicAdd(scr.prof + 5, 1ull);
-  }
-  if (scr.trace && tid == 0) scr.trace[chunk * 12 + 9] = gtimer();
-  // block reduction (mod 2^64, order-independent)
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) term += __shfl_xor_sync(0xffffffffu, term, o);
-  if (lane == 0) sh.red[warp] = term;
-  __syncthreads();
-  if (tid == 0) {
-    uint64_t s = 0;
-    for (int q = 0; q < kWarps; ++q) s += sh.red[q];
-    atomicAdd(scr.accum, static_cast<unsigned long long>(s));
-    __threadfence();
-    const uint32_t done = atomicAdd(scr.finished, 1u) + 1;
-    if (done == n_chunks) {
-      const unsigned long long total = atomicAdd(scr.accum, 0ull);
-      const unsigned long long h = pow_p(n) * seed + total;
-      *scr.result = h;
-      sh.pc = h;
-      return true;
-    }
-  }
-  return false;
 }
 
 }  // namespace fnv

@@ -14,115 +14,308 @@ namespace mlck {
 // ---------------------------------------------------------------- FNV (K2)
 namespace {
 
-// K1 fused into K2: the thread's 64 output bytes gathered from the record's
-// segment table (header bytes + arena spans at arbitrary alignment) with
-// aligned 128-bit loads and a funnel shift, written to the local record and
-// every replica (peer pointers: NVLink stores), then hashed from registers'
-// worth of data the thread just wrote.
-__device__ __forceinline__ void gather_write64(const pack::Segment* __restrict__ segs, int n_segs,
-                                               uint64_t pos0, uint64_t n, const pack::Dsts& d) {
-  if (pos0 >= n) return;
-  const int s = pack::find_segment(segs, n_segs, pos0);
-  const pack::Segment seg = segs[s];
-  if (pos0 + 64 <= n && seg.dst + seg.len >= pos0 + 64) {
-    const uint8_t* src = seg.src + (pos0 - seg.dst);
-    const uint32_t sh = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(src) & 15u);
-    const uint8_t* base = src - sh;
-    uint4 a[5];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = ld_stream(base + 16 * i);
-    a[4] = sh ? ld_stream(base + 64) : a[3];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint4 o = sh ? pack::funnel16(a[i], a[i + 1], sh) : a[i];
-#pragma unroll
-      for (int r = 0; r < pack::kMaxDst; ++r)
-        if (r < d.n) st_v4(d.p[r] + pos0 + 16 * i, o);
-    }
-    return;
+using fnv::kSlots;
+// named barriers: PUB(s) compute warps -> look-back warp, RES(s) back
+__device__ __forceinline__ int bar_pub(int s) { return 1 + s; }
+__device__ __forceinline__ int bar_res(int s) { return 1 + kSlots + s; }
+
+// Profile laps of one thread's clock (kProf only): consecutive buckets, so
+// they add up to the loop time.
+template <bool kProf, int N>
+struct Laps {
+  long long t[N] = {};
+  long long last = 0;
+  __device__ __forceinline__ void start() {
+    if (kProf) last = clock64();
   }
-  int k = s;  // straddles segments (headers) or the record end: byte path
-  const uint64_t end = pos0 + 64 < n ? pos0 + 64 : n;
-  for (uint64_t p = pos0; p < end; ++p) {
-    while (k + 1 < n_segs && segs[k + 1].dst <= p) ++k;
-    const uint8_t b = segs[k].src[p - segs[k].dst];
+  __device__ __forceinline__ void mark(int b) {
+    if (kProf) {
+      const long long now = clock64();
+      t[b] += now - last;
+      last = now;
+    }
+  }
+};
+
+// Compute warps: per slot turn, take the look-back result of the round
+// published on the previous turn, then (after round 3) hash the slot's bytes
+// and refill it, else compute and publish the next round.
+template <bool kProf>
+__device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* data, uint64_t n,
+                                                const fnv::Scratch& scr, int64_t n_chunks,
+                                                const int64_t (&first)[kSlots], int64_t stride) {
+  using namespace fnv;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint64_t pinv_t = pow_u64(kPrimeInv, static_cast<uint64_t>(kThreadBytes) * (tid + 1));
+  int64_t chunk[kSlots];
+  int rnd[kSlots];
+  bool pend[kSlots];
+  uint32_t st[kSlots];    // segment start bits, byte i = segment i
+  uint32_t keep[kSlots];  // pending round: lane exclusive map [0,3), segment maps 0..kSegs-2 above
+  uint32_t par = 0;       // mbarrier phase parity per slot
+  uint64_t acc = 0;
 #pragma unroll
-    for (int r = 0; r < pack::kMaxDst; ++r)
-      if (r < d.n) d.p[r][p] = b;
+  for (int s = 0; s < kSlots; ++s) {
+    chunk[s] = first[s];
+    rnd[s] = 0;
+    pend[s] = false;
+    st[s] = 0;
+    keep[s] = 0;
+    if (chunk[s] >= 0) load_thread(sh, s, tid, data, n, chunk[s]);
+  }
+  // [0] rounds, [1] waits for look-back results, [2] final passes, [3] other
+  Laps<kProf, 4> lap;
+  lap.start();
+  for (bool any = true; any;) {
+    any = false;
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s) {
+      if (chunk[s] < 0) continue;
+      any = true;
+      if (pend[s]) {
+        lap.mark(3);
+        bar_sync(bar_res(s), kBarThreads);
+        // lane start -> segment starts through the segment maps
+        uint32_t ss = map_apply(keep[s] & 7u, sh.wstart[s][warp]);
+        uint32_t add = ss;
+#pragma unroll
+        for (int i = 1; i < kSegs; ++i) {
+          ss = map_apply((keep[s] >> (3 * i)) & 7u, ss);
+          add |= ss << (8 * i);
+        }
+        st[s] |= add << (2 * rnd[s]);
+        lap.mark(1);
+        pend[s] = false;
+        if (++rnd[s] == kRounds) {
+          // ---- final pass: the real recurrence from each segment's start
+          uint32_t w[kThreadWords];
+          read_thread(sh, s, tid, w);
+          const uint64_t p0 = static_cast<uint64_t>(chunk[s]) * kChunk + static_cast<uint64_t>(tid) * kThreadBytes;
+          if (p0 + kThreadBytes <= n) {
+            uint32_t lo[kSegs], hi[kSegs];
+#pragma unroll
+            for (int i = 0; i < kSegs; ++i) {
+              lo[i] = (st[s] >> (8 * i)) & 0xffu;
+              hi[i] = 0;
+            }
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+#pragma unroll
+              for (int i = 0; i < kSegs; ++i) fnv_byte(lo[i], hi[i], (w[8 * i + (k >> 2)] >> (8 * (k & 3))) & 0xffu);
+            uint64_t g = 0;  // sum_i G_i P^(32 (kSegs-1-i))
+#pragma unroll
+            for (int i = 0; i < kSegs; ++i)
+              g = g * kPow32 + ((static_cast<uint64_t>(hi[i]) << 32) | (lo[i] & ~0xffu));
+            acc += g * (pinv_t * chunk_weight(chunk[s]));
+            if (p0 + kThreadBytes == n) {
+              *scr.ulast = lo[kSegs - 1] & 0xffu;
+              __threadfence();
+            }
+          } else if (p0 < n) {  // holds the last byte: one chain to n
+            uint32_t lo = st[s] & 0xffu, hi = 0;
+            for (int k = 0; k < kThreadBytes && p0 + k < n; ++k)
+              fnv_byte(lo, hi, (w[k >> 2] >> (8 * (k & 3))) & 0xffu);
+            const uint64_t g = (static_cast<uint64_t>(hi) << 32) | (lo & ~0xffu);
+            acc += g * pow_u64(kPrimeInv, n);
+            *scr.ulast = lo & 0xffu;
+            __threadfence();
+          }
+          if (kProf && scr.trace && tid == 0) scr.trace[chunk[s] * 12 + 9] = gtimer();
+          // ---- refill (thread-private granules: no CTA barrier needed); the
+          // bytes land while the other slots take their turns
+          const int64_t nx = chunk[s] + stride;
+          chunk[s] = nx < n_chunks ? nx : -1;
+          rnd[s] = 0;
+          st[s] = 0;
+          par ^= 1u << s;
+          if (chunk[s] >= 0) load_thread(sh, s, tid, data, n, chunk[s]);
+          lap.mark(2);
+          continue;
+        }
+      }
+      // ---- compute and publish round rnd[s]
+      if (rnd[s] == 0) {
+        fnv::mbar_wait(&sh.mbar[s], (par >> s) & 1u);
+        if (kProf && scr.trace && tid == 0) {
+          scr.trace[chunk[s] * 12 + 0] = gtimer();
+          scr.trace[chunk[s] * 12 + 10] = smid();
+        }
+      }
+      uint32_t w[kThreadWords];
+      read_thread(sh, s, tid, w);
+      uint32_t m[kSegs];
+      if (rnd[s] < 2)
+        round_maps_low(w, st[s], rnd[s], m);
+      else
+        round_maps_high(w, st[s], rnd[s], m);
+      uint32_t tm = m[0], kp = 0;
+#pragma unroll
+      for (int i = 1; i < kSegs; ++i) {
+        kp |= m[i - 1] << (3 * i);
+        tm = map_compose(m[i], tm);
+      }
+      uint32_t wtot;
+      keep[s] = map_scan_warp(tm, &wtot) | kp;
+      if (lane == 0) sh.wmap[s][warp] = wtot;
+      bar_arrive(bar_pub(s), kBarThreads);
+      pend[s] = true;
+      lap.mark(0);
+    }
+  }
+  if (kProf && tid == 0) {
+    lap.mark(3);
+    atomicAdd(scr.prof + 2, static_cast<unsigned long long>(lap.t[0]));
+    atomicAdd(scr.prof + 3, static_cast<unsigned long long>(lap.t[1]));
+    atomicAdd(scr.prof + 4, static_cast<unsigned long long>(lap.t[2]));
+    atomicAdd(scr.prof + 6, static_cast<unsigned long long>(lap.t[3]));
+  }
+  return acc;
+}
+
+// Look-back warp of slot s: for every round the compute warps publish on
+// the slot it folds their warp maps into the chunk's map, publishes it,
+// looks back for the chunk's start bits and hands each warp its start.  Only
+// this slot's turns involve it, so the slots' look-backs run concurrently.
+template <bool kProf>
+__device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t seed, const fnv::Scratch& scr,
+                                             int64_t chunk, int64_t n_chunks, int64_t stride) {
+  using namespace fnv;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long tag = static_cast<unsigned long long>(scr.epoch) << 32;
+  // [1] idle at PUB, [2] probe loads, [3] spins, [4] compose, [5] publish + hand-off
+  long long lb[6] = {0, 0, 0, 0, 0, 0};
+  long long* lp = kProf ? lb : nullptr;
+  const long long t_begin = kProf ? clock64() : 0;
+  lb[0] = t_begin;
+  auto mark = [&](int b) {
+    if (kProf) {
+      const long long now = clock64();
+      lb[b] += now - lb[0];
+      lb[0] = now;
+    }
+  };
+  for (; chunk < n_chunks; chunk += stride) {
+    uint32_t word = 0;  // the chunk's status bits as published
+    for (int r = 0; r < kRounds; ++r) {
+      mark(5);
+      bar_sync(bar_pub(s), kBarThreads);
+      const uint32_t wm = lane < kComputeWarps ? sh.wmap[s][lane] : 0u;
+      mark(1);
+      uint32_t ctot;
+      const uint32_t wex = map_scan_warp(wm, &ctot);
+      if (lane == 0) {
+        word = (word & ~(7u << 20)) | (ctot << (3 * r)) | (static_cast<uint32_t>(r + 1) << 20);
+        st_relaxed_gpu_u64(scr.status + chunk * kStatusStride, tag | word);
+        if (kProf && scr.trace) scr.trace[chunk * 12 + 1 + 2 * r] = gtimer();
+      }
+      mark(5);
+      const uint32_t start = look_back2_warp(scr, chunk, r, static_cast<uint32_t>(seed >> (2 * r)) & 3u, lp);
+      if (lane == 0) {
+        word = (word & ~(7u << 24)) | (map_apply(ctot, start) << (12 + 2 * r)) |
+               (static_cast<uint32_t>(r + 1) << 24);
+        st_relaxed_gpu_u64(scr.status + chunk * kStatusStride, tag | word);
+        if (kProf && scr.trace) scr.trace[chunk * 12 + 2 + 2 * r] = gtimer();
+      }
+      if (lane < kComputeWarps) sh.wstart[s][lane] = map_apply(wex, start);
+      if (kProf && r == kRounds - 1 && lane == 0) atomicAdd(scr.prof + 5, 1ull);
+      __syncwarp();
+      bar_arrive(bar_res(s), kBarThreads);
+    }
+  }
+  mark(5);
+  if (kProf && lane == 0) {
+    for (int b = 1; b <= 5; ++b) atomicAdd(scr.prof + 7 + b, static_cast<unsigned long long>(lb[b]));
+    atomicAdd(scr.prof + 13, static_cast<unsigned long long>(clock64() - t_begin));
   }
 }
 
-// `data` is not __restrict__: in the fused mode it is the local record the
-// same kernel just wrote (no read-only / non-coherent cache path allowed).
-__global__ void __launch_bounds__(fnv::kThreads, 65536 / (64 * fnv::kThreads)) fnv_kernel(const uint8_t* data,
-                                                             uint64_t n, uint64_t seed,
-                                                             fnv::Scratch scr, uint64_t n_chunks,
-                                                             TrailerDsts trailer,
-                                                             const pack::Segment* __restrict__ segs,
-                                                             int n_segs, pack::Dsts dsts) {
-  __shared__ fnv::SharedState sh;
-  __shared__ int64_t s_chunk;
-  // Persistent CTAs take chunks in ticket order, so every predecessor of a
-  // chunk is resident or finished when its look-back spins on it.
-  while (true) {
-    if (threadIdx.x == 0) s_chunk = atomicAdd(scr.ticket, 1u);
-    __syncthreads();
-    const int64_t chunk = s_chunk;
-    if (chunk >= static_cast<int64_t>(n_chunks)) return;
-    if (n_segs > 0)  // fused pack: write this thread's bytes, then hash them
-      gather_write64(segs, n_segs,
-                     static_cast<uint64_t>(chunk) * fnv::kChunk + threadIdx.x * 64ull, n, dsts);
-    const bool last = fnv::chunk_contribution(data, chunk, n, seed, scr, n_chunks, sh);
-    // the block that finished last also writes the trailer bytes
-    // (serialize_record appends the checksum, snapshot.hpp:142)
-    if (last) {
-      const unsigned long long h = sh.pc;
+// Persistent CTAs (one per SM, kSlots chunks in flight each).  The CTA that
+// finishes last combines the terms and writes the trailer (serialize_record
+// appends the checksum, snapshot.hpp:142).
+template <bool kProf>
+__global__ void __launch_bounds__(fnv::kThreads, 1)
+    fnv_kernel(const uint8_t* data, uint64_t n, uint64_t seed, fnv::Scratch scr, int64_t n_chunks,
+               TrailerDsts trailer) {
+  using namespace fnv;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0)
+    for (int s = 0; s < kSlots; ++s) mbar_init(&sh.mbar[s], kComputeThreads);
+  __syncthreads();
+  // Slot-major chunk order: generation g of slot s on CTA i is chunk
+  // (g*kSlots + s)*G + i, so the compute warps' turn order is the chunk order
+  // and a chunk's predecessors publish on the same turn (same slot, lower
+  // CTAs) or an earlier one.  Needs all G CTAs co-resident: G <= SM count at
+  // one CTA per SM (launch_fnv).
+  const int64_t G = gridDim.x, stride = kSlots * G;
+  int64_t first[kSlots];
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) {
+    const int64_t c = s * G + blockIdx.x;
+    first[s] = c < n_chunks ? c : -1;
+  }
+  uint64_t acc = 0;
+  if (compute_warp(warp) >= 0) {
+    acc = fnv_compute<kProf>(sh, data, n, scr, n_chunks, first, stride);
+  } else {
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s)
+      if (warp == lookback_warp(s) && first[s] >= 0) fnv_lookback<kProf>(sh, s, seed, scr, first[s], n_chunks, stride);
+  }
+  // CTA sum -> global accumulator; the last CTA finishes the hash
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) sh.red[warp] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t sum = 0;
+    for (int q = 0; q < kWarps; ++q) sum += sh.red[q];
+    atomicAdd(scr.accum, static_cast<unsigned long long>(sum));
+    __threadfence();
+    const uint32_t done = atomicAdd(scr.finished, 1u) + 1;
+    if (done == gridDim.x) {
+      __threadfence();
+      const uint64_t total = atomicAdd(scr.accum, 0ull);
+      const uint32_t u = atomicAdd(scr.ulast, 0u);
+      const uint64_t h = pow_p(n) * (total + (seed & ~0xffull)) + u;
+      *scr.result = atomicAdd(scr.error, 0u) ? 0ull : h;
       for (int r = 0; r < trailer.n; ++r)
         for (int b = 0; b < 8; ++b) trailer.p[r][b] = static_cast<uint8_t>(h >> (8 * b));
     }
-    __syncthreads();  // s_chunk is rewritten next iteration
   }
 }
 
 }  // namespace
 
 void init_constants() {
-  unsigned long long t[fnv::kThreads];
-  const uint64_t p64 = fnv::pow_p(64);
-  uint64_t x = 1;
-  for (int k = 0; k < fnv::kThreads; ++k) {
-    t[k] = x;
-    x *= p64;
+  // P^-(c * kChunk) = T0[c & 1023] * T1[(c >> 10) & 1023] * T2[c >> 20]
+  static unsigned long long t[3][1024];
+  for (int l = 0; l < 3; ++l) {
+    const uint64_t step = fnv::pow_u64(fnv::kPrimeInv, static_cast<uint64_t>(fnv::kChunk) << (10 * l));
+    uint64_t x = 1;
+    for (int i = 0; i < 1024; ++i) {
+      t[l][i] = x;
+      x *= step;
+    }
   }
-  MLCK_CUDA(cudaMemcpyToSymbol(fnv::c_pow64, t, sizeof(t)));
-  uint32_t qlo[fnv::kBytesPerThread], qhi[fnv::kBytesPerThread];
-  unsigned long long qsum = 0;
-  for (int k = 0; k < fnv::kBytesPerThread; ++k) {
-    const uint64_t q = fnv::pow_p(static_cast<uint64_t>(fnv::kBytesPerThread - k));
-    qlo[k] = static_cast<uint32_t>(q);
-    qhi[k] = static_cast<uint32_t>(q >> 32);
-    qsum += q;
-  }
-  const unsigned long long qbias = 512ull * qsum;
-  MLCK_CUDA(cudaMemcpyToSymbol(fnv::c_qlo, qlo, sizeof(qlo)));
-  MLCK_CUDA(cudaMemcpyToSymbol(fnv::c_qhi, qhi, sizeof(qhi)));
-  MLCK_CUDA(cudaMemcpyToSymbol(fnv::c_qbias, &qbias, sizeof(qbias)));
+  MLCK_CUDA(cudaMemcpyToSymbol(fnv::c_wchunk, t, sizeof(t)));
 }
 
 uint64_t fnv_chunks(uint64_t n) { return div_up(n, fnv::kChunk); }
-// [256 B header: ticket u32 @0, finished u32 @8, accum u64 @16]
-// [status: n_chunks words of 8 B at a 256 B stride]
+// [256 B header: finished u32 @8, accum u64 @16, ulast u32 @24,
+//  error u32 @28] [status: n_chunks words of 8 B at a 256 B stride]
 size_t fnv_scratch_words(uint64_t n) { return (256 + fnv_chunks(n) * fnv::kStatusStride * 8) / 4; }
 
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
-                unsigned long long* prof, unsigned long long* trace, const pack::Segment* segs,
-                int n_segs, const pack::Dsts* dsts) {
+                unsigned long long* prof, unsigned long long* trace) {
   const uint64_t n_chunks = fnv_chunks(n);
   fnv::Scratch scr;
-  scr.ticket = scratch;
   scr.finished = scratch + 2;
   scr.accum = reinterpret_cast<unsigned long long*>(scratch + 4);
+  scr.ulast = scratch + 6;
+  scr.error = scratch + 7;
   scr.result = result;
   scr.status = reinterpret_cast<unsigned long long*>(scratch + 64);
   scr.epoch = epoch;
@@ -134,22 +327,25 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
     launch_fnv_empty(seed, result, trailer, stream);
     return;
   }
-  static int resident = 0;  // CTAs per SM at full occupancy
-  if (resident == 0) {
-    MLCK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, fnv_kernel, fnv::kThreads, 0));
-    if (resident < 1) resident = 1;
-  }
-  int sms = kSmCount;
-  {
-    int dev = 0;
-    MLCK_CUDA(cudaGetDevice(&dev));
+  // one CTA per SM, all co-resident (the slot-major chunk order relies on it)
+  static int sms_of[64] = {0};
+  int dev = 0;
+  MLCK_CUDA(cudaGetDevice(&dev));
+  int& sms = sms_of[dev & 63];
+  if (sms == 0) {
+    for (auto* k : {fnv_kernel<false>, fnv_kernel<true>})
+      MLCK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(fnv::kSmemBytes)));
+    int per_sm = 0;
+    MLCK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fnv_kernel<false>, fnv::kThreads,
+                                                             fnv::kSmemBytes));
+    if (per_sm < 1) throw Error(kCuda, "fnv_kernel does not fit on an SM");
     MLCK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  const uint64_t grid = std::min<uint64_t>(n_chunks, static_cast<uint64_t>(resident) * sms);
-  pack::Dsts d{};
-  if (dsts) d = *dsts;
-  fnv_kernel<<<static_cast<unsigned>(grid), fnv::kThreads, 0, stream>>>(
-      data, n, seed, scr, n_chunks, trailer, segs, segs ? n_segs : 0, d);
+  const uint64_t grid = std::min<uint64_t>(n_chunks, static_cast<uint64_t>(sms));
+  auto k = (prof || trace) ? fnv_kernel<true> : fnv_kernel<false>;
+  k<<<static_cast<unsigned>(grid), fnv::kThreads, fnv::kSmemBytes, stream>>>(
+      data, n, seed, scr, static_cast<int64_t>(n_chunks), trailer);
   MLCK_CUDA(cudaGetLastError());
 }
 

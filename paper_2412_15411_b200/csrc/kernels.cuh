@@ -43,9 +43,7 @@ uint64_t fnv_chunks(uint64_t n);
 size_t fnv_scratch_words(uint64_t n);
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
-                unsigned long long* prof = nullptr, unsigned long long* trace = nullptr,
-                const pack::Segment* segs = nullptr, int n_segs = 0,
-                const pack::Dsts* dsts = nullptr);
+                unsigned long long* prof = nullptr, unsigned long long* trace = nullptr);
 void launch_fnv_empty(uint64_t seed, unsigned long long* result, const TrailerDsts& trailer,
                       cudaStream_t stream);
 void launch_pack(const pack::Segment* segs, int n_segs, uint64_t total, const pack::Dsts& d,

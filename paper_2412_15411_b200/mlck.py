@@ -19,7 +19,8 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_build", "libmlck_b200.so")
+# MLCK_B200_LIB: a development build variant (scripts/build_variant.sh)
+LIB_PATH = os.environ.get("MLCK_B200_LIB") or os.path.join(HERE, "_build", "libmlck_b200.so")
 
 u8p = C.POINTER(C.c_uint8)
 f32p = C.POINTER(C.c_float)
@@ -79,7 +80,6 @@ def lib():
             "mlck_ctx_synchronize": (C.c_int, [vp]),
             "mlck_ctx_kernel_launches": (C.c_uint64, [vp]),
             "mlck_ctx_set_timing": (C.c_int, [vp, C.c_int]),
-            "mlck_ctx_set_fused_pack": (C.c_int, [vp, C.c_int]),
             "mlck_ctx_set_replica_mode": (C.c_int, [vp, C.c_int]),
             "mlck_ctx_timings": (C.c_int, [vp, C.c_char_p, C.c_uint64, f32p, C.c_uint32, u32p]),
             "mlck_state_create": (C.c_int, [vp, C.c_uint32, u64p, C.c_int, C.POINTER(vp)]),
@@ -213,9 +213,6 @@ class Context:
     def kernel_launches(self) -> int:
         return int(lib().mlck_ctx_kernel_launches(self.h))
 
-    def set_fused_pack(self, on: bool):
-        check(lib().mlck_ctx_set_fused_pack(self.h, int(on)))
-
     def set_replica_mode(self, mode: int):
         """1: copy engines overlapped with the hash (default); 0: SM stores."""
         check(lib().mlck_ctx_set_replica_mode(self.h, mode))
@@ -288,10 +285,12 @@ class Context:
 
     def fnv1a64_profile(self, device_ptr: int, n: int, seed: int = 0xcbf29ce484222325, trace=None):
         out = C.c_uint64()
-        cnt = (C.c_uint64 * 6)()
+        cnt = (C.c_uint64 * 16)()
         check(lib().mlck_fnv1a64_profile(self.h, device_ptr, n, seed, C.byref(out), cnt,
                                          trace.ctypes.data if trace is not None else None))
-        keys = ["lookback_probes", "spin_rereads", "cycles_compute", "cycles_lookback", "cycles_phaseB", "chunks"]
+        keys = ["lookback_probes", "spin_rereads", "cycles_rounds", "cycles_wait", "cycles_final", "chunks",
+                "cycles_other", "cycles_refill",
+                "lb_idle", "lb_probe", "lb_spin", "lb_compose", "lb_publish", "lb_total", "lb_handoff", "lb_arrive"]
         return out.value, dict(zip(keys, [int(x) for x in cnt]))
 
     def enable_peer_access(self, peer: int):

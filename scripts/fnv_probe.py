@@ -22,13 +22,16 @@ for mb in (16, 256, 1024):
     ch = max(1, prof["chunks"])
     print(f"{mb} MB: {ms:.3f} ms  {n / ms / 1e6:.1f} GB/s  same={h0 == h1}  per-chunk: "
           f"probes {prof['lookback_probes'] / ch:.2f} spins {prof['spin_rereads'] / ch:.1f} "
-          f"cyc compute {prof['cycles_compute'] / ch:.0f} lookback {prof['cycles_lookback'] / ch:.0f} "
-          f"phaseB {prof['cycles_phaseB'] / ch:.0f}")
+          f"thread0 cycles/chunk: rounds {prof['cycles_rounds'] / ch:.0f} wait {prof['cycles_wait'] / ch:.0f} "
+          f"final {prof['cycles_final'] / ch:.0f} other {prof['cycles_other'] / ch:.0f} "
+          f"| lb: idle {prof['lb_idle'] / ch:.0f} probe {prof['lb_probe'] / ch:.0f} "
+          f"spin {prof['lb_spin'] / ch:.0f} compose {prof['lb_compose'] / ch:.0f} pub {prof['lb_publish'] / ch:.0f} "
+          f"handoff {prof['lb_handoff'] / ch:.0f} arrive {prof['lb_arrive'] / ch:.0f} total {prof['lb_total'] / ch:.0f}")
     st.close()
 
 # per-chunk trace on 64 MB
 n = 64 << 20
-CH = int(os.environ.get("FNV_CHUNK", "65536"))
+CH = int(os.environ.get("FNV_CHUNK", "57344"))
 st = mlck.DeviceState(ctx, [n // 12], 4)
 st.fill_synthetic(1, 1)
 ptr = st.op_ptrs(0)[0]
@@ -39,7 +42,7 @@ tr = tr.reshape(chunks, 12).astype(np.int64)
 t0 = tr[:, 0].min()
 np.set_printoptions(linewidth=200)
 print("columns: start, agg0, res0, agg1, res1, agg2, res2, agg3, res3, end (us rel. to first start), sm")
-for c in list(range(0, 8)) + list(range(1000, 1008)) + list(range(3000, 3004)):
+for c in [c for c in list(range(0, 8)) + list(range(1000, 1008)) + list(range(3000, 3004)) if c < chunks]:
     row = tr[c]
     print(c, [(int(x - t0) // 100) / 10 for x in row[:10]], int(row[10]))
 dur = (tr[:, 9] - tr[:, 0]) / 1000
@@ -51,3 +54,14 @@ for r in range(4):
 # dependency: time res(c, r) vs agg(c-1, r)
 lag = (tr[1:, 2] - tr[:-1, 1]) / 1000
 print("res0(c) - agg0(c-1) median %.2f us" % np.median(lag))
+# wave analysis (slot-major order: wave = G consecutive chunks)
+G = int(os.environ.get("FNV_GRID", "148"))
+for w in [3, 6, 9, 12]:
+    if (w + 1) * G > chunks:
+        break
+    rows = tr[w * G:(w + 1) * G]
+    for r in range(4):
+        agg = (rows[:, 1 + 2 * r] - t0) / 1000
+        res = (rows[:, 2 + 2 * r] - t0) / 1000
+        print(f"wave {w} round {r}: agg min {agg.min():.1f} med {np.median(agg):.1f} max {agg.max():.1f} "
+              f"(argmax cta {int(np.argmax(agg))}) | res min {res.min():.1f} med {np.median(res):.1f} max {res.max():.1f}")
