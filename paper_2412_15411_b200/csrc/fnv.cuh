@@ -50,7 +50,7 @@ constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
 #define MLCK_FNV_SLOTS 3
 #endif
 #ifndef MLCK_FNV_WARPS
-#define MLCK_FNV_WARPS 14
+#define MLCK_FNV_WARPS 16
 #endif
 constexpr int kSlots = MLCK_FNV_SLOTS;         // chunks in flight per CTA
 constexpr int kComputeWarps = MLCK_FNV_WARPS;  // + one look-back warp per slot
@@ -61,7 +61,7 @@ constexpr int kBarThreads = kComputeThreads + 32;  // named barriers: compute wa
 constexpr int kSegs = 4;                           // 32-byte segments per thread
 constexpr int kThreadBytes = 32 * kSegs;
 constexpr int kThreadWords = kThreadBytes / 4;
-constexpr int kChunk = kComputeThreads * kThreadBytes;  // 57,344 bytes by default
+constexpr int kChunk = kComputeThreads * kThreadBytes;  // 65,536 bytes by default
 constexpr int kRounds = 4;
 static_assert(kSegs % 2 == 0, "segments are processed in pairs");
 // One 64-bit look-back word per chunk, kStatusStride words apart (256 B) so
@@ -169,73 +169,80 @@ __device__ __forceinline__ uint32_t map_scan_warp(uint32_t m, uint32_t* total) {
   return ea | ((__popc(bal0 & lt) & 1u) << 1) | ((__popc(bal1 & lt) & 1u) << 2);
 }
 
-// ---- round r of one thread: the maps of its kSegs segments (segment i =
-// words w[8i..8i+7]) on state bits (2r, 2r+1), given their start bits < 2r
-// (st byte i).  Segments are processed in pairs sharing one byte-select.
-// Rounds 0-1 track the state mod 4 / mod 16 only (0xb3 = 3 mod 16) in 8-bit
-// lanes {S2p v0, S2p+1 v0, S2p v1, S2p+1 v1} (each < 46 after the multiply);
-// rounds 2-3 track the full byte in 16-bit lanes {S2p, S2p+1}, one register
-// per start variant.
+// ---- thread data layout.  A thread owns kSegs = 4 consecutive 32-byte
+// segments A, B, C, D of the chunk.  Once its bytes land they are
+// byte-interleaved in place: word k = {A_k, B_k, C_k, D_k}, so a round feeds
+// byte k of all four segments to its SIMD lanes without any byte selects.
+static_assert(kSegs == 4, "one byte lane per segment");
+__device__ __forceinline__ void interleave(uint32_t (&w)[kThreadWords]) {
+  uint32_t o[kThreadWords];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t r0 = w[j], r1 = w[8 + j], r2 = w[16 + j], r3 = w[24 + j];
+    const uint32_t t0 = __byte_perm(r0, r1, 0x5140), t1 = __byte_perm(r2, r3, 0x5140);
+    const uint32_t t2 = __byte_perm(r0, r1, 0x7362), t3 = __byte_perm(r2, r3, 0x7362);
+    o[4 * j] = __byte_perm(t0, t1, 0x5410);
+    o[4 * j + 1] = __byte_perm(t0, t1, 0x7632);
+    o[4 * j + 2] = __byte_perm(t2, t3, 0x5410);
+    o[4 * j + 3] = __byte_perm(t2, t3, 0x7632);
+  }
+#pragma unroll
+  for (int k = 0; k < kThreadWords; ++k) w[k] = o[k];
+}
+
+// ---- round r of one thread: the maps of its four segments on state bits
+// (2r, 2r+1), given their start bits < 2r (st byte i = segment i).
+// Rounds 0-1 track the state mod 4 / mod 16 only (0xb3 = 3 mod 16): one
+// register per start variant, 8-bit lanes {A, B, C, D} (each < 46 after the
+// multiply).  Rounds 2-3 track the full byte in 16-bit lanes {A, C} and
+// {B, D}, one register per (pair, variant).
 __device__ __forceinline__ void round_maps_low(const uint32_t (&w)[kThreadWords], uint32_t st, int r,
                                                uint32_t (&map)[kSegs]) {
   const uint32_t bit = 1u << (2 * r);
   const uint32_t M = r == 0 ? 0x03030303u : 0x0f0f0f0fu;
-  uint32_t x[kSegs / 2];
-#pragma unroll
-  for (int p = 0; p < kSegs / 2; ++p) {
-    const uint32_t a = (st >> (16 * p)) & (bit - 1u), b = (st >> (16 * p + 8)) & (bit - 1u);
-    x[p] = a | (b << 8) | ((a | bit) << 16) | ((b | bit) << 24);
-  }
+  const uint32_t lo = st & ((bit - 1u) * 0x01010101u);
+  uint32_t x0 = lo, x1 = lo | (bit * 0x01010101u);
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
-    const uint32_t sel = (k & 3) | ((4 + (k & 3)) << 4) | ((k & 3) << 8) | ((4 + (k & 3)) << 12);
-#pragma unroll
-    for (int p = 0; p < kSegs / 2; ++p) {
-      const uint32_t y = __byte_perm(w[16 * p + (k >> 2)], w[16 * p + 8 + (k >> 2)], sel);
-      x[p] = ((x[p] ^ y) & M) * 3u;
-    }
+    x0 = ((x0 ^ w[k]) & M) * 3u;
+    x1 = ((x1 ^ w[k]) & M) * 3u;
   }
+  const uint32_t e0 = x0 >> (2 * r), e1 = x1 >> (2 * r);  // lane bit 0 = a / bit 1 = b
 #pragma unroll
-  for (int p = 0; p < kSegs / 2; ++p) {
-    const uint32_t e = x[p] >> (2 * r);  // lane bytes: bit0 = a, bit1 = b (of each variant)
-    map[2 * p] = (e & 3u) | (((e >> 16) & 2u) << 1);
-    map[2 * p + 1] = ((e >> 8) & 3u) | (((e >> 24) & 2u) << 1);
-  }
+  for (int i = 0; i < kSegs; ++i)
+    map[i] = ((e0 >> (8 * i)) & 3u) | (((e1 >> (8 * i)) & 2u) << 1);
 }
 __device__ __forceinline__ void round_maps_high(const uint32_t (&w)[kThreadWords], uint32_t st, int r,
                                                 uint32_t (&map)[kSegs]) {
   const uint32_t bit = 1u << (2 * r);
   constexpr uint32_t M = 0x00ff00ffu;
-  uint32_t x0[kSegs / 2], x1[kSegs / 2];
-#pragma unroll
-  for (int p = 0; p < kSegs / 2; ++p) {
-    const uint32_t a = (st >> (16 * p)) & (bit - 1u), b = (st >> (16 * p + 8)) & (bit - 1u);
-    x0[p] = a | (b << 16);
-    x1[p] = x0[p] | bit | (bit << 16);
-  }
+  const uint32_t lo = st & ((bit - 1u) * 0x01010101u);
+  uint32_t ac0 = lo & M, bd0 = (lo >> 8) & M;
+  uint32_t ac1 = ac0 | (bit * 0x00010001u), bd1 = bd0 | (bit * 0x00010001u);
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
-    const uint32_t sel = (k & 3) | ((4 + (k & 3)) << 8);
-#pragma unroll
-    for (int p = 0; p < kSegs / 2; ++p) {
-      const uint32_t y = __byte_perm(w[16 * p + (k >> 2)], w[16 * p + 8 + (k >> 2)], sel);
-      x0[p] = ((x0[p] ^ y) & M) * 0xb3u;
-      x1[p] = ((x1[p] ^ y) & M) * 0xb3u;
-    }
+    const uint32_t y = w[k];
+    const uint32_t yb = __umulhi(y, 1u << 24);  // y >> 8 on the FMA pipe
+    ac0 = ((ac0 ^ y) & M) * 0xb3u;
+    ac1 = ((ac1 ^ y) & M) * 0xb3u;
+    bd0 = ((bd0 ^ yb) & M) * 0xb3u;
+    bd1 = ((bd1 ^ yb) & M) * 0xb3u;
   }
-#pragma unroll
-  for (int p = 0; p < kSegs / 2; ++p) {
-    const uint32_t e0 = x0[p] >> (2 * r), e1 = x1[p] >> (2 * r);
-    map[2 * p] = (e0 & 3u) | ((e1 & 2u) << 1);
-    map[2 * p + 1] = ((e0 >> 16) & 3u) | (((e1 >> 16) & 2u) << 1);
-  }
+  const uint32_t a0 = ac0 >> (2 * r), a1 = ac1 >> (2 * r), b0 = bd0 >> (2 * r), b1 = bd1 >> (2 * r);
+  map[0] = (a0 & 3u) | ((a1 & 2u) << 1);
+  map[1] = (b0 & 3u) | ((b1 & 2u) << 1);
+  map[2] = ((a0 >> 16) & 3u) | (((a1 >> 16) & 2u) << 1);
+  map[3] = ((b0 >> 16) & 3u) | (((b1 >> 16) & 2u) << 1);
 }
 
 // Look-back for round r of `chunk` (one warp): lane l reads the 8
 // predecessors base-8l .. base-8l-7 with all loads in flight.  If an entry
 // nearer than the nearest inclusive one is not published yet, the whole
 // window is re-read (one round trip per retry, not one per stale entry).
-// Returns the chunk's two start bits.
+// The window's aggregates are folded without shuffles: with s0 known before
+// each entry (an xor of the farther entries' a bits), every entry's toggle of
+// s1 is known, and both fold to parities (two ballots).  Returns the chunk's
+// two start bits.
 constexpr int kProbePerLane = 8;
 __device__ __forceinline__ uint32_t look_back2_warp(const Scratch& scr, int64_t chunk, int r,
                                                     uint32_t seed2, long long* lap = nullptr) {
@@ -247,24 +254,22 @@ __device__ __forceinline__ uint32_t look_back2_warp(const Scratch& scr, int64_t 
       lap[0] = now;
     }
   };
-  uint32_t acc = 0;  // identity map
+  uint32_t acc = 0;  // identity map: the nearer windows, applied last
   int64_t base = chunk - 1;
   uint32_t retries = 0;
   while (true) {
     if (scr.prof && lane == 0) atomicAdd(scr.prof + 0, 1ull);
-    unsigned long long v[kProbePerLane];
-    uint32_t m, incl_val;
+    uint32_t am, b0m, b1m, incl_val;  // bit q: entry q's map bits (aggregates to apply)
     int first;
     while (true) {
+      unsigned long long v[kProbePerLane];
 #pragma unroll
       for (int q = 0; q < kProbePerLane; ++q) {
         const int64_t k = base - kProbePerLane * lane - q;
         v[q] = k < 0 ? 0ull : ld_relaxed_gpu_u64(scr.status + k * kStatusStride);
       }
-      // nearest-first: compose aggregates up to the first inclusive entry,
-      // stop at the first unpublished one
-      m = 0;
-      incl_val = 0;
+      // nearest-first up to the first inclusive entry; stop at an unpublished one
+      am = b0m = b1m = incl_val = 0;
       bool has_incl = false, blocked = false;
 #pragma unroll
       for (int q = 0; q < kProbePerLane; ++q) {
@@ -282,7 +287,10 @@ __device__ __forceinline__ uint32_t look_back2_warp(const Scratch& scr, int64_t 
           has_incl = true;
           incl_val = (s >> (12 + 2 * r)) & 3u;
         } else {
-          m = map_compose(m, (s >> (3 * r)) & 7u);  // the farther map applies first
+          const uint32_t m = s >> (3 * r);
+          am |= (m & 1u) << q;
+          b0m |= ((m >> 1) & 1u) << q;
+          b1m |= ((m >> 2) & 1u) << q;
         }
       }
       const uint32_t bal = __ballot_sync(0xffffffffu, has_incl);
@@ -299,20 +307,27 @@ __device__ __forceinline__ uint32_t look_back2_warp(const Scratch& scr, int64_t 
     }
     mark(3);
     if (scr.prof && lane == 0 && retries) atomicAdd(scr.prof + 1, static_cast<unsigned long long>(retries));
-    // L_0 o L_1 o ... o L_first (lanes past the nearest inclusive: identity)
-    uint32_t t = lane <= first ? m : 0u;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t o = __shfl_down_sync(0xffffffffu, t, off);
-      if (lane + off < 32) t = map_compose(t, o);
-    }
-    t = __shfl_sync(0xffffffffu, t, 0);
-    acc = map_compose(acc, t);
+    if (lane > first) am = b0m = b1m = 0;
+    // s0 before entry q of this lane = s0_far ^ far ^ (xor of am above q)
+    const uint32_t bal_a = __ballot_sync(0xffffffffu, __popc(am) & 1u);
+    const uint32_t far = __popc(bal_a & ~((2u << lane) - 1u)) & 1u;  // lanes farther than this one
+    uint32_t suf = am;  // suf_q = xor of am_j for j >= q
+    suf ^= suf >> 1;
+    suf ^= suf >> 2;
+    suf ^= suf >> 4;
+    const uint32_t x = (suf >> 1) ^ (far ? 0xffu : 0u);  // s0 before entry, for s0 = 0 at the far end
+    const uint32_t t0 = (x & b1m) | (~x & b0m);  // toggles of s1, far-end s0 = 0
+    const uint32_t t1 = (~x & b1m) | (x & b0m);  // far-end s0 = 1
+    const uint32_t bal0 = __ballot_sync(0xffffffffu, __popc(t0) & 1u);
+    const uint32_t bal1 = __ballot_sync(0xffffffffu, __popc(t1) & 1u);
+    // the window's map (farthest entry first)
+    const uint32_t wmap = (__popc(bal_a) & 1u) | ((__popc(bal0) & 1u) << 1) | ((__popc(bal1) & 1u) << 2);
     if (first < 32) {
-      const uint32_t res = map_apply(acc, __shfl_sync(0xffffffffu, incl_val, first));
+      const uint32_t res = map_apply(acc, map_apply(wmap, __shfl_sync(0xffffffffu, incl_val, first)));
       mark(4);
       return res;
     }
+    acc = map_compose(acc, wmap);
     base -= 32 * kProbePerLane;
     retries = 0;
   }
@@ -321,7 +336,8 @@ __device__ __forceinline__ uint32_t look_back2_warp(const Scratch& scr, int64_t 
 // ---- shared memory ----------------------------------------------------------
 struct alignas(16) Shared {
   uint4 data[kSlots][kComputeThreads * kThreadBytes / 16];  // thread t: 8 swizzled granules
-  unsigned long long mbar[kSlots];                          // slot data landed (cp.async)
+  unsigned long long mbar[kSlots][kComputeWarps];  // a warp's slot bytes landed (cp.async)
+  unsigned long long res[kSlots];                  // look-back result of the slot's round
   uint32_t wmap[kSlots][32];    // warp maps of the round (compute -> look-back)
   uint32_t wstart[kSlots][32];  // warp start bits (look-back -> compute)
   unsigned long long red[32];
@@ -371,7 +387,7 @@ __device__ __forceinline__ void load_thread(Shared& sh, int slot, int t, const u
   if (p + kThreadBytes <= n && (reinterpret_cast<uintptr_t>(data) & 15u) == 0) {
 #pragma unroll
     for (int q = 0; q < kGranules; ++q) cp_async16(dst + granule(t, q), data + p + 16 * q);
-    cp_async_arrive(&sh.mbar[slot]);
+    cp_async_arrive(&sh.mbar[slot][t >> 5]);
   } else {
     for (int q = 0; q < kGranules; ++q) {
       uint32_t v[4];
@@ -386,8 +402,13 @@ __device__ __forceinline__ void load_thread(Shared& sh, int slot, int t, const u
       }
       dst[granule(t, q)] = make_uint4(v[0], v[1], v[2], v[3]);
     }
-    mbar_arrive(&sh.mbar[slot]);
+    mbar_arrive(&sh.mbar[slot][t >> 5]);
   }
+}
+__device__ __forceinline__ void write_thread(Shared& sh, int slot, int t, const uint32_t (&w)[kThreadWords]) {
+#pragma unroll
+  for (int q = 0; q < kGranules; ++q)
+    sh.data[slot][granule(t, q)] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
 }
 __device__ __forceinline__ void read_thread(const Shared& sh, int slot, int t, uint32_t (&w)[kThreadWords]) {
 #pragma unroll

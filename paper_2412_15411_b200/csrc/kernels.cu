@@ -15,9 +15,11 @@ namespace mlck {
 namespace {
 
 using fnv::kSlots;
-// named barriers: PUB(s) compute warps -> look-back warp, RES(s) back
+// Hand-offs: PUB(s) is a named barrier (compute warps arrive, the look-back
+// warp of slot s waits for all of them); the result goes back through the
+// mbarrier res[s] (one arrival per round), so compute warps never wait for
+// each other -- a fast warp moves on to the next slot's turn.
 __device__ __forceinline__ int bar_pub(int s) { return 1 + s; }
-__device__ __forceinline__ int bar_res(int s) { return 1 + kSlots + s; }
 
 // Profile laps of one thread's clock (kProf only): consecutive buckets, so
 // they add up to the loop time.
@@ -52,7 +54,8 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
   bool pend[kSlots];
   uint32_t st[kSlots];    // segment start bits, byte i = segment i
   uint32_t keep[kSlots];  // pending round: lane exclusive map [0,3), segment maps 0..kSegs-2 above
-  uint32_t par = 0;       // mbarrier phase parity per slot
+  uint32_t par = 0;       // data mbarrier phase parity per slot
+  uint32_t rpar = 0;      // result mbarrier phase parity per slot
   uint64_t acc = 0;
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
@@ -63,6 +66,7 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
     keep[s] = 0;
     if (chunk[s] >= 0) load_thread(sh, s, tid, data, n, chunk[s]);
   }
+  (void)warp;
   // [0] rounds, [1] waits for look-back results, [2] final passes, [3] other
   Laps<kProf, 4> lap;
   lap.start();
@@ -74,7 +78,8 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
       any = true;
       if (pend[s]) {
         lap.mark(3);
-        bar_sync(bar_res(s), kBarThreads);
+        fnv::mbar_wait(&sh.res[s], (rpar >> s) & 1u);
+        rpar ^= 1u << s;
         // lane start -> segment starts through the segment maps
         uint32_t ss = map_apply(keep[s] & 7u, sh.wstart[s][warp]);
         uint32_t add = ss;
@@ -99,9 +104,9 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
               hi[i] = 0;
             }
 #pragma unroll
-            for (int k = 0; k < 32; ++k)
+            for (int k = 0; k < 32; ++k)  // interleaved: byte i of word k = segment i, byte k
 #pragma unroll
-              for (int i = 0; i < kSegs; ++i) fnv_byte(lo[i], hi[i], (w[8 * i + (k >> 2)] >> (8 * (k & 3))) & 0xffu);
+              for (int i = 0; i < kSegs; ++i) fnv_byte(lo[i], hi[i], (w[k] >> (8 * i)) & 0xffu);
             uint64_t g = 0;  // sum_i G_i P^(32 (kSegs-1-i))
 #pragma unroll
             for (int i = 0; i < kSegs; ++i)
@@ -113,8 +118,8 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
             }
           } else if (p0 < n) {  // holds the last byte: one chain to n
             uint32_t lo = st[s] & 0xffu, hi = 0;
-            for (int k = 0; k < kThreadBytes && p0 + k < n; ++k)
-              fnv_byte(lo, hi, (w[k >> 2] >> (8 * (k & 3))) & 0xffu);
+            for (int k = 0; k < kThreadBytes && p0 + k < n; ++k)  // stream byte k: segment k/32
+              fnv_byte(lo, hi, (w[k & 31] >> (8 * (k >> 5))) & 0xffu);
             const uint64_t g = (static_cast<uint64_t>(hi) << 32) | (lo & ~0xffu);
             acc += g * pow_u64(kPrimeInv, n);
             *scr.ulast = lo & 0xffu;
@@ -135,7 +140,7 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
       }
       // ---- compute and publish round rnd[s]
       if (rnd[s] == 0) {
-        fnv::mbar_wait(&sh.mbar[s], (par >> s) & 1u);
+        fnv::mbar_wait(&sh.mbar[s][warp], (par >> s) & 1u);
         if (kProf && scr.trace && tid == 0) {
           scr.trace[chunk[s] * 12 + 0] = gtimer();
           scr.trace[chunk[s] * 12 + 10] = smid();
@@ -143,6 +148,10 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
       }
       uint32_t w[kThreadWords];
       read_thread(sh, s, tid, w);
+      if (rnd[s] == 0) {  // fresh bytes: interleave the segments once, in place
+        interleave(w);
+        write_thread(sh, s, tid, w);
+      }
       uint32_t m[kSegs];
       if (rnd[s] < 2)
         round_maps_low(w, st[s], rnd[s], m);
@@ -219,7 +228,7 @@ __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t se
       if (lane < kComputeWarps) sh.wstart[s][lane] = map_apply(wex, start);
       if (kProf && r == kRounds - 1 && lane == 0) atomicAdd(scr.prof + 5, 1ull);
       __syncwarp();
-      bar_arrive(bar_res(s), kBarThreads);
+      if (lane == 0) mbar_arrive(&sh.res[s]);  // release: wstart is visible to the waiters
     }
   }
   mark(5);
@@ -241,7 +250,10 @@ __global__ void __launch_bounds__(fnv::kThreads, 1)
   Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0)
-    for (int s = 0; s < kSlots; ++s) mbar_init(&sh.mbar[s], kComputeThreads);
+    for (int s = 0; s < kSlots; ++s) {
+      for (int w = 0; w < kComputeWarps; ++w) mbar_init(&sh.mbar[s][w], 32);
+      mbar_init(&sh.res[s], 1);
+    }
   __syncthreads();
   // Slot-major chunk order: generation g of slot s on CTA i is chunk
   // (g*kSlots + s)*G + i, so the compute warps' turn order is the chunk order

@@ -31,7 +31,7 @@ for mb in (16, 256, 1024):
 
 # per-chunk trace on 64 MB
 n = 64 << 20
-CH = int(os.environ.get("FNV_CHUNK", "57344"))
+CH = int(os.environ.get("FNV_CHUNK", "65536"))
 st = mlck.DeviceState(ctx, [n // 12], 4)
 st.fill_synthetic(1, 1)
 ptr = st.op_ptrs(0)[0]
