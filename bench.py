@@ -283,6 +283,114 @@ def run_reference(args, d: Dist):
 
 
 # --------------------------------------------------------------------------
+# upstream logging (configs[4]): one interior pipeline stage per GPU
+# --------------------------------------------------------------------------
+def bench_logging(ctx, d, mlck, iterations=3):
+    """configs[4]: dp=2 x pp=4, M=8 micro-batches, boundary tensors
+    [4096 tokens x 2048] fp32 = 33,554,432 B.  An interior stage owns 16
+    entries per iteration (8 fwd sends + 8 bwd sends, engine.hpp:381-387,
+    404-411) = 537 MB per GPU per iteration.  Each rank logs them (a) to a
+    pinned host ring (kind 0, the paper's design: PCIe/C2C) and (b) to device
+    HBM: its ring successor's buffer over NVLink (kind 2, CUDA IPC) at N > 1,
+    a local ring at N = 1.  Copies run on the log's low-priority side stream;
+    `overlap` is the slowdown of a concurrent HBM-bound kernel on the
+    producer stream."""
+    entry_floats, m, per_it = 4096 * 2048, 8, 16
+    entry_b = 4 * entry_floats
+    it_bytes = per_it * entry_b
+    src = [ctx.alloc(entry_b) for _ in range(2)]  # the stage's send buffers
+    for p in src:
+        ctx.memset(p, 0x3c, entry_b)
+    cap = 2 * it_bytes + (1 << 20)
+
+    def run(log):
+        log.sync()
+        log.gc(1 << 62)  # empty ring
+        t0 = time.perf_counter()
+        for it in range(iterations):
+            for mb in range(m):
+                log.put(1000 + it, mb, 1, 0, src[mb & 1], entry_floats)       # fwd: boundary 1 (sender)
+                log.put(1000 + it, mb, 1, 1, src[(mb + 1) & 1], entry_floats)  # bwd: boundary 1 (receiver side)
+            log.sync()
+            log.gc(1000 + it)  # keep one iteration (persisted window advanced)
+        return (time.perf_counter() - t0) / iterations
+
+    out = {"workload": "dp2 x pp4, M=8, [4096x2048] f32 boundary tensors (configs[4]); interior stage",
+           "entries_per_iteration": per_it, "bytes_per_iteration": it_bytes}
+    # raw copy-engine peaks for the same bytes (the roofline of a copy)
+    hbuf = ctx.alloc_pinned(entry_b)
+    ctx.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(per_it):
+        ctx.d2h(hbuf, src[0], entry_b)
+    ctx.synchronize()
+    d2h_peak = it_bytes / (time.perf_counter() - t0) / GB
+    ctx.free_pinned(hbuf)
+    host = mlck.UpstreamLog(ctx, cap, kind=0)
+    run(host)
+    s = d.max(run(host))
+    out["pinned_host"] = {"ms_per_iteration": 1000 * s, "gbs": it_bytes / s / GB,
+                          "peak_gbs": d2h_peak, "peak_kind": "measured cudaMemcpyAsync D2H, same bytes",
+                          "frac": it_bytes / s / GB / d2h_peak}
+    host.close()
+    # device ring: successor's HBM (IPC) at N > 1, local HBM at N = 1
+    ring = ctx.alloc(cap)
+    handles = d.all_gather(ctx.ipc_export(ring))
+    opened = None
+    if d.world > 1:
+        opened = ctx.ipc_open(handles[(d.rank + 1) % d.world])
+        dev = mlck.UpstreamLog(ctx, cap, kind=2, external=opened)
+        target, peak, peak_kind = "successor HBM over NVLink (CUDA IPC, copy engine)", 770.0, "B200_PROFILING.md peer copy"
+    else:
+        dev = mlck.UpstreamLog(ctx, cap, kind=2, external=ring)
+        target, peak, peak_kind = ("local HBM ring (copy engine)", peaks()[0] / 2,
+                                   "MEASURED_PEAKS hbm_gbs / 2 (a copy reads and writes every byte)")
+    d.barrier()
+    run(dev)
+    d.barrier()
+    s = d.max(run(dev))
+    g = it_bytes / s / GB
+    out["device_ring"] = {"target": target, "ms_per_iteration": 1000 * s, "gbs": g, "peak_gbs": peak,
+                          "peak_kind": peak_kind, "frac": g / peak if peak else None}
+    # overlap: an HBM-bound kernel on the producer stream with and without
+    # the host-ring copies of one iteration running beside it
+    n = 1 << 28
+    a = ctx.alloc(8 * n)
+    ctx.memset(a, 0, 8 * n)
+    ctx.synchronize()
+
+    def busy(reps):  # quantize_inplace-shaped HBM stream (read 4n, write 4n bytes)
+        ctx.event_record(4)
+        for _ in range(reps):
+            ctx.quantize(a, a + 4 * n, n, 2)
+        ctx.event_record(5)
+
+    busy(2)
+    ctx.synchronize()
+    busy(16)
+    ctx.synchronize()
+    base_ms = ctx.event_ms(4, 5)
+    host = mlck.UpstreamLog(ctx, cap, kind=0)
+    for mb in range(m):
+        host.put(2000, mb, 1, 0, src[mb & 1], entry_floats)
+        host.put(2000, mb, 1, 1, src[(mb + 1) & 1], entry_floats)
+    busy(16)
+    ctx.synchronize()
+    host.sync()
+    with_ms = ctx.event_ms(4, 5)
+    host.close()
+    out["overlap"] = {"producer": "quantize kernel stream, 16 x 2 GiB HBM", "producer_kernel_ms": base_ms,
+                      "with_host_logging_ms": with_ms, "slowdown": with_ms / base_ms - 1}
+    dev.close()
+    if opened:
+        ctx.ipc_close(opened)
+    d.barrier()
+    for p in src + [ring, a]:
+        ctx.free(p)
+    return out
+
+
+# --------------------------------------------------------------------------
 # GPU leg
 # --------------------------------------------------------------------------
 def run_ours(args, d: Dist):
@@ -463,6 +571,9 @@ def run_ours(args, d: Dist):
         g.close()
         out.close()
 
+    # ---- upstream logging (configs[4])
+    logging = None if args.no_log else bench_logging(ctx, d, mlck)
+
     # ---- parity spot check on this run's bytes (trailer vs CPU oracle FNV)
     parity = None
     if d.rank == 0 and not args.no_parity:
@@ -502,6 +613,7 @@ def run_ours(args, d: Dist):
             "roofline_nvlink": roofline_nvlink,
             "kernels": kernels,
             "conversion": conv,
+            "logging": logging,
             "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": h2d // e2e_steps,
                     "d2h_bytes_per_step": e2e_bytes // e2e_steps, "path": "mlck_snapshot_record_host -> pinned host"},
             "cpu_baseline": cpu,
@@ -526,6 +638,7 @@ def main():
     ap.add_argument("--no-convert", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-log", action="store_true")
     args = ap.parse_args()
     world, rank, local = dist_env()
     d = Dist(world, rank, local)

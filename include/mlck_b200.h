@@ -212,6 +212,11 @@ int mlck_sparse_to_dense_convert(mlck_state* out, mlck_blob* const* blobs, uint3
  * on `device` (peer HBM over NVLink when device != ctx device). */
 int mlck_log_create(mlck_ctx* ctx, int kind, int device, uint64_t capacity_bytes,
                     mlck_log** out);
+/* kind 2: a ring on caller-owned device memory (e.g. a peer GPU's buffer
+ * opened with mlck_ipc_open: the pipeline successor's HBM); not freed by
+ * mlck_log_destroy. */
+int mlck_log_create_external(mlck_ctx* ctx, void* device_base, uint64_t capacity_bytes,
+                             mlck_log** out);
 int mlck_log_destroy(mlck_log* l);
 /* Records the sender-side copy of a boundary tensor (engine.hpp:383-385,
  * 407-409); src is device memory produced on the ctx stream. Overwrites an

@@ -6,7 +6,9 @@
 // event on the producer stream; the copy runs on a low-priority side stream:
 //   kind 0 -> pinned host ring, copy engine D2H (PCIe / C2C bound);
 //   kind 1 -> device ring (a peer GPU's HBM over NVLink when `device`
-//             differs from the context's device), SM copy kernel.
+//             differs from the context's device), SM copy kernel;
+//   kind 2 -> a caller-owned device ring (e.g. a ring successor's buffer
+//             opened through CUDA IPC), copy engine over NVLink.
 // The key index stays on the host in std::map order, so entry(i) enumerates
 // exactly like the reference map; gc_logs drops iteration < window start and
 // returns the ring ranges to a first-fit free list.
@@ -47,7 +49,7 @@ extern "C" int mlck_ctx_device_stream_(mlck_ctx* ctx, int* device, void** stream
 
 struct mlck_log {
   mlck_ctx* ctx = nullptr;
-  int kind = 0, device = 0, ctx_device = 0;
+  int kind = 0, device = 0, ctx_device = 0;  // kind 2: caller-owned device ring
   uint8_t* base = nullptr;
   uint64_t cap = 0, used = 0;
   std::map<Key, Entry> entries;
@@ -130,12 +132,35 @@ int mlck_log_create(mlck_ctx* ctx, int kind, int device, uint64_t capacity, mlck
   });
 }
 
+int mlck_log_create_external(mlck_ctx* ctx, void* device_base, uint64_t capacity, mlck_log** out) {
+  return log_api([&] {
+    if (!device_base || capacity < 256) throw_invalid("external log ring: null base or capacity < 256");
+    auto* l = new mlck_log();
+    l->ctx = ctx;
+    l->kind = 2;
+    void* stream = nullptr;
+    mlck_ctx_device_stream_(ctx, &l->ctx_device, &stream);
+    l->device = l->ctx_device;
+    l->base = static_cast<uint8_t*>(device_base);
+    l->cap = capacity / 256 * 256;
+    int lo = 0, hi = 0;
+    MLCK_CUDA(cudaSetDevice(l->ctx_device));
+    MLCK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    MLCK_CUDA(cudaStreamCreateWithPriority(&l->side, cudaStreamNonBlocking, lo));  // lowest
+    MLCK_CUDA(cudaEventCreateWithFlags(&l->ev, cudaEventDisableTiming));
+    l->free_list[0] = l->cap;
+    *out = l;
+  });
+}
+
 int mlck_log_destroy(mlck_log* l) {
   return log_api([&] {
     if (!l) return;
     cudaSetDevice(l->ctx_device);
     cudaStreamSynchronize(l->side);
-    if (l->kind == 0) {
+    if (l->kind == 2) {
+      // the ring belongs to the caller
+    } else if (l->kind == 0) {
       cudaFreeHost(l->base);
     } else {
       cudaSetDevice(l->device);
@@ -169,6 +194,8 @@ int mlck_log_put(mlck_log* l, uint64_t it, uint32_t mb, uint32_t boundary, uint8
     if (n) {
       if (l->kind == 0) {
         MLCK_CUDA(cudaMemcpyAsync(l->base + off, src, 4 * n, cudaMemcpyDeviceToHost, l->side));
+      } else if (l->kind == 2) {  // copy engine (a peer's HBM over NVLink for an IPC ring)
+        MLCK_CUDA(cudaMemcpyAsync(l->base + off, src, 4 * n, cudaMemcpyDefault, l->side));
       } else if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
         launch_copy16(l->base + off, src, 4 * n, l->side);
       } else {

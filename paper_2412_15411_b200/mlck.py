@@ -80,6 +80,7 @@ def lib():
             "mlck_ctx_synchronize": (C.c_int, [vp]),
             "mlck_ctx_kernel_launches": (C.c_uint64, [vp]),
             "mlck_ctx_set_timing": (C.c_int, [vp, C.c_int]),
+            "mlck_log_create_external": (C.c_int, [vp, vp, C.c_uint64, C.POINTER(vp)]),
             "mlck_ctx_set_replica_mode": (C.c_int, [vp, C.c_int]),
             "mlck_ctx_timings": (C.c_int, [vp, C.c_char_p, C.c_uint64, f32p, C.c_uint32, u32p]),
             "mlck_state_create": (C.c_int, [vp, C.c_uint32, u64p, C.c_int, C.POINTER(vp)]),
@@ -582,10 +583,15 @@ class UpstreamLog:
     """Boundary log (LogKey/UpstreamLog, engine.hpp:55-94) on a side stream.
     kind 0 = pinned host ring, 1 = device ring on `device`."""
 
-    def __init__(self, ctx: Context, capacity_bytes: int, kind: int = 0, device: int = 0):
+    def __init__(self, ctx: Context, capacity_bytes: int, kind: int = 0, device: int = 0, external: int = 0):
+        """kind 2: ring on caller-owned device memory at `external` (e.g. an
+        IPC-opened peer buffer)."""
         self.ctx = ctx
         self.h = vp()
-        check(lib().mlck_log_create(ctx.h, kind, device, capacity_bytes, C.byref(self.h)))
+        if kind == 2:
+            check(lib().mlck_log_create_external(ctx.h, external, capacity_bytes, C.byref(self.h)))
+        else:
+            check(lib().mlck_log_create(ctx.h, kind, device, capacity_bytes, C.byref(self.h)))
 
     def close(self):
         if self.h:
