@@ -112,11 +112,28 @@ struct mlck_ctx {
     s.used = true;
   }
   uint32_t fnv_epoch = 0;
-  // Replica transport: 1 = copy engines on a side stream, overlapping the FNV
-  // kernel (default); 0 = remote stores issued by the pack kernel itself.
+  // Snapshot transport: 1 = pack kernel, then copy engines push the replicas
+  // while the FNV kernel hashes (default, fastest measured); 2 = one fused
+  // kernel gathers, stores (local record and replicas, NVLink stores for
+  // peers) and hashes; 0 = the pack kernel stores the replicas, then the FNV
+  // kernel.
   int replica_mode = 1;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_packed = nullptr, ev_hashed = nullptr, ev_pushed = nullptr;
+  // the push may be split over kPushStreams copy streams (measured: more
+  // streams do not raise NVLink throughput and slow the concurrent hash)
+  static constexpr int kPushStreams = 1;
+  cudaStream_t side[kPushStreams] = {};
+  cudaEvent_t ev_packed = nullptr, ev_hashed = nullptr, ev_pushed[kPushStreams] = {};
+  uint8_t* patch = nullptr;
+  uint64_t patch_cap = 0;
+  uint8_t* patch_for(uint64_t bytes) {
+    if (bytes > patch_cap) {
+      MLCK_CUDA(cudaStreamSynchronize(stream));
+      if (patch) MLCK_CUDA(cudaFree(patch));
+      patch_cap = align_up(std::max<uint64_t>(bytes, 1 << 16), 1 << 16);
+      MLCK_CUDA(cudaMalloc(&patch, patch_cap));
+    }
+    return patch;
+  }
   uint32_t* fnv_scratch_for(uint64_t n) {
     const size_t need = fnv_scratch_words(n);
     if (need > fnv_words) {
@@ -260,19 +277,73 @@ void run_pack(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
   out->size = total;
   const size_t seg_bytes = b.segs.size() * sizeof(pack::Segment);
   const size_t meta_off = align_up(seg_bytes, 16);
-  auto& s = ctx->stage_for(meta_off + b.meta.size());
+  const bool fused = trailer && body && ctx->replica_mode == 2;
+  // fused: chunk -> first segment table, and the windows that straddle a
+  // segment boundary or the record end (pre-gathered by launch_patch)
+  const uint64_t n_chunks = fused ? fnv_chunks(body) : 0;
+  const uint64_t cb = fused ? fnv_chunk_bytes() : 1;
+  std::vector<uint64_t> win;
+  if (fused) {
+    for (size_t k = 1; k < b.segs.size(); ++k)
+      if (b.segs[k].dst % 128) win.push_back(b.segs[k].dst / 128 * 128);
+    if (body % 128) win.push_back(body / 128 * 128);
+    std::sort(win.begin(), win.end());
+    win.erase(std::unique(win.begin(), win.end()), win.end());
+  }
+  const size_t cs_off = align_up(meta_off + b.meta.size(), 16);
+  const size_t pf_off = align_up(cs_off + 4 * n_chunks, 16);
+  const size_t po_off = align_up(pf_off + 4 * (n_chunks + 1), 16);
+  const size_t stage_bytes = fused ? po_off + 8 * win.size() : meta_off + b.meta.size();
+  auto& s = ctx->stage_for(stage_bytes);
   for (size_t i = 0; i < b.segs.size(); ++i)
     if (b.is_meta[i])
       b.segs[i].src = s.dev + meta_off + reinterpret_cast<uint64_t>(b.segs[i].src);
   std::memcpy(s.host, b.segs.data(), seg_bytes);
   std::memcpy(s.host + meta_off, b.meta.data(), b.meta.size());
-  ctx->stage_upload(s, meta_off + b.meta.size());
+  if (fused) {
+    auto* cs = reinterpret_cast<uint32_t*>(s.host + cs_off);
+    auto* pf = reinterpret_cast<uint32_t*>(s.host + pf_off);
+    uint32_t k = 0, w = 0;
+    for (uint64_t c = 0; c <= n_chunks; ++c) {
+      while (k + 1 < b.segs.size() && b.segs[k].dst + b.segs[k].len <= c * cb) ++k;
+      while (w < win.size() && win[w] < c * cb) ++w;
+      if (c < n_chunks) cs[c] = k;
+      pf[c] = w;
+    }
+    std::memcpy(s.host + po_off, win.data(), 8 * win.size());
+  }
+  ctx->stage_upload(s, stage_bytes);
   pack::Dsts d{};
   d.p[0] = out->dev;
   d.n = 1;
   for (auto& r : out->replicas) d.p[d.n++] = r.first;
   const auto* segs = reinterpret_cast<const pack::Segment*>(s.dev);
   const int n_segs = static_cast<int>(b.segs.size());
+  if (fused) {
+    // one pass: gather from the arena, store to the record and every replica
+    // (NVLink stores for peers), hash, append the trailer everywhere
+    uint8_t* patch = ctx->patch_for(128 * win.size());
+    launch_patch(segs, n_segs, reinterpret_cast<const uint64_t*>(s.dev + po_off), win.size(), body, patch,
+                 ctx->stream);
+    ctx->launches += win.empty() ? 0 : 1;
+    FnvGather g{segs,
+                n_segs,
+                reinterpret_cast<const uint32_t*>(s.dev + cs_off),
+                reinterpret_cast<const uint32_t*>(s.dev + pf_off),
+                reinterpret_cast<const uint64_t*>(s.dev + po_off),
+                patch,
+                d};
+    TrailerDsts t{};
+    for (int r = 0; r < d.n; ++r) t.p[r] = d.p[r] + body;
+    t.n = d.n;
+    uint32_t* scratch = ctx->fnv_scratch_for(body);
+    const int tf = ctx->tbegin("pack_fnv");
+    launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream,
+               nullptr, nullptr, &g);
+    ctx->tend(tf);
+    ctx->launches += 1;
+    return;
+  }
   if (trailer && ctx->replica_mode == 1 && !out->replicas.empty() && body) {
     // pack the local record; push it to every replica with the copy engines
     // (NVLink for peers) on the side stream while the FNV kernel hashes it;
@@ -285,9 +356,15 @@ void run_pack(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
     ctx->tend(tp);
     ctx->launches += 1;
     MLCK_CUDA(cudaEventRecord(ctx->ev_packed, ctx->stream));
-    MLCK_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_packed, 0));
-    for (auto& r : out->replicas)
-      MLCK_CUDA(cudaMemcpyAsync(r.first, out->dev, body, cudaMemcpyDefault, ctx->side));
+    constexpr int kS = mlck_ctx::kPushStreams;
+    const uint64_t piece = align_up(div_up(body, kS), 4096);
+    for (int q = 0; q < kS; ++q) {
+      MLCK_CUDA(cudaStreamWaitEvent(ctx->side[q], ctx->ev_packed, 0));
+      const uint64_t lo = std::min<uint64_t>(body, q * piece), hi = std::min<uint64_t>(body, lo + piece);
+      if (hi > lo)
+        for (auto& r : out->replicas)
+          MLCK_CUDA(cudaMemcpyAsync(r.first + lo, out->dev + lo, hi - lo, cudaMemcpyDefault, ctx->side[q]));
+    }
     TrailerDsts t{};
     t.p[0] = out->dev + body;
     t.n = 1;
@@ -297,11 +374,13 @@ void run_pack(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
     ctx->tend(tf);
     ctx->launches += 1;
     MLCK_CUDA(cudaEventRecord(ctx->ev_hashed, ctx->stream));
-    MLCK_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_hashed, 0));
+    MLCK_CUDA(cudaStreamWaitEvent(ctx->side[0], ctx->ev_hashed, 0));
     for (auto& r : out->replicas)
-      MLCK_CUDA(cudaMemcpyAsync(r.first + body, out->dev + body, 8, cudaMemcpyDefault, ctx->side));
-    MLCK_CUDA(cudaEventRecord(ctx->ev_pushed, ctx->side));
-    MLCK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_pushed, 0));  // record complete everywhere
+      MLCK_CUDA(cudaMemcpyAsync(r.first + body, out->dev + body, 8, cudaMemcpyDefault, ctx->side[0]));
+    for (int q = 0; q < kS; ++q) {
+      MLCK_CUDA(cudaEventRecord(ctx->ev_pushed[q], ctx->side[q]));
+      MLCK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_pushed[q], 0));  // record complete everywhere
+    }
     return;
   }
   const int tp = ctx->tbegin("pack");
@@ -530,9 +609,10 @@ int mlck_ctx_create(int device, mlck_ctx** out) {
     MLCK_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
     c->stream = c->own;
     for (auto& s : c->stage) MLCK_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
-    MLCK_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&c->ev_packed, &c->ev_hashed, &c->ev_pushed})
+    for (auto& sd : c->side) MLCK_CUDA(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&c->ev_packed, &c->ev_hashed})
       MLCK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    for (auto& e : c->ev_pushed) MLCK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : c->ev) MLCK_CUDA(cudaEventCreate(&e));
     MLCK_CUDA(cudaMalloc(&c->results, 64 * 8));
     MLCK_CUDA(cudaMallocHost(&c->host_results, 64 * 8));
@@ -559,6 +639,7 @@ int mlck_ctx_destroy(mlck_ctx* c) {
     }
     for (auto& e : c->ev) cudaEventDestroy(e);
     if (c->fnv_scratch) cudaFree(c->fnv_scratch);
+    if (c->patch) cudaFree(c->patch);
     cudaFree(c->results);
     cudaFreeHost(c->host_results);
     cudaStreamDestroy(c->own);
@@ -583,7 +664,8 @@ uint64_t mlck_ctx_kernel_launches(mlck_ctx* c) { return c ? c->launches : 0; }
 
 int mlck_ctx_set_replica_mode(mlck_ctx* c, int mode) {
   return api([&] {
-    if (mode != 0 && mode != 1) throw_invalid("replica mode must be 0 (SM stores) or 1 (copy engines)");
+    if (mode < 0 || mode > 2)
+      throw_invalid("replica mode must be 0 (pack-kernel stores), 1 (copy engines) or 2 (fused pack+hash+push)");
     c->replica_mode = mode;
   });
 }

@@ -40,6 +40,7 @@
 #pragma once
 
 #include "mlck_common.cuh"
+#include "pack.cuh"
 
 namespace mlck {
 namespace fnv {
@@ -334,8 +335,17 @@ __device__ __forceinline__ uint32_t look_back2_warp(const Scratch& scr, int64_t 
 }
 
 // ---- shared memory ----------------------------------------------------------
+// Thread t's bytes sit in 9 granules at 16 * (9t + q): a stride of 9 makes
+// the lanes of a quarter-warp hit 8 distinct granules mod 8 (no bank
+// conflicts), and the 9th granule holds the spill of an unaligned gather.
+constexpr int kGranules = kThreadBytes / 16;  // 8
+#ifdef MLCK_FNV_STRIDE8
+constexpr int kGranStride = kGranules;  // experiment: no gather spill granule
+#else
+constexpr int kGranStride = kGranules + 1;     // 9
+#endif
 struct alignas(16) Shared {
-  uint4 data[kSlots][kComputeThreads * kThreadBytes / 16];  // thread t: 8 swizzled granules
+  uint4 data[kSlots][kComputeThreads * kGranStride];
   unsigned long long mbar[kSlots][kComputeWarps];  // a warp's slot bytes landed (cp.async)
   unsigned long long res[kSlots];                  // look-back result of the slot's round
   uint32_t wmap[kSlots][32];    // warp maps of the round (compute -> look-back)
@@ -345,9 +355,31 @@ struct alignas(16) Shared {
 constexpr size_t kSmemBytes = sizeof(Shared);
 static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
 
-// conflict-free 128-bit reads: lanes 8m..8m+7 hit 8 distinct granules mod 8
-constexpr int kGranules = kThreadBytes / 16;
-__device__ __forceinline__ int granule(int t, int q) { return kGranules * t + ((q + t) & (kGranules - 1)); }
+#ifdef MLCK_FNV_STRIDE8
+__device__ __forceinline__ int granule(int t, int q) { return 8 * t + ((q + t) & 7); }
+#else
+__device__ __forceinline__ int granule(int t, int q) { return kGranStride * t + q; }
+#endif
+
+// Fused snapshot (pack + hash + push): the kernel gathers the record from
+// its segment list instead of reading a packed record, writes the bytes to
+// the record and every replica (peer pointers: NVLink stores), and hashes
+// them.  chunk_seg[c] = the segment holding byte c * kChunk.
+// Thread windows (128 record bytes at 128-aligned offsets) that straddle a
+// segment boundary or the record end are pre-gathered into `patch` (128
+// bytes each, aligned; patch_off sorted, patch_first[c] = first patch of
+// chunk c), so every window is one aligned or unaligned 16-byte async copy
+// stream -- no byte-serial loads on the hash's critical path.
+struct Gather {
+  const pack::Segment* segs;
+  int n_segs;
+  const uint32_t* chunk_seg;
+  const uint32_t* patch_first;
+  const uint64_t* patch_off;
+  const uint8_t* patch;
+  uint8_t* dst[pack::kMaxDst];
+  int n_dst;
+};
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -378,33 +410,72 @@ __device__ __forceinline__ void cp_async_arrive(unsigned long long* m) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_addr(m)) : "memory");
 }
 
-// Thread t's bytes of `chunk` into its slot granules, zero past n; one
-// arrival on the slot's mbarrier when they have landed.
+// Byte path (unaligned input, the record's tail, a thread straddling
+// segments): thread t's bytes into its granules, zero past n.
+template <typename ByteAt>
+__device__ __forceinline__ void load_thread_bytes(Shared& sh, int slot, int t, ByteAt byte_at) {
+  uint4* dst = sh.data[slot];
+  for (int q = 0; q < kGranules; ++q) {
+    uint32_t v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t x = 0;
+      for (int k = 0; k < 4; ++k) x |= static_cast<uint32_t>(byte_at(16 * q + 4 * i + k)) << (8 * k);
+      v[i] = x;
+    }
+    dst[granule(t, q)] = make_uint4(v[0], v[1], v[2], v[3]);
+  }
+  mbar_arrive(&sh.mbar[slot][t >> 5]);
+}
+
+// Thread t's bytes of `chunk` of a packed buffer into its slot granules,
+// zero past n; one arrival on the warp's mbarrier when they have landed.
 __device__ __forceinline__ void load_thread(Shared& sh, int slot, int t, const uint8_t* data,
                                             uint64_t n, int64_t chunk) {
   const uint64_t p = static_cast<uint64_t>(chunk) * kChunk + static_cast<uint64_t>(t) * kThreadBytes;
-  uint4* dst = sh.data[slot];
   if (p + kThreadBytes <= n && (reinterpret_cast<uintptr_t>(data) & 15u) == 0) {
+    uint4* dst = sh.data[slot];
 #pragma unroll
     for (int q = 0; q < kGranules; ++q) cp_async16(dst + granule(t, q), data + p + 16 * q);
     cp_async_arrive(&sh.mbar[slot][t >> 5]);
   } else {
-    for (int q = 0; q < kGranules; ++q) {
-      uint32_t v[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        uint32_t x = 0;
-        for (int k = 0; k < 4; ++k) {
-          const uint64_t b = p + 16 * q + 4 * i + k;
-          if (b < n) x |= static_cast<uint32_t>(data[b]) << (8 * k);
-        }
-        v[i] = x;
-      }
-      dst[granule(t, q)] = make_uint4(v[0], v[1], v[2], v[3]);
-    }
-    mbar_arrive(&sh.mbar[slot][t >> 5]);
+    load_thread_bytes(sh, slot, t, [&](int i) -> uint32_t { return p + i < n ? data[p + i] : 0u; });
   }
 }
+
+// Gather variant: the thread's 128 record bytes -- from the patch buffer for
+// a straddling window, else the aligned source window in its segment (9
+// granules; *phase = source misalignment, undone when the round-0 turn reads
+// them); zeros past the record end.
+__device__ __forceinline__ void load_thread_gather(Shared& sh, int slot, int t, const Gather& g, uint64_t n,
+                                                   int64_t chunk, uint32_t* phase) {
+  const uint64_t p = static_cast<uint64_t>(chunk) * kChunk + static_cast<uint64_t>(t) * kThreadBytes;
+  *phase = 0;
+  uint4* dst = sh.data[slot];
+  if (p >= n) {
+#pragma unroll
+    for (int q = 0; q < kGranules; ++q) dst[granule(t, q)] = make_uint4(0, 0, 0, 0);
+    mbar_arrive(&sh.mbar[slot][t >> 5]);
+    return;
+  }
+  const uint8_t* src = nullptr;
+  for (uint32_t j = g.patch_first[chunk], e = g.patch_first[chunk + 1]; j < e; ++j)
+    if (g.patch_off[j] == p) src = g.patch + static_cast<uint64_t>(kThreadBytes) * j;
+  uint32_t ph = 0;
+  if (!src) {  // inside one segment (the host patched every other window)
+    int s = static_cast<int>(g.chunk_seg[chunk]);
+    while (s + 1 < g.n_segs && g.segs[s].dst + g.segs[s].len <= p) ++s;
+    src = g.segs[s].src + (p - g.segs[s].dst);
+    ph = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(src) & 15u);
+    src -= ph;
+  }
+#pragma unroll
+  for (int q = 0; q < kGranules; ++q) cp_async16(dst + granule(t, q), src + 16 * q);
+  if (ph) cp_async16(dst + granule(t, kGranules), src + 16 * kGranules);
+  cp_async_arrive(&sh.mbar[slot][t >> 5]);
+  *phase = ph;
+}
+
 __device__ __forceinline__ void write_thread(Shared& sh, int slot, int t, const uint32_t (&w)[kThreadWords]) {
 #pragma unroll
   for (int q = 0; q < kGranules; ++q)
@@ -418,6 +489,60 @@ __device__ __forceinline__ void read_thread(const Shared& sh, int slot, int t, u
     w[4 * q + 1] = v.y;
     w[4 * q + 2] = v.z;
     w[4 * q + 3] = v.w;
+  }
+}
+// The thread's 128 bytes from its unaligned gather window (phase 1..15):
+// nine 128-bit loads, then a word select (warp-uniform in practice: the
+// windows of a segment share its alignment) and a byte funnel, in place.
+__device__ __forceinline__ void read_thread_unaligned(const Shared& sh, int slot, int t, uint32_t ph,
+                                                     uint32_t (&w)[kThreadWords]) {
+  uint32_t x[kThreadWords + 4];
+#pragma unroll
+  for (int q = 0; q < kGranStride; ++q) {
+    const uint4 v = sh.data[slot][granule(t, q)];
+    x[4 * q] = v.x;
+    x[4 * q + 1] = v.y;
+    x[4 * q + 2] = v.z;
+    x[4 * q + 3] = v.w;
+  }
+  const uint32_t sel = 0x3210u + 0x1111u * (ph & 3u);  // bytes (ph&3) .. (ph&3)+3 of a:b
+  switch (ph >> 2) {
+#define MLCK_REALIGN(W)                                                      \
+  case W:                                                                    \
+    _Pragma("unroll") for (int i = 0; i < kThreadWords; ++i) x[i] = __byte_perm(x[i + W], x[i + W + 1], sel); \
+    break;
+    MLCK_REALIGN(0)
+    MLCK_REALIGN(1)
+    MLCK_REALIGN(2)
+    MLCK_REALIGN(3)
+#undef MLCK_REALIGN
+  }
+#pragma unroll
+  for (int i = 0; i < kThreadWords; ++i) w[i] = x[i];
+}
+
+// Coalesced store of a warp's 4 KB of record bytes (thread t's 128 bytes in
+// its granules of `slot`, aligned): store q moves granules 32q .. 32q+31 of
+// the warp's region, 512 contiguous bytes per instruction, to every dst.
+__device__ __forceinline__ void store_warp_region(const Shared& sh, int slot, int t, const Gather& g,
+                                                  uint64_t warp_base, uint64_t n) {
+  const int lane = t & 31, t0 = t - lane;
+#pragma unroll
+  for (int q = 0; q < kGranules; ++q) {
+    const int G = 32 * q + lane;  // granule of the warp region, record order
+    const uint4 v = sh.data[slot][granule(t0 + G / kGranules, G % kGranules)];
+    const uint64_t off = warp_base + 16ull * G;
+    if (off + 16 <= n) {
+#pragma unroll
+      for (int d = 0; d < pack::kMaxDst; ++d)
+        if (d < g.n_dst) st_v4(g.dst[d] + off, v);
+    } else if (off < n) {  // the record's last partial granule
+      const uint32_t c[4] = {v.x, v.y, v.z, v.w};
+      for (uint64_t k = 0; off + k < n; ++k)
+#pragma unroll
+        for (int d = 0; d < pack::kMaxDst; ++d)
+          if (d < g.n_dst) g.dst[d][off + k] = static_cast<uint8_t>(c[k >> 2] >> (8 * (k & 3)));
+    }
   }
 }
 

@@ -42,10 +42,11 @@ struct Laps {
 // Compute warps: per slot turn, take the look-back result of the round
 // published on the previous turn, then (after round 3) hash the slot's bytes
 // and refill it, else compute and publish the next round.
-template <bool kProf>
+template <bool kProf, bool kGather>
 __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* data, uint64_t n,
                                                 const fnv::Scratch& scr, int64_t n_chunks,
-                                                const int64_t (&first)[kSlots], int64_t stride) {
+                                                const int64_t (&first)[kSlots], int64_t stride,
+                                                const fnv::Gather& gth) {
   using namespace fnv;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t pinv_t = pow_u64(kPrimeInv, static_cast<uint64_t>(kThreadBytes) * (tid + 1));
@@ -54,6 +55,7 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
   bool pend[kSlots];
   uint32_t st[kSlots];    // segment start bits, byte i = segment i
   uint32_t keep[kSlots];  // pending round: lane exclusive map [0,3), segment maps 0..kSegs-2 above
+  uint32_t ph[kSlots];    // kGather: source misalignment of the slot's bytes
   uint32_t par = 0;       // data mbarrier phase parity per slot
   uint32_t rpar = 0;      // result mbarrier phase parity per slot
   uint64_t acc = 0;
@@ -64,7 +66,13 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
     pend[s] = false;
     st[s] = 0;
     keep[s] = 0;
-    if (chunk[s] >= 0) load_thread(sh, s, tid, data, n, chunk[s]);
+    ph[s] = 0;
+    if (chunk[s] >= 0) {
+      if (kGather)
+        load_thread_gather(sh, s, tid, gth, n, chunk[s], &ph[s]);
+      else
+        load_thread(sh, s, tid, data, n, chunk[s]);
+    }
   }
   (void)warp;
   // [0] rounds, [1] waits for look-back results, [2] final passes, [3] other
@@ -117,9 +125,12 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
               __threadfence();
             }
           } else if (p0 < n) {  // holds the last byte: one chain to n
+            // (bytes from shared memory: a run-time index into w[] would put
+            // w in local memory on the hot path too)
+            const uint32_t* sw = reinterpret_cast<const uint32_t*>(&sh.data[s][granule(tid, 0)]);
             uint32_t lo = st[s] & 0xffu, hi = 0;
             for (int k = 0; k < kThreadBytes && p0 + k < n; ++k)  // stream byte k: segment k/32
-              fnv_byte(lo, hi, (w[k & 31] >> (8 * (k >> 5))) & 0xffu);
+              fnv_byte(lo, hi, (sw[k & 31] >> (8 * (k >> 5))) & 0xffu);
             const uint64_t g = (static_cast<uint64_t>(hi) << 32) | (lo & ~0xffu);
             acc += g * pow_u64(kPrimeInv, n);
             *scr.ulast = lo & 0xffu;
@@ -133,7 +144,12 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
           rnd[s] = 0;
           st[s] = 0;
           par ^= 1u << s;
-          if (chunk[s] >= 0) load_thread(sh, s, tid, data, n, chunk[s]);
+          if (chunk[s] >= 0) {
+            if (kGather)
+              load_thread_gather(sh, s, tid, gth, n, chunk[s], &ph[s]);
+            else
+              load_thread(sh, s, tid, data, n, chunk[s]);
+          }
           lap.mark(2);
           continue;
         }
@@ -147,9 +163,19 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
         }
       }
       uint32_t w[kThreadWords];
-      read_thread(sh, s, tid, w);
-      if (rnd[s] == 0) {  // fresh bytes: interleave the segments once, in place
-        interleave(w);
+      if (kGather && rnd[s] == 0 && ph[s])
+        read_thread_unaligned(sh, s, tid, ph[s], w);
+      else
+        read_thread(sh, s, tid, w);
+      if (rnd[s] == 0) {
+        if (kGather) {  // fused pack: the gathered bytes go to the record and its replicas
+          write_thread(sh, s, tid, w);  // aligned, then out through coalesced warp stores
+          __syncwarp();
+          store_warp_region(sh, s, tid, gth,
+                            static_cast<uint64_t>(chunk[s]) * kChunk + static_cast<uint64_t>(tid - lane) * kThreadBytes, n);
+          __syncwarp();
+        }
+        interleave(w);  // fresh bytes: interleave the segments once, in place
         write_thread(sh, s, tid, w);
       }
       uint32_t m[kSegs];
@@ -241,10 +267,10 @@ __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t se
 // Persistent CTAs (one per SM, kSlots chunks in flight each).  The CTA that
 // finishes last combines the terms and writes the trailer (serialize_record
 // appends the checksum, snapshot.hpp:142).
-template <bool kProf>
+template <bool kProf, bool kGather>
 __global__ void __launch_bounds__(fnv::kThreads, 1)
     fnv_kernel(const uint8_t* data, uint64_t n, uint64_t seed, fnv::Scratch scr, int64_t n_chunks,
-               TrailerDsts trailer) {
+               TrailerDsts trailer, fnv::Gather gth) {
   using namespace fnv;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
@@ -269,7 +295,7 @@ __global__ void __launch_bounds__(fnv::kThreads, 1)
   }
   uint64_t acc = 0;
   if (compute_warp(warp) >= 0) {
-    acc = fnv_compute<kProf>(sh, data, n, scr, n_chunks, first, stride);
+    acc = fnv_compute<kProf, kGather>(sh, data, n, scr, n_chunks, first, stride, gth);
   } else {
 #pragma unroll
     for (int s = 0; s < kSlots; ++s)
@@ -319,9 +345,11 @@ uint64_t fnv_chunks(uint64_t n) { return div_up(n, fnv::kChunk); }
 //  error u32 @28] [status: n_chunks words of 8 B at a 256 B stride]
 size_t fnv_scratch_words(uint64_t n) { return (256 + fnv_chunks(n) * fnv::kStatusStride * 8) / 4; }
 
+uint64_t fnv_chunk_bytes() { return fnv::kChunk; }
+
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
-                unsigned long long* prof, unsigned long long* trace) {
+                unsigned long long* prof, unsigned long long* trace, const FnvGather* gather) {
   const uint64_t n_chunks = fnv_chunks(n);
   fnv::Scratch scr;
   scr.finished = scratch + 2;
@@ -345,19 +373,55 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
   MLCK_CUDA(cudaGetDevice(&dev));
   int& sms = sms_of[dev & 63];
   if (sms == 0) {
-    for (auto* k : {fnv_kernel<false>, fnv_kernel<true>})
+    for (auto* k : {fnv_kernel<false, false>, fnv_kernel<true, false>, fnv_kernel<false, true>,
+                    fnv_kernel<true, true>})
       MLCK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(fnv::kSmemBytes)));
     int per_sm = 0;
-    MLCK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fnv_kernel<false>, fnv::kThreads,
+    MLCK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fnv_kernel<false, false>, fnv::kThreads,
                                                              fnv::kSmemBytes));
     if (per_sm < 1) throw Error(kCuda, "fnv_kernel does not fit on an SM");
     MLCK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   const uint64_t grid = std::min<uint64_t>(n_chunks, static_cast<uint64_t>(sms));
-  auto k = (prof || trace) ? fnv_kernel<true> : fnv_kernel<false>;
+  fnv::Gather g{};
+  if (gather) {
+    g.segs = gather->segs;
+    g.n_segs = gather->n_segs;
+    g.chunk_seg = gather->chunk_seg;
+    g.patch_first = gather->patch_first;
+    g.patch_off = gather->patch_off;
+    g.patch = gather->patch;
+    g.n_dst = gather->dsts.n;
+    for (int d = 0; d < gather->dsts.n; ++d) g.dst[d] = gather->dsts.p[d];
+  }
+  const bool pf = prof || trace;
+  auto k = gather ? (pf ? fnv_kernel<true, true> : fnv_kernel<false, true>)
+                  : (pf ? fnv_kernel<true, false> : fnv_kernel<false, false>);
   k<<<static_cast<unsigned>(grid), fnv::kThreads, fnv::kSmemBytes, stream>>>(
-      data, n, seed, scr, static_cast<int64_t>(n_chunks), trailer);
+      data, n, seed, scr, static_cast<int64_t>(n_chunks), trailer, g);
+  MLCK_CUDA(cudaGetLastError());
+}
+
+namespace {
+// The straddling windows of a fused snapshot (fnv::Gather): block j gathers
+// the 128 record bytes at offs[j] (zeros past the record end).
+__global__ void patch_kernel(const pack::Segment* __restrict__ segs, int n_segs,
+                             const uint64_t* __restrict__ offs, uint64_t n, uint8_t* __restrict__ out) {
+  const uint64_t pos = offs[blockIdx.x] + threadIdx.x;
+  uint8_t b = 0;
+  if (pos < n) {
+    const int s = pack::find_segment(segs, n_segs, pos);
+    b = segs[s].src[pos - segs[s].dst];
+  }
+  out[static_cast<uint64_t>(blockIdx.x) * fnv::kThreadBytes + threadIdx.x] = b;
+}
+}  // namespace
+
+void launch_patch(const pack::Segment* segs, int n_segs, const uint64_t* offs, uint64_t n_win, uint64_t n,
+                  uint8_t* out, cudaStream_t stream) {
+  if (!n_win) return;
+  patch_kernel<<<static_cast<unsigned>(n_win), fnv::kThreadBytes, 0, stream>>>(segs, n_segs, offs, n, out);
   MLCK_CUDA(cudaGetLastError());
 }
 

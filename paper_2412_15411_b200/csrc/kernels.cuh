@@ -38,12 +38,29 @@ struct WalkJob {
   WalkResult* result;
 };
 
+// Fused snapshot: the FNV kernel gathers the record from `segs` (chunk_seg[c]
+// = segment holding byte c * fnv_chunk_bytes()), writes it to every dst and
+// hashes it in the same pass.
+struct FnvGather {
+  const pack::Segment* segs;
+  int n_segs;
+  const uint32_t* chunk_seg;
+  const uint32_t* patch_first;  // [n_chunks + 1]
+  const uint64_t* patch_off;    // sorted 128-aligned window offsets
+  const uint8_t* patch;         // 128 bytes per window (launch_patch)
+  pack::Dsts dsts;
+};
+void launch_patch(const pack::Segment* segs, int n_segs, const uint64_t* offs, uint64_t n_win, uint64_t n,
+                  uint8_t* out, cudaStream_t stream);
+
 void init_constants();
+uint64_t fnv_chunk_bytes();
 uint64_t fnv_chunks(uint64_t n);
 size_t fnv_scratch_words(uint64_t n);
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
-                unsigned long long* prof = nullptr, unsigned long long* trace = nullptr);
+                unsigned long long* prof = nullptr, unsigned long long* trace = nullptr,
+                const FnvGather* gather = nullptr);
 void launch_fnv_empty(uint64_t seed, unsigned long long* result, const TrailerDsts& trailer,
                       cudaStream_t stream);
 void launch_pack(const pack::Segment* segs, int n_segs, uint64_t total, const pack::Dsts& d,

@@ -215,7 +215,8 @@ class Context:
         return int(lib().mlck_ctx_kernel_launches(self.h))
 
     def set_replica_mode(self, mode: int):
-        """1: copy engines overlapped with the hash (default); 0: SM stores."""
+        """1: pack, then copy engines overlapped with the hash (default);
+        2: fused gather+store+hash kernel; 0: pack-kernel stores, then hash."""
         check(lib().mlck_ctx_set_replica_mode(self.h, mode))
 
     def set_timing(self, on: bool):

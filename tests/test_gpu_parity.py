@@ -120,8 +120,21 @@ def test_adam_goldens(mk, ctx):
 
 
 # ---------------------------------------------------------------- K1 snapshot
+# snapshot transports: 1 = pack kernel + copy-engine push + FNV kernel
+# (default), 2 = fused gather+store+hash kernel, 0 = pack-kernel replica stores
+MODES = [1, 2, 0]
+
+
+@pytest.fixture
+def mode(request, ctx):
+    ctx.set_replica_mode(request.param)
+    yield request.param
+    ctx.set_replica_mode(1)
+
+
+@pytest.mark.parametrize("mode", MODES, indirect=True)
 @pytest.mark.parametrize("name", CASE_NAMES)
-def test_snapshot_matches_reference_bytes(mk, ctx, name):
+def test_snapshot_matches_reference_bytes(mk, ctx, name, mode):
     c = load_case(name)
     for s in range(c.T + 1):
         st = upload_state(mk, ctx, c, s)
@@ -141,7 +154,8 @@ def test_dense_checkpoint_matches_reference(mk, ctx, name):
         assert mk.dense_checkpoint(st).to_host() == c.d[f"dense_s{s}"].tobytes()
 
 
-def test_snapshot_replicas_identical(mk, ctx):
+@pytest.mark.parametrize("mode", MODES, indirect=True)
+def test_snapshot_replicas_identical(mk, ctx, mode):
     c = load_case("verify_toy")
     st = upload_state(mk, ctx, c, 4)
     out = mk.Blob(ctx, 1 << 16)
@@ -174,7 +188,8 @@ def test_snapshot_errors(mk, ctx):
         mk.dense_checkpoint(st)
 
 
-def test_snapshot_large_synthetic_vs_oracle(mk, ctx, oracle):
+@pytest.mark.parametrize("mode", MODES, indirect=True)
+def test_snapshot_large_synthetic_vs_oracle(mk, ctx, oracle, mode):
     """Odd sizes and every compute width at MB scale against the oracle."""
     rng = np.random.default_rng(2)
     for cb in (1, 2, 4):
