@@ -209,6 +209,18 @@ int mlck_sparse_to_dense_convert(mlck_state* out, mlck_blob* const* blobs, uint3
                                  uint64_t window_start, uint32_t wsparse, uint64_t data_seed,
                                  mlck_gradlog* g, const mlck_optimizer* opt);
 
+/* localized_recover (recovery.hpp:240-289): conversion restricted to the
+ * operators `scope_ids` (the failed stages' operators, Engine::stage_of_op),
+ * then the lost iterations after the window up to target_iteration; every
+ * in-scope operator replays iterations a+k+1 .. max(a+W, target) from the
+ * gradient log.  Only in-scope operators of `out` are written.  Errors as
+ * the reference: "sparse checkpoint incomplete", "sparse checkpoint record
+ * (slot k): ...", "localized recovery left operator N frozen". */
+int mlck_localized_recover(mlck_state* out, const uint32_t* scope_ids, uint32_t n_scope,
+                           mlck_blob* const* blobs, uint32_t n_blobs, uint64_t window_start,
+                           uint32_t wsparse, uint64_t data_seed, mlck_gradlog* g,
+                           uint64_t target_iteration, const mlck_optimizer* opt);
+
 /* ---- K4: upstream boundary log (LogKey/UpstreamLog, engine.hpp:55-94) ----
  * kind 0: pinned host ring (copy engine, side stream); kind 1: device ring
  * on `device` (peer HBM over NVLink when device != ctx device). */

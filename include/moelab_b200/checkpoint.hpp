@@ -371,6 +371,33 @@ inline void sparse_to_dense_convert(DeviceState& out, const SparseCheckpoint& ck
                                      grads ? grads->get() : nullptr, &o));
 }
 
+// ---- localized recovery (recovery.hpp:240-289) ------------------------------
+// The reference's RecoverySegment names the failed stages; the caller passes
+// their operators (Engine::stage_of_op in [stage_lo, stage_hi]).  The
+// recovered operators land in `out`; the result mirrors
+// LocalizedRecoveryResult (the scope's operator states and the iteration).
+struct LocalizedRecoveryResult {
+  std::map<uint32_t, OperatorState> ops;
+  uint64_t iteration = 0;
+};
+inline LocalizedRecoveryResult localized_recover(DeviceState& out, const std::vector<uint32_t>& scope_ops,
+                                                 const SparseCheckpoint& ckpt, GradientLog* grads,
+                                                 uint64_t data_seed, uint64_t target_iteration,
+                                                 const OptimizerConfig& oc = {}) {
+  std::vector<mlck_blob*> hs;
+  for (const auto& b : ckpt.blobs) hs.push_back(b.get());
+  const mlck_optimizer o = oc.abi();
+  check(mlck_localized_recover(out.get(), scope_ops.data(), static_cast<uint32_t>(scope_ops.size()), hs.data(),
+                               static_cast<uint32_t>(hs.size()), ckpt.window_start, ckpt.wsparse, data_seed,
+                               grads ? grads->get() : nullptr, target_iteration, &o));
+  LocalizedRecoveryResult r;
+  uint64_t it = 0, seed = 0;
+  check(mlck_state_get_meta(out.get(), &it, &seed));
+  r.iteration = it;
+  for (uint32_t id : scope_ops) r.ops.emplace(id, out.op(id));
+  return r;
+}
+
 // ---- optimizer (engine.hpp:738-753) ---------------------------------------
 // Device spans; `step` is incremented before the bias corrections.
 inline void optimizer_step_adam(Context& ctx, float* master, float* m, float* v, uint64_t& step,

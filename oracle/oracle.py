@@ -342,6 +342,10 @@ class Reference:
         L.mlr_convert.restype = C.c_int64
         L.mlr_convert.argtypes = [cp, C.c_uint64, C.c_uint32, C.POINTER(u8p), u64p, C.c_uint32,
                                   u8p, C.c_size_t, C.c_char_p, C.c_size_t]
+        L.mlr_localized_recover.restype = C.c_int64
+        L.mlr_localized_recover.argtypes = [cp, C.c_uint64, C.c_uint32, C.POINTER(u8p), u64p, C.c_uint32,
+                                            C.c_void_p, C.c_int32, C.c_int32, C.c_uint64, u8p, C.c_size_t,
+                                            C.c_char_p, C.c_size_t]
         L.mlr_check_coverage.argtypes = [C.c_uint32, C.POINTER(u8p), u64p, C.c_uint32, C.c_uint64,
                                          C.c_int64, C.c_char_p, C.c_size_t]
         L.mlr_log_create.restype = C.c_void_p
@@ -530,6 +534,25 @@ def ref_convert(ref: Reference, cfg: MlrConfig, window_start: int, wsparse: int,
         raise RefError(err.value.decode())
     out = np.empty(n, dtype=np.uint8)
     ref.lib.mlr_convert(*args, _ptr(out, u8p), n, err, 1024)
+    return out.tobytes()
+
+
+def ref_localized_recover(ref: Reference, cfg: MlrConfig, window_start: int, wsparse: int, blobs: list, log,
+                          stage_lo: int, stage_hi: int, target: int) -> bytes:
+    """localized_recover (recovery.hpp:240-289) through oracle/_ref: the scope
+    image (u64 iteration, u32 n, then per op: u32 id, u64 step, u64 P,
+    master, m, v)."""
+    arrs = [np.frombuffer(b, dtype=np.uint8) for b in blobs]
+    ptrs = (u8p * max(1, len(arrs)))(*[_ptr(a, u8p) for a in arrs])
+    sizes = np.array([a.size for a in arrs], dtype=np.uint64)
+    err = ref._err()
+    args = (C.byref(cfg), window_start, wsparse, ptrs, _ptr(sizes, u64p), len(arrs), log.h, stage_lo, stage_hi,
+            target)
+    n = ref.lib.mlr_localized_recover(*args, None, 0, err, 1024)
+    if n < 0:
+        raise RefError(err.value.decode())
+    out = np.empty(n, dtype=np.uint8)
+    ref.lib.mlr_localized_recover(*args, _ptr(out, u8p), n, err, 1024)
     return out.tobytes()
 
 

@@ -278,6 +278,45 @@ int64_t mlr_convert(const mlr_config* c, uint64_t window_start, uint32_t wsparse
   return size;
 }
 
+// localized_recover(Engine(cfg), {pipeline 0, stage_lo, stage_hi}, ckpt, log,
+// target) (recovery.hpp:240-289).  Writes the "scope image": u64 iteration,
+// u32 n_ops, then per recovered operator in id order: u32 id, u64 step,
+// u64 P, f32 master[P], m[P], v[P].
+int64_t mlr_localized_recover(const mlr_config* c, uint64_t window_start, uint32_t wsparse,
+                              const uint8_t* const* blobs, const uint64_t* sizes, uint32_t n_blobs,
+                              void* log, int32_t stage_lo, int32_t stage_hi, uint64_t target,
+                              uint8_t* out, size_t cap, char* err, size_t ecap) {
+  int64_t size = -1;
+  guarded(err, ecap, [&] {
+    SparseCheckpoint ckpt;
+    ckpt.window_start = window_start;
+    ckpt.wsparse = wsparse;
+    for (uint32_t k = 0; k < n_blobs; ++k) {
+      ckpt.blobs.emplace_back(blobs[k], blobs[k] + sizes[k]);
+      ckpt.replication.push_back(0);
+    }
+    Engine scratch(to_cfg(c));
+    RecoverySegment seg;
+    seg.stage_lo = stage_lo;
+    seg.stage_hi = stage_hi;
+    const LocalizedRecoveryResult r =
+        localized_recover(scratch, seg, ckpt, *static_cast<const UpstreamLog*>(log), target);
+    ByteWriter w;
+    w.value<uint64_t>(r.iteration);
+    w.value<uint32_t>(static_cast<uint32_t>(r.ops.size()));
+    for (const auto& [id, op] : r.ops) {
+      w.value<uint32_t>(id);
+      w.value<uint64_t>(op.step);
+      w.value<uint64_t>(op.master.size());
+      w.floats(op.master);
+      w.floats(op.m);
+      w.floats(op.v);
+    }
+    size = static_cast<int64_t>(copy_out(w.buf, out, cap));
+  });
+  return size;
+}
+
 // SparseCheckpoint::check_coverage (snapshot.hpp:322-334).
 int mlr_check_coverage(uint32_t wsparse, const uint8_t* const* blobs, const uint64_t* sizes,
                        uint32_t n_blobs, uint64_t op_count, int64_t compute_bytes, char* err,

@@ -1213,80 +1213,122 @@ int mlck_state_apply_updates(mlck_state* st, const uint32_t* ids, uint32_t n_ids
 }
 
 // ------------------------------------------------------------------ K3
+}  // extern "C"
+
+namespace {
+// Merge + Adam replay over the window's records (sparse_to_dense_convert,
+// recovery.hpp:180-227) or, with a scope, localized recovery
+// (localized_recover, recovery.hpp:240-289): every in-scope operator takes
+// its (last) Full payload of the window -- slot k -- and replays the Adam
+// steps of iterations a+k+1 .. end from the gradient log, end = a+W for a
+// conversion and max(a+W, target) for a localized recovery (the reference
+// re-executes the lost iterations after the window from the boundary logs;
+// the logged weight gradients are those iterations' gradients).  A W = 1
+// conversion returns the record's own state (no replay, recovery.hpp:192-200);
+// a W = 1 localized recovery replays iteration a+1 like the reference loop.
+void convert_impl(mlck_state* out, mlck_blob* const* blobs, uint32_t n_blobs, uint64_t window_start,
+                  uint32_t W, uint64_t data_seed, mlck_gradlog* g, const mlck_optimizer* opt,
+                  const std::vector<uint8_t>* scope, uint64_t target) {
+  const bool localized = scope != nullptr;
+  if (n_blobs != W) {
+    if (localized) throw_runtime("sparse checkpoint incomplete");  // recovery.hpp:250-251
+    throw_runtime("sparse checkpoint incomplete: " + std::to_string(n_blobs) + " of " +  // 184-187
+                  std::to_string(W) + " records");
+  }
+  mlck_ctx* ctx = out->ctx;
+  ctx->activate();
+  std::vector<std::string> errs;
+  const uint32_t n_parse = (W == 1 && !localized) ? 1 : W;
+  auto parsed = parse_blobs(ctx, blobs, n_parse, out->cb, errs);
+  for (uint32_t k = 0; k < n_parse; ++k)  // recovery.hpp:163-171
+    if (!errs[k].empty())
+      throw_runtime("sparse checkpoint record (slot " + std::to_string(k) + "): " + errs[k]);
+  auto in_scope = [&](uint32_t id) { return !localized || (id < scope->size() && (*scope)[id]); };
+  // each operator's last Full payload in slot order (load_record overwrites)
+  struct Src {
+    int slot = -1;
+    const WalkEntry* e = nullptr;
+  };
+  std::vector<Src> src(out->n_ops);
+  for (uint32_t k = 0; k < n_parse; ++k)
+    for (const auto& e : parsed[k].entries) {
+      if (e.id >= out->n_ops) throw_runtime("conversion: record operator id out of range");
+      if (e.mode == 0 && in_scope(e.id)) {
+        if (e.param_count != out->P[e.id])
+          throw_invalid("conversion: operator " + std::to_string(e.id) + " size mismatch");
+        src[e.id] = {static_cast<int>(k), &e};
+      }
+    }
+  const adam::Opt o = to_opt(opt);
+  std::vector<adam::ConvOp> ops;
+  std::vector<const float*> gptr;
+  std::vector<float2> bc;
+  const bool replay = localized || W > 1;
+  if (replay)
+    for (uint32_t id = 0; id < out->n_ops; ++id)
+      if (in_scope(id) && src[id].slot < 0)
+        throw_runtime(localized ? "localized recovery left operator " + std::to_string(id) + " frozen"  // 263-266
+                                : "conversion finished with frozen operator " + std::to_string(id));  // 222-225
+  const uint64_t end = window_start + W + (localized && target > window_start + W ? target - window_start - W : 0);
+  std::vector<uint64_t> new_step(out->n_ops, 0);
+  for (uint32_t id = 0; id < out->n_ops; ++id) {
+    if (!in_scope(id)) continue;
+    out->present[id] = src[id].slot >= 0 ? 1 : 0;
+    out->has_full[id] = out->present[id];
+    if (src[id].slot < 0) continue;
+    const int k = src[id].slot;
+    const WalkEntry& e = *src[id].e;
+    adam::ConvOp c{};
+    c.src = blobs[k]->dev + e.payload_offset;
+    c.dst = out->master(id);
+    c.codes = out->codes(id);
+    c.P = e.param_count;
+    c.n_steps = replay ? static_cast<uint32_t>(end - window_start - static_cast<uint64_t>(k)) : 0;
+    c.grad_base = static_cast<uint32_t>(gptr.size());
+    c.bc_base = static_cast<uint32_t>(bc.size());
+    uint64_t stp = e.step;
+    for (uint32_t s = 0; s < c.n_steps; ++s) {
+      const uint64_t it = window_start + static_cast<uint64_t>(k) + 1 + s;
+      if (!g) throw_invalid("conversion: gradient log required for W > 1");
+      gptr.push_back(g->lookup(it, id));
+      stp += 1;
+      bc.push_back(make_float2(bias_correction(o.b1, stp), bias_correction(o.b2, stp)));
+    }
+    new_step[id] = stp;
+    ops.push_back(c);
+  }
+  run_replay(ctx, ops, gptr, bc, o, out->cb);
+  for (uint32_t id = 0; id < out->n_ops; ++id)
+    if (in_scope(id)) out->step[id] = new_step[id];
+  if (!replay) {
+    out->iteration = parsed[0].hdr.iteration;
+    out->data_seed = parsed[0].hdr.data_seed;
+  } else {
+    out->iteration = end;
+    out->data_seed = data_seed;
+  }
+}
+}  // namespace
+
+extern "C" {
+
 int mlck_sparse_to_dense_convert(mlck_state* out, mlck_blob* const* blobs, uint32_t n_blobs,
                                  uint64_t window_start, uint32_t W, uint64_t data_seed,
                                  mlck_gradlog* g, const mlck_optimizer* opt) {
+  return api([&] { convert_impl(out, blobs, n_blobs, window_start, W, data_seed, g, opt, nullptr, 0); });
+}
+
+int mlck_localized_recover(mlck_state* out, const uint32_t* scope_ids, uint32_t n_scope,
+                           mlck_blob* const* blobs, uint32_t n_blobs, uint64_t window_start, uint32_t W,
+                           uint64_t data_seed, mlck_gradlog* g, uint64_t target_iteration,
+                           const mlck_optimizer* opt) {
   return api([&] {
-    if (n_blobs != W)  // recovery.hpp:184-187
-      throw_runtime("sparse checkpoint incomplete: " + std::to_string(n_blobs) + " of " +
-                    std::to_string(W) + " records");
-    mlck_ctx* ctx = out->ctx;
-    ctx->activate();
-    std::vector<std::string> errs;
-    const uint32_t n_parse = (W == 1) ? 1 : W;
-    auto parsed = parse_blobs(ctx, blobs, n_parse, out->cb, errs);
-    for (uint32_t k = 0; k < n_parse; ++k)  // recovery.hpp:163-171
-      if (!errs[k].empty())
-        throw_runtime("sparse checkpoint record (slot " + std::to_string(k) + "): " + errs[k]);
-    // each operator's last Full payload in slot order (load_record overwrites)
-    struct Src {
-      int slot = -1;
-      const WalkEntry* e = nullptr;
-    };
-    std::vector<Src> src(out->n_ops);
-    for (uint32_t k = 0; k < n_parse; ++k)
-      for (const auto& e : parsed[k].entries) {
-        if (e.id >= out->n_ops) throw_runtime("conversion: record operator id out of range");
-        if (e.mode == 0) {
-          if (e.param_count != out->P[e.id])
-            throw_invalid("conversion: operator " + std::to_string(e.id) + " size mismatch");
-          src[e.id] = {static_cast<int>(k), &e};
-        }
-      }
-    const adam::Opt o = to_opt(opt);
-    std::vector<adam::ConvOp> ops;
-    std::vector<const float*> gptr;
-    std::vector<float2> bc;
-    if (W > 1) {
-      for (uint32_t id = 0; id < out->n_ops; ++id)  // recovery.hpp:222-225
-        if (src[id].slot < 0)
-          throw_runtime("conversion finished with frozen operator " + std::to_string(id));
+    std::vector<uint8_t> scope(out->n_ops, 0);
+    for (uint32_t i = 0; i < n_scope; ++i) {
+      if (scope_ids[i] >= out->n_ops) throw_invalid("unknown operator " + std::to_string(scope_ids[i]));
+      scope[scope_ids[i]] = 1;
     }
-    std::vector<uint64_t> new_step(out->n_ops, 0);
-    for (uint32_t id = 0; id < out->n_ops; ++id) {
-      out->present[id] = src[id].slot >= 0 ? 1 : 0;
-      out->has_full[id] = out->present[id];
-      if (src[id].slot < 0) continue;
-      const int k = src[id].slot;
-      const WalkEntry& e = *src[id].e;
-      adam::ConvOp c{};
-      c.src = blobs[k]->dev + e.payload_offset;
-      c.dst = out->master(id);
-      c.codes = out->codes(id);
-      c.P = e.param_count;
-      c.n_steps = W > 1 ? W - static_cast<uint32_t>(k) : 0;
-      c.grad_base = static_cast<uint32_t>(gptr.size());
-      c.bc_base = static_cast<uint32_t>(bc.size());
-      uint64_t stp = e.step;
-      for (uint32_t s = 0; s < c.n_steps; ++s) {
-        const uint64_t it = window_start + static_cast<uint64_t>(k) + 1 + s;
-        if (!g) throw_invalid("conversion: gradient log required for W > 1");
-        gptr.push_back(g->lookup(it, id));
-        stp += 1;
-        bc.push_back(make_float2(bias_correction(o.b1, stp), bias_correction(o.b2, stp)));
-      }
-      new_step[id] = stp;
-      ops.push_back(c);
-    }
-    run_replay(ctx, ops, gptr, bc, o, out->cb);
-    for (uint32_t id = 0; id < out->n_ops; ++id) out->step[id] = new_step[id];
-    if (W == 1) {
-      out->iteration = parsed[0].hdr.iteration;
-      out->data_seed = parsed[0].hdr.data_seed;
-    } else {
-      out->iteration = window_start + W;
-      out->data_seed = data_seed;
-    }
+    convert_impl(out, blobs, n_blobs, window_start, W, data_seed, g, opt, &scope, target_iteration);
   });
 }
 

@@ -125,6 +125,8 @@ def lib():
                                                    C.POINTER(Optimizer)]),
             "mlck_state_apply_updates": (C.c_int, [vp, u32p, C.c_uint32, vp, C.c_uint64,
                                                    C.POINTER(Optimizer)]),
+            "mlck_localized_recover": (C.c_int, [vp, u32p, C.c_uint32, C.POINTER(vp), C.c_uint32, C.c_uint64,
+                                                 C.c_uint32, C.c_uint64, vp, C.c_uint64, C.POINTER(Optimizer)]),
             "mlck_sparse_to_dense_convert": (C.c_int, [vp, C.POINTER(vp), C.c_uint32, C.c_uint64, C.c_uint32,
                                                        C.c_uint64, vp, C.POINTER(Optimizer)]),
             "mlck_log_create": (C.c_int, [vp, C.c_int, C.c_int, C.c_uint64, C.POINTER(vp)]),
@@ -569,6 +571,18 @@ def sparse_to_dense_convert(out: DeviceState, blobs, window_start: int, wsparse:
     opt = opt or Optimizer.adam()
     check(lib().mlck_sparse_to_dense_convert(out.h, arr, len(blobs), window_start, wsparse, data_seed,
                                              gradlog.h if gradlog else None, C.byref(opt)))
+
+
+def localized_recover(out: DeviceState, scope, blobs, window_start: int, wsparse: int, data_seed: int,
+                      gradlog: GradLog | None, target_iteration: int, opt: Optimizer | None = None):
+    """localized_recover (recovery.hpp:240-289): conversion of the operators in
+    `scope` plus the lost iterations up to target_iteration, from the
+    gradient log; only the scope's operators of `out` are written."""
+    ids = np.ascontiguousarray(np.array(list(scope), dtype=np.uint32))
+    arr = (vp * max(1, len(blobs)))(*[b.h for b in blobs])
+    opt = opt or Optimizer.adam()
+    check(lib().mlck_localized_recover(out.h, _ptr(ids, u32p), ids.size, arr, len(blobs), window_start, wsparse,
+                                       data_seed, gradlog.h if gradlog else None, target_iteration, C.byref(opt)))
 
 
 def optimizer_step_adam(ctx: Context, master: int, m: int, v: int, step: int, grad: int, n: int,

@@ -26,7 +26,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
-from oracle.oracle import (Reference, RefEngine, RefLog, ref_convert, toy_config)  # noqa: E402
+from oracle.oracle import (Reference, RefEngine, RefLog, ref_convert, ref_localized_recover,  # noqa: E402
+                           toy_config)
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 
@@ -88,7 +89,19 @@ def capture(ref: Reference, name: str, spec: dict) -> dict:
             d[f"conv_w{w}"] = np.frombuffer(st, dtype=np.uint8)
             converted.append(w)
 
+    localized = []
     if log is not None:
+        # localized recovery (recovery.hpp:240-289) of every stage (and the
+        # trailing stage pair) from every complete window, to the window's end
+        # and to the last logged iteration (lost-iteration catch-up)
+        stages = spec["cfg"].get("stages", 1)
+        ranges = [(s_, s_) for s_ in range(stages)] + ([(1, stages - 1)] if stages > 2 else [])
+        for w in converted:
+            for target in sorted({w + W, T}):
+                for lo, hi in ranges:
+                    img = ref_localized_recover(ref, cfg, w, W, windows[w], log, lo, hi, target)
+                    d[f"loc_w{w}_t{target}_s{lo}_{hi}"] = np.frombuffer(img, dtype=np.uint8)
+                    localized.append([w, target, lo, hi])
         ents = log.entries()
         d["log_keys"] = np.array([k for k, _ in ents], dtype=np.uint64).reshape(-1, 4)
         for j, (_, data) in enumerate(ents):
@@ -99,7 +112,7 @@ def capture(ref: Reference, name: str, spec: dict) -> dict:
         n_ops=n_ops, param_counts=[eng.param_count(i) for i in range(n_ops)],
         stage_of_op=[eng.stage_of_op(i) for i in range(n_ops)],
         slots=slots, data_seed=eng.data_seed, converted_windows=converted,
-        log=bool(spec["log"]),
+        log=bool(spec["log"]), localized=localized,
     )
     return meta, d
 

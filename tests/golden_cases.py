@@ -76,6 +76,30 @@ class GoldenCase:
     def converted(self, w) -> bytes:
         return self.d[f"conv_w{w}"].tobytes()
 
+    def localized(self):
+        """[(window, target, stage_lo, stage_hi)] with a reference result."""
+        return [tuple(x) for x in self.meta.get("localized", [])]
+
+    def scope(self, lo, hi):
+        return [i for i, st in enumerate(self.meta["stage_of_op"]) if lo <= st <= hi]
+
+    def localized_image(self, w, target, lo, hi):
+        """Parsed scope image of localized_recover: (iteration, {id: (step, master, m, v)})."""
+        b = self.d[f"loc_w{w}_t{target}_s{lo}_{hi}"].tobytes()
+        it = int.from_bytes(b[0:8], "little")
+        n = int.from_bytes(b[8:12], "little")
+        pos, ops = 12, {}
+        for _ in range(n):
+            i = int.from_bytes(b[pos:pos + 4], "little")
+            step = int.from_bytes(b[pos + 4:pos + 12], "little")
+            P = int.from_bytes(b[pos + 12:pos + 20], "little")
+            pos += 20
+            arrs = [np.frombuffer(b, dtype=np.float32, count=P, offset=pos + 4 * P * j) for j in range(3)]
+            pos += 12 * P
+            ops[i] = (step, *arrs)
+        assert pos == len(b)
+        return it, ops
+
     def header(self, s):
         w = s // self.W * self.W
         return dict(kind=1, iteration=s, window_start=w, wsparse=self.W, slot=s % self.W,

@@ -322,6 +322,59 @@ def test_conversion_errors(mk, ctx):
         mk.sparse_to_dense_convert(out, [blobs[0], blobs[1], blobs[1]], 0, 3, c.data_seed, g)
 
 
+# ---------------------------------------------------------------- localized recovery
+@pytest.mark.parametrize("name", ["verify_toy", "dp2_pp2"])
+def test_localized_recovery_matches_reference(mk, ctx, name):
+    """localized_recover (recovery.hpp:240-289) of every stage, from every
+    complete window, to the window's end and to the last logged iteration:
+    bit-identical to the reference's own localized recovery."""
+    c = load_case(name)
+    P = c.meta["param_counts"]
+    g = mk.GradLog(ctx, P, c.T)
+    for it in range(1, c.T + 1):
+        for i in range(c.n_ops):
+            g.put(it, i, c.grads(it, i))
+    cases = c.localized()
+    assert cases
+    for (w, target, lo, hi) in cases:
+        blobs = [mk.Blob.from_host(ctx, b) for b in c.window_blobs(w)]
+        out = mk.DeviceState(ctx, P, c.compute_bytes)
+        scope = c.scope(lo, hi)
+        mk.localized_recover(out, scope, blobs, w, c.W, c.data_seed, g, target)
+        it, ref = c.localized_image(w, target, lo, hi)
+        assert it == target
+        for i in scope:
+            step, master, m, v = ref[i]
+            got = out.download_op(i)
+            assert got.step == step, (name, w, target, lo, hi, i)
+            for a, b in ((got.master, master), (got.m, m), (got.v, v)):
+                assert np.array_equal(bits(a), bits(b)), (name, w, target, lo, hi, i)
+            # the compute weights are those of the recovered masters
+            assert np.array_equal(bits(got.compute), bits(c.op(target, i)["compute"]))
+
+
+def test_localized_recovery_errors(mk, ctx):
+    c = load_case("verify_toy")
+    g = gradlog_for(mk, ctx, c, 3)
+    blobs = [mk.Blob.from_host(ctx, b) for b in c.window_blobs(3)]
+    out = mk.DeviceState(ctx, c.meta["param_counts"], c.compute_bytes)
+    scope = c.scope(1, 1)
+    with pytest.raises(RuntimeError, match="^sparse checkpoint incomplete$"):
+        mk.localized_recover(out, scope, blobs[:2], 3, 3, c.data_seed, g, 6)
+    raw = bytearray(c.blob(5))
+    raw[17] ^= 0x01
+    bad = blobs[:2] + [mk.Blob.from_host(ctx, bytes(raw))]
+    with pytest.raises(RuntimeError, match=r"slot 2.*checksum"):
+        mk.localized_recover(out, scope, bad, 3, 3, c.data_seed, g, 6)
+    # a window without some scope operator's Full payload
+    dup = [blobs[0], blobs[1], blobs[1]]
+    frozen = [i for i in scope if i not in c.slot(0)[0] + c.slot(1)[0]]
+    with pytest.raises(RuntimeError, match=f"localized recovery left operator {frozen[0]} frozen"):
+        mk.localized_recover(out, scope, dup, 3, 3, c.data_seed, g, 6)
+    with pytest.raises(ValueError, match="unknown operator"):
+        mk.localized_recover(out, [10 ** 6], blobs, 3, 3, c.data_seed, g, 6)
+
+
 # ---------------------------------------------------------------- training step
 @pytest.mark.parametrize("name", ["verify_toy", "toy_sgd", "six_op_cb1"])
 def test_apply_updates_matches_engine(mk, ctx, name):

@@ -160,6 +160,56 @@ def test_merge_replay_equals_reference_conversion(oracle, name):
         assert c.converted(w) == c.mlst(it)
 
 
+@pytest.mark.parametrize("name", ["verify_toy", "dp2_pp2"])
+def test_localized_replay_equals_reference_localized_recovery(oracle, name):
+    """The logged-gradient restatement of localized_recover (recovery.hpp:
+    240-289): each scope operator's Full payload of the window, stepped with
+    optimizer_step_adam on the gradients of iterations a+k+1 .. max(a+W,
+    target), equals the reference's localized recovery -- which itself equals
+    the uninterrupted run at the target (test_recovery.cpp:190-284)."""
+    c = load_case(name)
+    opt = c.optimizer
+    assert c.localized()
+    for (w, target, lo, hi) in c.localized():
+        it, ref = c.localized_image(w, target, lo, hi)
+        assert it == target
+        end = max(w + c.W, target)
+        for i in c.scope(lo, hi):
+            k = next(k for k in range(c.W) if i in c.slot(k)[0])
+            o = c.op(w + k, i)
+            master, m, v = o["master"].copy(), o["m"].copy(), o["v"].copy()
+            grads = np.stack([c.grads(j, i) for j in range(w + k + 1, end + 1)])
+            step = oracle.replay_op(master, m, v, o["step"], grads, opt["kind"], opt["lr"], opt["beta1"],
+                                    opt["beta2"], opt["eps"])
+            rs, rmaster, rm, rv = ref[i]
+            assert step == rs
+            for a, b in ((master, rmaster), (m, rm), (v, rv)):
+                assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), (name, w, target, lo, hi, i)
+            tgt = c.op(target, i)
+            assert np.array_equal(rmaster.view(np.uint32), tgt["master"].view(np.uint32))
+
+
+def test_live_reference_localized_recovery(reference):
+    """The committed localized-recovery goldens reproduce from oracle/_ref."""
+    from oracle.oracle import RefEngine, RefLog, ref_localized_recover, toy_config
+    c = load_case("verify_toy")
+    cfg = toy_config(layers=3, stages=3, seed=1)
+    e = RefEngine(reference, cfg)
+    log = RefLog(reference)
+    windows = {}
+    slots = e.schedule(c.W, c.meta["O"])
+    while True:
+        s = e.iteration
+        w, k = s // c.W * c.W, s % c.W
+        windows.setdefault(w, []).append(e.snapshot(slots[k][0], slots[k][1], k, 1, w, c.W))
+        if s == c.T:
+            break
+        e.run_iteration(log)
+    w, target, lo, hi = c.localized()[-1]
+    img = ref_localized_recover(reference, cfg, w, c.W, windows[w], log, lo, hi, target)
+    assert img == c.d[f"loc_w{w}_t{target}_s{lo}_{hi}"].tobytes()
+
+
 # ---------------------------------------------------------------- live reference
 def test_live_reference_random_blobs(oracle, reference):
     """Random states through both serialize paths at odd sizes and widths."""
