@@ -579,6 +579,39 @@ def run_ours(args, d: Dist):
                               "gbs": replay_bytes / (replay_ms / 1000) / GB if replay_ms else None},
         }
         g.close()
+        # localized recovery (recovery.hpp:240-289): one failed
+        # pipeline stage = a quarter of the operators, from the same window,
+        # plus 3 lost iterations after it
+        extra = 3
+        g = mlck.GradLog(ctx, pcs, W + extra)
+        g.fill_synthetic(1001, W + extra, seed=11 + d.rank)
+        scope = list(range(len(pcs) // 4))
+        target = 1000 + W + extra
+        mlck.localized_recover(out, scope, blobs, 1000, W, 7, g, target)  # warm-up
+        ctx.synchronize()
+        ctx.event_record(2)
+        for _ in range(reps):
+            mlck.localized_recover(out, scope, blobs, 1000, W, 7, g, target)
+        ctx.event_record(3)
+        ctx.synchronize()
+        loc_ms = d.max(ctx.event_ms(2, 3) / reps)
+        ctx.set_timing(True)
+        mlck.localized_recover(out, scope, blobs, 1000, W, 7, g, target)
+        ltim = ctx.timings()
+        ctx.set_timing(False)
+        lper = {}
+        for n, t in ltim:
+            lper.setdefault(n, []).append(t)
+        steps_l = {i: W + extra - full_slot[i] for i in scope}
+        loc_bytes = blobs_b + sum(12 * pcs[i] + 4 * pcs[i] * steps_l[i] + (12 + cb) * pcs[i] for i in scope)
+        conv["localized_recovery"] = {
+            "workload": f"{len(scope)} of {len(pcs)} operators (one of 4 stages), window W={W} + {extra} lost "
+                        "iterations (SURVEY 8(f)-1)",
+            "ms": loc_ms, "algorithmic_bytes": loc_bytes, "achieved_gbs": loc_bytes / (loc_ms / 1000) / GB,
+            "adam_element_steps": sum(pcs[i] * steps_l[i] for i in scope),
+            "kernels": {n: {"ms_total": sum(v), "launches": len(v)} for n, v in lper.items()},
+            "note": "every record of the window is verified (parse_checked) before use, as the reference does"}
+        g.close()
         out.close()
 
     # ---- upstream logging (configs[4])
