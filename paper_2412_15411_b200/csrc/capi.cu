@@ -982,15 +982,15 @@ int mlck_fnv1a64(mlck_ctx* ctx, const void* ptr, uint64_t n, uint64_t seed, uint
   });
 }
 
-// FNV with the kernel's profile counters (development aid): 16 counters, see
+// FNV with the kernel's profile counters (development aid): 24 counters, see
 // fnv::Scratch::prof (fnv.cuh).
 int mlck_fnv1a64_profile(mlck_ctx* ctx, const void* ptr, uint64_t n, uint64_t seed, uint64_t* out,
                          uint64_t* counters, uint64_t* trace_host) {
   return api([&] {
     ctx->activate();
     unsigned long long* prof = nullptr;
-    MLCK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&prof), 16 * 8, ctx->stream));
-    MLCK_CUDA(cudaMemsetAsync(prof, 0, 16 * 8, ctx->stream));
+    MLCK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&prof), 24 * 8, ctx->stream));
+    MLCK_CUDA(cudaMemsetAsync(prof, 0, 24 * 8, ctx->stream));
     TrailerDsts none{};
     unsigned long long* trace = nullptr;
     const uint64_t tb = fnv_chunks(n) * 12 * 8;
@@ -1008,7 +1008,7 @@ int mlck_fnv1a64_profile(mlck_ctx* ctx, const void* ptr, uint64_t n, uint64_t se
     }
     MLCK_CUDA(cudaMemcpyAsync(ctx->host_results, ctx->results, 8, cudaMemcpyDeviceToHost,
                               ctx->stream));
-    MLCK_CUDA(cudaMemcpyAsync(counters, prof, 16 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    MLCK_CUDA(cudaMemcpyAsync(counters, prof, 24 * 8, cudaMemcpyDeviceToHost, ctx->stream));
     MLCK_CUDA(cudaFreeAsync(prof, ctx->stream));
     MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
     *out = ctx->host_results[0];

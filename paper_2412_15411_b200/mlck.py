@@ -289,12 +289,13 @@ class Context:
 
     def fnv1a64_profile(self, device_ptr: int, n: int, seed: int = 0xcbf29ce484222325, trace=None):
         out = C.c_uint64()
-        cnt = (C.c_uint64 * 16)()
+        cnt = (C.c_uint64 * 24)()
         check(lib().mlck_fnv1a64_profile(self.h, device_ptr, n, seed, C.byref(out), cnt,
                                          trace.ctypes.data if trace is not None else None))
         keys = ["lookback_probes", "spin_rereads", "cycles_rounds", "cycles_wait", "cycles_final", "chunks",
                 "cycles_other", "cycles_refill",
-                "lb_idle", "lb_probe", "lb_spin", "lb_compose", "lb_publish", "lb_total", "lb_handoff", "lb_arrive"]
+                "lb_idle", "lb_probe", "lb_spin", "lb_compose", "lb_publish", "lb_total", "lb_handoff", "lb_arrive",
+                "cyc_data_wait", "cyc_interleave", "cyc_round_core", "cyc_scan_pub", "cyc_finalize", "x21", "x22", "x23"]
         return out.value, dict(zip(keys, [int(x) for x in cnt]))
 
     def enable_peer_access(self, peer: int):

@@ -26,7 +26,9 @@ for mb in (16, 256, 1024):
           f"final {prof['cycles_final'] / ch:.0f} other {prof['cycles_other'] / ch:.0f} "
           f"| lb: idle {prof['lb_idle'] / ch:.0f} probe {prof['lb_probe'] / ch:.0f} "
           f"spin {prof['lb_spin'] / ch:.0f} compose {prof['lb_compose'] / ch:.0f} pub {prof['lb_publish'] / ch:.0f} "
-          f"handoff {prof['lb_handoff'] / ch:.0f} arrive {prof['lb_arrive'] / ch:.0f} total {prof['lb_total'] / ch:.0f}")
+          f"total {prof['lb_total'] / ch:.0f}")
+    print("   compute detail/chunk: data_wait %.0f interleave %.0f round_core %.0f scan_pub %.0f finalize %.0f" % tuple(
+        prof[k] / ch for k in ["cyc_data_wait", "cyc_interleave", "cyc_round_core", "cyc_scan_pub", "cyc_finalize"]))
     st.close()
 
 # per-chunk trace on 64 MB
@@ -65,3 +67,10 @@ for w in [3, 6, 9, 12]:
         res = (rows[:, 2 + 2 * r] - t0) / 1000
         print(f"wave {w} round {r}: agg min {agg.min():.1f} med {np.median(agg):.1f} max {agg.max():.1f} "
               f"(argmax cta {int(np.argmax(agg))}) | res min {res.min():.1f} med {np.median(res):.1f} max {res.max():.1f}")
+# one SM's chunks: the turn structure (times relative to the first start, us)
+sm = int(tr[100, 10])
+rows = tr[tr[:, 10] == sm]
+rows = rows[np.argsort(rows[:, 0])]
+print(f"SM {sm}: chunk events (start, agg0, res0, agg1, res1, agg2, res2, agg3, res3, end)")
+for rw in rows[:9]:
+    print([round((int(x) - t0) / 1000, 1) for x in rw[:10]])
