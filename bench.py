@@ -340,7 +340,7 @@ def bench_logging(ctx, d, mlck, iterations=3):
     if d.world > 1:
         opened = ctx.ipc_open(handles[(d.rank + 1) % d.world])
         dev = mlck.UpstreamLog(ctx, cap, kind=2, external=opened)
-        target, peak, peak_kind = "successor HBM over NVLink (CUDA IPC, copy engine)", 770.0, "B200_PROFILING.md peer copy"
+        target, peak, peak_kind = "successor HBM over NVLink (CUDA IPC, copy engine)", 782.0, "measured peer copy (scripts/micro/push.cu)"
     else:
         dev = mlck.UpstreamLog(ctx, cap, kind=2, external=ring)
         target, peak, peak_kind = ("local HBM ring (copy engine)", peaks()[0] / 2,
@@ -477,12 +477,24 @@ def run_ours(args, d: Dist):
     for i in range(args.steps):
         step(i)
     tim_sm = ctx.timings()
-    ctx.set_replica_mode(1)
     ctx.set_timing(False)
+    # transport 3 (push kernel on 16 reserved SMs beside the hash): whole-step time
+    ctx.set_replica_mode(3)
+    d.barrier()
+    ctx.synchronize()
+    ctx.event_record(0)
+    for i in range(args.steps):
+        step(i)
+    ctx.event_record(1)
+    ctx.synchronize()
+    d.barrier()
+    ms_t3 = d.max(ctx.event_ms(0, 1))
+    ctx.set_replica_mode(-1)
     pack_ms = [t for n, t in tim if n == "pack"]
     fnv_ms = [t for n, t in tim if n == "fnv"]
     fused_ms = [t for n, t in tim_fused if n == "pack_fnv"]
     pack_sm_ms = [t for n, t in tim_sm if n == "pack"]
+    push_ms = [t for n, t in tim if n == "push"]
 
     def kstat(ms_list, total_bytes, note):
         return {"ms_avg": statistics.mean(ms_list), "launches": len(ms_list),
@@ -491,6 +503,8 @@ def run_ours(args, d: Dist):
 
     kernels = {
         "pack": kstat(pack_ms, sum(payload) + sum(rec), "HBM: payload read + record write"),
+        "push": kstat(push_ms, r * sum(rec), "replica copies on the copy engines, beside the hash ("
+                      + ("local HBM" if d.world == 1 else "NVLink egress") + ")"),
         "fnv": kstat(fnv_ms, sum(rec), "HBM: record read (ALU-bound 8-bit automaton)"),
         "ablation_fused_pack_fnv (transport 2)": kstat(
             fused_ms, sum(payload) + (1 + local_rep) * sum(rec),
@@ -499,6 +513,9 @@ def run_ours(args, d: Dist):
         "ablation_pack_with_replica_stores (transport 0)": kstat(
             pack_sm_ms, sum(payload) + (1 + local_rep) * sum(rec),
             "HBM: payload read + local writes" + ("" if d.world == 1 else f" (+{r}x record over NVLink)")),
+        "ablation_sm_push_step (transport 3)": {
+            "ms_per_step": ms_t3 / args.steps, "value": total_bytes / (ms_t3 / 1000) / GB,
+            "note": "whole step, pack + push kernel on 16 reserved SMs concurrent with the hash on the rest"},
     }
     kd = kernels["fnv"]
     ach = kd["bytes_per_launch"] / (kd["ms_avg"] / 1000) / GB
@@ -509,10 +526,10 @@ def run_ours(args, d: Dist):
                 "note": "dominant kernel of the step (the pack kernel alone: kernels['pack']); it is bound by the "
                         "integer ALU work of the FNV automaton, not by HBM (DESIGN.md 3.2)"}
     if d.world > 1:
-        nv_peak = 770.0
+        nv_peak = 782.0  # one copy engine, GPU->peer (scripts/micro/push.cu on this pool)
         egress = r * bytes_local / (ms_local / 1000) / GB
         roofline_nvlink = {"bound": "nvlink", "achieved": egress, "peak": nv_peak, "unit": "GB/s",
-                           "frac": egress / nv_peak, "peak_kind": "measured peer copy (B200_PROFILING.md)"}
+                           "frac": egress / nv_peak, "peak_kind": "measured peer copy (scripts/micro/push.cu)"}
     else:
         roofline_nvlink = None
 
@@ -543,7 +560,9 @@ def run_ours(args, d: Dist):
             mlck.snapshot_record(st, a, c, k, 1, 1000, W, blobs[k])
         g = mlck.GradLog(ctx, pcs, W)
         g.fill_synthetic(1001, W, seed=11 + d.rank)
-        out = mlck.DeviceState(ctx, pcs, cb)
+        # the dense result overwrites the live arena (the snapshot phase is
+        # over): at N >= 3 a second 39 GB arena does not fit beside the window
+        out = st
         mlck.sparse_to_dense_convert(out, blobs, 1000, W, 7, g)  # warm-up
         ctx.synchronize()
         reps = max(1, min(3, args.steps))
@@ -579,9 +598,11 @@ def run_ours(args, d: Dist):
                               "gbs": replay_bytes / (replay_ms / 1000) / GB if replay_ms else None},
         }
         g.close()
-        # localized recovery (recovery.hpp:240-289): one failed
-        # pipeline stage = a quarter of the operators, from the same window,
-        # plus 3 lost iterations after it
+    # localized recovery (recovery.hpp:240-289): one failed
+    # pipeline stage = a quarter of the operators, from the same window, plus 3
+    # lost iterations after it (N = 1: at N >= 3 a W+3-iteration gradient log
+    # of the 2.8 G-parameter shard does not fit beside the window)
+    if conv is not None and d.world == 1:
         extra = 3
         g = mlck.GradLog(ctx, pcs, W + extra)
         g.fill_synthetic(1001, W + extra, seed=11 + d.rank)
@@ -612,7 +633,6 @@ def run_ours(args, d: Dist):
             "kernels": {n: {"ms_total": sum(v), "launches": len(v)} for n, v in lper.items()},
             "note": "every record of the window is verified (parse_checked) before use, as the reference does"}
         g.close()
-        out.close()
 
     # ---- upstream logging (configs[4])
     logging = None if args.no_log else bench_logging(ctx, d, mlck)

@@ -79,15 +79,15 @@ struct mlck_ctx {
     return ev_pool[ev_used++];
   }
   // Brackets one launch; returns -1 when timing is off.
-  int tbegin(const char* label) {
+  int tbegin(const char* label, cudaStream_t on = nullptr) {
     if (!timing) return -1;
     Timed t{label, next_event(), next_event()};
-    MLCK_CUDA(cudaEventRecord(t.a, stream));
+    MLCK_CUDA(cudaEventRecord(t.a, on ? on : stream));
     timed.push_back(t);
     return static_cast<int>(timed.size()) - 1;
   }
-  void tend(int idx) {
-    if (idx >= 0) MLCK_CUDA(cudaEventRecord(timed[idx].b, stream));
+  void tend(int idx, cudaStream_t on = nullptr) {
+    if (idx >= 0) MLCK_CUDA(cudaEventRecord(timed[idx].b, on ? on : stream));
   }
 
   // Pinned staging + device mirror for one call's metadata.
@@ -112,15 +112,21 @@ struct mlck_ctx {
     s.used = true;
   }
   uint32_t fnv_epoch = 0;
-  // Snapshot transport: 1 = pack kernel, then copy engines push the replicas
-  // while the FNV kernel hashes (default, fastest measured); 2 = one fused
+  // Snapshot transport (-1 = auto = 1, measured fastest for local and peer
+  // replicas; scripts/micro/push.cu: one copy engine drives 782 GB/s of
+  // NVLink egress, SM stores saturate at ~717 GB/s and need >= 48 SMs):
+  // 3 = pack kernel, then kPushSms SMs push the replicas with NVLink
+  // stores while the FNV kernel hashes on the other SMs; 1 = pack kernel,
+  // then copy engines push the replicas while the FNV kernel hashes; 2 = one fused
   // kernel gathers, stores (local record and replicas, NVLink stores for
   // peers) and hashes; 0 = the pack kernel stores the replicas, then the FNV
   // kernel.
-  int replica_mode = 1;
-  // the push may be split over kPushStreams copy streams (measured: more
-  // streams do not raise NVLink throughput and slow the concurrent hash)
+  int replica_mode = -1;
+  // one copy stream for the replica push (measured: more streams do not
+  // raise NVLink throughput and slow the concurrent hash)
   static constexpr int kPushStreams = 1;
+  // transport 3: SMs reserved for the replica push (the FNV kernel runs on the rest)
+  static constexpr int kPushSms = 16;
   cudaStream_t side[kPushStreams] = {};
   cudaEvent_t ev_packed = nullptr, ev_hashed = nullptr, ev_pushed[kPushStreams] = {};
   uint8_t* patch = nullptr;
@@ -186,7 +192,7 @@ struct mlck_blob {
     MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
     if (dev) MLCK_CUDA(cudaFree(dev));
     cap = align_up(n, kAlign);
-    MLCK_CUDA(cudaMalloc(&dev, cap));
+    dev_malloc(reinterpret_cast<void**>(&dev), cap);
   }
 };
 
@@ -344,43 +350,72 @@ void run_pack(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
     ctx->launches += 1;
     return;
   }
-  if (trailer && ctx->replica_mode == 1 && !out->replicas.empty() && body) {
-    // pack the local record; push it to every replica with the copy engines
-    // (NVLink for peers) on the side stream while the FNV kernel hashes it;
-    // the 8-byte trailer follows the hash.
+  int mode = ctx->replica_mode;
+  if (mode == -1) mode = 1;
+  if (trailer && mode == 3 && !out->replicas.empty() && body) {
+    // pack the local record; push it to the replicas with SM stores from
+    // kPushSms reserved SMs while the FNV kernel hashes on the others; the
+    // FNV kernel appends the trailer to every copy.
     pack::Dsts local{};
     local.p[0] = out->dev;
     local.n = 1;
     const int tp = ctx->tbegin("pack");
     launch_pack(segs, n_segs, body, local, ctx->stream);
     ctx->tend(tp);
-    ctx->launches += 1;
     MLCK_CUDA(cudaEventRecord(ctx->ev_packed, ctx->stream));
-    constexpr int kS = mlck_ctx::kPushStreams;
-    const uint64_t piece = align_up(div_up(body, kS), 4096);
-    for (int q = 0; q < kS; ++q) {
-      MLCK_CUDA(cudaStreamWaitEvent(ctx->side[q], ctx->ev_packed, 0));
-      const uint64_t lo = std::min<uint64_t>(body, q * piece), hi = std::min<uint64_t>(body, lo + piece);
-      if (hi > lo)
-        for (auto& r : out->replicas)
-          MLCK_CUDA(cudaMemcpyAsync(r.first + lo, out->dev + lo, hi - lo, cudaMemcpyDefault, ctx->side[q]));
-    }
+    MLCK_CUDA(cudaStreamWaitEvent(ctx->side[0], ctx->ev_packed, 0));
+    pack::Dsts peers{};
+    for (auto& r : out->replicas) peers.p[peers.n++] = r.first;
+    const int tq = ctx->tbegin("push", ctx->side[0]);
+    launch_push(out->dev, body, peers, mlck_ctx::kPushSms, ctx->side[0]);
+    ctx->tend(tq, ctx->side[0]);
+    TrailerDsts t{};
+    for (int r = 0; r < d.n; ++r) t.p[r] = d.p[r] + body;
+    t.n = d.n;
+    uint32_t* scratch = ctx->fnv_scratch_for(body);
+    const int tf = ctx->tbegin("fnv");
+    launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream, nullptr,
+               nullptr, nullptr, mlck_ctx::kPushSms);
+    ctx->tend(tf);
+    ctx->launches += 3;
+    MLCK_CUDA(cudaEventRecord(ctx->ev_pushed[0], ctx->side[0]));
+    MLCK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_pushed[0], 0));  // record complete everywhere
+    return;
+  }
+  if (trailer && (mode == 1 || mode == 4) && !out->replicas.empty() && body) {
+    // pack the local record; push it to every replica with the copy engines
+    // (NVLink for peers) on the side stream while the FNV kernel hashes it
+    // (mode 4, ablation: after the hash); the 8-byte trailer follows the hash.
+    pack::Dsts local{};
+    local.p[0] = out->dev;
+    local.n = 1;
+    const int tp = ctx->tbegin("pack");
+    launch_pack(segs, n_segs, body, local, ctx->stream);
+    ctx->tend(tp);
+    MLCK_CUDA(cudaEventRecord(ctx->ev_packed, ctx->stream));
     TrailerDsts t{};
     t.p[0] = out->dev + body;
     t.n = 1;
     uint32_t* scratch = ctx->fnv_scratch_for(body);
-    const int tf = ctx->tbegin("fnv");
-    launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream);
-    ctx->tend(tf);
-    ctx->launches += 1;
-    MLCK_CUDA(cudaEventRecord(ctx->ev_hashed, ctx->stream));
-    MLCK_CUDA(cudaStreamWaitEvent(ctx->side[0], ctx->ev_hashed, 0));
+    auto hash = [&] {
+      const int tf = ctx->tbegin("fnv");
+      launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream);
+      ctx->tend(tf);
+      MLCK_CUDA(cudaEventRecord(ctx->ev_hashed, ctx->stream));
+    };
+    if (mode == 4) hash();
+    cudaStream_t side = ctx->side[0];
+    MLCK_CUDA(cudaStreamWaitEvent(side, mode == 4 ? ctx->ev_hashed : ctx->ev_packed, 0));
+    const int tq = ctx->tbegin("push", side);
+    for (auto& r : out->replicas) ce_copy(r.first, out->dev, body, cudaMemcpyDefault, side);
+    ctx->tend(tq, side);
+    if (mode == 1) hash();
+    ctx->launches += 2;
+    MLCK_CUDA(cudaStreamWaitEvent(side, ctx->ev_hashed, 0));
     for (auto& r : out->replicas)
-      MLCK_CUDA(cudaMemcpyAsync(r.first + body, out->dev + body, 8, cudaMemcpyDefault, ctx->side[0]));
-    for (int q = 0; q < kS; ++q) {
-      MLCK_CUDA(cudaEventRecord(ctx->ev_pushed[q], ctx->side[q]));
-      MLCK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_pushed[q], 0));  // record complete everywhere
-    }
+      MLCK_CUDA(cudaMemcpyAsync(r.first + body, out->dev + body, 8, cudaMemcpyDefault, side));
+    MLCK_CUDA(cudaEventRecord(ctx->ev_pushed[0], side));
+    MLCK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_pushed[0], 0));  // record complete everywhere
     return;
   }
   const int tp = ctx->tbegin("pack");
@@ -664,8 +699,10 @@ uint64_t mlck_ctx_kernel_launches(mlck_ctx* c) { return c ? c->launches : 0; }
 
 int mlck_ctx_set_replica_mode(mlck_ctx* c, int mode) {
   return api([&] {
-    if (mode < 0 || mode > 2)
-      throw_invalid("replica mode must be 0 (pack-kernel stores), 1 (copy engines) or 2 (fused pack+hash+push)");
+    if (mode < -1 || mode > 4)
+      throw_invalid("replica mode must be -1 (auto), 0 (pack-kernel stores), 1 (copy engines), "
+                    "2 (fused pack+hash+push), 3 (SM push beside the hash) or 4 (copy engines "
+                    "after the hash)");
     c->replica_mode = mode;
   });
 }
@@ -721,7 +758,7 @@ int mlck_state_create(mlck_ctx* ctx, uint32_t n_ops, const uint64_t* pc, int cb,
       off += align_up(static_cast<uint64_t>(cb) * st->P[i] + 16, kAlign);
     }
     st->arena_bytes = std::max<uint64_t>(off, kAlign);
-    MLCK_CUDA(cudaMalloc(&st->arena, st->arena_bytes));
+    dev_malloc(reinterpret_cast<void**>(&st->arena), st->arena_bytes);
     MLCK_CUDA(cudaMemsetAsync(st->arena, 0, st->arena_bytes, ctx->stream));
     *out = st;
   });
@@ -859,7 +896,7 @@ int mlck_state_serialize(mlck_state* st, uint8_t* host_out, uint64_t cap, uint64
     SegmentBuilder b;
     build_state_image(st, b);
     run_pack(st->ctx, b, &tmp, false);
-    MLCK_CUDA(cudaMemcpyAsync(host_out, tmp.dev, n, cudaMemcpyDeviceToHost, st->ctx->stream));
+    ce_copy(host_out, tmp.dev, n, cudaMemcpyDeviceToHost, st->ctx->stream);
     MLCK_CUDA(cudaStreamSynchronize(st->ctx->stream));
     MLCK_CUDA(cudaFree(tmp.dev));
   });
@@ -903,7 +940,7 @@ int mlck_blob_to_host(const mlck_blob* b, uint8_t* host, uint64_t cap) {
     if (cap < b->size) throw_invalid("blob_to_host: buffer too small");
     b->ctx->activate();
     if (b->size)
-      MLCK_CUDA(cudaMemcpyAsync(host, b->dev, b->size, cudaMemcpyDeviceToHost, b->ctx->stream));
+      ce_copy(host, b->dev, b->size, cudaMemcpyDeviceToHost, b->ctx->stream);
     MLCK_CUDA(cudaStreamSynchronize(b->ctx->stream));
   });
 }
@@ -947,7 +984,7 @@ int mlck_snapshot_record_host(mlck_state* st, const uint32_t* active, uint32_t n
     if (!host_out) return;
     if (cap < n) throw_invalid("snapshot: host buffer too small");
     run_pack(st->ctx, b, scratch, true);
-    MLCK_CUDA(cudaMemcpyAsync(host_out, scratch->dev, n, cudaMemcpyDeviceToHost, st->ctx->stream));
+    ce_copy(host_out, scratch->dev, n, cudaMemcpyDeviceToHost, st->ctx->stream);
     MLCK_CUDA(cudaStreamSynchronize(st->ctx->stream));
   });
 }
@@ -1103,7 +1140,7 @@ int mlck_gradlog_create(mlck_ctx* ctx, uint32_t n_ops, const uint64_t* pc, uint3
     }
     g->per_iter = std::max<uint64_t>(g->per_iter, 64);
     g->cap = cap;
-    MLCK_CUDA(cudaMalloc(&g->pool, 4 * g->per_iter * cap));
+    dev_malloc(reinterpret_cast<void**>(&g->pool), 4 * g->per_iter * cap);
     g->ring_iter.assign(cap, -1);
     g->present.assign(cap, std::vector<uint8_t>(n_ops, 0));
     *out = g;
@@ -1410,7 +1447,7 @@ int mlck_event_elapsed_ms(mlck_ctx* ctx, int a, int b, float* ms) {
 int mlck_device_alloc(mlck_ctx* ctx, uint64_t bytes, void** ptr) {
   return api([&] {
     ctx->activate();
-    MLCK_CUDA(cudaMalloc(ptr, std::max<uint64_t>(bytes, 16)));
+    dev_malloc(ptr, std::max<uint64_t>(bytes, 16));
   });
 }
 int mlck_device_free(mlck_ctx* ctx, void* ptr) {

@@ -349,7 +349,8 @@ uint64_t fnv_chunk_bytes() { return fnv::kChunk; }
 
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
-                unsigned long long* prof, unsigned long long* trace, const FnvGather* gather) {
+                unsigned long long* prof, unsigned long long* trace, const FnvGather* gather,
+                int reserve_sms) {
   const uint64_t n_chunks = fnv_chunks(n);
   fnv::Scratch scr;
   scr.finished = scratch + 2;
@@ -383,7 +384,7 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
     if (per_sm < 1) throw Error(kCuda, "fnv_kernel does not fit on an SM");
     MLCK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  const uint64_t grid = std::min<uint64_t>(n_chunks, static_cast<uint64_t>(sms));
+  const uint64_t grid = std::min<uint64_t>(n_chunks, static_cast<uint64_t>(std::max(1, sms - reserve_sms)));
   fnv::Gather g{};
   if (gather) {
     g.segs = gather->segs;
@@ -662,6 +663,38 @@ __global__ void copy_kernel(uint4* dst, const uint4* src, uint64_t n_vec) {
     dst[i] = src[i];
 }
 }  // namespace
+
+namespace {
+// Replica push on a fixed set of SMs: one CTA per SM (the dynamic shared
+// memory request keeps any other CTA off it), 128-bit loads from the local
+// record and stores to every replica (peer pointers: NVLink stores).
+__global__ void __launch_bounds__(1024, 1)
+    push_kernel(const uint4* __restrict__ src, uint64_t n_vec, pack::Dsts d) {
+  for (uint64_t i = blockIdx.x * 1024ull + threadIdx.x; i < n_vec; i += gridDim.x * 1024ull) {
+    const uint4 v = ld_stream(src + i);
+#pragma unroll
+    for (int r = 0; r < pack::kMaxDst; ++r)
+      if (r < d.n) st_v4(d.p[r] + 16 * i, v);
+  }
+}
+}  // namespace
+
+void launch_push(const uint8_t* src, uint64_t bytes, const pack::Dsts& d, int ctas, cudaStream_t stream) {
+  static size_t smem = 0;
+  if (smem == 0) {
+    smem = 120 * 1024;  // > half an SM's shared memory: one CTA per SM
+    MLCK_CUDA(cudaFuncSetAttribute(push_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+  }
+  const uint64_t n_vec = bytes / 16;
+  if (n_vec)
+    push_kernel<<<ctas, 1024, smem, stream>>>(reinterpret_cast<const uint4*>(src), n_vec, d);
+  MLCK_CUDA(cudaGetLastError());
+  for (int r = 0; r < d.n; ++r)
+    if (bytes > n_vec * 16)
+      MLCK_CUDA(cudaMemcpyAsync(d.p[r] + n_vec * 16, src + n_vec * 16, bytes - n_vec * 16, cudaMemcpyDefault,
+                                stream));
+}
 
 void launch_copy16(void* dst, const void* src, uint64_t bytes, cudaStream_t stream) {
   const uint64_t n_vec = bytes / 16;

@@ -60,7 +60,9 @@ size_t fnv_scratch_words(uint64_t n);
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
                 unsigned long long* prof = nullptr, unsigned long long* trace = nullptr,
-                const FnvGather* gather = nullptr);
+                const FnvGather* gather = nullptr, int reserve_sms = 0);
+// Copy `bytes` from src to every dst with `ctas` CTAs of one SM each.
+void launch_push(const uint8_t* src, uint64_t bytes, const pack::Dsts& d, int ctas, cudaStream_t stream);
 void launch_fnv_empty(uint64_t seed, unsigned long long* result, const TrailerDsts& trailer,
                       cudaStream_t stream);
 void launch_pack(const pack::Segment* segs, int n_segs, uint64_t total, const pack::Dsts& d,

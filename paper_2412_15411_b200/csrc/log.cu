@@ -115,7 +115,7 @@ int mlck_log_create(mlck_ctx* ctx, int kind, int device, uint64_t capacity, mlck
       MLCK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&l->base), l->cap, cudaHostAllocPortable));
     } else {
       MLCK_CUDA(cudaSetDevice(l->device));
-      MLCK_CUDA(cudaMalloc(&l->base, l->cap));
+      dev_malloc(reinterpret_cast<void**>(&l->base), l->cap);
       MLCK_CUDA(cudaSetDevice(l->ctx_device));
       if (l->device != l->ctx_device) {
         const cudaError_t e = cudaDeviceEnablePeerAccess(l->device, 0);
@@ -195,11 +195,11 @@ int mlck_log_put(mlck_log* l, uint64_t it, uint32_t mb, uint32_t boundary, uint8
       if (l->kind == 0) {
         MLCK_CUDA(cudaMemcpyAsync(l->base + off, src, 4 * n, cudaMemcpyDeviceToHost, l->side));
       } else if (l->kind == 2) {  // copy engine (a peer's HBM over NVLink for an IPC ring)
-        MLCK_CUDA(cudaMemcpyAsync(l->base + off, src, 4 * n, cudaMemcpyDefault, l->side));
+        ce_copy(l->base + off, src, 4 * n, cudaMemcpyDefault, l->side);
       } else if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
         launch_copy16(l->base + off, src, 4 * n, l->side);
       } else {
-        MLCK_CUDA(cudaMemcpyAsync(l->base + off, src, 4 * n, cudaMemcpyDefault, l->side));
+        ce_copy(l->base + off, src, 4 * n, cudaMemcpyDefault, l->side);
       }
     }
     l->entries[k] = {off, n};

@@ -217,8 +217,10 @@ class Context:
         return int(lib().mlck_ctx_kernel_launches(self.h))
 
     def set_replica_mode(self, mode: int):
-        """1: pack, then copy engines overlapped with the hash (default);
-        2: fused gather+store+hash kernel; 0: pack-kernel stores, then hash."""
+        """-1 (default): auto (= 1, measured fastest); 1: pack, then
+        copy engines overlapped with the hash; 3: pack, then a push kernel on
+        reserved SMs overlapped with the hash; 2: fused gather+store+hash
+        kernel; 0: pack-kernel stores, then hash."""
         check(lib().mlck_ctx_set_replica_mode(self.h, mode))
 
     def set_timing(self, on: bool):

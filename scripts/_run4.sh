@@ -1,3 +1,3 @@
-python bench.py --steps 2 --warmup 3 --no-cpu --no-log --no-convert --no-parity > gpurun_out/plain.log 2>&1 || exit 1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:fnv_kernel -s 3 -c 1 -o gpurun_out/prof_fused python bench.py --steps 2 --warmup 3 --no-cpu --no-log --no-convert --no-parity > gpurun_out/ncu_fused.log 2>&1
-echo ncu rc=$?
+timeout 400 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+timeout 300 python bench.py > gpurun_out/bench1.log 2>gpurun_out/bench1.err; echo rc=$?
+timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 4 --steps 8 --warmup 3 > gpurun_out/bench4.log 2>gpurun_out/bench4.err; echo rc=$?

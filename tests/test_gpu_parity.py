@@ -121,15 +121,17 @@ def test_adam_goldens(mk, ctx):
 
 # ---------------------------------------------------------------- K1 snapshot
 # snapshot transports: 1 = pack kernel + copy-engine push + FNV kernel
-# (default), 2 = fused gather+store+hash kernel, 0 = pack-kernel replica stores
-MODES = [1, 2, 0]
+# (default for local replicas), 3 = pack kernel + SM push on reserved SMs
+# beside the FNV kernel (default for peer replicas), 2 = fused
+# gather+store+hash kernel, 0 = pack-kernel replica stores
+MODES = [1, 3, 2, 0]
 
 
 @pytest.fixture
 def mode(request, ctx):
     ctx.set_replica_mode(request.param)
     yield request.param
-    ctx.set_replica_mode(1)
+    ctx.set_replica_mode(-1)
 
 
 @pytest.mark.parametrize("mode", MODES, indirect=True)
