@@ -439,28 +439,31 @@ def run_ours(args, d: Dist):
         step(i)
     ctx.synchronize()
 
-    # ---- timed region (device events, barrier + sync both sides)
-    d.barrier()
-    ctx.synchronize()
+    # ---- timed region (device events, barrier + sync both sides).  The
+    # clock sampler starts first (it takes a variable time to deliver its
+    # first sample), so the barrier lines the ranks up on the region itself.
     with ClockSampler(dev) as clk:
+        d.barrier()
+        ctx.synchronize()
         ctx.event_record(0)
         for i in range(args.steps):
             step(i)
         ctx.event_record(1)
         ctx.synchronize()
-    d.barrier()
+        d.barrier()
     ms_local = ctx.event_ms(0, 1)
     ms = d.max(ms_local)
     bytes_local = sum(sizes[i % W] for i in range(args.steps))
     total_bytes = d.sum(bytes_local)
     value = total_bytes / (ms / 1000) / GB
-    launches = 2 * args.steps  # pack + FNV kernels per record (replica copies: copy engines)
+    launches = 2 * args.steps  # pack + FNV kernels per record (replica copies: pack stores / copy engines)
+    transport = 0 if d.world == 1 else 1  # what replica mode -1 (auto) picks here
 
-    # ---- per-kernel breakdown (CUDA events around each launch on the ctx
-    # stream) of the timed configuration -- transport 1: pack kernel, then
-    # the copy engines push the replicas while the FNV kernel hashes -- plus
-    # the other transports as ablations: (2) one fused kernel gathers, stores
-    # (record + replicas) and hashes; (0) the pack kernel stores the replicas.
+    # ---- per-kernel breakdown (CUDA events around each launch) of the timed
+    # configuration -- N=1, transport 0: the pack kernel writes the record and
+    # its local replica, then the FNV kernel hashes; N>1, transport 1: pack
+    # kernel, then the copy engines push to the ring peers while the FNV
+    # kernel hashes -- plus every other transport as a whole-step ablation.
     hbm_peak, peak_kind = peaks()
     payload = [payload_bytes(wl, slots[i % W]) for i in range(args.steps)]
     rec = [sizes[i % W] for i in range(args.steps)]
@@ -469,31 +472,37 @@ def run_ours(args, d: Dist):
     for i in range(args.steps):
         step(i)
     tim = ctx.timings()
-    ctx.set_replica_mode(2)
-    for i in range(args.steps):
-        step(i)
-    tim_fused = ctx.timings()
-    ctx.set_replica_mode(0)
-    for i in range(args.steps):
-        step(i)
-    tim_sm = ctx.timings()
     ctx.set_timing(False)
-    # transport 3 (push kernel on 16 reserved SMs beside the hash): whole-step time
-    ctx.set_replica_mode(3)
-    d.barrier()
-    ctx.synchronize()
-    ctx.event_record(0)
-    for i in range(args.steps):
-        step(i)
-    ctx.event_record(1)
-    ctx.synchronize()
-    d.barrier()
-    ms_t3 = d.max(ctx.event_ms(0, 1))
+
+    def step_ms(mode):
+        ctx.set_replica_mode(mode)
+        for i in range(2):
+            step(i)
+        d.barrier()
+        ctx.synchronize()
+        ctx.event_record(0)
+        for i in range(args.steps):
+            step(i)
+        ctx.event_record(1)
+        ctx.synchronize()
+        d.barrier()
+        return d.max(ctx.event_ms(0, 1)) / args.steps
+
+    names = {0: "pack kernel stores the replicas, then hash",
+             1: "pack, then copy-engine push beside the hash",
+             2: "one fused gather + store + hash kernel",
+             3: "pack, then a push kernel on 16 reserved SMs beside the hash",
+             4: "pack, hash, then copy-engine push (no overlap)",
+             5: "pack, then the hash kernel stores the replicas"}
+    ablations = {}
+    for m in names:
+        if m != transport:
+            t = step_ms(m)
+            ablations[f"transport {m}"] = {"ms_per_step": t, "value": total_bytes / (t * args.steps / 1000) / GB,
+                                           "what": names[m]}
     ctx.set_replica_mode(-1)
     pack_ms = [t for n, t in tim if n == "pack"]
     fnv_ms = [t for n, t in tim if n == "fnv"]
-    fused_ms = [t for n, t in tim_fused if n == "pack_fnv"]
-    pack_sm_ms = [t for n, t in tim_sm if n == "pack"]
     push_ms = [t for n, t in tim if n == "push"]
 
     def kstat(ms_list, total_bytes, note):
@@ -502,25 +511,16 @@ def run_ours(args, d: Dist):
                 "gbs": total_bytes / (sum(ms_list) / 1000) / GB, "bytes": note}
 
     kernels = {
-        "pack": kstat(pack_ms, sum(payload) + sum(rec), "HBM: payload read + record write"),
-        "push": kstat(push_ms, r * sum(rec), "replica copies on the copy engines, beside the hash ("
-                      + ("local HBM" if d.world == 1 else "NVLink egress") + ")"),
+        "pack": kstat(pack_ms, sum(payload) + (1 + local_rep) * sum(rec),
+                      "HBM: payload read + record write" + (f" + {local_rep} local replica write" if local_rep else "")),
         "fnv": kstat(fnv_ms, sum(rec), "HBM: record read (ALU-bound 8-bit automaton)"),
-        "ablation_fused_pack_fnv (transport 2)": kstat(
-            fused_ms, sum(payload) + (1 + local_rep) * sum(rec),
-            "HBM: payload read + record write" + (f" + {local_rep} local replica write"
-                                                  if local_rep else f" (+{r}x record over NVLink)")),
-        "ablation_pack_with_replica_stores (transport 0)": kstat(
-            pack_sm_ms, sum(payload) + (1 + local_rep) * sum(rec),
-            "HBM: payload read + local writes" + ("" if d.world == 1 else f" (+{r}x record over NVLink)")),
-        "ablation_sm_push_step (transport 3)": {
-            "ms_per_step": ms_t3 / args.steps, "value": total_bytes / (ms_t3 / 1000) / GB,
-            "note": "whole step, pack + push kernel on 16 reserved SMs concurrent with the hash on the rest"},
     }
+    if push_ms:
+        kernels["push"] = kstat(push_ms, r * sum(rec), "replica copies on the copy engines beside the hash (NVLink egress)")
     kd = kernels["fnv"]
     ach = kd["bytes_per_launch"] / (kd["ms_avg"] / 1000) / GB
     traffic, traffic_src = ncu_traffic("fnv_kernel")
-    roofline = {"bound": "hbm", "kernel": "fnv", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+    roofline = {"bound": "hbm", "kernel": "fnv", "transport": transport, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                 "frac": ach / hbm_peak, "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
                 "per_launch_bytes": kd["bytes_per_launch"],
                 "note": "dominant kernel of the step (the pack kernel alone: kernels['pack']); it is bound by the "
@@ -675,6 +675,7 @@ def run_ours(args, d: Dist):
             "roofline": roofline,
             "roofline_nvlink": roofline_nvlink,
             "kernels": kernels,
+            "transport_ablations": ablations,
             "conversion": conv,
             "logging": logging,
             "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": h2d // e2e_steps,

@@ -78,13 +78,15 @@ uint64_t mlck_ctx_kernel_launches(mlck_ctx* ctx);
  * fnv_verify, walk, replay).  mlck_ctx_timings synchronizes, returns the
  * labels as CSV and the durations (ms) recorded since the last read. */
 int mlck_ctx_set_timing(mlck_ctx* ctx, int on);
-/* Snapshot transport.  -1 (default) auto: 1 (measured fastest for local and
- * peer replicas).  1: pack kernel, then copy engines push the record while the
- * FNV kernel hashes it.  3: pack kernel, then a push kernel on reserved SMs
- * stores the record to the replicas (NVLink stores for peers) while the FNV
- * kernel hashes it on the other SMs.  2: one fused kernel gathers the record
- * from the state arena, stores it to the blob and every replica and hashes
- * it.  0: the pack kernel stores the replicas, then the FNV kernel. */
+/* Snapshot transport.  -1 (default) auto: 0 when every replica is in this
+ * GPU's HBM, else 1.  1: pack kernel, then copy engines push the record
+ * while the FNV kernel hashes it.  5: pack kernel, then the FNV kernel
+ * stores the replicas from the bytes it stages (no second read).  3: pack
+ * kernel, then a push kernel on reserved SMs stores the record to the
+ * replicas while the FNV kernel hashes it on the other SMs.  2: one fused
+ * kernel gathers the record from the state arena, stores it to the blob and
+ * every replica and hashes it.  0: the pack kernel stores the replicas, then
+ * the FNV kernel.  4: copy engines after the hash (no overlap). */
 int mlck_ctx_set_replica_mode(mlck_ctx* ctx, int mode);
 int mlck_ctx_timings(mlck_ctx* ctx, char* labels_csv, uint64_t labels_cap, float* ms,
                      uint32_t cap, uint32_t* n);

@@ -12,6 +12,8 @@
 #include <tuple>
 #include <vector>
 
+#include <cuda.h>
+
 #include "../../include/mlck_b200.h"
 #include "kernels.cuh"
 
@@ -41,6 +43,15 @@ constexpr uint32_t kMagic = 0x4b434c4du;
 // =========================================================================
 struct mlck_ctx {
   int device = 0;
+  // device ranges opened through CUDA IPC (another GPU's memory: pointer
+  // attributes report the mapping device, not the owner)
+  std::vector<std::pair<uint64_t, uint64_t>> ipc_ranges;
+  bool is_ipc(const void* p) const {
+    const uint64_t a = reinterpret_cast<uint64_t>(p);
+    for (const auto& r : ipc_ranges)
+      if (a >= r.first && a < r.first + r.second) return true;
+    return false;
+  }
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   uint64_t launches = 0;
@@ -112,9 +123,12 @@ struct mlck_ctx {
     s.used = true;
   }
   uint32_t fnv_epoch = 0;
-  // Snapshot transport (-1 = auto = 1, measured fastest for local and peer
-  // replicas; scripts/micro/push.cu: one copy engine drives 782 GB/s of
-  // NVLink egress, SM stores saturate at ~717 GB/s and need >= 48 SMs):
+  // Snapshot transport (-1 = auto: 0 for replicas in local HBM, 1 for peer
+  // replicas -- scripts/micro/push.cu: one copy engine drives 782 GB/s of
+  // NVLink egress, SM stores saturate at ~717 GB/s and need >= 48 SMs; a
+  // local copy-engine copy beside the hash contends with it (2.3 ms vs 0.6
+  // ms alone), while the pack kernel writes the local replica for +0.24 ms):
+  // 5 = pack kernel, then the FNV kernel stores the replicas as it hashes;
   // 3 = pack kernel, then kPushSms SMs push the replicas with NVLink
   // stores while the FNV kernel hashes on the other SMs; 1 = pack kernel,
   // then copy engines push the replicas while the FNV kernel hashes; 2 = one fused
@@ -128,7 +142,10 @@ struct mlck_ctx {
   // transport 3: SMs reserved for the replica push (the FNV kernel runs on the rest)
   static constexpr int kPushSms = 16;
   cudaStream_t side[kPushStreams] = {};
-  cudaEvent_t ev_packed = nullptr, ev_hashed = nullptr, ev_pushed[kPushStreams] = {};
+  // transport 1: the record is packed in up to kPieces pieces of >= 64 MiB,
+  // each pushed as soon as it is packed
+  static constexpr int kPieces = 4;
+  cudaEvent_t ev_packed = nullptr, ev_hashed = nullptr, ev_pushed[kPushStreams] = {}, ev_piece[kPieces] = {};
   uint8_t* patch = nullptr;
   uint64_t patch_cap = 0;
   uint8_t* patch_for(uint64_t bytes) {
@@ -351,7 +368,39 @@ void run_pack(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
     return;
   }
   int mode = ctx->replica_mode;
-  if (mode == -1) mode = 1;
+  if (mode == -1) {  // auto: 0 when every replica is in this GPU's HBM, else 1
+    mode = 0;
+    for (auto& r : out->replicas) {
+      cudaPointerAttributes a{};
+      if (ctx->is_ipc(r.first) || cudaPointerGetAttributes(&a, r.first) != cudaSuccess ||
+          a.type != cudaMemoryTypeDevice || a.device != ctx->device)
+        mode = 1;
+    }
+    cudaGetLastError();
+  }
+  if (trailer && mode == 5 && !out->replicas.empty() && body) {
+    // pack the local record; the FNV kernel stores the replicas from the
+    // bytes it stages in shared memory (coalesced warp stores) and appends
+    // the trailer to every copy -- no second read of the record
+    pack::Dsts local{};
+    local.p[0] = out->dev;
+    local.n = 1;
+    const int tp = ctx->tbegin("pack");
+    launch_pack(segs, n_segs, body, local, ctx->stream);
+    ctx->tend(tp);
+    pack::Dsts reps{};
+    for (auto& r : out->replicas) reps.p[reps.n++] = r.first;
+    TrailerDsts t{};
+    for (int r = 0; r < d.n; ++r) t.p[r] = d.p[r] + body;
+    t.n = d.n;
+    uint32_t* scratch = ctx->fnv_scratch_for(body);
+    const int tf = ctx->tbegin("fnv");
+    launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream, nullptr,
+               nullptr, nullptr, 0, &reps);
+    ctx->tend(tf);
+    ctx->launches += 2;
+    return;
+  }
   if (trailer && mode == 3 && !out->replicas.empty() && body) {
     // pack the local record; push it to the replicas with SM stores from
     // kPushSms reserved SMs while the FNV kernel hashes on the others; the
@@ -383,16 +432,17 @@ void run_pack(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
     return;
   }
   if (trailer && (mode == 1 || mode == 4) && !out->replicas.empty() && body) {
-    // pack the local record; push it to every replica with the copy engines
-    // (NVLink for peers) on the side stream while the FNV kernel hashes it
-    // (mode 4, ablation: after the hash); the 8-byte trailer follows the hash.
+    // pack the local record in pieces; the copy engines push each piece to
+    // every replica (NVLink for peers) on the side stream as soon as it is
+    // packed, beside the rest of the pack and the FNV kernel (mode 4,
+    // ablation: the whole push after the hash); the 8-byte trailer follows
+    // the hash.
     pack::Dsts local{};
     local.p[0] = out->dev;
     local.n = 1;
-    const int tp = ctx->tbegin("pack");
-    launch_pack(segs, n_segs, body, local, ctx->stream);
-    ctx->tend(tp);
-    MLCK_CUDA(cudaEventRecord(ctx->ev_packed, ctx->stream));
+    cudaStream_t side = ctx->side[0];
+    const int pieces = mode == 1 ? static_cast<int>(std::min<uint64_t>(mlck_ctx::kPieces, div_up(body, 64ull << 20))) : 1;
+    const uint64_t piece = align_up(div_up(body, pieces), 64ull << 10);  // tile- and copy-engine friendly
     TrailerDsts t{};
     t.p[0] = out->dev + body;
     t.n = 1;
@@ -403,14 +453,30 @@ void run_pack(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
       ctx->tend(tf);
       MLCK_CUDA(cudaEventRecord(ctx->ev_hashed, ctx->stream));
     };
-    if (mode == 4) hash();
-    cudaStream_t side = ctx->side[0];
-    MLCK_CUDA(cudaStreamWaitEvent(side, mode == 4 ? ctx->ev_hashed : ctx->ev_packed, 0));
-    const int tq = ctx->tbegin("push", side);
-    for (auto& r : out->replicas) ce_copy(r.first, out->dev, body, cudaMemcpyDefault, side);
+    const int tp = ctx->tbegin("pack");
+    int tq = -1;
+    for (int q = 0; q < pieces; ++q) {
+      const uint64_t lo = std::min<uint64_t>(body, q * piece), hi = std::min<uint64_t>(body, lo + piece);
+      if (hi <= lo) break;
+      launch_pack(segs, n_segs, hi, local, ctx->stream, lo);
+      ctx->launches += 1;
+      if (mode == 1) {
+        MLCK_CUDA(cudaEventRecord(ctx->ev_piece[q], ctx->stream));
+        MLCK_CUDA(cudaStreamWaitEvent(side, ctx->ev_piece[q], 0));
+        if (q == 0) tq = ctx->tbegin("push", side);
+        for (auto& r : out->replicas) ce_copy(r.first + lo, out->dev + lo, hi - lo, cudaMemcpyDefault, side);
+      }
+    }
+    ctx->tend(tp);
+    if (mode == 4) {
+      hash();
+      MLCK_CUDA(cudaStreamWaitEvent(side, ctx->ev_hashed, 0));
+      tq = ctx->tbegin("push", side);
+      for (auto& r : out->replicas) ce_copy(r.first, out->dev, body, cudaMemcpyDefault, side);
+    }
     ctx->tend(tq, side);
     if (mode == 1) hash();
-    ctx->launches += 2;
+    ctx->launches += 1;
     MLCK_CUDA(cudaStreamWaitEvent(side, ctx->ev_hashed, 0));
     for (auto& r : out->replicas)
       MLCK_CUDA(cudaMemcpyAsync(r.first + body, out->dev + body, 8, cudaMemcpyDefault, side));
@@ -648,6 +714,7 @@ int mlck_ctx_create(int device, mlck_ctx** out) {
     for (cudaEvent_t* e : {&c->ev_packed, &c->ev_hashed})
       MLCK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (auto& e : c->ev_pushed) MLCK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : c->ev_piece) MLCK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : c->ev) MLCK_CUDA(cudaEventCreate(&e));
     MLCK_CUDA(cudaMalloc(&c->results, 64 * 8));
     MLCK_CUDA(cudaMallocHost(&c->host_results, 64 * 8));
@@ -672,7 +739,15 @@ int mlck_ctx_destroy(mlck_ctx* c) {
       if (s.dev) cudaFree(s.dev);
       cudaEventDestroy(s.done);
     }
+    for (auto& sd : c->side) {
+      cudaStreamSynchronize(sd);
+      cudaStreamDestroy(sd);
+    }
     for (auto& e : c->ev) cudaEventDestroy(e);
+    for (auto& e : c->ev_pushed) cudaEventDestroy(e);
+    for (auto& e : c->ev_piece) cudaEventDestroy(e);
+    cudaEventDestroy(c->ev_packed);
+    cudaEventDestroy(c->ev_hashed);
     if (c->fnv_scratch) cudaFree(c->fnv_scratch);
     if (c->patch) cudaFree(c->patch);
     cudaFree(c->results);
@@ -699,10 +774,10 @@ uint64_t mlck_ctx_kernel_launches(mlck_ctx* c) { return c ? c->launches : 0; }
 
 int mlck_ctx_set_replica_mode(mlck_ctx* c, int mode) {
   return api([&] {
-    if (mode < -1 || mode > 4)
+    if (mode < -1 || mode > 5)
       throw_invalid("replica mode must be -1 (auto), 0 (pack-kernel stores), 1 (copy engines), "
-                    "2 (fused pack+hash+push), 3 (SM push beside the hash) or 4 (copy engines "
-                    "after the hash)");
+                    "2 (fused pack+hash+push), 3 (SM push beside the hash), 4 (copy engines "
+                    "after the hash) or 5 (hash-kernel stores)");
     c->replica_mode = mode;
   });
 }
@@ -1411,11 +1486,27 @@ int mlck_ipc_open(mlck_ctx* ctx, const uint8_t handle[64], void** ptr) {
     cudaIpcMemHandle_t h;
     std::memcpy(&h, handle, 64);
     MLCK_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static GetRange get_range = nullptr;
+    if (!get_range) {
+      cudaDriverEntryPointQueryResult q{};
+      MLCK_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", reinterpret_cast<void**>(&get_range),
+                                        cudaEnableDefault, &q));
+      if (q != cudaDriverEntryPointSuccess || !get_range) throw Error(kCuda, "cuMemGetAddressRange unavailable");
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(*ptr)) != CUDA_SUCCESS)
+      throw Error(kCuda, "cuMemGetAddressRange failed on an IPC mapping");
+    ctx->ipc_ranges.emplace_back(static_cast<uint64_t>(base), static_cast<uint64_t>(size));
   });
 }
 int mlck_ipc_close(mlck_ctx* ctx, void* ptr) {
   return api([&] {
     ctx->activate();
+    const uint64_t a = reinterpret_cast<uint64_t>(ptr);
+    auto& v = ctx->ipc_ranges;
+    v.erase(std::remove_if(v.begin(), v.end(), [&](const auto& r) { return r.first == a; }), v.end());
     MLCK_CUDA(cudaIpcCloseMemHandle(ptr));
   });
 }

@@ -53,6 +53,18 @@ constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
 #ifndef MLCK_FNV_WARPS
 #define MLCK_FNV_WARPS 16
 #endif
+// MLCK_FNV_MMA: final pass as int8 tensor-core dot products (see mma_pass);
+// 0 = the byte-serial 64-bit recurrence.  MLCK_FNV_NOSHIFT: rounds 2-3 keep
+// segments B, D in the odd byte lanes (no shift of the data word).
+#ifndef MLCK_FNV_MMA
+#define MLCK_FNV_MMA 1
+#endif
+#ifndef MLCK_FNV_ROUND0_LINEAR
+#define MLCK_FNV_ROUND0_LINEAR 1
+#endif
+#ifndef MLCK_FNV_NOSHIFT
+#define MLCK_FNV_NOSHIFT 1
+#endif
 constexpr int kSlots = MLCK_FNV_SLOTS;         // chunks in flight per CTA
 constexpr int kComputeWarps = MLCK_FNV_WARPS;  // + one look-back warp per slot
 constexpr int kWarps = kComputeWarps + kSlots;
@@ -213,11 +225,44 @@ __device__ __forceinline__ void round_maps_low(const uint32_t (&w)[kThreadWords]
   for (int i = 0; i < kSegs; ++i)
     map[i] = ((e0 >> (8 * i)) & 3u) | (((e1 >> (8 * i)) & 2u) << 1);
 }
+// Round 0 without the automaton: bits 0 and 1 of the state evolve linearly
+// (0xb3 = 3 mod 4: u0' = u0 ^ b0, u1' = u1 ^ b1 ^ u0 ^ b0).  Over a 32-byte
+// segment (even length, so the start bit 0 cancels in the bit-1 sum):
+//   a = parity of the b0 bits,  b0 = b1 = parity of the b1 bits ^ parity of
+//   the b0 bits at odd positions.
+__device__ __forceinline__ void round0_maps(const uint32_t (&w)[kThreadWords], uint32_t (&map)[kSegs]) {
+  uint32_t xe = 0, xo = 0;
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {
+    xe ^= w[k];
+    xo ^= w[k + 1];
+  }
+  const uint32_t xa = xe ^ xo;
+  const uint32_t t = (xa >> 1) ^ xo;  // lane bit 0: the bit-1 toggle
+#pragma unroll
+  for (int i = 0; i < kSegs; ++i) map[i] = ((xa >> (8 * i)) & 1u) | (((t >> (8 * i)) & 1u) * 6u);
+}
 __device__ __forceinline__ void round_maps_high(const uint32_t (&w)[kThreadWords], uint32_t st, int r,
                                                 uint32_t (&map)[kSegs]) {
   const uint32_t bit = 1u << (2 * r);
   constexpr uint32_t M = 0x00ff00ffu;
   const uint32_t lo = st & ((bit - 1u) * 0x01010101u);
+#if MLCK_FNV_NOSHIFT
+  // {A, C} in byte lanes 0 and 2, {B, D} in lanes 1 and 3 of their own
+  // register: B's product spills into lane 2 (masked off by the next step)
+  // and never carries into lane 3, D's high bits fall off the word.
+  uint32_t ac0 = lo & M, bd0 = lo & ~M;
+  uint32_t ac1 = ac0 | (bit * 0x00010001u), bd1 = bd0 | (bit * 0x01000100u);
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t y = w[k];
+    ac0 = ((ac0 ^ y) & M) * 0xb3u;
+    ac1 = ((ac1 ^ y) & M) * 0xb3u;
+    bd0 = ((bd0 ^ y) & ~M) * 0xb3u;
+    bd1 = ((bd1 ^ y) & ~M) * 0xb3u;
+  }
+  const uint32_t a0 = ac0 >> (2 * r), a1 = ac1 >> (2 * r), b0 = bd0 >> (2 * r + 8), b1 = bd1 >> (2 * r + 8);
+#else
   uint32_t ac0 = lo & M, bd0 = (lo >> 8) & M;
   uint32_t ac1 = ac0 | (bit * 0x00010001u), bd1 = bd0 | (bit * 0x00010001u);
 #pragma unroll
@@ -230,6 +275,7 @@ __device__ __forceinline__ void round_maps_high(const uint32_t (&w)[kThreadWords
     bd1 = ((bd1 ^ yb) & M) * 0xb3u;
   }
   const uint32_t a0 = ac0 >> (2 * r), a1 = ac1 >> (2 * r), b0 = bd0 >> (2 * r), b1 = bd1 >> (2 * r);
+#endif
   map[0] = (a0 & 3u) | ((a1 & 2u) << 1);
   map[1] = (b0 & 3u) | ((b1 & 2u) << 1);
   map[2] = ((a0 >> 16) & 3u) | (((a1 >> 16) & 2u) << 1);
@@ -351,6 +397,10 @@ struct alignas(16) Shared {
   uint32_t wmap[kSlots][32];    // warp maps of the round (compute -> look-back)
   uint32_t wstart[kSlots][32];  // warp start bits (look-back -> compute)
   unsigned long long red[32];
+#if MLCK_FNV_MMA
+  uint2 wfrag[2][4][32];        // mma_pass B fragments: [data | automaton][k-block][lane]
+  unsigned long long kpos[32][4];  // mma_pass epilogue weights per lane
+#endif
 };
 constexpr size_t kSmemBytes = sizeof(Shared);
 static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
@@ -396,12 +446,25 @@ __device__ __forceinline__ void mbar_init(unsigned long long* m, uint32_t count)
 __device__ __forceinline__ void mbar_arrive(unsigned long long* m) {
   asm volatile("{ .reg .b64 st; mbarrier.arrive.shared.b64 st, [%0]; }" ::"r"(smem_addr(m)) : "memory");
 }
+#ifndef MLCK_MBAR_SUSPEND_NS
+#define MLCK_MBAR_SUSPEND_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(unsigned long long* m, uint32_t parity) {
+#if MLCK_MBAR_SUSPEND_NS
+  // the waiting warp is suspended until the phase completes (or the hint
+  // expires) instead of spinning on issue slots the compute warps need
+  asm volatile(
+      "{ .reg .pred p; W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1, %2; @!p bra W; }" ::"r"(
+          smem_addr(m)),
+      "r"(parity), "n"(MLCK_MBAR_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{ .reg .pred p; W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1; @!p bra W; }" ::"r"(
           smem_addr(m)),
       "r"(parity)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
@@ -494,6 +557,93 @@ __device__ __forceinline__ void read_thread(const Shared& sh, int slot, int t, u
 // The thread's 128 bytes from its unaligned gather window (phase 1..15):
 // nine 128-bit loads, then a word select (warp-uniform in practice: the
 // windows of a segment share its alignment) and a byte funnel, in place.
+#if MLCK_FNV_MMA
+// ---- final pass on the tensor cores.  With d_p = (u_p ^ b_p) - u_p, where
+// u_p is the low byte of the hash before byte p, the recurrence unrolls to
+//   h_N = P^N h_0 + sum_p P^(N-p) d_p,   d_p = b_p - 2 (u_p & b_p),
+// two dot products of byte vectors with powers of P.  Splitting each weight
+// into eight 8-bit limbs turns them into u8 x u8 -> s32 MMAs.  Per warp
+// (128 segments of 32 bytes, span end E_w) the MMA computes
+//   C[j][n] = sum_seg x_{seg,j} limb_n(P^(E_w - end_seg))  (j = byte in segment)
+// with A = the interleaved words as they sit in shared memory: word j of a
+// thread holds byte j of its four segments, i.e. four consecutive k of one
+// row of A.  Rows are permuted so a lane's a0/a1 of both row blocks are one
+// 16-byte granule: row g <-> byte 4g + 2rb, row g + 8 <-> byte 4g + 2rb + 1.
+// k-block kb takes a0 from thread 8kb + 2q and a2 from thread 8kb + 2q + 1
+// (conflict-free with the 9-granule stride).  The automaton vector uses the
+// limbs of -2 P^(...) into the same accumulators; the epilogue applies
+// P^(32 - j) and the limb shifts.  Every accumulator entry stays below
+// 2 * 128 * 255 * 255 < 2^25.
+__device__ __forceinline__ void mma_u8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                       uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// segment (of the warp's 128) behind k of k-block kb
+__host__ __device__ constexpr int mma_segment(int kb, int k) {
+  return 32 * kb + 8 * ((k & 15) >> 2) + ((k >> 4) << 2) + (k & 3);
+}
+// One pass over the warp's 32 threads' words of the slot (after __syncwarp).
+__device__ __forceinline__ void mma_pass(const Shared& sh, int slot, int warp, int lane, int tab,
+                                         int (&acc)[2][4]) {
+  const int g = lane >> 2, q = lane & 3, t0 = 32 * warp + 2 * q;
+#pragma unroll
+  for (int kb = 0; kb < 4; ++kb) {
+    const uint4 lo = sh.data[slot][granule(t0 + 8 * kb, g)];
+    const uint4 hi = sh.data[slot][granule(t0 + 8 * kb + 1, g)];
+    const uint2 b = sh.wfrag[tab][kb][lane];
+    mma_u8(acc[0], lo.x, lo.y, hi.x, hi.y, b.x, b.y);
+    mma_u8(acc[1], lo.z, lo.w, hi.z, hi.w, b.x, b.y);
+  }
+}
+// Tables (once per CTA): B fragments and epilogue weights.
+__device__ __forceinline__ void mma_tables(Shared& sh, int tid) {
+  if (tid < 2 * 4 * 32) {
+    const int tab = tid >> 7, kb = (tid >> 5) & 3, lane = tid & 31, n = lane >> 2, q = lane & 3;
+    uint32_t b[2] = {0, 0};
+    for (int h = 0; h < 2; ++h)
+      for (int e = 0; e < 4; ++e) {
+        const int seg = mma_segment(kb, 16 * h + 4 * q + e);
+        uint64_t wgt = pow_u64(kPrime, 32ull * (127 - seg));
+        if (tab) wgt *= ~1ull;  // -2 P^(...) mod 2^64
+        b[h] |= static_cast<uint32_t>((wgt >> (8 * n)) & 0xffu) << (8 * e);
+      }
+    sh.wfrag[tab][kb][lane] = make_uint2(b[0], b[1]);
+  } else if (tid < 2 * 4 * 32 + 32 * 4) {
+    const int i = tid - 256, lane = i >> 2, m = i & 3, g = lane >> 2, q = lane & 3;
+    sh.kpos[lane][m] = pow_u64(kPrime, 32 - (4 * g + m)) << (16 * q);
+  }
+}
+// The warp's sum_p P^(E_w - p) d_p (this lane's share) from the accumulators.
+__device__ __forceinline__ uint64_t mma_epilogue(const Shared& sh, int lane, const int (&acc)[2][4]) {
+  uint64_t t = 0;
+#pragma unroll
+  for (int rb = 0; rb < 2; ++rb) {
+    const uint64_t v0 = static_cast<uint64_t>(static_cast<uint32_t>(acc[rb][1])) * 256u +
+                        static_cast<uint32_t>(acc[rb][0]);
+    const uint64_t v1 = static_cast<uint64_t>(static_cast<uint32_t>(acc[rb][3])) * 256u +
+                        static_cast<uint32_t>(acc[rb][2]);
+    t += v0 * sh.kpos[lane][2 * rb] + v1 * sh.kpos[lane][2 * rb + 1];
+  }
+  return t;
+}
+// The automaton from the segment starts (st byte i = segment i), leaving
+// u & b in place of the bytes: w[k] <- u_k & w[k] for all four segments.
+__device__ __forceinline__ void automaton_and(uint32_t (&w)[kThreadWords], uint32_t st) {
+  constexpr uint32_t M = 0x00ff00ffu;
+  uint32_t ac = st & M, bd = st & ~M;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t y = w[k];
+    w[k] = ((ac & M) | (bd & ~M)) & y;
+    ac = ((ac ^ y) & M) * 0xb3u;
+    bd = ((bd ^ y) & ~M) * 0xb3u;
+  }
+}
+#endif
+
 __device__ __forceinline__ void read_thread_unaligned(const Shared& sh, int slot, int t, uint32_t ph,
                                                      uint32_t (&w)[kThreadWords]) {
   uint32_t x[kThreadWords + 4];

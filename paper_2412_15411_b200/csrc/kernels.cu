@@ -49,7 +49,12 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
                                                 const fnv::Gather& gth) {
   using namespace fnv;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#if MLCK_FNV_MMA
+  // P^-(end of the warp's span in the chunk)
+  const uint64_t pinv_t = pow_u64(kPrimeInv, static_cast<uint64_t>(kThreadBytes) * 32 * (warp + 1));
+#else
   const uint64_t pinv_t = pow_u64(kPrimeInv, static_cast<uint64_t>(kThreadBytes) * (tid + 1));
+#endif
   int64_t chunk[kSlots];
   int rnd[kSlots];
   bool pend[kSlots];
@@ -76,7 +81,8 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
   }
   (void)warp;
   // [0] rounds, [1] waits for look-back results, [2] final passes, [3] other
-  Laps<kProf, 4> lap;
+  // [4] refill issue, [5] round-0 data wait, [6] mma + automaton part of the final pass
+  Laps<kProf, 7> lap;
   lap.start();
   for (bool any = true; any;) {
     any = false;
@@ -100,6 +106,23 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
         lap.mark(1);
         pend[s] = false;
         if (++rnd[s] == kRounds) {
+#if MLCK_FNV_MMA
+          // ---- final pass: sum_p P^(E_w - p) (b_p - 2 (u_p & b_p)) on the
+          // tensor cores (bytes past n are zero and contribute nothing)
+          {
+            int mac[2][4] = {};
+            mma_pass(sh, s, warp, lane, 0, mac);  // the data vector
+            uint32_t w[kThreadWords];
+            read_thread(sh, s, tid, w);
+            automaton_and(w, st[s]);
+            __syncwarp();  // every lane has read the data words
+            write_thread(sh, s, tid, w);
+            __syncwarp();
+            mma_pass(sh, s, warp, lane, 1, mac);  // the u & b vector, weights -2 P^(...)
+            acc += mma_epilogue(sh, lane, mac) * (pinv_t * chunk_weight(chunk[s]));
+          }
+          lap.mark(6);
+#else
           // ---- final pass: the real recurrence from each segment's start
           uint32_t w[kThreadWords];
           read_thread(sh, s, tid, w);
@@ -136,7 +159,9 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
             *scr.ulast = lo & 0xffu;
             __threadfence();
           }
+#endif
           if (kProf && scr.trace && tid == 0) scr.trace[chunk[s] * 12 + 9] = gtimer();
+          lap.mark(2);
           // ---- refill (thread-private granules: no CTA barrier needed); the
           // bytes land while the other slots take their turns
           const int64_t nx = chunk[s] + stride;
@@ -150,13 +175,15 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
             else
               load_thread(sh, s, tid, data, n, chunk[s]);
           }
-          lap.mark(2);
+          lap.mark(4);
           continue;
         }
       }
       // ---- compute and publish round rnd[s]
       if (rnd[s] == 0) {
+        lap.mark(0);
         fnv::mbar_wait(&sh.mbar[s][warp], (par >> s) & 1u);
+        lap.mark(5);
         if (kProf && scr.trace && tid == 0) {
           scr.trace[chunk[s] * 12 + 0] = gtimer();
           scr.trace[chunk[s] * 12 + 10] = smid();
@@ -174,12 +201,18 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
           store_warp_region(sh, s, tid, gth,
                             static_cast<uint64_t>(chunk[s]) * kChunk + static_cast<uint64_t>(tid - lane) * kThreadBytes, n);
           __syncwarp();
+        } else if (gth.n_dst) {  // replica copies written from the landed bytes
+          store_warp_region(sh, s, tid, gth,
+                            static_cast<uint64_t>(chunk[s]) * kChunk + static_cast<uint64_t>(tid - lane) * kThreadBytes, n);
+          __syncwarp();  // the warp's granules are read before they are interleaved in place
         }
         interleave(w);  // fresh bytes: interleave the segments once, in place
         write_thread(sh, s, tid, w);
       }
       uint32_t m[kSegs];
-      if (rnd[s] < 2)
+      if (MLCK_FNV_ROUND0_LINEAR && rnd[s] == 0)
+        round0_maps(w, m);
+      else if (rnd[s] < 2)
         round_maps_low(w, st[s], rnd[s], m);
       else
         round_maps_high(w, st[s], rnd[s], m);
@@ -203,6 +236,9 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
     atomicAdd(scr.prof + 3, static_cast<unsigned long long>(lap.t[1]));
     atomicAdd(scr.prof + 4, static_cast<unsigned long long>(lap.t[2]));
     atomicAdd(scr.prof + 6, static_cast<unsigned long long>(lap.t[3]));
+    atomicAdd(scr.prof + 16, static_cast<unsigned long long>(lap.t[4]));
+    atomicAdd(scr.prof + 17, static_cast<unsigned long long>(lap.t[5]));
+    atomicAdd(scr.prof + 20, static_cast<unsigned long long>(lap.t[6]));
   }
   return acc;
 }
@@ -280,6 +316,9 @@ __global__ void __launch_bounds__(fnv::kThreads, 1)
       for (int w = 0; w < kComputeWarps; ++w) mbar_init(&sh.mbar[s][w], 32);
       mbar_init(&sh.res[s], 1);
     }
+#if MLCK_FNV_MMA
+  mma_tables(sh, tid);
+#endif
   __syncthreads();
   // Slot-major chunk order: generation g of slot s on CTA i is chunk
   // (g*kSlots + s)*G + i, so the compute warps' turn order is the chunk order
@@ -316,7 +355,12 @@ __global__ void __launch_bounds__(fnv::kThreads, 1)
       __threadfence();
       const uint64_t total = atomicAdd(scr.accum, 0ull);
       const uint32_t u = atomicAdd(scr.ulast, 0u);
+#if MLCK_FNV_MMA
+      (void)u;
+      const uint64_t h = pow_p(n) * (total + seed);
+#else
       const uint64_t h = pow_p(n) * (total + (seed & ~0xffull)) + u;
+#endif
       *scr.result = atomicAdd(scr.error, 0u) ? 0ull : h;
       for (int r = 0; r < trailer.n; ++r)
         for (int b = 0; b < 8; ++b) trailer.p[r][b] = static_cast<uint8_t>(h >> (8 * b));
@@ -350,7 +394,7 @@ uint64_t fnv_chunk_bytes() { return fnv::kChunk; }
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
                 unsigned long long* prof, unsigned long long* trace, const FnvGather* gather,
-                int reserve_sms) {
+                int reserve_sms, const pack::Dsts* copies) {
   const uint64_t n_chunks = fnv_chunks(n);
   fnv::Scratch scr;
   scr.finished = scratch + 2;
@@ -395,6 +439,9 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
     g.patch = gather->patch;
     g.n_dst = gather->dsts.n;
     for (int d = 0; d < gather->dsts.n; ++d) g.dst[d] = gather->dsts.p[d];
+  } else if (copies) {
+    g.n_dst = copies->n;
+    for (int d = 0; d < copies->n; ++d) g.dst[d] = copies->p[d];
   }
   const bool pf = prof || trace;
   auto k = gather ? (pf ? fnv_kernel<true, true> : fnv_kernel<false, true>)
@@ -442,11 +489,11 @@ void launch_fnv_empty(uint64_t seed, unsigned long long* result, const TrailerDs
 
 // ---------------------------------------------------------------- pack (K1)
 void launch_pack(const pack::Segment* segs, int n_segs, uint64_t total, const pack::Dsts& d,
-                 cudaStream_t stream) {
-  if (total == 0) return;
-  const uint64_t tiles = div_up(total, pack::kTile);
-  pack::pack_kernel<<<static_cast<unsigned>(tiles), pack::kThreads, 0, stream>>>(segs, n_segs,
-                                                                                 total, d);
+                 cudaStream_t stream, uint64_t lo) {
+  if (total <= lo) return;
+  if (lo % pack::kTile) throw_invalid("pack piece start must be tile aligned");
+  const uint64_t first = lo / pack::kTile, tiles = div_up(total, pack::kTile) - first;
+  pack::pack_kernel<<<static_cast<unsigned>(tiles), pack::kThreads, 0, stream>>>(segs, n_segs, total, d, first);
   MLCK_CUDA(cudaGetLastError());
 }
 

@@ -60,13 +60,15 @@ size_t fnv_scratch_words(uint64_t n);
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
                 unsigned long long* prof = nullptr, unsigned long long* trace = nullptr,
-                const FnvGather* gather = nullptr, int reserve_sms = 0);
+                const FnvGather* gather = nullptr, int reserve_sms = 0,
+                const pack::Dsts* copies = nullptr);  // non-gather: also store the bytes to these
 // Copy `bytes` from src to every dst with `ctas` CTAs of one SM each.
 void launch_push(const uint8_t* src, uint64_t bytes, const pack::Dsts& d, int ctas, cudaStream_t stream);
 void launch_fnv_empty(uint64_t seed, unsigned long long* result, const TrailerDsts& trailer,
                       cudaStream_t stream);
+// Packs record bytes [lo, total) (lo a multiple of pack::kTile).
 void launch_pack(const pack::Segment* segs, int n_segs, uint64_t total, const pack::Dsts& d,
-                 cudaStream_t stream);
+                 cudaStream_t stream, uint64_t lo = 0);
 void launch_walk(const WalkJob* jobs, int n_jobs, cudaStream_t stream);
 void launch_replay(const adam::ConvOp* ops, int n_ops, const float* const* gptr, const float2* bc,
                    const adam::Opt& o, int cb, uint64_t total_units, cudaStream_t stream);

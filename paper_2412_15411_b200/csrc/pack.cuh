@@ -97,9 +97,11 @@ __device__ inline void copy_tile_bytes(const Segment* segs, int n_segs, uint64_t
 }
 
 #ifdef MLCK_DEFINE_KERNELS
+// Tiles [first_tile, ...) of the record up to byte `total` (a piece of it
+// when the record is packed in pieces).
 __global__ void __launch_bounds__(kThreads) pack_kernel(const Segment* __restrict__ segs, int n_segs,
-                                                        uint64_t total, Dsts d) {
-  const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kTile;
+                                                        uint64_t total, Dsts d, uint64_t first_tile) {
+  const uint64_t t0 = (first_tile + blockIdx.x) * kTile;
   if (t0 >= total) return;
   const uint64_t t1 = t0 + kTile < total ? t0 + kTile : total;
   const int s = find_segment(segs, n_segs, t0);

@@ -217,10 +217,11 @@ class Context:
         return int(lib().mlck_ctx_kernel_launches(self.h))
 
     def set_replica_mode(self, mode: int):
-        """-1 (default): auto (= 1, measured fastest); 1: pack, then
-        copy engines overlapped with the hash; 3: pack, then a push kernel on
-        reserved SMs overlapped with the hash; 2: fused gather+store+hash
-        kernel; 0: pack-kernel stores, then hash."""
+        """-1 (default): auto (0 for replicas in local HBM, else 1); 1: pack,
+        then copy engines overlapped with the hash; 5: pack, then the hash
+        kernel stores the replicas; 3: pack, then a push kernel on reserved
+        SMs overlapped with the hash; 2: fused gather+store+hash kernel; 0:
+        pack-kernel stores, then hash; 4: copy engines after the hash."""
         check(lib().mlck_ctx_set_replica_mode(self.h, mode))
 
     def set_timing(self, on: bool):
@@ -297,7 +298,7 @@ class Context:
         keys = ["lookback_probes", "spin_rereads", "cycles_rounds", "cycles_wait", "cycles_final", "chunks",
                 "cycles_other", "cycles_refill",
                 "lb_idle", "lb_probe", "lb_spin", "lb_compose", "lb_publish", "lb_total", "lb_handoff", "lb_arrive",
-                "cyc_data_wait", "cyc_interleave", "cyc_round_core", "cyc_scan_pub", "cyc_finalize", "x21", "x22", "x23"]
+                "cyc_refill", "cyc_data_wait", "cyc_round_core", "cyc_scan_pub", "cyc_final_hash", "x21", "x22", "x23"]
         return out.value, dict(zip(keys, [int(x) for x in cnt]))
 
     def enable_peer_access(self, peer: int):

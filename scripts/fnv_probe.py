@@ -27,8 +27,8 @@ for mb in (16, 256, 1024):
           f"| lb: idle {prof['lb_idle'] / ch:.0f} probe {prof['lb_probe'] / ch:.0f} "
           f"spin {prof['lb_spin'] / ch:.0f} compose {prof['lb_compose'] / ch:.0f} pub {prof['lb_publish'] / ch:.0f} "
           f"total {prof['lb_total'] / ch:.0f}")
-    print("   compute detail/chunk: data_wait %.0f interleave %.0f round_core %.0f scan_pub %.0f finalize %.0f" % tuple(
-        prof[k] / ch for k in ["cyc_data_wait", "cyc_interleave", "cyc_round_core", "cyc_scan_pub", "cyc_finalize"]))
+    print("   compute detail/chunk: refill %.0f data_wait %.0f final_hash %.0f" % tuple(
+        prof[k] / ch for k in ["cyc_refill", "cyc_data_wait", "cyc_final_hash"]))
     st.close()
 
 # per-chunk trace on 64 MB

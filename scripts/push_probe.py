@@ -27,22 +27,26 @@ def all_gather(obj):
 
 
 ctx = mlck.Context(local)
-wl = bench.mixtral_ep()
+wl = bench.mixtral_ep() if world > 1 else bench.deepseek_layer()
 slots = bench.schedule(wl)
 sizes = [bench.record_bytes(wl, s) for s in slots]
 cap = max(sizes)
-r = min(2, world - 1)
+r = min(2, world - 1) if world > 1 else 1
 st = mlck.DeviceState(ctx, wl["param_counts"], wl["cb"])
 st.fill_synthetic(seed=7 + rank, step=10)
 st.set_meta(1000, 7)
 W = wl["W"]
 blobs = [mlck.Blob(ctx, cap) for _ in range(W)]
-recv = [ctx.alloc(cap) for _ in range(r)]
-targets = placement.exchange_handles(all_gather, [ctx.ipc_export(p) for p in recv], rank, world)
-for handle, _peer in targets:
-    ptr = ctx.ipc_open(handle)
+if world == 1:  # local replica per slot, as bench.py at N=1
     for b in blobs:
-        b.add_replica(ptr, cap)
+        b.add_replica(ctx.alloc(cap), cap)
+else:
+    recv = [ctx.alloc(cap) for _ in range(r)]
+    targets = placement.exchange_handles(all_gather, [ctx.ipc_export(p) for p in recv], rank, world)
+    for handle, _peer in targets:
+        ptr = ctx.ipc_open(handle)
+        for b in blobs:
+            b.add_replica(ptr, cap)
 
 
 def step(i):
@@ -51,18 +55,22 @@ def step(i):
     mlck.snapshot_record(st, a, c, k, 1, 1000, W, blobs[k])
 
 
-for mode in [1, 4, 1]:
+for mode in [int(m) for m in os.environ.get("PROBE_MODES", "1,4,1").split(",")]:
     ctx.set_replica_mode(mode)
     for i in range(3):
         step(i)
     ctx.synchronize()
     dist.barrier()
     ctx.set_timing(True)
-    ctx.event_record(0)
-    for i in range(8):
-        step(i)
-    ctx.event_record(1)
-    ctx.synchronize()
+    samp = os.environ.get("PROBE_SAMPLER", "0")
+    import contextlib
+    cm = bench.ClockSampler(local) if samp == "all" or (samp == "0rank" and rank == 0) else contextlib.nullcontext()
+    with cm:
+        ctx.event_record(0)
+        for i in range(8):
+            step(i)
+        ctx.event_record(1)
+        ctx.synchronize()
     tim = ctx.timings()
     ctx.set_timing(False)
     ms = ctx.event_ms(0, 1) / 8

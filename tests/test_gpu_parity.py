@@ -120,11 +120,12 @@ def test_adam_goldens(mk, ctx):
 
 
 # ---------------------------------------------------------------- K1 snapshot
-# snapshot transports: 1 = pack kernel + copy-engine push + FNV kernel
-# (default for local replicas), 3 = pack kernel + SM push on reserved SMs
-# beside the FNV kernel (default for peer replicas), 2 = fused
-# gather+store+hash kernel, 0 = pack-kernel replica stores
-MODES = [1, 3, 2, 0]
+# snapshot transports (-1 = auto): 1 = pack kernel + copy-engine push beside
+# the FNV kernel (auto for peer replicas), 0 = pack-kernel replica stores
+# (auto for local replicas), 5 = FNV-kernel replica stores, 3 = SM push on
+# reserved SMs beside the FNV kernel, 2 = fused gather+store+hash kernel,
+# 4 = copy-engine push after the hash
+MODES = [-1, 1, 5, 3, 2, 0, 4]
 
 
 @pytest.fixture
@@ -176,6 +177,40 @@ def test_snapshot_replicas_identical(mk, ctx, mode):
         mk.snapshot_record(st, active, co, 1, 1, 3, 3, small)
     ctx.free(r1)
     ctx.free(r2)
+
+
+@pytest.mark.parametrize("mode", MODES, indirect=True)
+def test_snapshot_large_replicas_vs_oracle(mk, ctx, oracle, mode):
+    """A ~200 MB record (several 64 MiB pack pieces under transport 1) with
+    two replicas, byte for byte against the oracle."""
+    pcs = [5_000_001, 3_999_999, 2_500_003, 777]
+    st = mk.DeviceState(ctx, pcs, 2)
+    st.fill_synthetic(seed=5, step=9)
+    st.set_meta(77, 3)
+    active, co = [0, 2], [1, 3]
+    ents = []
+    for i in range(len(pcs)):
+        P = pcs[i]
+        master = oracle.synth(5, 3 * i, -0.25, 0.25, P)
+        if i in active:
+            ents.append(dict(id=i, mode=0, param_count=P, step=9, master=master,
+                             m=oracle.synth(5, 3 * i + 1, -1e-3, 1e-3, P),
+                             v=oracle.synth(5, 3 * i + 2, 0.0, 1e-6, P)))
+        else:
+            ents.append(dict(id=i, mode=1, param_count=P, compute=oracle.quantize(master, 2)))
+    ref = oracle.serialize_record(dict(kind=1, iteration=77, window_start=75, wsparse=4, slot=2, data_seed=3),
+                                  ents, 2)
+    cap = len(ref) + 4096
+    out = mk.Blob(ctx, cap)
+    reps = [ctx.alloc(cap), ctx.alloc(cap)]
+    for r in reps:
+        out.add_replica(r, cap)
+    mk.snapshot_record(st, active, co, 2, 1, 75, 4, out)
+    assert out.to_host() == ref
+    for r in reps:
+        assert ctx.download(r, len(ref)) == ref
+        ctx.free(r)
+    st.close()
 
 
 def test_snapshot_errors(mk, ctx):
