@@ -1058,9 +1058,22 @@ int mlck_snapshot_record_host(mlck_state* st, const uint32_t* active, uint32_t n
     if (size) *size = n;
     if (!host_out) return;
     if (cap < n) throw_invalid("snapshot: host buffer too small");
-    run_pack(st->ctx, b, scratch, true);
-    ce_copy(host_out, scratch->dev, n, cudaMemcpyDeviceToHost, st->ctx->stream);
-    MLCK_CUDA(cudaStreamSynchronize(st->ctx->stream));
+    // the host buffer is one more replica of the record, pushed piece by
+    // piece by the copy engines as the pack kernel produces it (transport 1)
+    mlck_ctx* ctx = st->ctx;
+    struct Restore {
+      mlck_ctx* c;
+      mlck_blob* b;
+      int mode;
+      ~Restore() {
+        c->replica_mode = mode;
+        b->replicas.pop_back();
+      }
+    } restore{ctx, scratch, ctx->replica_mode};
+    scratch->replicas.emplace_back(host_out, cap);
+    ctx->replica_mode = 1;
+    run_pack(ctx, b, scratch, true);
+    MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

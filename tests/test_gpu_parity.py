@@ -207,6 +207,7 @@ def test_snapshot_large_replicas_vs_oracle(mk, ctx, oracle, mode):
         out.add_replica(r, cap)
     mk.snapshot_record(st, active, co, 2, 1, 75, 4, out)
     assert out.to_host() == ref
+    assert mk.snapshot_record_host(st, active, co, 2, 1, 75, 4) == ref  # host replica, pushed in pieces
     for r in reps:
         assert ctx.download(r, len(ref)) == ref
         ctx.free(r)
