@@ -134,6 +134,21 @@ int mlck_blob_to_host(const mlck_blob* b, uint8_t* host, uint64_t cap);
 int mlck_blob_add_replica(mlck_blob* b, void* device_ptr, uint64_t capacity);
 int mlck_blob_clear_replicas(mlck_blob* b);
 
+/* ---- window lifecycle and durability (SparseCheckpoint::replication /
+ * persisted(), snapshot.hpp:300-320; "one persisted + one
+ * in-flight") -------------------------------------------------------------
+ * Replication of the blob's last record without blocking: *done = the
+ * number of replicas holding the complete record (trailer included), 0 while
+ * its push is in flight or before any record was written. */
+int mlck_blob_replication(mlck_blob* b, uint32_t* done);
+/* Persist the record bytes -- the MLCK v1 wire format, i.e. the reference's
+ * SparseCheckpoint::blobs element -- to a file (D2H in pinned 64 MiB pieces
+ * overlapped with the writes, then fsync).  Errors: "persist: ..." (2). */
+int mlck_blob_save(mlck_blob* b, const char* path, uint64_t* written);
+/* Read a record file into a new device blob (unparsed: parse_record and the
+ * conversion verify it). */
+int mlck_blob_load(mlck_ctx* ctx, const char* path, mlck_blob** out);
+
 /* ---- K1+K2: snapshot pack ----------------------------------------------
  * serialize_record(take_sparse_snapshot(engine, slot, slot_index), plan,
  * kind, window_start, wsparse)  (snapshot.hpp:204-241 + 115-144):

@@ -13,9 +13,11 @@
 // Header-only; link with libmlck_b200.so.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -188,8 +190,22 @@ class DeviceBlob {
   void add_replica(void* device_ptr, uint64_t capacity) {
     check(mlck_blob_add_replica(h_, device_ptr, capacity));
   }
+  // replicas holding the complete last record (0 while its push is in flight)
+  uint32_t replication() const {
+    uint32_t n = 0;
+    check(mlck_blob_replication(h_, &n));
+    return n;
+  }
+  // the record bytes (MLCK v1 wire format) to / from a file
+  void save(const std::string& path) const { check(mlck_blob_save(h_, path.c_str(), nullptr)); }
+  static DeviceBlob load(Context& ctx, const std::string& path) {
+    DeviceBlob b(ctx, nullptr);
+    check(mlck_blob_load(ctx.get(), path.c_str(), &b.h_));
+    return b;
+  }
 
  private:
+  DeviceBlob(Context& ctx, std::nullptr_t) : ctx_(&ctx) {}
   Context* ctx_;
   mlck_blob* h_ = nullptr;
 };
@@ -325,6 +341,92 @@ struct SparseCheckpoint {
     check(mlck_check_coverage(hs.data(), static_cast<uint32_t>(hs.size()), op_count,
                               static_cast<int>(plan.compute_bytes)));
   }
+  // Device-driven counters: a record's replicas count once its
+  // push completed; a durable file copy (save) counts as one more.
+  std::vector<int32_t> durable;
+  void poll_replication() {
+    durable.resize(blobs.size(), 0);
+    for (size_t k = 0; k < blobs.size(); ++k)
+      replication[k] = std::max<int32_t>(replication[k],
+                                         static_cast<int32_t>(blobs[k].replication()) + durable[k]);
+  }
+  // Persist the window: record k as <dir>/window_<start>_slot_<k>.mlck (the
+  // bytes of the reference's blobs[k]); the caller owns the directory.
+  void save(const std::string& dir) {
+    durable.resize(blobs.size(), 0);
+    for (size_t k = 0; k < blobs.size(); ++k) {
+      blobs[k].save(dir + "/window_" + std::to_string(window_start) + "_slot_" + std::to_string(k) + ".mlck");
+      durable[k] += 1;
+    }
+    poll_replication();
+  }
+  static SparseCheckpoint load(Context& ctx, const std::string& dir, uint64_t window_start,
+                               uint32_t wsparse) {
+    SparseCheckpoint ck;
+    ck.window_start = window_start;
+    ck.wsparse = wsparse;
+    for (uint32_t k = 0; k < wsparse; ++k) {
+      ck.blobs.push_back(DeviceBlob::load(
+          ctx, dir + "/window_" + std::to_string(window_start) + "_slot_" + std::to_string(k) + ".mlck"));
+      ck.replication.push_back(0);
+      ck.durable.push_back(1);
+    }
+    ck.poll_replication();
+    return ck;
+  }
+};
+
+// "One persisted checkpoint and another in flight, garbage-collecting the
+// oldest after persisting a new one".  Records go to the window
+// of their state index (capture_windows, verify.hpp:63-84).
+class WindowRing {
+ public:
+  WindowRing(uint32_t wsparse, int32_t replication_target) : w_(wsparse), target_(replication_target) {}
+  uint64_t window_of(uint64_t state_index) const { return state_index / w_ * w_; }
+  SparseCheckpoint& add_record(uint64_t state_index, DeviceBlob blob) {
+    const uint64_t ws = window_of(state_index);
+    if (persisted_ && ws <= persisted_->window_start)
+      throw std::runtime_error("record for window " + std::to_string(ws) +
+                               " is older than the persisted window");
+    auto it = in_flight_.find(ws);
+    if (it == in_flight_.end()) {
+      SparseCheckpoint ck;
+      ck.window_start = ws;
+      ck.wsparse = w_;
+      ck.replication_target = target_;
+      it = in_flight_.emplace(ws, std::move(ck)).first;
+    }
+    SparseCheckpoint& ck = it->second;
+    if (ck.complete()) throw std::runtime_error("sparse checkpoint window is full");
+    ck.blobs.push_back(std::move(blob));
+    ck.replication.push_back(0);
+    return ck;
+  }
+  // Returns the new persisted window start when a window persisted (the
+  // caller's gc_logs point), after releasing the windows it replaces.
+  std::optional<uint64_t> poll() {
+    std::optional<uint64_t> newest;
+    for (auto& [ws, ck] : in_flight_) {
+      ck.poll_replication();
+      if (ck.persisted()) newest = ws;
+    }
+    if (!newest) return std::nullopt;
+    persisted_ = std::move(in_flight_.at(*newest));
+    in_flight_.erase(in_flight_.begin(), in_flight_.upper_bound(*newest));
+    return newest;
+  }
+  const SparseCheckpoint* persisted() const { return persisted_ ? &*persisted_ : nullptr; }
+  size_t in_flight() const { return in_flight_.size(); }
+  SparseCheckpoint* window(uint64_t window_start) {
+    auto it = in_flight_.find(window_start);
+    return it == in_flight_.end() ? nullptr : &it->second;
+  }
+
+ private:
+  uint32_t w_;
+  int32_t target_;
+  std::optional<SparseCheckpoint> persisted_;
+  std::map<uint64_t, SparseCheckpoint> in_flight_;
 };
 
 // ---- dense checkpoint (snapshot.hpp:245-295) --------------------------------

@@ -4,8 +4,11 @@
 // per-call segment tables and launches the sm_100a kernels of kernels.cu.
 // Error texts follow the reference exceptions they replace (file:line at
 // each site) so the C++ shim (include/moelab_b200) can rethrow them verbatim.
+#include <unistd.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <string>
@@ -203,6 +206,10 @@ struct mlck_blob {
   uint8_t* dev = nullptr;
   uint64_t cap = 0, size = 0;
   std::vector<std::pair<uint8_t*, uint64_t>> replicas;
+  // recorded on the ctx stream once the last record is complete in the blob
+  // and in every replica (mlck_blob_replication polls it)
+  cudaEvent_t written = nullptr;
+  uint32_t written_replicas = 0;
 
   void reserve(uint64_t n) {
     if (n <= cap) return;
@@ -289,7 +296,14 @@ struct SegmentBuilder {
 
 // Uploads the segment table + meta, launches pack (and the FNV trailer when
 // `trailer`): the blob body is [0, builder.pos), the trailer at pos.
+void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer);
 void run_pack(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
+  run_pack_impl(ctx, b, out, trailer);
+  if (!out->written) MLCK_CUDA(cudaEventCreateWithFlags(&out->written, cudaEventDisableTiming));
+  MLCK_CUDA(cudaEventRecord(out->written, ctx->stream));  // every path ends with the pushes joined
+  out->written_replicas = static_cast<uint32_t>(out->replicas.size());
+}
+void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
   const uint64_t body = b.pos;
   const uint64_t total = body + (trailer ? 8 : 0);
   out->reserve(total);
@@ -993,6 +1007,7 @@ int mlck_blob_destroy(mlck_blob* b) {
     b->ctx->activate();
     cudaStreamSynchronize(b->ctx->stream);
     if (b->dev) cudaFree(b->dev);
+    if (b->written) cudaEventDestroy(b->written);
     delete b;
   });
 }
@@ -1030,6 +1045,111 @@ int mlck_blob_add_replica(mlck_blob* b, void* ptr, uint64_t capacity) {
 }
 int mlck_blob_clear_replicas(mlck_blob* b) {
   return api([&] { b->replicas.clear(); });
+}
+
+// ---- window lifecycle and durability ----------------------
+int mlck_blob_replication(mlck_blob* b, uint32_t* done) {
+  return api([&] {
+    *done = 0;
+    if (!b->written) return;
+    const cudaError_t e = cudaEventQuery(b->written);
+    if (e == cudaSuccess)
+      *done = b->written_replicas;
+    else if (e != cudaErrorNotReady)
+      MLCK_CUDA(e);
+  });
+}
+
+namespace {
+// Double-buffered pinned staging for file I/O: the copy of one piece
+// overlaps the file operation on the other.
+constexpr uint64_t kIoPiece = 64ull << 20;
+struct IoStage {
+  uint8_t* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  IoStage() {
+    for (int i = 0; i < 2; ++i) {
+      MLCK_CUDA(cudaMallocHost(&buf[i], kIoPiece));
+      MLCK_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+  }
+  ~IoStage() {
+    for (int i = 0; i < 2; ++i) {
+      if (ev[i]) cudaEventSynchronize(ev[i]), cudaEventDestroy(ev[i]);
+      if (buf[i]) cudaFreeHost(buf[i]);
+    }
+  }
+};
+struct File {
+  std::FILE* f;
+  File(const char* path, const char* mode) : f(std::fopen(path, mode)) {}
+  ~File() {
+    if (f) std::fclose(f);
+  }
+};
+}  // namespace
+
+int mlck_blob_save(mlck_blob* b, const char* path, uint64_t* written) {
+  return api([&] {
+    b->ctx->activate();
+    File file(path, "wb");
+    if (!file.f) throw_runtime(std::string("persist: cannot open ") + path);
+    IoStage io;
+    const uint64_t n = b->size, pieces = div_up(n, kIoPiece);
+    cudaStream_t s = b->ctx->stream;
+    auto piece_len = [&](uint64_t i) { return std::min(kIoPiece, n - i * kIoPiece); };
+    for (uint64_t i = 0; i <= pieces; ++i) {
+      if (i < pieces) {  // D2H of piece i into buffer i % 2
+        MLCK_CUDA(cudaMemcpyAsync(io.buf[i & 1], b->dev + i * kIoPiece, piece_len(i), cudaMemcpyDeviceToHost, s));
+        MLCK_CUDA(cudaEventRecord(io.ev[i & 1], s));
+      }
+      if (i >= 1) {  // write piece i - 1 while piece i is in flight
+        const uint64_t j = i - 1;
+        MLCK_CUDA(cudaEventSynchronize(io.ev[j & 1]));
+        if (std::fwrite(io.buf[j & 1], 1, piece_len(j), file.f) != piece_len(j))
+          throw_runtime(std::string("persist: short write to ") + path);
+      }
+    }
+    if (std::fflush(file.f) != 0 || fsync(fileno(file.f)) != 0)
+      throw_runtime(std::string("persist: cannot flush ") + path);
+    if (written) *written = n;
+  });
+}
+
+int mlck_blob_load(mlck_ctx* ctx, const char* path, mlck_blob** out) {
+  return api([&] {
+    ctx->activate();
+    File file(path, "rb");
+    if (!file.f) throw_runtime(std::string("persist: cannot open ") + path);
+    if (std::fseek(file.f, 0, SEEK_END) != 0) throw_runtime(std::string("persist: cannot seek ") + path);
+    const long len = std::ftell(file.f);
+    if (len < 0) throw_runtime(std::string("persist: cannot size ") + path);
+    std::rewind(file.f);
+    const uint64_t n = static_cast<uint64_t>(len), pieces = div_up(n, kIoPiece);
+    auto* b = new mlck_blob();
+    b->ctx = ctx;
+    try {
+      b->reserve(std::max<uint64_t>(n, kAlign));
+      IoStage io;
+      cudaStream_t s = ctx->stream;
+      for (uint64_t i = 0; i < pieces; ++i) {
+        const uint64_t len_i = std::min(kIoPiece, n - i * kIoPiece);
+        MLCK_CUDA(cudaEventSynchronize(io.ev[i & 1]));  // the buffer's previous H2D is done
+        if (std::fread(io.buf[i & 1], 1, len_i, file.f) != len_i)
+          throw_runtime(std::string("persist: short read from ") + path);
+        MLCK_CUDA(cudaMemcpyAsync(b->dev + i * kIoPiece, io.buf[i & 1], len_i, cudaMemcpyHostToDevice, s));
+        MLCK_CUDA(cudaEventRecord(io.ev[i & 1], s));
+      }
+      MLCK_CUDA(cudaStreamSynchronize(s));
+      b->size = n;
+    } catch (...) {
+      cudaStreamSynchronize(ctx->stream);
+      if (b->dev) cudaFree(b->dev);
+      delete b;
+      throw;
+    }
+    *out = b;
+  });
 }
 
 // ------------------------------------------------------------------ snapshot

@@ -104,6 +104,9 @@ def lib():
             "mlck_blob_to_host": (C.c_int, [vp, u8p, C.c_uint64]),
             "mlck_blob_add_replica": (C.c_int, [vp, vp, C.c_uint64]),
             "mlck_blob_clear_replicas": (C.c_int, [vp]),
+            "mlck_blob_replication": (C.c_int, [vp, C.POINTER(C.c_uint32)]),
+            "mlck_blob_save": (C.c_int, [vp, C.c_char_p, C.POINTER(C.c_uint64)]),
+            "mlck_blob_load": (C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
             "mlck_snapshot_record": (C.c_int, [vp, u32p, C.c_uint32, u32p, C.c_uint32, C.c_uint32, C.c_uint8,
                                                C.c_uint64, C.c_uint32, vp]),
             "mlck_snapshot_record_host": (C.c_int, [vp, u32p, C.c_uint32, u32p, C.c_uint32, C.c_uint32,
@@ -464,6 +467,24 @@ class Blob:
 
     def clear_replicas(self):
         check(lib().mlck_blob_clear_replicas(self.h))
+
+    def replication(self) -> int:
+        """Replicas holding the complete last record (0 while in flight)."""
+        n = C.c_uint32()
+        check(lib().mlck_blob_replication(self.h, C.byref(n)))
+        return int(n.value)
+
+    def save(self, path: str) -> int:
+        """Persist the record bytes (MLCK v1 wire format) to `path`."""
+        n = C.c_uint64()
+        check(lib().mlck_blob_save(self.h, os.fsencode(path), C.byref(n)))
+        return int(n.value)
+
+    @classmethod
+    def load(cls, ctx: Context, path: str) -> "Blob":
+        h = vp()
+        check(lib().mlck_blob_load(ctx.h, os.fsencode(path), C.byref(h)))
+        return cls(ctx, _h=h)
 
 
 def snapshot_record(state: DeviceState, active, compute_only, slot_index: int, kind: int = 1,

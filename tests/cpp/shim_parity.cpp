@@ -6,6 +6,7 @@
 // error texts for the failure paths.
 #include <cstdio>
 #include <cstring>
+#include <filesystem>
 #include <fstream>
 #include <iostream>
 #include <stdexcept>
@@ -112,6 +113,26 @@ int main(int argc, char** argv) {
   }
   ckpt.check_coverage(n_ops, plan);
   std::cout << "complete " << ckpt.complete() << " persisted " << ckpt.persisted() << "\n";
+
+  // window durability: files back byte-exact; a window of the
+  // ring persists once every record has its copies, here a durable file
+  {
+    std::filesystem::create_directories(out + "/window");
+    ckpt.save(out + "/window");
+    SparseCheckpoint back = SparseCheckpoint::load(ctx, out + "/window", ws, W);
+    bool same = back.blobs.size() == W;
+    for (uint32_t k = 0; same && k < W; ++k) same = back.blobs[k].bytes() == ckpt.blobs[k].bytes();
+    back.check_coverage(n_ops, plan);
+    std::cout << "SAVED same " << same << " durable_persisted " << back.persisted() << "\n";
+    WindowRing ring(W, 1);
+    for (uint32_t k = 0; k < W; ++k) ring.add_record(ws + k, DeviceBlob(ctx, ckpt.blobs[k].bytes()));
+    const bool before = ring.poll().has_value();
+    std::filesystem::create_directories(out + "/ring");
+    ring.window(ws)->save(out + "/ring");
+    const auto after = ring.poll();
+    std::cout << "RING before " << before << " after " << (after ? static_cast<int64_t>(*after) : -1)
+              << " in_flight " << ring.in_flight() << "\n";
+  }
 
   GradientLog g(ctx, P, W);
   for (uint32_t s = 1; s <= W; ++s)

@@ -65,3 +65,8 @@ def test_cpp_shim_window_matches_reference(tmp_path, name, w):
     assert f"ERR runtime_error: sparse checkpoint incomplete: 0 of {c.W + 1} records" in out
     assert f"PARSED iteration {w} entries" in out
     assert "complete 1 persisted 0" in out
+    # window durability: the saved records load back byte-exact; a file copy is
+    # one durable copy (persisted only at target 1); the ring promotes the window
+    assert "SAVED same 1 durable_persisted 0" in out
+    assert f"RING before 0 after {w} in_flight 0" in out
+    assert (tmp_path / "window" / f"window_{w}_slot_0.mlck").read_bytes() == c.blob(w)
