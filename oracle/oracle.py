@@ -575,6 +575,48 @@ def ref_parse_record(ref: Reference, blob: bytes, compute_bytes: int):
     return int(n), it.value, sl.value
 
 
+def ref_build_schedule(ref: Reference, ops, compute_bytes, master_bytes, optimizer_bytes, bandwidth, t_iter,
+                       ordering=0, allow_single=False):
+    """build_schedule (schedule.hpp:177-209) of the compiled reference.  ops:
+    dicts with cls (0 expert / 1 non-expert / 2 gate), params, hard, soft,
+    ema, capacity.  Returns (wsparse, o_active, fits, [(active, compute_only)])."""
+    L = ref.lib
+    n = len(ops)
+    if not getattr(L, "_bs_typed", False):
+        f64p = C.POINTER(C.c_double)
+        L.mlr_build_schedule.argtypes = [C.c_uint32, u8p, C.POINTER(C.c_int64), f64p, f64p, f64p, f64p, C.c_int64,
+                                         C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int64,
+                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32), u32p,
+                                         u32p, u32p, C.c_char_p, C.c_size_t]
+        L._bs_typed = True
+    cls = np.array([o["cls"] for o in ops], dtype=np.uint8)
+    params = np.array([o["params"] for o in ops], dtype=np.int64)
+    cols = {k: np.array([float(o.get(k, 0.0)) for o in ops], dtype=np.float64)
+            for k in ("hard", "soft", "ema", "capacity")}
+    max_slots = n
+    ids = np.zeros(max_slots * n, dtype=np.uint32)
+    na = np.zeros(max_slots, dtype=np.uint32)
+    nc = np.zeros(max_slots, dtype=np.uint32)
+    w, o, fits = C.c_int64(), C.c_int64(), C.c_int32()
+    err = C.create_string_buffer(1024)
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    rc = L.mlr_build_schedule(n, cls.ctypes.data_as(u8p), params.ctypes.data_as(C.POINTER(C.c_int64)),
+                              dp(cols["hard"]), dp(cols["soft"]), dp(cols["ema"]), dp(cols["capacity"]),
+                              compute_bytes, master_bytes, optimizer_bytes, bandwidth, t_iter, ordering,
+                              int(allow_single), max_slots, C.byref(w), C.byref(o), C.byref(fits),
+                              ids.ctypes.data_as(u32p), na.ctypes.data_as(u32p), nc.ctypes.data_as(u32p), err,
+                              len(err))
+    if rc != 0:
+        msg = err.value.decode()
+        raise (ValueError if "invalid" in msg or "non-positive" in msg or "no capacity" in msg
+               or "no operators" in msg else RuntimeError)(msg)
+    slots = []
+    for k in range(w.value):
+        row = ids[k * n:(k + 1) * n]
+        slots.append((row[:na[k]].tolist(), row[na[k]:na[k] + nc[k]].tolist()))
+    return w.value, o.value, bool(fits.value), slots
+
+
 def load_reference():
     """Reference handle or None when oracle/_ref was not built here."""
     try:

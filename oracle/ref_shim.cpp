@@ -210,6 +210,47 @@ int mlr_schedule(void* e, int64_t wsparse, int64_t o_active, uint32_t* ids, uint
   });
 }
 
+// build_schedule (schedule.hpp:177-209) over explicit descriptors: cls[i]
+// 0 expert / 1 non-expert / 2 gate, hard/soft/ema popularity, capacity.
+// Writes W, O, fits and the slot layout like mlr_schedule (ids sized
+// max_slots * n).
+int mlr_build_schedule(uint32_t n, const uint8_t* cls, const int64_t* params, const double* hard,
+                       const double* soft, const double* ema, const double* capacity, int64_t compute_bytes,
+                       int64_t master_bytes, int64_t optimizer_bytes, double bandwidth, double t_iter,
+                       int ordering, int allow_single, int64_t max_slots, int64_t* wsparse, int64_t* o_active,
+                       int32_t* fits, uint32_t* ids, uint32_t* n_active, uint32_t* n_co, char* err, size_t cap) {
+  return guarded(err, cap, [&] {
+    std::vector<OperatorDescriptor> ops(n);
+    for (uint32_t i = 0; i < n; ++i) {
+      ops[i].id = i;
+      ops[i].cls = static_cast<OperatorClass>(cls[i]);
+      ops[i].param_count = params[i];
+      ops[i].capacity = capacity[i];
+      ops[i].popularity.hard_count = hard[i];
+      ops[i].popularity.soft_count = soft[i];
+      ops[i].popularity.ema = ema[i];
+    }
+    PrecisionPlan plan;
+    plan.compute_bytes = compute_bytes;
+    plan.master_bytes = master_bytes;
+    plan.optimizer_bytes = optimizer_bytes;
+    const auto s = build_schedule(ops, plan, bandwidth, t_iter, static_cast<OrderingScheme>(ordering),
+                                  allow_single != 0);
+    *wsparse = s.wsparse;
+    *o_active = s.o_active;
+    *fits = s.fits_budget ? 1 : 0;
+    if (static_cast<int64_t>(s.slots.size()) > max_slots) throw std::runtime_error("too many slots");
+    for (size_t k = 0; k < s.slots.size(); ++k) {
+      const auto& sl = s.slots[k];
+      n_active[k] = static_cast<uint32_t>(sl.active.size());
+      n_co[k] = static_cast<uint32_t>(sl.compute_only.size());
+      uint32_t* dst = ids + k * n;
+      for (uint32_t id : sl.active) *dst++ = id;
+      for (uint32_t id : sl.compute_only) *dst++ = id;
+    }
+  });
+}
+
 // ---------------------------------------------------------------- snapshot
 // serialize_record(take_sparse_snapshot(engine, slot, slot_index), ...)
 // (snapshot.hpp:204-241, 115-144).  Returns the blob size (writes when cap
