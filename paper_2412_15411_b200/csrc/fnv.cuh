@@ -59,6 +59,11 @@ constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
 #ifndef MLCK_FNV_MMA
 #define MLCK_FNV_MMA 1
 #endif
+// MLCK_FNV_BULK: a thread's 128 bytes arrive with one cp.async.bulk (TMA)
+// instead of eight 16-byte cp.async; 0 = cp.async.
+#ifndef MLCK_FNV_BULK
+#define MLCK_FNV_BULK 1
+#endif
 #ifndef MLCK_FNV_ROUND0_LINEAR
 #define MLCK_FNV_ROUND0_LINEAR 1
 #endif
@@ -476,7 +481,7 @@ __device__ __forceinline__ void cp_async_arrive(unsigned long long* m) {
 // Byte path (unaligned input, the record's tail, a thread straddling
 // segments): thread t's bytes into its granules, zero past n.
 template <typename ByteAt>
-__device__ __forceinline__ void load_thread_bytes(Shared& sh, int slot, int t, ByteAt byte_at) {
+__device__ __forceinline__ void load_thread_bytes(Shared& sh, int slot, int t, ByteAt byte_at, bool arrive = true) {
   uint4* dst = sh.data[slot];
   for (int q = 0; q < kGranules; ++q) {
     uint32_t v[4];
@@ -488,7 +493,17 @@ __device__ __forceinline__ void load_thread_bytes(Shared& sh, int slot, int t, B
     }
     dst[granule(t, q)] = make_uint4(v[0], v[1], v[2], v[3]);
   }
-  mbar_arrive(&sh.mbar[slot][t >> 5]);
+  if (arrive) mbar_arrive(&sh.mbar[slot][t >> 5]);
+}
+
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, unsigned long long* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(mbar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* m, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(m)), "r"(tx) : "memory");
 }
 
 // Thread t's bytes of `chunk` of a packed buffer into its slot granules,
@@ -496,6 +511,23 @@ __device__ __forceinline__ void load_thread_bytes(Shared& sh, int slot, int t, B
 __device__ __forceinline__ void load_thread(Shared& sh, int slot, int t, const uint8_t* data,
                                             uint64_t n, int64_t chunk) {
   const uint64_t p = static_cast<uint64_t>(chunk) * kChunk + static_cast<uint64_t>(t) * kThreadBytes;
+#if MLCK_FNV_BULK
+  // whole warp: one bulk copy per thread with its full 128 bytes, the byte
+  // path for the rest; lane 0 arrives with the warp's expected byte count
+  // (the warp's mbarrier counts one arrival in this mode)
+  const bool full = p + kThreadBytes <= n && (reinterpret_cast<uintptr_t>(data) & 15u) == 0;
+  unsigned long long* mb = &sh.mbar[slot][t >> 5];
+  __syncwarp();  // every lane is done with the slot's previous bytes
+  if (full) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    bulk_copy(&sh.data[slot][granule(t, 0)], data + p, kThreadBytes, mb);
+  } else {
+    load_thread_bytes(sh, slot, t, [&](int i) -> uint32_t { return p + i < n ? data[p + i] : 0u; }, false);
+  }
+  const uint32_t n_full = __popc(__ballot_sync(0xffffffffu, full));
+  if ((t & 31) == 0) mbar_arrive_expect_tx(mb, n_full * kThreadBytes);
+  return;
+#endif
   if (p + kThreadBytes <= n && (reinterpret_cast<uintptr_t>(data) & 15u) == 0) {
     uint4* dst = sh.data[slot];
 #pragma unroll

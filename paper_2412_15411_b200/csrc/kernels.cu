@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(fnv::kThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0)
     for (int s = 0; s < kSlots; ++s) {
-      for (int w = 0; w < kComputeWarps; ++w) mbar_init(&sh.mbar[s][w], 32);
+      for (int w = 0; w < kComputeWarps; ++w) mbar_init(&sh.mbar[s][w], kGather || !MLCK_FNV_BULK ? 32 : 1);
       mbar_init(&sh.res[s], 1);
     }
 #if MLCK_FNV_MMA
