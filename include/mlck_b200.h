@@ -171,6 +171,11 @@ int mlck_snapshot_record_host(mlck_state* st, const uint32_t* active, uint32_t n
  * "dense checkpoint: operator N is frozen" when an op lacks full state. */
 int mlck_dense_checkpoint(mlck_state* st, mlck_blob* out);
 
+/* Self-check of the conversion replay's exact-IEEE fast paths: n_div random
+ * divisions inside their range and every float32 inside the sqrt range,
+ * each against __fdiv_rn / __fsqrt_rn.  mismatches[0] = division,
+ * mismatches[1] = square root (both must be 0). */
+int mlck_fastmath_check(mlck_ctx* ctx, uint64_t n_div, uint64_t seed, uint64_t* mismatches);
 /* fnv1a64 (digest.hpp:18-25) over n device bytes. */
 int mlck_fnv1a64(mlck_ctx* ctx, const void* device_ptr, uint64_t n, uint64_t seed, uint64_t* out);
 

@@ -1212,6 +1212,22 @@ int mlck_dense_checkpoint(mlck_state* st, mlck_blob* out) {
   });
 }
 
+int mlck_fastmath_check(mlck_ctx* ctx, uint64_t n_div, uint64_t seed, uint64_t* mismatches) {
+  return api([&] {
+    ctx->activate();
+    unsigned long long* d = nullptr;
+    MLCK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), 16, ctx->stream));
+    MLCK_CUDA(cudaMemsetAsync(d, 0, 16, ctx->stream));
+    launch_fastmath_check(n_div, seed, d, ctx->stream);
+    unsigned long long h[2] = {0, 0};
+    MLCK_CUDA(cudaMemcpyAsync(h, d, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    MLCK_CUDA(cudaFreeAsync(d, ctx->stream));
+    MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+    mismatches[0] = h[0];
+    mismatches[1] = h[1];
+  });
+}
+
 int mlck_fnv1a64(mlck_ctx* ctx, const void* ptr, uint64_t n, uint64_t seed, uint64_t* out) {
   return api([&] {
     ctx->activate();

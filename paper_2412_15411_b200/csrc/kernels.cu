@@ -593,6 +593,11 @@ void launch_replay(const adam::ConvOp* ops, int n_ops, const float* const* gptr,
   MLCK_CUDA(cudaGetLastError());
 }
 
+void launch_fastmath_check(uint64_t n, uint64_t seed, unsigned long long* counts, cudaStream_t stream) {
+  adam::fastmath_check_kernel<<<148 * 8, 256, 0, stream>>>(n, seed, counts);
+  MLCK_CUDA(cudaGetLastError());
+}
+
 namespace {
 __global__ void adam_arrays_kernel(float* w, float* m, float* v, const float* g, uint64_t n,
                                    adam::Opt o, float bc1, float bc2) {

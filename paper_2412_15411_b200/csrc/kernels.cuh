@@ -72,6 +72,8 @@ void launch_pack(const pack::Segment* segs, int n_segs, uint64_t total, const pa
 void launch_walk(const WalkJob* jobs, int n_jobs, cudaStream_t stream);
 void launch_replay(const adam::ConvOp* ops, int n_ops, const float* const* gptr, const float2* bc,
                    const adam::Opt& o, int cb, uint64_t total_units, cudaStream_t stream);
+// Self-check of the replay kernel's spelled-out IEEE fast paths (adam.cuh).
+void launch_fastmath_check(uint64_t n, uint64_t seed, unsigned long long* counts, cudaStream_t stream);
 void launch_adam_arrays(float* w, float* m, float* v, const float* g, uint64_t n,
                         const adam::Opt& o, float bc1, float bc2, cudaStream_t stream);
 void launch_quantize(const float* in, float* out, uint64_t n, int cb, cudaStream_t stream);

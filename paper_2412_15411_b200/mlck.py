@@ -105,6 +105,7 @@ def lib():
             "mlck_blob_add_replica": (C.c_int, [vp, vp, C.c_uint64]),
             "mlck_blob_clear_replicas": (C.c_int, [vp]),
             "mlck_blob_replication": (C.c_int, [vp, C.POINTER(C.c_uint32)]),
+            "mlck_fastmath_check": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64)]),
             "mlck_blob_save": (C.c_int, [vp, C.c_char_p, C.POINTER(C.c_uint64)]),
             "mlck_blob_load": (C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
             "mlck_snapshot_record": (C.c_int, [vp, u32p, C.c_uint32, u32p, C.c_uint32, C.c_uint32, C.c_uint8,
@@ -226,6 +227,12 @@ class Context:
         SMs overlapped with the hash; 2: fused gather+store+hash kernel; 0:
         pack-kernel stores, then hash; 4: copy engines after the hash."""
         check(lib().mlck_ctx_set_replica_mode(self.h, mode))
+
+    def fastmath_check(self, n_div: int, seed: int = 1) -> tuple[int, int]:
+        """(division, sqrt) mismatches of the replay's spelled-out fast paths."""
+        out = (C.c_uint64 * 2)()
+        check(lib().mlck_fastmath_check(self.h, n_div, seed, out))
+        return int(out[0]), int(out[1])
 
     def set_timing(self, on: bool):
         check(lib().mlck_ctx_set_timing(self.h, int(on)))

@@ -214,6 +214,13 @@ def test_snapshot_large_replicas_vs_oracle(mk, ctx, oracle, mode):
     st.close()
 
 
+def test_replay_fast_paths_match_ieee_intrinsics(mk, ctx):
+    """The conversion's hoisted-reciprocal division and spelled-out square root
+    equal __fdiv_rn / __fsqrt_rn: 2^28 divisions over every exponent pair of
+    their range, and all 2^32 float32 patterns for the square root."""
+    assert ctx.fastmath_check(1 << 28, seed=7) == (0, 0)
+
+
 def test_snapshot_errors(mk, ctx):
     c = load_case("six_op_cb4")
     st = upload_state(mk, ctx, c, 1)
