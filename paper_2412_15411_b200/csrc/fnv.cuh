@@ -39,6 +39,8 @@
 // complete before its result is needed.
 #pragma once
 
+#include <cuda.h>
+
 #include "mlck_common.cuh"
 #include "pack.cuh"
 
@@ -58,11 +60,6 @@ constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
 // segments B, D in the odd byte lanes (no shift of the data word).
 #ifndef MLCK_FNV_MMA
 #define MLCK_FNV_MMA 1
-#endif
-// MLCK_FNV_BULK: a thread's 128 bytes arrive with one cp.async.bulk (TMA)
-// instead of eight 16-byte cp.async; 0 = cp.async.
-#ifndef MLCK_FNV_BULK
-#define MLCK_FNV_BULK 1
 #endif
 #ifndef MLCK_FNV_ROUND0_LINEAR
 #define MLCK_FNV_ROUND0_LINEAR 1
@@ -386,18 +383,16 @@ __device__ __forceinline__ uint32_t look_back2_warp(const Scratch& scr, int64_t 
 }
 
 // ---- shared memory ----------------------------------------------------------
-// Thread t's bytes sit in 9 granules at 16 * (9t + q): a stride of 9 makes
-// the lanes of a quarter-warp hit 8 distinct granules mod 8 (no bank
-// conflicts), and the 9th granule holds the spill of an unaligned gather.
+// Thread t's 128 bytes are row t of its slot (8 granules of 16 bytes) in the
+// TMA 128-byte swizzle: granule q of row t sits at 16 * (8t + (q ^ (t & 7))),
+// so a tensor-map load lands the chunk in place and the lanes of a
+// quarter-warp hit 8 distinct bank groups for every access pattern below.
+// An unaligned gather's ninth source granule goes to `spill`.
 constexpr int kGranules = kThreadBytes / 16;  // 8
-#ifdef MLCK_FNV_STRIDE8
-constexpr int kGranStride = kGranules;  // experiment: no gather spill granule
-#else
-constexpr int kGranStride = kGranules + 1;     // 9
-#endif
-struct alignas(16) Shared {
-  uint4 data[kSlots][kComputeThreads * kGranStride];
-  unsigned long long mbar[kSlots][kComputeWarps];  // a warp's slot bytes landed (cp.async)
+struct alignas(1024) Shared {
+  uint4 data[kSlots][kComputeThreads * kGranules];  // 1024-byte aligned rows (TMA swizzle atoms)
+  uint4 spill[kSlots][kComputeThreads];
+  unsigned long long mbar[kSlots][kComputeWarps];  // the slot's bytes landed (per warp; [s][0] under TMA)
   unsigned long long res[kSlots];                  // look-back result of the slot's round
   uint32_t wmap[kSlots][32];    // warp maps of the round (compute -> look-back)
   uint32_t wstart[kSlots][32];  // warp start bits (look-back -> compute)
@@ -409,12 +404,16 @@ struct alignas(16) Shared {
 };
 constexpr size_t kSmemBytes = sizeof(Shared);
 static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
+static_assert(sizeof(uint4) * kComputeThreads * kGranules % 1024 == 0, "slots keep the swizzle alignment");
 
-#ifdef MLCK_FNV_STRIDE8
-__device__ __forceinline__ int granule(int t, int q) { return 8 * t + ((q + t) & 7); }
-#else
-__device__ __forceinline__ int granule(int t, int q) { return kGranStride * t + q; }
-#endif
+__device__ __forceinline__ int granule(int t, int q) { return kGranules * t + (q ^ (t & 7)); }
+// granule q (0..8) of thread t's gather window: 8 = the spill granule
+__device__ __forceinline__ uint4* window_granule(Shared& sh, int slot, int t, int q) {
+  return q < kGranules ? &sh.data[slot][granule(t, q)] : &sh.spill[slot][t];
+}
+__device__ __forceinline__ const uint4* window_granule(const Shared& sh, int slot, int t, int q) {
+  return q < kGranules ? &sh.data[slot][granule(t, q)] : &sh.spill[slot][t];
+}
 
 // Fused snapshot (pack + hash + push): the kernel gathers the record from
 // its segment list instead of reading a packed record, writes the bytes to
@@ -450,6 +449,9 @@ __device__ __forceinline__ void mbar_init(unsigned long long* m, uint32_t count)
 }
 __device__ __forceinline__ void mbar_arrive(unsigned long long* m) {
   asm volatile("{ .reg .b64 st; mbarrier.arrive.shared.b64 st, [%0]; }" ::"r"(smem_addr(m)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* m, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(m)), "r"(tx) : "memory");
 }
 #ifndef MLCK_MBAR_SUSPEND_NS
 #define MLCK_MBAR_SUSPEND_NS 0
@@ -496,38 +498,39 @@ __device__ __forceinline__ void load_thread_bytes(Shared& sh, int slot, int t, B
   if (arrive) mbar_arrive(&sh.mbar[slot][t >> 5]);
 }
 
-__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, unsigned long long* mbar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_addr(dst)),
-               "l"(src), "r"(bytes), "r"(smem_addr(mbar))
-               : "memory");
+// Tensor-map load of `rows` x 128 bytes starting at record row `row` into
+// swizzled rows at dst (rows past the tensor arrive as zeros).
+__device__ __forceinline__ void tma_load_rows(void* dst, const CUtensorMap* map, int32_t row,
+                                              unsigned long long* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(row), "r"(smem_addr(mbar))
+      : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* m, uint32_t tx) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(m)), "r"(tx) : "memory");
+// The chunk of `slot` by one thread: the 256-row boxes that start inside the
+// map's rows_full full rows (the compute threads write the rest), one
+// mbarrier arrival with their byte count.
+constexpr int kTmaBoxRows = 256;
+__device__ __forceinline__ void tma_load_chunk(Shared& sh, int slot, const CUtensorMap* map, int64_t chunk,
+                                               uint64_t rows_full) {
+  unsigned long long* mb = &sh.mbar[slot][0];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const uint64_t row0 = static_cast<uint64_t>(chunk) * kComputeThreads;
+  int boxes = 0;
+#pragma unroll
+  for (int b = 0; b < kComputeThreads / kTmaBoxRows; ++b) boxes += row0 + kTmaBoxRows * b < rows_full;
+  mbar_arrive_expect_tx(mb, boxes * kTmaBoxRows * kThreadBytes);
+  for (int b = 0; b < boxes; ++b)
+    tma_load_rows(&sh.data[slot][kGranules * kTmaBoxRows * b], map, static_cast<int32_t>(row0 + kTmaBoxRows * b), mb);
 }
+
 
 // Thread t's bytes of `chunk` of a packed buffer into its slot granules,
 // zero past n; one arrival on the warp's mbarrier when they have landed.
 __device__ __forceinline__ void load_thread(Shared& sh, int slot, int t, const uint8_t* data,
                                             uint64_t n, int64_t chunk) {
   const uint64_t p = static_cast<uint64_t>(chunk) * kChunk + static_cast<uint64_t>(t) * kThreadBytes;
-#if MLCK_FNV_BULK
-  // whole warp: one bulk copy per thread with its full 128 bytes, the byte
-  // path for the rest; lane 0 arrives with the warp's expected byte count
-  // (the warp's mbarrier counts one arrival in this mode)
-  const bool full = p + kThreadBytes <= n && (reinterpret_cast<uintptr_t>(data) & 15u) == 0;
-  unsigned long long* mb = &sh.mbar[slot][t >> 5];
-  __syncwarp();  // every lane is done with the slot's previous bytes
-  if (full) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    bulk_copy(&sh.data[slot][granule(t, 0)], data + p, kThreadBytes, mb);
-  } else {
-    load_thread_bytes(sh, slot, t, [&](int i) -> uint32_t { return p + i < n ? data[p + i] : 0u; }, false);
-  }
-  const uint32_t n_full = __popc(__ballot_sync(0xffffffffu, full));
-  if ((t & 31) == 0) mbar_arrive_expect_tx(mb, n_full * kThreadBytes);
-  return;
-#endif
   if (p + kThreadBytes <= n && (reinterpret_cast<uintptr_t>(data) & 15u) == 0) {
     uint4* dst = sh.data[slot];
 #pragma unroll
@@ -566,7 +569,7 @@ __device__ __forceinline__ void load_thread_gather(Shared& sh, int slot, int t, 
   }
 #pragma unroll
   for (int q = 0; q < kGranules; ++q) cp_async16(dst + granule(t, q), src + 16 * q);
-  if (ph) cp_async16(dst + granule(t, kGranules), src + 16 * kGranules);
+  if (ph) cp_async16(window_granule(sh, slot, t, kGranules), src + 16 * kGranules);
   cp_async_arrive(&sh.mbar[slot][t >> 5]);
   *phase = ph;
 }
@@ -680,8 +683,8 @@ __device__ __forceinline__ void read_thread_unaligned(const Shared& sh, int slot
                                                      uint32_t (&w)[kThreadWords]) {
   uint32_t x[kThreadWords + 4];
 #pragma unroll
-  for (int q = 0; q < kGranStride; ++q) {
-    const uint4 v = sh.data[slot][granule(t, q)];
+  for (int q = 0; q <= kGranules; ++q) {
+    const uint4 v = *window_granule(sh, slot, t, q);
     x[4 * q] = v.x;
     x[4 * q + 1] = v.y;
     x[4 * q + 2] = v.z;

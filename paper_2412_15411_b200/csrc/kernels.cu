@@ -8,6 +8,8 @@
 #include "pack.cuh"
 
 #include <algorithm>
+#include <cstring>
+#include <string>
 
 namespace mlck {
 
@@ -46,8 +48,11 @@ template <bool kProf, bool kGather>
 __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* data, uint64_t n,
                                                 const fnv::Scratch& scr, int64_t n_chunks,
                                                 const int64_t (&first)[kSlots], int64_t stride,
-                                                const fnv::Gather& gth) {
+                                                const fnv::Gather& gth, bool tma) {
   using namespace fnv;
+  // TMA mode: the slot's look-back warp loads whole chunks through the tensor
+  // map; rows at or past the last full 128-byte row are written here
+  const uint64_t rows_full = n / kThreadBytes;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 #if MLCK_FNV_MMA
   // P^-(end of the warp's span in the chunk)
@@ -72,7 +77,7 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
     st[s] = 0;
     keep[s] = 0;
     ph[s] = 0;
-    if (chunk[s] >= 0) {
+    if (chunk[s] >= 0 && !tma) {
       if (kGather)
         load_thread_gather(sh, s, tid, gth, n, chunk[s], &ph[s]);
       else
@@ -150,10 +155,11 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
           } else if (p0 < n) {  // holds the last byte: one chain to n
             // (bytes from shared memory: a run-time index into w[] would put
             // w in local memory on the hot path too)
-            const uint32_t* sw = reinterpret_cast<const uint32_t*>(&sh.data[s][granule(tid, 0)]);
             uint32_t lo = st[s] & 0xffu, hi = 0;
-            for (int k = 0; k < kThreadBytes && p0 + k < n; ++k)  // stream byte k: segment k/32
-              fnv_byte(lo, hi, (sw[k & 31] >> (8 * (k >> 5))) & 0xffu);
+            for (int k = 0; k < kThreadBytes && p0 + k < n; ++k) {  // stream byte k: segment k/32
+              const uint32_t* g = reinterpret_cast<const uint32_t*>(&sh.data[s][granule(tid, (k & 31) >> 2)]);
+              fnv_byte(lo, hi, (g[k & 3] >> (8 * (k >> 5))) & 0xffu);
+            }
             const uint64_t g = (static_cast<uint64_t>(hi) << 32) | (lo & ~0xffu);
             acc += g * pow_u64(kPrimeInv, n);
             *scr.ulast = lo & 0xffu;
@@ -169,7 +175,9 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
           rnd[s] = 0;
           st[s] = 0;
           par ^= 1u << s;
-          if (chunk[s] >= 0) {
+          if (tma) {
+            bar_arrive(bar_pub(s), kBarThreads);  // done with the bytes: the look-back warp refills
+          } else if (chunk[s] >= 0) {
             if (kGather)
               load_thread_gather(sh, s, tid, gth, n, chunk[s], &ph[s]);
             else
@@ -182,7 +190,14 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
       // ---- compute and publish round rnd[s]
       if (rnd[s] == 0) {
         lap.mark(0);
-        fnv::mbar_wait(&sh.mbar[s][warp], (par >> s) & 1u);
+        fnv::mbar_wait(&sh.mbar[s][tma ? 0 : warp], (par >> s) & 1u);
+        if (tma) {
+          const uint64_t row = static_cast<uint64_t>(chunk[s]) * kComputeThreads + tid;
+          if (row >= rows_full) {  // the partial last row, or zeros past the record
+            const uint64_t p = row * kThreadBytes;
+            load_thread_bytes(sh, s, tid, [&](int i) -> uint32_t { return p + i < n ? data[p + i] : 0u; }, false);
+          }
+        }
         lap.mark(5);
         if (kProf && scr.trace && tid == 0) {
           scr.trace[chunk[s] * 12 + 0] = gtimer();
@@ -249,7 +264,8 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
 // this slot's turns involve it, so the slots' look-backs run concurrently.
 template <bool kProf>
 __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t seed, const fnv::Scratch& scr,
-                                             int64_t chunk, int64_t n_chunks, int64_t stride) {
+                                             int64_t chunk, int64_t n_chunks, int64_t stride,
+                                             const CUtensorMap* tmap, uint64_t n) {
   using namespace fnv;
   const int lane = threadIdx.x & 31;
   const unsigned long long tag = static_cast<unsigned long long>(scr.epoch) << 32;
@@ -265,6 +281,7 @@ __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t se
       lb[0] = now;
     }
   };
+  if (tmap && lane == 0) tma_load_chunk(sh, s, tmap, chunk, n / kThreadBytes);
   for (; chunk < n_chunks; chunk += stride) {
     uint32_t word = 0;  // the chunk's status bits as published
     for (int r = 0; r < kRounds; ++r) {
@@ -292,6 +309,10 @@ __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t se
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.res[s]);  // release: wstart is visible to the waiters
     }
+    if (tmap) {  // the compute warps are done with the bytes: load the slot's next chunk
+      bar_sync(bar_pub(s), kBarThreads);
+      if (lane == 0 && chunk + stride < n_chunks) tma_load_chunk(sh, s, tmap, chunk + stride, n / kThreadBytes);
+    }
   }
   mark(5);
   if (kProf && lane == 0) {
@@ -306,14 +327,15 @@ __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t se
 template <bool kProf, bool kGather>
 __global__ void __launch_bounds__(fnv::kThreads, 1)
     fnv_kernel(const uint8_t* data, uint64_t n, uint64_t seed, fnv::Scratch scr, int64_t n_chunks,
-               TrailerDsts trailer, fnv::Gather gth) {
+               TrailerDsts trailer, fnv::Gather gth, const __grid_constant__ CUtensorMap tmap, int use_tma) {
   using namespace fnv;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0 && (smem_addr(smem_raw) & 1023u)) __trap();  // the TMA swizzle needs 1 KiB-aligned rows
   if (tid == 0)
     for (int s = 0; s < kSlots; ++s) {
-      for (int w = 0; w < kComputeWarps; ++w) mbar_init(&sh.mbar[s][w], kGather || !MLCK_FNV_BULK ? 32 : 1);
+      for (int w = 0; w < kComputeWarps; ++w) mbar_init(&sh.mbar[s][w], use_tma ? 1 : 32);
       mbar_init(&sh.res[s], 1);
     }
 #if MLCK_FNV_MMA
@@ -333,12 +355,14 @@ __global__ void __launch_bounds__(fnv::kThreads, 1)
     first[s] = c < n_chunks ? c : -1;
   }
   uint64_t acc = 0;
+  const bool tma = !kGather && use_tma;
   if (compute_warp(warp) >= 0) {
-    acc = fnv_compute<kProf, kGather>(sh, data, n, scr, n_chunks, first, stride, gth);
+    acc = fnv_compute<kProf, kGather>(sh, data, n, scr, n_chunks, first, stride, gth, tma);
   } else {
 #pragma unroll
     for (int s = 0; s < kSlots; ++s)
-      if (warp == lookback_warp(s) && first[s] >= 0) fnv_lookback<kProf>(sh, s, seed, scr, first[s], n_chunks, stride);
+      if (warp == lookback_warp(s) && first[s] >= 0)
+        fnv_lookback<kProf>(sh, s, seed, scr, first[s], n_chunks, stride, tma ? &tmap : nullptr, n);
   }
   // CTA sum -> global accumulator; the last CTA finishes the hash
 #pragma unroll
@@ -443,11 +467,38 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
     g.n_dst = copies->n;
     for (int d = 0; d < copies->n; ++d) g.dst[d] = copies->p[d];
   }
+  // the record as a [n / 128 rows x 128 bytes] tensor, loaded in 256-row
+  // boxes in the 128-byte swizzle the shared-memory rows use
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  int use_tma = 0;
+  const uint64_t rows = n / fnv::kThreadBytes;
+  if (!gather && rows > 0 && (reinterpret_cast<uintptr_t>(data) & 15u) == 0 && rows < (1ull << 31)) {
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Encode encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q{};
+      MLCK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode),
+                                        cudaEnableDefault, &q));
+      if (q != cudaDriverEntryPointSuccess || !encode) throw Error(kCuda, "cuTensorMapEncodeTiled unavailable");
+    }
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(fnv::kThreadBytes), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(fnv::kThreadBytes)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(fnv::kThreadBytes), static_cast<cuuint32_t>(fnv::kTmaBoxRows)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(data), dims, strides,
+                              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(kCuda, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    use_tma = 1;
+  }
   const bool pf = prof || trace;
   auto k = gather ? (pf ? fnv_kernel<true, true> : fnv_kernel<false, true>)
                   : (pf ? fnv_kernel<true, false> : fnv_kernel<false, false>);
   k<<<static_cast<unsigned>(grid), fnv::kThreads, fnv::kSmemBytes, stream>>>(
-      data, n, seed, scr, static_cast<int64_t>(n_chunks), trailer, g);
+      data, n, seed, scr, static_cast<int64_t>(n_chunks), trailer, g, tmap, use_tma);
   MLCK_CUDA(cudaGetLastError());
 }
 
