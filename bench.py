@@ -244,6 +244,20 @@ def cpu_pack_sample(wl, threads, iters=1):
                 co_params=co_p, threads=threads, iters=iters)
 
 
+METRIC = "snapshot+replicate GB/s/GPU and sparse-to-dense conversion time vs HBM/NVLink roofline"
+
+
+def arm_config(wl, world):
+    """The workload description both arms print (same metric, same config)."""
+    slots = schedule(wl)
+    r = 1 if world == 1 else min(2, world - 1)
+    return {"workload": wl["name"], "params_per_gpu": sum(wl["param_counts"]), "wsparse": wl["W"],
+            "o_active": wl["O"], "compute_bytes": wl["cb"], "replicas": r,
+            "replica_target": "second HBM buffer" if world == 1 else "ring peers over NVLink (IPC)",
+            "record_bytes_per_slot": [record_bytes(wl, sl) for sl in slots], "parallelism": f"ep{world}",
+            "l2": "inputs larger than L2 (records 1.3-12.7 GB)"}
+
+
 def cpu_threads():
     n = os.cpu_count() or 1
     return max(1, min(n, 32))
@@ -270,11 +284,13 @@ def run_reference(args, d: Dist):
     sample = (f"per thread: {s['n_full']} Full x {s['full_params']} params + {s['n_co']} ComputeOnly x "
               f"{s['co_params']} params (slot-0 mix), {threads} independent engines")
     out = {
-        "impl": "reference", "metric": "snapshot+replicate GB/s/GPU (sparse record pack, reference CPU path)",
+        "impl": "reference", "metric": METRIC,
         "value": value, "unit": "GB/s", "n_gpus": d.world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * secs / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8/f32", "data": "synthetic",
-        "config": {"workload": wl["name"], "parallelism": "cpu-threads", "threads": threads},
+        "vs_baseline": None, "dtype": "u8 (byte-exact container) / f32 Adam", "data": "synthetic",
+        "config": arm_config(wl, d.world),
+        "reference_path": "take_sparse_snapshot + serialize_record (snapshot.hpp:115-144, 204-241) compiled from "
+                          f"/root/reference (oracle/_ref), {threads} host threads, bounded sample per step",
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
@@ -662,15 +678,11 @@ def run_ours(args, d: Dist):
     launches_total = ctx.kernel_launches
     if d.rank == 0:
         res = {
-            "metric": "snapshot+replicate GB/s/GPU and sparse-to-dense conversion time vs HBM/NVLink roofline",
+            "metric": METRIC,
             "value": value, "unit": "GB/s", "n_gpus": d.world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u8 (byte-exact container) / f32 Adam", "data": "synthetic",
-            "config": {"workload": wl["name"], "params_per_gpu": sum(pcs), "wsparse": W, "o_active": wl["O"],
-                       "compute_bytes": cb, "replicas": r,
-                       "replica_target": "second HBM buffer" if d.world == 1 else "ring peers over NVLink (IPC)",
-                       "record_bytes_per_slot": sizes, "parallelism": f"ep{d.world}",
-                       "l2": "inputs larger than L2 (records 1.3-12.7 GB)"},
+            "config": arm_config(wl, d.world),
             "per_gpu_gbs": value / d.world,
             "roofline": roofline,
             "roofline_nvlink": roofline_nvlink,
