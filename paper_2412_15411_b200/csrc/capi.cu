@@ -160,10 +160,31 @@ struct mlck_ctx {
     }
     return patch;
   }
+  // The hash kernel's look-back watchdog (fnv.cuh kSpinLimit) leaves a sticky
+  // word in the scratch header; checked after the stream synchronizes.
+  bool watchdog_seen = false;
+  void read_watchdog() {
+    if (!fnv_scratch) return;
+    uint32_t w = 0;
+    MLCK_CUDA(cudaMemcpy(&w, fnv_scratch + fnv_sticky_word(), 4, cudaMemcpyDeviceToHost));
+    if (w) {
+      MLCK_CUDA(cudaMemset(fnv_scratch + fnv_sticky_word(), 0, 4));
+      watchdog_seen = true;
+    }
+  }
+  void check_watchdog() {  // the stream is synchronized
+    read_watchdog();
+    if (watchdog_seen) {
+      watchdog_seen = false;
+      throw_runtime("fnv: the look-back watchdog tripped (a CTA of the hash kernel was not resident; "
+                    "the hash of this call is invalid)");
+    }
+  }
   uint32_t* fnv_scratch_for(uint64_t n) {
     const size_t need = fnv_scratch_words(n);
     if (need > fnv_words) {
       MLCK_CUDA(cudaStreamSynchronize(stream));
+      read_watchdog();
       if (fnv_scratch) MLCK_CUDA(cudaFree(fnv_scratch));
       fnv_words = align_up(std::max<size_t>(need, 4096), 1024);
       MLCK_CUDA(cudaMalloc(&fnv_scratch, fnv_words * 4));
@@ -648,6 +669,7 @@ std::vector<Parsed> parse_blobs(mlck_ctx* ctx, mlck_blob* const* blobs, uint32_t
   MLCK_CUDA(cudaMemcpyAsync(ctx->host_results, ctx->results, 64 * 8, cudaMemcpyDeviceToHost,
                             ctx->stream));
   MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->check_watchdog();
   std::vector<WalkJob> jobs;
   std::vector<uint32_t> job_blob;
   for (uint32_t k = 0; k < n; ++k) {
@@ -721,7 +743,11 @@ int mlck_ctx_create(int device, mlck_ctx** out) {
     auto* c = new mlck_ctx();
     c->device = device;
     c->activate();
-    MLCK_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    // highest priority: the hash kernel's CTAs must all become resident
+    // (slot-major look-back), so they go ahead of other work queued on the GPU
+    int least = 0, greatest = 0;
+    MLCK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    MLCK_CUDA(cudaStreamCreateWithPriority(&c->own, cudaStreamNonBlocking, greatest));
     c->stream = c->own;
     for (auto& s : c->stage) MLCK_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
     for (auto& sd : c->side) MLCK_CUDA(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
@@ -781,6 +807,7 @@ int mlck_ctx_synchronize(mlck_ctx* c) {
   return api([&] {
     c->activate();
     MLCK_CUDA(cudaStreamSynchronize(c->stream));
+    c->check_watchdog();
   });
 }
 uint64_t mlck_ctx_kernel_launches(mlck_ctx* c) { return c ? c->launches : 0; }
@@ -1032,6 +1059,7 @@ int mlck_blob_to_host(const mlck_blob* b, uint8_t* host, uint64_t cap) {
     if (b->size)
       ce_copy(host, b->dev, b->size, cudaMemcpyDeviceToHost, b->ctx->stream);
     MLCK_CUDA(cudaStreamSynchronize(b->ctx->stream));
+    b->ctx->check_watchdog();
   });
 }
 int mlck_blob_add_replica(mlck_blob* b, void* ptr, uint64_t capacity) {
@@ -1194,6 +1222,7 @@ int mlck_snapshot_record_host(mlck_state* st, const uint32_t* active, uint32_t n
     ctx->replica_mode = 1;
     run_pack(ctx, b, scratch, true);
     MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->check_watchdog();
   });
 }
 
@@ -1239,6 +1268,7 @@ int mlck_fnv1a64(mlck_ctx* ctx, const void* ptr, uint64_t n, uint64_t seed, uint
     MLCK_CUDA(cudaMemcpyAsync(ctx->host_results, ctx->results, 8, cudaMemcpyDeviceToHost,
                               ctx->stream));
     MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->check_watchdog();
     *out = ctx->host_results[0];
   });
 }

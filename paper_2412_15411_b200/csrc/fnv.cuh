@@ -92,6 +92,7 @@ struct Scratch {
   uint32_t* finished;          // completed-CTA counter
   uint32_t* ulast;             // low byte of the final hash
   uint32_t* error;             // watchdog tripped (look-back never resolved)
+  uint32_t* sticky;            // ... and stays set until the host reads it
   unsigned long long* result;  // final 64-bit hash
   // optional profile counters (null = off): [0] look-back probes, [1] spin
   // re-reads, compute thread 0 of each CTA: [2] cycles in rounds, [3] cycles

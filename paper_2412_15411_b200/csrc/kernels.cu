@@ -385,7 +385,9 @@ __global__ void __launch_bounds__(fnv::kThreads, 1)
 #else
       const uint64_t h = pow_p(n) * (total + (seed & ~0xffull)) + u;
 #endif
-      *scr.result = atomicAdd(scr.error, 0u) ? 0ull : h;
+      const uint32_t err = atomicAdd(scr.error, 0u);
+      if (err) atomicOr(scr.sticky, 1u);  // reported by the host at its next synchronization
+      *scr.result = err ? 0ull : h;
       for (int r = 0; r < trailer.n; ++r)
         for (int b = 0; b < 8; ++b) trailer.p[r][b] = static_cast<uint8_t>(h >> (8 * b));
     }
@@ -409,11 +411,13 @@ void init_constants() {
 }
 
 uint64_t fnv_chunks(uint64_t n) { return div_up(n, fnv::kChunk); }
-// [256 B header: finished u32 @8, accum u64 @16, ulast u32 @24,
-//  error u32 @28] [status: n_chunks words of 8 B at a 256 B stride]
+// [256 B header: finished u32 @8, accum u64 @16, ulast u32 @24, error u32
+//  @28, sticky watchdog u32 @32 (not cleared per launch)] [status: n_chunks
+//  words of 8 B at a 256 B stride]
 size_t fnv_scratch_words(uint64_t n) { return (256 + fnv_chunks(n) * fnv::kStatusStride * 8) / 4; }
 
 uint64_t fnv_chunk_bytes() { return fnv::kChunk; }
+uint32_t fnv_sticky_word() { return 8; }
 
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
@@ -425,12 +429,13 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
   scr.accum = reinterpret_cast<unsigned long long*>(scratch + 4);
   scr.ulast = scratch + 6;
   scr.error = scratch + 7;
+  scr.sticky = scratch + fnv_sticky_word();
   scr.result = result;
   scr.status = reinterpret_cast<unsigned long long*>(scratch + 64);
   scr.epoch = epoch;
   scr.prof = prof;
   scr.trace = trace;
-  MLCK_CUDA(cudaMemsetAsync(scratch, 0, 256, stream));  // header only: status is epoch-tagged
+  MLCK_CUDA(cudaMemsetAsync(scratch, 0, 32, stream));  // words 0-7: status is epoch-tagged, word 8 sticky
   if (n_chunks == 0) {
     // empty input: h = seed
     launch_fnv_empty(seed, result, trailer, stream);

@@ -55,6 +55,7 @@ void launch_patch(const pack::Segment* segs, int n_segs, const uint64_t* offs, u
 
 void init_constants();
 uint64_t fnv_chunk_bytes();
+uint32_t fnv_sticky_word();  // scratch word of the sticky watchdog flag
 uint64_t fnv_chunks(uint64_t n);
 size_t fnv_scratch_words(uint64_t n);
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
