@@ -154,6 +154,24 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def ncu_pipes(kernel):
+    """The compute-side bound of `kernel` from the same committed capture:
+    issue-slot and ALU/FMA/tensor pipe utilisation (% of peak while active)."""
+    pdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+    try:
+        names = sorted(n for n in os.listdir(pdir) if n.endswith("_ncu_summary.json"))
+        with open(os.path.join(pdir, names[-1])) as fh:
+            k = json.load(fh)["full_captures"][kernel]
+        f = lambda key: float(str(k[key]).split()[0])  # noqa: E731
+        return {"issue_active_pct": f("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                "alu_pipe_pct": f("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                "fma_pipe_pct": f("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                "tensor_pipe_pct": f("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
+                "source": f"profiles/{names[-1]}"}
+    except (OSError, IndexError, KeyError, ValueError):
+        return None
+
+
 def ncu_traffic(kernel):
     """dram read+write bytes of one launch of `kernel` from the newest committed
     `ncu --set full` summary (profiles/rNN_ncu_summary.json, scripts/profile.sh)."""
@@ -539,8 +557,10 @@ def run_ours(args, d: Dist):
     roofline = {"bound": "hbm", "kernel": "fnv", "transport": transport, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                 "frac": ach / hbm_peak, "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
                 "per_launch_bytes": kd["bytes_per_launch"],
+                "compute_side": ncu_pipes("fnv_kernel"),
                 "note": "dominant kernel of the step (the pack kernel alone: kernels['pack']); it is bound by the "
-                        "integer ALU work of the FNV automaton, not by HBM (DESIGN.md 3.2)"}
+                        "integer ALU work of the FNV automaton and its per-round look-back latency, not by HBM "
+                        "(compute_side: issue / pipe utilisation from the committed ncu capture; DESIGN.md 3.2)"}
     if d.world > 1:
         nv_peak = 782.0  # one copy engine, GPU->peer (scripts/micro/push.cu on this pool)
         egress = r * bytes_local / (ms_local / 1000) / GB
