@@ -162,7 +162,7 @@ def ncu_pipes(kernel):
         names = sorted(n for n in os.listdir(pdir) if n.endswith("_ncu_summary.json"))
         with open(os.path.join(pdir, names[-1])) as fh:
             k = json.load(fh)["full_captures"][kernel]
-        f = lambda key: float(str(k[key]).split()[0])  # noqa: E731
+        f = lambda key: float(k[key][0] if isinstance(k[key], list) else k[key])  # noqa: E731
         return {"issue_active_pct": f("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                 "alu_pipe_pct": f("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
                 "fma_pipe_pct": f("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
