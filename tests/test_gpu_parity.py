@@ -47,7 +47,11 @@ def test_fnv_goldens(mk, ctx):
         i += 1
 
 
-@pytest.mark.parametrize("n", [16383, 16384, 16385, 1 << 20, 5 * (1 << 20) + 77, 64 * (1 << 20) + 13])
+# sizes around the kernel's units: a 128-byte row (one thread), a 256-row TMA
+# box, a 64 KiB chunk, a wave of 3 x 148 chunks
+@pytest.mark.parametrize("n", [127, 128, 129, 255, 256, 32767, 32768, 32769, 65535, 65536, 65537, 131200,
+                               444 * 65536, 444 * 65536 + 5, 16383, 16384, 16385, 1 << 20, 5 * (1 << 20) + 77,
+                               64 * (1 << 20) + 13])
 def test_fnv_large_vs_oracle(mk, ctx, oracle, n):
     rng = np.random.default_rng(n)
     data = rng.integers(0, 256, n, dtype=np.uint8)
@@ -59,6 +63,8 @@ def test_fnv_large_vs_oracle(mk, ctx, oracle, n):
         assert ctx.fnv1a64(ptr, n) == oracle.fnv1a64(data)
         # unaligned start (parse of a sub-range)
         assert ctx.fnv1a64(ptr + 3, n - 3) == oracle.fnv1a64(data[3:])
+        # 16-byte aligned sub-range: the tensor-map path on another base
+        assert ctx.fnv1a64(ptr + 16, n - 16) == oracle.fnv1a64(data[16:])
         assert ctx.fnv1a64(ptr, n, seed=12345) == oracle.fnv1a64(data, seed=12345)
     finally:
         ctx.free(ptr)
