@@ -293,7 +293,12 @@ __device__ __forceinline__ void round_maps_high(const uint32_t (&w)[kThreadWords
 // each entry (an xor of the farther entries' a bits), every entry's toggle of
 // s1 is known, and both fold to parities (two ballots).  Returns the chunk's
 // two start bits.
-constexpr int kProbePerLane = 8;
+#ifndef MLCK_FNV_PROBE
+#define MLCK_FNV_PROBE 1
+#endif
+constexpr int kProbePerLane = MLCK_FNV_PROBE;  // window = 32 * kProbePerLane chunks
+static_assert(kProbePerLane >= 1 && kProbePerLane <= 16, "lane masks hold up to 16 entries");
+constexpr uint32_t kLaneEntries = (1u << kProbePerLane) - 1u;
 __device__ __forceinline__ uint32_t look_back2_warp(const Scratch& scr, int64_t chunk, int r,
                                                     uint32_t seed2, long long* lap = nullptr) {
   const int lane = threadIdx.x & 31;
@@ -365,7 +370,8 @@ __device__ __forceinline__ uint32_t look_back2_warp(const Scratch& scr, int64_t 
     suf ^= suf >> 1;
     suf ^= suf >> 2;
     suf ^= suf >> 4;
-    const uint32_t x = (suf >> 1) ^ (far ? 0xffu : 0u);  // s0 before entry, for s0 = 0 at the far end
+    if (kProbePerLane > 8) suf ^= suf >> 8;
+    const uint32_t x = (suf >> 1) ^ (far ? kLaneEntries : 0u);  // s0 before entry, for s0 = 0 at the far end
     const uint32_t t0 = (x & b1m) | (~x & b0m);  // toggles of s1, far-end s0 = 0
     const uint32_t t1 = (~x & b1m) | (x & b0m);  // far-end s0 = 1
     const uint32_t bal0 = __ballot_sync(0xffffffffu, __popc(t0) & 1u);
