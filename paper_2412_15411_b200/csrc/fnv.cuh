@@ -82,7 +82,10 @@ static_assert(kSegs % 2 == 0, "segments are processed in pairs");
 // One 64-bit look-back word per chunk, kStatusStride words apart (256 B) so
 // the in-flight chunks' words land in different L2 slices.  The high half is
 // the launch epoch, so the array is never cleared between launches.
-constexpr int kStatusStride = 32;
+#ifndef MLCK_FNV_STATUS_STRIDE
+#define MLCK_FNV_STATUS_STRIDE 32
+#endif
+constexpr int kStatusStride = MLCK_FNV_STATUS_STRIDE;
 constexpr uint32_t kSpinLimit = 1u << 24;  // watchdog: never hang the GPU
 
 struct Scratch {
@@ -358,7 +361,10 @@ __device__ __forceinline__ uint32_t look_back2_warp(const Scratch& scr, int64_t 
         first = 0;
         break;
       }
-      __nanosleep(32);
+#ifndef MLCK_FNV_BACKOFF_NS
+#define MLCK_FNV_BACKOFF_NS 32
+#endif
+      if (MLCK_FNV_BACKOFF_NS) __nanosleep(MLCK_FNV_BACKOFF_NS);
     }
     mark(3);
     if (scr.prof && lane == 0 && retries) atomicAdd(scr.prof + 1, static_cast<unsigned long long>(retries));

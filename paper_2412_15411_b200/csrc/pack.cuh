@@ -23,9 +23,15 @@
 namespace mlck {
 namespace pack {
 
-constexpr int kThreads = 256;
-constexpr int kVecPerThread = 4;
-constexpr int kTile = kThreads * kVecPerThread * 16;  // 16 KiB
+#ifndef MLCK_PACK_THREADS
+#define MLCK_PACK_THREADS 256
+#endif
+#ifndef MLCK_PACK_VEC
+#define MLCK_PACK_VEC 2
+#endif
+constexpr int kThreads = MLCK_PACK_THREADS;
+constexpr int kVecPerThread = MLCK_PACK_VEC;
+constexpr int kTile = kThreads * kVecPerThread * 16;  // 8 KiB (swept: 4-16 KiB, 128-512 threads)
 constexpr int kMaxDst = 4;                            // local + up to 3 replicas
 
 struct Segment {
