@@ -643,9 +643,9 @@ void launch_walk(const WalkJob* jobs, int n_jobs, cudaStream_t stream) {
 void launch_replay(const adam::ConvOp* ops, int n_ops, const float* const* gptr, const float2* bc,
                    const adam::Opt& o, int cb, uint64_t total_units, cudaStream_t stream) {
   if (total_units == 0) return;
-  const uint64_t blocks = div_up(total_units, 256);
-  adam::replay_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(ops, n_ops, gptr, bc, o,
-                                                                         cb, total_units);
+  const uint64_t blocks = div_up(total_units, adam::kReplayThreads);
+  adam::replay_kernel<<<static_cast<unsigned>(blocks), adam::kReplayThreads, 0, stream>>>(ops, n_ops, gptr, bc, o,
+                                                                                        cb, total_units);
   MLCK_CUDA(cudaGetLastError());
 }
 
