@@ -64,6 +64,12 @@ constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
 #ifndef MLCK_FNV_ROUND0_LINEAR
 #define MLCK_FNV_ROUND0_LINEAR 1
 #endif
+// MLCK_FNV_PACKED_MAPS: a thread's four segment maps of a round as three
+// 4-bit vectors (a, b0, b1), composed and applied with bit-parallel prefix
+// xors instead of map by map.
+#ifndef MLCK_FNV_PACKED_MAPS
+#define MLCK_FNV_PACKED_MAPS 1
+#endif
 #ifndef MLCK_FNV_NOSHIFT
 #define MLCK_FNV_NOSHIFT 1
 #endif
@@ -286,6 +292,80 @@ __device__ __forceinline__ void round_maps_high(const uint32_t (&w)[kThreadWords
   map[1] = (b0 & 3u) | ((b1 & 2u) << 1);
   map[2] = ((a0 >> 16) & 3u) | (((a1 >> 16) & 2u) << 1);
   map[3] = ((b0 >> 16) & 3u) | (((b1 >> 16) & 2u) << 1);
+}
+
+// ---- packed segment maps.  A round's per-segment maps arrive as two "lane
+// words": byte lane i of e0 holds segment i's a (bit 0) and b0 (bit 1), byte
+// lane i of e1 its b1 (bit 1).
+__device__ __forceinline__ uint32_t gather4(uint32_t v) { return (v * 0x01020408u) >> 24; }  // bits 0,8,16,24 -> 0..3
+__device__ __forceinline__ uint32_t scatter4(uint32_t v) { return (v * 0x00204081u) & 0x01010101u; }  // inverse
+__device__ __forceinline__ uint32_t prefix_xor4_excl(uint32_t v) {  // bit i = xor of bits < i
+  v ^= v << 1;
+  v ^= v << 2;
+  return (v << 1) & 0xfu;
+}
+// The thread's composed map (bits 0-2) and, in bits 3-14, what the segment
+// starts need after the look-back: X (s0 entering each segment for a thread
+// start s0 = 0) and the s1 toggles T0 / T1 for thread start s0 = 0 / 1.
+__device__ __forceinline__ uint32_t compose_lanes(uint32_t e0, uint32_t e1, uint32_t* packed) {
+  const uint32_t A = gather4(e0 & 0x01010101u), B0 = gather4((e0 >> 1) & 0x01010101u),
+                 B1 = gather4((e1 >> 1) & 0x01010101u);
+  const uint32_t X = prefix_xor4_excl(A);
+  const uint32_t T0 = (X & B1) | (~X & B0 & 0xfu), T1 = (~X & B1 & 0xfu) | (X & B0);
+  *packed = (X << 3) | (T0 << 7) | (T1 << 11);
+  return (__popc(A) & 1u) | ((__popc(T0) & 1u) << 1) | ((__popc(T1) & 1u) << 2);
+}
+// Segment start bits (byte lane i: bits 0-1) from the thread's start state s.
+__device__ __forceinline__ uint32_t starts_lanes(uint32_t packed, uint32_t s) {
+  const uint32_t s0 = s & 1u, s1 = (s >> 1) & 1u;
+  const uint32_t X = (packed >> 3) & 0xfu, T = s0 ? (packed >> 11) & 0xfu : (packed >> 7) & 0xfu;
+  const uint32_t S0 = X ^ (0u - s0) & 0xfu, S1 = prefix_xor4_excl(T) ^ ((0u - s1) & 0xfu);
+  return scatter4(S0) | (scatter4(S1) << 1);
+}
+// The rounds' lane words.
+__device__ __forceinline__ void round0_lanes(const uint32_t (&w)[kThreadWords], uint32_t* e0, uint32_t* e1) {
+  uint32_t xe = 0, xo = 0;
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {
+    xe ^= w[k];
+    xo ^= w[k + 1];
+  }
+  const uint32_t xa = xe ^ xo, t = ((xa >> 1) ^ xo) & 0x01010101u;
+  *e0 = (xa & 0x01010101u) | (t << 1);
+  *e1 = t << 1;
+}
+__device__ __forceinline__ void round_lanes_low(const uint32_t (&w)[kThreadWords], uint32_t st, int r, uint32_t* e0,
+                                                uint32_t* e1) {
+  const uint32_t bit = 1u << (2 * r);
+  const uint32_t M = r == 0 ? 0x03030303u : 0x0f0f0f0fu;
+  const uint32_t lo = st & ((bit - 1u) * 0x01010101u);
+  uint32_t x0 = lo, x1 = lo | (bit * 0x01010101u);
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    x0 = ((x0 ^ w[k]) & M) * 3u;
+    x1 = ((x1 ^ w[k]) & M) * 3u;
+  }
+  *e0 = x0 >> (2 * r);
+  *e1 = x1 >> (2 * r);
+}
+__device__ __forceinline__ void round_lanes_high(const uint32_t (&w)[kThreadWords], uint32_t st, int r, uint32_t* e0,
+                                                 uint32_t* e1) {
+  static_assert(MLCK_FNV_NOSHIFT, "packed maps expect the shift-free high rounds");
+  const uint32_t bit = 1u << (2 * r);
+  constexpr uint32_t M = 0x00ff00ffu;
+  const uint32_t lo = st & ((bit - 1u) * 0x01010101u);
+  uint32_t ac0 = lo & M, bd0 = lo & ~M;
+  uint32_t ac1 = ac0 | (bit * 0x00010001u), bd1 = bd0 | (bit * 0x01000100u);
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t y = w[k];
+    ac0 = ((ac0 ^ y) & M) * 0xb3u;
+    ac1 = ((ac1 ^ y) & M) * 0xb3u;
+    bd0 = ((bd0 ^ y) & ~M) * 0xb3u;
+    bd1 = ((bd1 ^ y) & ~M) * 0xb3u;
+  }
+  *e0 = ((ac0 >> (2 * r)) & 0x00030003u) | ((bd0 >> (2 * r)) & 0x03000300u);
+  *e1 = ((ac1 >> (2 * r)) & 0x00020002u) | ((bd1 >> (2 * r)) & 0x02000200u);
 }
 
 // Look-back for round r of `chunk` (one warp): lane l reads the 8

@@ -100,6 +100,9 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
         fnv::mbar_wait(&sh.res[s], (rpar >> s) & 1u);
         rpar ^= 1u << s;
         // lane start -> segment starts through the segment maps
+#if MLCK_FNV_PACKED_MAPS
+        const uint32_t add = starts_lanes(keep[s], map_apply(keep[s] & 7u, sh.wstart[s][warp]));
+#else
         uint32_t ss = map_apply(keep[s] & 7u, sh.wstart[s][warp]);
         uint32_t add = ss;
 #pragma unroll
@@ -107,6 +110,7 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
           ss = map_apply((keep[s] >> (3 * i)) & 7u, ss);
           add |= ss << (8 * i);
         }
+#endif
         st[s] |= add << (2 * rnd[s]);
         lap.mark(1);
         pend[s] = false;
@@ -224,6 +228,16 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
         interleave(w);  // fresh bytes: interleave the segments once, in place
         write_thread(sh, s, tid, w);
       }
+#if MLCK_FNV_PACKED_MAPS
+      uint32_t e0, e1, kp;
+      if (MLCK_FNV_ROUND0_LINEAR && rnd[s] == 0)
+        round0_lanes(w, &e0, &e1);
+      else if (rnd[s] < 2)
+        round_lanes_low(w, st[s], rnd[s], &e0, &e1);
+      else
+        round_lanes_high(w, st[s], rnd[s], &e0, &e1);
+      const uint32_t tm = compose_lanes(e0, e1, &kp);
+#else
       uint32_t m[kSegs];
       if (MLCK_FNV_ROUND0_LINEAR && rnd[s] == 0)
         round0_maps(w, m);
@@ -237,6 +251,7 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
         kp |= m[i - 1] << (3 * i);
         tm = map_compose(m[i], tm);
       }
+#endif
       uint32_t wtot;
       keep[s] = map_scan_warp(tm, &wtot) | kp;
       if (lane == 0) sh.wmap[s][warp] = wtot;
