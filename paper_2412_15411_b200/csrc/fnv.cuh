@@ -495,7 +495,9 @@ struct alignas(1024) Shared {
   unsigned long long kpos[32][4];  // mma_pass epilogue weights per lane
 #endif
 };
-constexpr size_t kSmemBytes = sizeof(Shared);
+// + 1 KiB of slack: the kernel aligns Shared to 1 KiB inside its dynamic
+// shared memory (the TMA swizzle pattern is anchored to 1 KiB boundaries)
+constexpr size_t kSmemBytes = sizeof(Shared) + 1024;
 static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
 static_assert(sizeof(uint4) * kComputeThreads * kGranules % 1024 == 0, "slots keep the swizzle alignment");
 

@@ -345,9 +345,9 @@ __global__ void __launch_bounds__(fnv::kThreads, 1)
                TrailerDsts trailer, fnv::Gather gth, const __grid_constant__ CUtensorMap tmap, int use_tma) {
   using namespace fnv;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
+  // 1 KiB-aligned rows whatever the base of the dynamic window
+  Shared& sh = *reinterpret_cast<Shared*>(smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0 && (smem_addr(smem_raw) & 1023u)) __trap();  // the TMA swizzle needs 1 KiB-aligned rows
   if (tid == 0)
     for (int s = 0; s < kSlots; ++s) {
       for (int w = 0; w < kComputeWarps; ++w) mbar_init(&sh.mbar[s][w], use_tma ? 1 : 32);
