@@ -67,6 +67,8 @@ typedef struct {
 /* ---- errors / context -------------------------------------------------- */
 const char* mlck_last_error(void);
 int mlck_ctx_create(int device, mlck_ctx** out);
+/* Destroy a context's blobs, states, gradient logs and upstream logs first:
+ * their handles refer to it. */
 int mlck_ctx_destroy(mlck_ctx* ctx);
 /* Launch all work of this ctx on `stream` (a cudaStream_t; NULL = the
  * context's own non-blocking stream). */

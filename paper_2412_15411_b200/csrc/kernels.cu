@@ -8,6 +8,7 @@
 #include "pack.cuh"
 
 #include <algorithm>
+#include <mutex>
 #include <cstring>
 #include <string>
 
@@ -517,9 +518,22 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
   const bool pf = prof || trace;
   auto k = gather ? (pf ? fnv_kernel<true, true> : fnv_kernel<false, true>)
                   : (pf ? fnv_kernel<true, false> : fnv_kernel<false, false>);
+  // Hash kernels of this process never overlap on a device: each needs all
+  // its CTAs resident (slot-major look-back), and two grids interleaved on
+  // the SMs could each leave CTAs unscheduled.  Every launch waits for the
+  // previous one on the device, whichever context issued it.
+  static std::mutex order_mu;
+  static cudaEvent_t last_of[64] = {};
+  std::lock_guard<std::mutex> lock(order_mu);
+  cudaEvent_t& last = last_of[dev & 63];
+  if (last)
+    MLCK_CUDA(cudaStreamWaitEvent(stream, last, 0));
+  else
+    MLCK_CUDA(cudaEventCreateWithFlags(&last, cudaEventDisableTiming));
   k<<<static_cast<unsigned>(grid), fnv::kThreads, fnv::kSmemBytes, stream>>>(
       data, n, seed, scr, static_cast<int64_t>(n_chunks), trailer, g, tmap, use_tma);
   MLCK_CUDA(cudaGetLastError());
+  MLCK_CUDA(cudaEventRecord(last, stream));
 }
 
 namespace {

@@ -362,7 +362,8 @@ class DeviceState:
 
     def close(self):
         if self.h:
-            lib().mlck_state_destroy(self.h)
+            if self.ctx.h:  # not after its context: the handle refers to it (memory returns at exit)
+                lib().mlck_state_destroy(self.h)
             self.h = vp()
 
     def __del__(self):
@@ -447,7 +448,8 @@ class Blob:
 
     def close(self):
         if self.h:
-            lib().mlck_blob_destroy(self.h)
+            if self.ctx.h:  # not after its context: the handle refers to it (memory returns at exit)
+                lib().mlck_blob_destroy(self.h)
             self.h = vp()
 
     def __del__(self):

@@ -227,6 +227,34 @@ def test_replay_fast_paths_match_ieee_intrinsics(mk, ctx):
     assert ctx.fastmath_check(1 << 28, seed=7) == (0, 0)
 
 
+def test_concurrent_contexts_hash_correctly(mk):
+    """Two contexts on one device snapshot ~0.5 GB records at once: the hash
+    kernels take turns on the device (each needs its whole grid resident)
+    and both records match their one-context bytes."""
+    a, b = mk.Context(0), mk.Context(0)
+    pcs = [20_000_000, 20_000_000]
+    sts = []
+    for c, seed in ((a, 3), (b, 4)):
+        st = mk.DeviceState(c, pcs, 2)
+        st.fill_synthetic(seed=seed, step=5)
+        st.set_meta(10, 1)
+        sts.append(st)
+    ref = [mk.snapshot_record(st, [0], [1], 0, 1, 10, 2).to_host() for st in sts]
+    outs = [mk.Blob(st.ctx, len(ref[0]) + 4096) for st in sts]
+    for _ in range(3):
+        for st, o in zip(sts, outs):
+            mk.snapshot_record(st, [0], [1], 0, 1, 10, 2, o)  # asynchronous on each context's stream
+    a.synchronize()
+    b.synchronize()
+    assert [o.to_host() for o in outs] == ref
+    for o in outs:  # blobs and states before their contexts
+        o.close()
+    for st in sts:
+        st.close()
+    a.close()
+    b.close()
+
+
 def test_snapshot_errors(mk, ctx):
     c = load_case("six_op_cb4")
     st = upload_state(mk, ctx, c, 1)
