@@ -555,6 +555,9 @@ def run_ours(args, d: Dist):
     kd = kernels["fnv"]
     ach = kd["bytes_per_launch"] / (kd["ms_avg"] / 1000) / GB
     traffic, traffic_src = ncu_traffic("fnv_kernel")
+    if d.world > 1 and traffic is not None:
+        # the committed capture is an N=1 launch (config-2 record); N>1 hashes config-3 records
+        traffic, traffic_src = None, f"none: {traffic_src} is an N=1 (config-2) launch, not this workload's"
     roofline = {"bound": "hbm", "kernel": "fnv", "transport": transport, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                 "frac": ach / hbm_peak, "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
                 "per_launch_bytes": kd["bytes_per_launch"],
