@@ -1,0 +1,116 @@
+"""Multi-GPU replica placement on real devices: each rank packs
+its expert shard's record (`take_sparse_snapshot` on `slot ∩ shard`,
+`snapshot.hpp:204-241`) and the replicas land in its ring peers' HBM over
+NVLink (CUDA IPC, `placement.ring_targets`).  Every peer's copy must equal the
+sender's record byte for byte, under every replica transport, and the record's
+trailer must equal the CPU oracle's FNV-1a-64 (`digest.hpp:18-25`).
+
+One process per GPU; gloo carries only the IPC handles and the host copies the
+checker compares (the data path itself has no collective)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+E = 8  # experts per layer (configs[0] shape), sizes not multiples of 4 so payloads sit at odd offsets
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _record_bytes(pcs, a, c, cb):
+    return 45 + 8 + sum(13 + 8 + 12 * pcs[i] for i in a) + sum(13 + cb * pcs[i] for i in c)
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ok, msg, cur_mode = True, "", None
+    try:
+        from oracle.oracle import Oracle
+        from paper_2412_15411_b200 import mlck
+        from paper_2412_15411_b200 import placement as pl
+
+        cb = 2
+        classes = ["E"] * E + ["NE", "G"]
+        pcs = [40_001 + 4_099 * i for i in range(E)] + [70_003, 517]
+        owned = pl.shard_operators(classes, E, world, rank)
+        ctx = mlck.Context(rank)
+        st = mlck.DeviceState(ctx, pcs, cb)
+        st.fill_synthetic(seed=11, step=3)
+        st.set_meta(40, 11)
+        active = owned[:2]
+        compute_only = owned[2:]
+        # one capacity for every rank's buffers: a sender's record must fit its peers' receive buffers
+        cap = _record_bytes(pcs, range(len(pcs)), [], cb) + 4096
+        r = pl.replicas(world)
+        recv = [ctx.alloc(cap) for _ in range(r)]
+
+        def all_gather(obj):
+            out = [None] * world
+            dist.all_gather_object(out, obj)
+            return out
+
+        targets = pl.exchange_handles(all_gather, [ctx.ipc_export(p) for p in recv], rank, world)
+        opened = [ctx.ipc_open(h) for h, _peer in targets]
+        blob = mlck.Blob(ctx, cap)
+        for p in opened:
+            blob.add_replica(p, cap)
+        orc = Oracle()
+        for mode in (-1, 0, 1, 2, 3, 4, 5):
+            cur_mode = mode
+            for p in recv:
+                ctx.memset(p, 0, cap)
+            ctx.synchronize()
+            dist.barrier()
+            ctx.set_replica_mode(mode)
+            mlck.snapshot_record(st, active, compute_only, 1, 1, 36, 4, blob)
+            ctx.synchronize()
+            dist.barrier()  # every sender's stores are complete before anyone reads
+            mine = blob.to_host()
+            assert len(mine) == _record_bytes(pcs, active, compute_only, cb)
+            trailer = int.from_bytes(mine[-8:], "little")
+            if trailer != orc.fnv1a64(np.frombuffer(mine[:-8], dtype=np.uint8)):
+                ok, msg = False, f"mode {mode}: rank {rank} trailer differs from the oracle FNV"
+            records = all_gather(mine)
+            for j, src in enumerate(pl.ring_sources(rank, world)):
+                want = records[src]
+                if ctx.download(recv[j], len(want)) != want:
+                    ok, msg = False, f"mode {mode}: rank {rank} replica {j} of rank {src} differs"
+            dist.barrier()
+        ctx.set_replica_mode(-1)
+        blob.clear_replicas()
+        blob.close()
+        for p in opened:
+            ctx.ipc_close(p)
+        dist.barrier()
+    except Exception as e:  # report, do not hang the other ranks' queue reads
+        ok, msg = False, f"rank {rank}, mode {cur_mode}: {type(e).__name__}: {e}"
+    q.put((rank, ok, msg))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ring_replicas_byte_exact(world):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    bad = [m for _, ok, m in res if not ok]
+    assert not bad, bad
