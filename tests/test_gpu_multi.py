@@ -2,8 +2,9 @@
 its expert shard's record (`take_sparse_snapshot` on `slot ∩ shard`,
 `snapshot.hpp:204-241`) and the replicas land in its ring peers' HBM over
 NVLink (CUDA IPC, `placement.ring_targets`).  Every peer's copy must equal the
-sender's record byte for byte, under every replica transport, and the record's
-trailer must equal the CPU oracle's FNV-1a-64 (`digest.hpp:18-25`).
+sender's record byte for byte, under every replica transport; the record must
+equal the oracle's serialize_record of the same shard state, and its trailer
+the CPU oracle's FNV-1a-64 (`digest.hpp:18-25`).
 
 One process per GPU; gloo carries only the IPC handles and the host copies the
 checker compares (the data path itself has no collective)."""
@@ -66,6 +67,19 @@ def _worker(rank, world, port, q):
         for p in opened:
             blob.add_replica(p, cap)
         orc = Oracle()
+        # the shard record the reference's take_sparse_snapshot + serialize_record makes from the same
+        # state on slot ∩ shard (fill_synthetic follows the oracle's synth streams 3i, 3i+1, 3i+2)
+        ents = []
+        for i in sorted(active + compute_only):
+            P = pcs[i]
+            master = orc.synth(11, 3 * i, -0.25, 0.25, P)
+            if i in active:
+                ents.append(dict(id=i, mode=0, param_count=P, step=3, master=master,
+                                 m=orc.synth(11, 3 * i + 1, -1e-3, 1e-3, P), v=orc.synth(11, 3 * i + 2, 0.0, 1e-6, P)))
+            else:
+                ents.append(dict(id=i, mode=1, param_count=P, compute=orc.quantize(master, cb)))
+        ref = orc.serialize_record(dict(kind=1, iteration=40, window_start=36, wsparse=4, slot=1, data_seed=11),
+                                   ents, cb)
         for mode in (-1, 0, 1, 2, 3, 4, 5):
             cur_mode = mode
             for p in recv:
@@ -78,6 +92,8 @@ def _worker(rank, world, port, q):
             dist.barrier()  # every sender's stores are complete before anyone reads
             mine = blob.to_host()
             assert len(mine) == _record_bytes(pcs, active, compute_only, cb)
+            if mine != ref:
+                ok, msg = False, f"mode {mode}: rank {rank} record differs from the reference's shard record"
             trailer = int.from_bytes(mine[-8:], "little")
             if trailer != orc.fnv1a64(np.frombuffer(mine[:-8], dtype=np.uint8)):
                 ok, msg = False, f"mode {mode}: rank {rank} trailer differs from the oracle FNV"
