@@ -130,3 +130,63 @@ def test_ring_replicas_byte_exact(world):
         p.join(timeout=60)
     bad = [m for _, ok, m in res if not ok]
     assert not bad, bad
+
+
+def _log_worker(rank, world, port, q):
+    """Upstream logging into the ring successor's HBM (kind 2 over an IPC
+    mapping, what bench.py's N>1 logging does): the entries read back through
+    the log equal the reference's UpstreamLog bit for bit (engine.hpp:55-94)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ok, msg = True, ""
+    try:
+        from golden_cases import load_case
+        from paper_2412_15411_b200 import mlck
+
+        ref = load_case("dp2_pp2").log_entries()
+        cap = 1 << 22
+        ctx = mlck.Context(rank)
+        mine = ctx.alloc(cap)  # this rank hosts its predecessor's log
+        handles = [None] * world
+        dist.all_gather_object(handles, ctx.ipc_export(mine))
+        peer = ctx.ipc_open(handles[(rank + 1) % world])
+        log = mlck.UpstreamLog(ctx, cap, kind=2, external=peer)
+        bufs = []
+        for j in np.random.default_rng(rank).permutation(len(ref)):
+            key, data = ref[j]
+            p = ctx.upload(data)
+            bufs.append(p)
+            log.put(*key, p, data.size)
+        log.sync()
+        got = log.entries()
+        if [k for k, _ in got] != [k for k, _ in ref]:
+            ok, msg = False, f"rank {rank}: key order differs"
+        elif not all(np.array_equal(a.view(np.uint32), b.view(np.uint32)) for (_, a), (_, b) in zip(got, ref)):
+            ok, msg = False, f"rank {rank}: entry bytes differ"
+        log.close()
+        dist.barrier()
+        for p in bufs:
+            ctx.free(p)
+        ctx.ipc_close(peer)
+        dist.barrier()
+    except Exception as e:
+        ok, msg = False, f"rank {rank}: {type(e).__name__}: {e}"
+    q.put((rank, ok, msg))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_upstream_log_in_peer_hbm(world):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_log_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    bad = [m for _, ok, m in res if not ok]
+    assert not bad, bad
