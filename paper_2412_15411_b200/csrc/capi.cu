@@ -1087,6 +1087,13 @@ int mlck_blob_add_replica(mlck_blob* b, void* ptr, uint64_t capacity) {
       throw_invalid("at most " + std::to_string(pack::kMaxDst - 1) + " replicas per blob");
     if (reinterpret_cast<uintptr_t>(ptr) % 16)
       throw_invalid("replica buffers must be 16-byte aligned");
+    // a replica inside a peer's IPC mapping must fit in it: the pack kernel and
+    // the copy engines would otherwise write past the peer's allocation
+    const uint64_t a = reinterpret_cast<uint64_t>(ptr);
+    for (const auto& r : b->ctx->ipc_ranges)
+      if (a >= r.first && a < r.first + r.second && capacity > r.first + r.second - a)
+        throw_invalid("replica capacity " + std::to_string(capacity) + " exceeds its IPC mapping (" +
+                      std::to_string(r.first + r.second - a) + " bytes from the replica pointer)");
     b->replicas.push_back({static_cast<uint8_t*>(ptr), capacity});
   });
 }

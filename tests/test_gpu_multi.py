@@ -63,6 +63,15 @@ def _worker(rank, world, port, q):
 
         targets = pl.exchange_handles(all_gather, [ctx.ipc_export(p) for p in recv], rank, world)
         opened = [ctx.ipc_open(h) for h, _peer in targets]
+        # a replica claiming more than the peer allocated is refused before any write
+        probe = mlck.Blob(ctx, 256)
+        try:
+            probe.add_replica(opened[0], cap + (8 << 20))
+            ok, msg = False, f"rank {rank}: oversized replica capacity accepted"
+        except mlck.MlckInvalid as e:
+            if "exceeds its IPC mapping" not in str(e):
+                ok, msg = False, f"rank {rank}: unexpected error text: {e}"
+        probe.close()
         blob = mlck.Blob(ctx, cap)
         for p in opened:
             blob.add_replica(p, cap)
