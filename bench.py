@@ -4,22 +4,34 @@
 HBM/NVLink roofline").
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload auto|deepseek|mixtral]
+
+--gpus N > 1 without torchrun: the script relaunches itself under
+torch.distributed.run (N ranks, one per GPU, 127.0.0.1); under torchrun the
+world size must equal N.
 
 A step = one training iteration's sparse snapshot: serialize_record(
 take_sparse_snapshot(state, slot[i mod W])) packed on the GPU into the
 byte-exact MLCK record (+ FNV-1a-64 trailer) and pushed to its replicas.
-  N = 1 : workload "deepseek_moe_layer" (BASELINE configs[1]): one layer of
-          proj/configs/deepseek_moe.json (64 x 7,898,100 + NE 80,140,000 +
-          G 100,000 params), W=6, O=11, fp16 compute; replica = a second HBM
-          buffer written by the same kernel.
-  N > 1 : workload "mixtral_8x7b_ep" (configs[2]): 16 experts x 176,160,768
-          params per GPU (expert-parallel, weak scaling), W=4, O=4; each GPU
-          pushes its record to r = min(2, N-1) ring peers over NVLink with
-          remote stores from the pack kernel (CUDA IPC buffers).
+  workload auto = deepseek at N = 1, mixtral at N > 1:
+  deepseek: "deepseek_moe_layer" (BASELINE configs[1]): one layer of
+            proj/configs/deepseek_moe.json (64 x 7,898,100 + NE 80,140,000 +
+            G 100,000 params), W=6, O=11, fp16 compute; replica = a second
+            HBM buffer written by the same kernel.
+  mixtral:  "mixtral_8x7b_ep" (configs[2]): 16 experts x 176,160,768 params
+            per GPU (expert-parallel, weak scaling), W=4, O=4; each GPU pushes
+            its record to r = min(2, N-1) ring peers over NVLink (CUDA IPC
+            buffers; at N = 1 the replica is a second HBM buffer).  The N = 1
+            line also carries this workload (`same_workload_n1`), so the
+            1 -> N curve exists on one workload.
 Then the sparse-to-dense conversion of one full window (configs[3]) with
-fused Adam replay from logged gradients is timed on the same device.
-Rank 0 prints one JSON line.  `--impl reference` times the reference's own
-CPU path (oracle/_ref: the unmodified proj/include headers) on the host.
+fused Adam replay from logged gradients, localized recovery, the upstream
+log (configs[4]), gradient-log capture and snapshot-beside-training
+interference are timed on the same device.  `value` is the whole-job
+aggregate (record bytes of all ranks / max-over-ranks time, the bench
+contract); `per_gpu_gbs` is the metric's GB/s/GPU.  Rank 0 prints one JSON
+line.  `--impl reference` times the reference's own CPU path (oracle/_ref:
+the unmodified proj/include headers) on the host.
 """
 from __future__ import annotations
 
@@ -262,6 +274,69 @@ def cpu_pack_sample(wl, threads, iters=1):
                 co_params=co_p, threads=threads, iters=iters)
 
 
+def cpu_convert_sample(threads, scale=256):
+    """The reference's sparse_to_dense_convert (recovery.hpp:180-227, its
+    recompute replay included) and the merge + logged-gradient replay, on the
+    configs[3] window shape scaled down by `scale` (64 experts + NE + G,
+    W=6, O=11), `threads` independent engines."""
+    import ctypes as C
+    from oracle.oracle import load_reference
+    ref = load_reference()
+    if ref is None:
+        return None
+    L = ref.lib
+    L.mlr_time_convert.restype = C.c_double
+    L.mlr_time_convert.argtypes = [C.c_uint32, C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_uint32, C.c_uint32,
+                                   C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+    secs = (C.c_double * 2)()
+    blob = C.c_uint64()
+    steps = L.mlr_time_convert(threads, 64, 7_898_100 // scale, 80_140_000 // scale, 100_000 // scale, 6, 11, secs,
+                               C.byref(blob))
+    full_steps = 1_888_904_900  # configs[3]
+    conv_rate = threads * steps / secs[0]
+    replay_rate = threads * steps / secs[1]
+    return {"threads": threads, "sample": f"configs[3] window shape / {scale} (64 x {7_898_100 // scale} + "
+                                          f"{80_140_000 // scale} + {100_000 // scale} params, W=6, O=11), "
+                                          f"{threads} independent engines",
+            "element_steps_per_thread": steps, "convert_s": secs[0], "replay_s": secs[1],
+            "convert_msteps_per_s": conv_rate / 1e6, "replay_msteps_per_s": replay_rate / 1e6,
+            "convert_ms_extrapolated_configs3": 1000 * full_steps / conv_rate,
+            "replay_ms_extrapolated_configs3": 1000 * full_steps / replay_rate}
+
+
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def cpu_baseline_full(wl):
+    """cpu_baseline: the headline all-core pack number plus the 1-core and
+    all-core pack and conversion numbers of the reference."""
+    n = cpu_threads()
+    p_all = cpu_pack_sample(wl, n)
+    if p_all is None:
+        return None
+    p_one = cpu_pack_sample(wl, 1)
+    c_one = cpu_convert_sample(1)
+    c_all = cpu_convert_sample(n)
+    out = {"value": p_all["bytes_per_s"] / GB, "unit": "GB/s", "cores": n, "kind": "reference",
+           "sample": (f"reference take_sparse_snapshot+serialize_record, per thread {p_all['n_full']} Full x "
+                      f"{p_all['full_params']} + {p_all['n_co']} CO x {p_all['co_params']} params, "
+                      f"{n} independent engines, {p_all['seconds']:.1f} s"),
+           "pack_1core_gbs": p_one["bytes_per_s"] / GB, "pack_all_cores_gbs": p_all["bytes_per_s"] / GB,
+           "conversion_1core": c_one, "conversion_all_cores": c_all}
+    out.update(host_info())
+    return out
+
+
 METRIC = "snapshot+replicate GB/s/GPU and sparse-to-dense conversion time vs HBM/NVLink roofline"
 
 
@@ -281,10 +356,15 @@ def cpu_threads():
     return max(1, min(n, 32))
 
 
+def pick_workload(args, world):
+    name = args.workload if args.workload != "auto" else ("deepseek" if world == 1 else "mixtral")
+    return deepseek_layer() if name == "deepseek" else mixtral_ep()
+
+
 def run_reference(args, d: Dist):
     if d.rank != 0:
         return
-    wl = deepseek_layer() if d.world == 1 else mixtral_ep()
+    wl = pick_workload(args, d.world)
     threads = cpu_threads()
     vals, secs = [], 0.0
     for _ in range(args.warmup):
@@ -309,10 +389,13 @@ def run_reference(args, d: Dist):
         "config": arm_config(wl, d.world),
         "reference_path": "take_sparse_snapshot + serialize_record (snapshot.hpp:115-144, 204-241) compiled from "
                           f"/root/reference (oracle/_ref), {threads} host threads, bounded sample per step",
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "reference", "sample": sample},
+        "cpu_baseline": dict({"value": value, "unit": "GB/s", "cores": threads, "kind": "reference",
+                              "sample": sample}, **host_info()),
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }
+    if not args.no_convert:  # the conversion half of the metric on the same host cores
+        out["conversion"] = cpu_convert_sample(threads)
     print(json.dumps(out))
 
 
@@ -425,14 +508,160 @@ def bench_logging(ctx, d, mlck, iterations=3):
 
 
 # --------------------------------------------------------------------------
+# gradient-log capture (the replay's input)
+# --------------------------------------------------------------------------
+def bench_gradlog_capture(ctx, mlck, wl, st, iterations=4):
+    """Per-iteration cost of logging the weight gradients the conversion
+    replays: (a) copy capture -- the trainer's gradient buffers (here the
+    state's m arrays stand in) copied into the log slot of the iteration on
+    the ctx stream; (b) zero copy -- the trainer's backward writes straight
+    into mlck_gradlog_slot, no extra traffic.  Plus the HBM the log holds."""
+    pcs, W = wl["param_counts"], wl["W"]
+    g = mlck.GradLog(ctx, pcs, W)
+    srcs = [st.op_ptrs(i)[1] for i in range(len(pcs))]
+
+    def capture(it):
+        for i in range(len(pcs)):
+            g.capture(it, i, srcs[i])
+
+    capture(1)
+    ctx.synchronize()
+    ctx.event_record(6)
+    for it in range(2, 2 + iterations):
+        capture(it)
+    ctx.event_record(7)
+    ctx.synchronize()
+    ms = ctx.event_ms(6, 7) / iterations
+    it_bytes = 4 * sum(pcs)
+    full_slot = {i: k for k, (a, _) in enumerate(schedule(wl)) for i in a}
+    need = sum(4 * pcs[i] * (W - full_slot[i]) for i in range(len(pcs)))
+    out = {"workload": wl["name"], "gradient_bytes_per_iteration": it_bytes,
+           "copy_capture": {"ms_per_iteration": ms, "gbs": 2 * it_bytes / (ms / 1000) / GB,
+                            "note": "D2D copy of every operator's gradient into the log (read + write)"},
+           "zero_copy_capture": {"ms_per_iteration": 0.0,
+                                 "note": "backward writes into mlck_gradlog_slot(iteration, op): no copy"},
+           "hbm_resident_gb": g.nbytes / GB,
+           "hbm_minimum_gb": need / GB,
+           "resident_note": f"a ring of W={W} iterations x all operators; the replay reads only sum 4P(W-k) "
+                            "(each operator's gradients after its Full slot)"}
+    g.close()
+    return out
+
+
+# --------------------------------------------------------------------------
+# snapshot beside training (PAPER.md:66, 451: snapshots overlap compute)
+# --------------------------------------------------------------------------
+def bench_interference(ctx, mlck, st, blobs, slots, dev, gemms=200):
+    """A training-like stream (bf16 GEMMs 8192^3 on the tensor cores plus an
+    HBM-bound elementwise pass per GEMM) on a high-priority stream, alone and
+    with one snapshot (pack + hash + replica of slot 0) issued beside it.
+    Reports the training slowdown and the snapshot's latency per setting."""
+    import torch
+    torch.cuda.set_device(dev)
+    hi = torch.cuda.Stream(device=dev, priority=-1)
+    lo = torch.cuda.Stream(device=dev, priority=0)
+    a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+    b = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+    c = torch.empty(8192, 8192, device=dev, dtype=torch.bfloat16)
+    x = torch.empty(1 << 28, device=dev, dtype=torch.float32)  # 1 GiB: the HBM-bound pass
+    x.fill_(1.0)
+
+    def train():
+        with torch.cuda.stream(hi):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(gemms):
+                torch.matmul(a, b, out=c)
+                x.mul_(1.0000001)
+            e1.record()
+        return e0, e1
+
+    def run(stream_handle, reserve, with_snapshot):
+        ctx.set_stream(stream_handle)
+        ctx.set_hash_reserve(reserve)
+        torch.cuda.synchronize()
+        e0, e1 = train()
+        if with_snapshot:
+            ctx.event_record(8)
+            a0, c0 = slots[0]
+            mlck.snapshot_record(st, a0, c0, 0, 1, 1000, len(slots), blobs[0])
+            ctx.event_record(9)
+        torch.cuda.synchronize()
+        ctx.synchronize()
+        t = e0.elapsed_time(e1)
+        snap = ctx.event_ms(8, 9) if with_snapshot else None
+        return t, snap
+
+    run(None, 0, False)
+    base = statistics.median(run(None, 0, False)[0] for _ in range(3))
+    out = {"training": f"{gemms} x (bf16 GEMM 8192^3 + 1 GiB fp32 elementwise), high-priority stream",
+           "training_ms_alone": base, "settings": {}}
+    for name, handle, reserve in (("ctx stream (highest priority), all SMs", None, 0),
+                                  ("low-priority stream, all SMs", lo.cuda_stream, 0),
+                                  ("low-priority stream, hash on 74 SMs", lo.cuda_stream, 74)):
+        run(handle, reserve, True)
+        res = [run(handle, reserve, True) for _ in range(3)]
+        t = statistics.median(r[0] for r in res)
+        sn = statistics.median(r[1] for r in res)
+        out["settings"][name] = {"training_ms": t, "slowdown": t / base - 1, "delay_ms": t - base, "snapshot_ms": sn}
+    ctx.set_stream(None)
+    ctx.set_hash_reserve(0)
+    best = min(out["settings"].values(), key=lambda v: v["slowdown"])
+    out["best_slowdown"] = best["slowdown"]
+    # the same delay against a real iteration: DeepSeek-MoE's t_iter in the
+    # reference's profile (sim.hpp:35-47, PAPER.md) is 3.45 s
+    out["best_delay_vs_deepseek_iteration"] = best["delay_ms"] / 3450.0
+    del a, b, c, x
+    torch.cuda.empty_cache()
+    return out
+
+
+# --------------------------------------------------------------------------
 # GPU leg
 # --------------------------------------------------------------------------
+def bench_snapshot_n1(ctx, mlck, wl, args):
+    """Snapshot steps of `wl` on one GPU: one record buffer + a replica in a
+    second HBM buffer (transport 0), records rotating through the slots."""
+    pcs, cb, W = wl["param_counts"], wl["cb"], wl["W"]
+    slots = schedule(wl)
+    sizes = [record_bytes(wl, sl) for sl in slots]
+    cap = max(sizes)
+    st = mlck.DeviceState(ctx, pcs, cb)
+    st.fill_synthetic(seed=7, step=10)
+    st.set_meta(1000, 7)
+    blob = mlck.Blob(ctx, cap)
+    rep = ctx.alloc(cap)
+    blob.add_replica(rep, cap)
+
+    def step(i):
+        a, c = slots[i % W]
+        mlck.snapshot_record(st, a, c, i % W, 1, 1000, W, blob)
+
+    for i in range(args.warmup):
+        step(i)
+    ctx.synchronize()
+    ctx.event_record(0)
+    for i in range(args.steps):
+        step(i)
+    ctx.event_record(1)
+    ctx.synchronize()
+    ms = ctx.event_ms(0, 1)
+    total = sum(sizes[i % W] for i in range(args.steps))
+    out = {"workload": wl["name"], "n_gpus": 1, "replica_target": "second HBM buffer (transport 0)",
+           "ms_per_step": ms / args.steps, "value": total / (ms / 1000) / GB, "unit": "GB/s",
+           "record_bytes_per_slot": sizes}
+    st.close()
+    blob.close()
+    ctx.free(rep)
+    return out
+
+
 def run_ours(args, d: Dist):
     from paper_2412_15411_b200 import mlck
 
     dev = d.local
     ctx = mlck.Context(dev)
-    wl = deepseek_layer() if d.world == 1 else mixtral_ep()
+    wl = pick_workload(args, d.world)
     pcs, cb, W = wl["param_counts"], wl["cb"], wl["W"]
     slots = schedule(wl)
     sizes = [record_bytes(wl, s) for s in slots]
@@ -688,15 +917,27 @@ def run_ours(args, d: Dist):
         if d.world == 1:
             parity = parity and ctx.download(recv[k], len(host)) == host
 
+    # ---- gradient-log capture and snapshot beside training (N = 1)
+    extras = {}
+    if d.world == 1 and not args.no_extras:
+        extras["gradlog_capture"] = bench_gradlog_capture(ctx, mlck, wl, st)
+        extras["interference"] = bench_interference(ctx, mlck, st, blobs, slots, dev)
+
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if d.rank == 0 and d.world == 1 and not args.no_cpu:
-        s = cpu_pack_sample(wl, cpu_threads())
-        if s is not None:
-            cpu = {"value": s["bytes_per_s"] / GB, "unit": "GB/s", "cores": s["threads"], "kind": "reference",
-                   "sample": (f"reference take_sparse_snapshot+serialize_record, per thread {s['n_full']} Full x "
-                              f"{s['full_params']} + {s['n_co']} CO x {s['co_params']} params, "
-                              f"{s['threads']} independent engines, {s['seconds']:.1f} s")}
+        cpu = cpu_baseline_full(wl)
+
+    # ---- the configs[2] workload at N = 1 (replica in a second HBM buffer),
+    # so the 1 -> N scaling curve has a point on one workload
+    if d.world == 1 and not args.no_extras and wl["name"] != "mixtral_8x7b_ep":
+        st.close()
+        for b in blobs:
+            b.close()
+        for p in recv:
+            ctx.free(p)
+        recv = []
+        extras["same_workload_n1"] = bench_snapshot_n1(ctx, mlck, mixtral_ep(), args)
 
     clocks = clk.summary()
     launches_total = ctx.kernel_launches
@@ -722,11 +963,21 @@ def run_ours(args, d: Dist):
             "parity_trailer_ok": parity,
             "clocks": clocks,
         }
+        res.update(extras)
         print(json.dumps(res))
 
     for p in opened:
         ctx.ipc_close(p)
     d.barrier()
+
+
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
 
 
 def main():
@@ -735,12 +986,22 @@ def main():
     ap.add_argument("--steps", type=int, default=12)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="auto", choices=["auto", "deepseek", "mixtral"])
     ap.add_argument("--no-convert", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-log", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the N=1 same-workload leg, gradient-log capture and interference keys")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: relaunch under torchrun (the driver's own launch sets WORLD_SIZE)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} ranks")
     d = Dist(world, rank, local)
     try:
         if args.impl == "reference":

@@ -90,6 +90,10 @@ int mlck_ctx_set_timing(mlck_ctx* ctx, int on);
  * every replica and hashes it.  0: the pack kernel stores the replicas, then
  * the FNV kernel.  4: copy engines after the hash (no overlap). */
 int mlck_ctx_set_replica_mode(mlck_ctx* ctx, int mode);
+/* SMs the hash kernel leaves to co-scheduled work (training kernels beside
+ * a snapshot); 0 = all SMs.  The kernel hands chunks out by ticket, so any
+ * grid is correct -- this only trades hash throughput for room. */
+int mlck_ctx_set_hash_reserve(mlck_ctx* ctx, int sms);
 int mlck_ctx_timings(mlck_ctx* ctx, char* labels_csv, uint64_t labels_cap, float* ms,
                      uint32_t cap, uint32_t* n);
 
@@ -194,6 +198,14 @@ int mlck_read_entry(mlck_blob* b, const mlck_entry_info* e, int compute_bytes, f
 /* SparseCheckpoint::check_coverage (snapshot.hpp:322-334). */
 int mlck_check_coverage(mlck_blob* const* blobs, uint32_t n_blobs, uint64_t op_count,
                         int compute_bytes);
+/* conversion_plan (recovery.hpp:123-137): parse_record of every record (raw
+ * parse errors, as the reference: no slot wrapping) and, per record k, the
+ * ids of its Full entries in entry order -- step k's `activating`
+ * (record_index = k, replay_iteration = window_start + k + 1 follow from k).
+ * counts[k] = number of ids of record k; ids concatenated in record order
+ * into `activating` (cap entries; *total = the number needed). */
+int mlck_conversion_plan(mlck_blob* const* blobs, uint32_t n_blobs, int compute_bytes,
+                         uint32_t* activating, uint64_t cap, uint64_t* counts, uint64_t* total);
 
 /* ---- gradient log (inputs of Adam replay) --------------------------------
  * Per-iteration, per-operator fp32 gradients, device resident.  The reference
@@ -209,6 +221,12 @@ int mlck_gradlog_put(mlck_gradlog* g, uint64_t iteration, uint32_t op_id, const 
 int mlck_gradlog_slot(mlck_gradlog* g, uint64_t iteration, uint32_t op_id, float** device_ptr);
 int mlck_gradlog_fill_synthetic(mlck_gradlog* g, uint64_t first_iteration, uint32_t n_iterations,
                                 uint64_t seed);
+/* Capture of a trainer-owned device gradient into the log: a copy on the
+ * ctx stream, ordered after the trainer's work queued there (the zero-copy
+ * alternative: the trainer's backward writes into mlck_gradlog_slot). */
+int mlck_gradlog_capture(mlck_gradlog* g, uint64_t iteration, uint32_t op_id, const float* device_src);
+/* Device bytes the log holds (capacity_iterations x sum of the ops' slots). */
+uint64_t mlck_gradlog_bytes(const mlck_gradlog* g);
 
 /* ---- Adam ----------------------------------------------------------------
  * optimizer_step_adam (engine.hpp:738-753) on device arrays; *step is the
@@ -235,6 +253,23 @@ int mlck_sparse_to_dense_convert(mlck_state* out, mlck_blob* const* blobs, uint3
                                  uint64_t window_start, uint32_t wsparse, uint64_t data_seed,
                                  mlck_gradlog* g, const mlck_optimizer* opt);
 
+/* localized_recover(engine, RecoverySegment, ckpt, logs, target)
+ * (recovery.hpp:240-244) with the scope given as the reference does: the
+ * segment's stage range [stage_lo, stage_hi] and Engine::stage_of_op for
+ * every operator (stage_of_op[id], n_ops entries).  Before replaying it
+ * checks, like run_scoped (engine.hpp:361-366, 393-400), that `log` holds
+ * every boundary tensor the segment consumes for iterations a+1 .. target:
+ * (it, gmb, stage_lo-1, fwd) when stage_lo > 0 and (it, gmb, stage_hi, bwd)
+ * when stage_hi < n_stages-1, gmb < n_global_microbatches (dp x M) --
+ * "upstream log missing entry: ..." otherwise (log may be NULL only when
+ * the segment spans every stage).  Then as mlck_localized_recover. */
+int mlck_localized_recover_segment(mlck_state* out, int32_t stage_lo, int32_t stage_hi,
+                                   const int32_t* stage_of_op, int32_t n_stages,
+                                   mlck_blob* const* blobs, uint32_t n_blobs, uint64_t window_start,
+                                   uint32_t wsparse, uint64_t data_seed, mlck_log* log,
+                                   uint32_t n_global_microbatches, mlck_gradlog* g,
+                                   uint64_t target_iteration, const mlck_optimizer* opt);
+
 /* localized_recover (recovery.hpp:240-289): conversion restricted to the
  * operators `scope_ids` (the failed stages' operators, Engine::stage_of_op),
  * then the lost iterations after the window up to target_iteration; every
@@ -260,9 +295,20 @@ int mlck_log_create_external(mlck_ctx* ctx, void* device_base, uint64_t capacity
 int mlck_log_destroy(mlck_log* l);
 /* Records the sender-side copy of a boundary tensor (engine.hpp:383-385,
  * 407-409); src is device memory produced on the ctx stream. Overwrites an
- * existing key like the reference's map assignment. */
+ * existing key like the reference's map assignment.
+ * Source lifetime: the copy runs on the log's low-priority side stream once
+ * the ctx stream's work so far is done.  In the default ORDERED mode the ctx
+ * stream then waits for the copy, so any later work on the ctx stream may
+ * overwrite src -- the reference's synchronous copy, seen from the stream.
+ * In ASYNC mode (mlck_log_set_async(l, 1)) nothing waits: src must stay
+ * unmodified until mlck_log_fence() has ordered the writer's stream after
+ * the copies (or mlck_log_sync() returned). */
 int mlck_log_put(mlck_log* l, uint64_t iteration, uint32_t micro_batch, uint32_t boundary,
                  uint8_t direction, const float* device_src, uint64_t n_floats);
+int mlck_log_set_async(mlck_log* l, int async);
+/* Makes `stream` (a cudaStream_t; NULL = the ctx stream) wait for every
+ * copy put() issued so far, without blocking the host. */
+int mlck_log_fence(mlck_log* l, void* stream);
 /* UpstreamLog::at (engine.hpp:71-79): "upstream log missing entry: ..." */
 int mlck_log_get(mlck_log* l, uint64_t iteration, uint32_t micro_batch, uint32_t boundary,
                  uint8_t direction, float* host_out, uint64_t cap_floats, uint64_t* n_floats);
@@ -278,10 +324,37 @@ int mlck_log_entry(mlck_log* l, uint64_t index, uint64_t* iteration, uint32_t* m
                    uint64_t* n_floats);
 /* gc_logs (engine.hpp:90-94): drop iteration < persisted_window_start. */
 int mlck_gc_logs(mlck_log* l, uint64_t persisted_window_start);
+/* upstream_log_bytes(model, plan, wsparse) (recovery.hpp:296-304): the
+ * retained worst case, 2 windows x W x 2(S-1)M dp entries of mb x d floats. */
+int64_t mlck_upstream_log_bytes(int32_t token_dim, int32_t pp_stages, int32_t microbatches,
+                                int64_t microbatch_size, int32_t dp_degree, int64_t wsparse);
+/* check_log_budget(model, plan, wsparse, cluster) (recovery.hpp:308-317):
+ * MLCK_EINVAL with "upstream log budget exceeded: need N bytes of host
+ * memory, budget B" when cpu_mem_per_node * nodes cannot hold it (a budget
+ * <= 0 is unchecked). */
+int mlck_check_log_budget(int32_t token_dim, int32_t pp_stages, int32_t microbatches,
+                          int64_t microbatch_size, int32_t dp_degree, int64_t wsparse,
+                          double cpu_mem_per_node, int32_t nodes);
 /* Wait until every put() has landed. */
 int mlck_log_sync(mlck_log* l);
 
-/* ---- codecs (tensor.hpp:99-183), bulk on device --------------------------- */
+/* ---- codecs (tensor.hpp:99-183), on device --------------------------------
+ * Generic reduced formats: pack_reduced(x, ebits, mbits) / unpack_reduced
+ * (tensor.hpp:127-183) over n device values (codes are uint16), 2 <= ebits <= 8,
+ * 1 <= mbits, ebits + mbits <= 15. */
+int mlck_pack_reduced(mlck_ctx* ctx, const float* device_in, uint16_t* device_codes, uint64_t n,
+                      int ebits, int mbits);
+int mlck_unpack_reduced(mlck_ctx* ctx, const uint16_t* device_codes, float* device_out, uint64_t n,
+                        int ebits, int mbits);
+/* The reference's scalar forms quantize_value (tensor.hpp:99-111),
+ * pack_reduced, unpack_reduced: n host values through the device kernels
+ * (the scalar API of the shim is n = 1). */
+int mlck_quantize_values(mlck_ctx* ctx, const float* host_in, float* host_out, uint64_t n,
+                         int compute_bytes);
+int mlck_pack_reduced_values(mlck_ctx* ctx, const float* host_in, uint16_t* host_codes, uint64_t n,
+                             int ebits, int mbits);
+int mlck_unpack_reduced_values(mlck_ctx* ctx, const uint16_t* host_codes, float* host_out, uint64_t n,
+                               int ebits, int mbits);
 int mlck_quantize(mlck_ctx* ctx, const float* device_in, float* device_out, uint64_t n,
                   int compute_bytes);
 int mlck_encode_compute(mlck_ctx* ctx, const float* device_in, void* device_codes, uint64_t n,

@@ -67,6 +67,47 @@ struct OptimizerConfig {
   }
 };
 
+// The slices of ModelSpec / ParallelPlan / ClusterSpec (core.hpp:66-190)
+// the checkpoint path reads: operator layout, pipeline shape, host budget.
+struct ModelSpec {
+  int32_t layers = 1;
+  int32_t experts_per_layer = 1;
+  int32_t token_dim = 4;
+  int64_t operator_count() const { return static_cast<int64_t>(layers) * (experts_per_layer + 2); }
+};
+struct ParallelPlan {
+  int32_t pp_stages = 1;
+  int32_t dp_degree = 1;
+  int32_t microbatches = 1;
+  int64_t microbatch_size = 1;
+  int32_t stage_of_layer(int32_t layer, int32_t layers) const {  // core.hpp:187-190
+    return static_cast<int32_t>((static_cast<int64_t>(layer) * pp_stages) / layers);
+  }
+};
+struct ClusterSpec {
+  int32_t nodes = 1;
+  double cpu_mem_per_node = 0.0;  // bytes; 0 = unchecked
+};
+// Engine::stage_of_op for every operator id (engine.hpp:170-172): ids are
+// layer-major, E experts then the non-expert block and the gate per layer
+// (ModelSpec::operators, core.hpp:105-134).
+inline std::vector<int32_t> stage_of_ops(const ModelSpec& m, const ParallelPlan& p) {
+  std::vector<int32_t> st(static_cast<size_t>(m.operator_count()));
+  for (size_t id = 0; id < st.size(); ++id)
+    st[id] = p.stage_of_layer(static_cast<int32_t>(id / (m.experts_per_layer + 2)), m.layers);
+  return st;
+}
+
+// upstream_log_bytes / check_log_budget (recovery.hpp:296-317)
+inline int64_t upstream_log_bytes(const ModelSpec& m, const ParallelPlan& p, int64_t wsparse) {
+  return mlck_upstream_log_bytes(m.token_dim, p.pp_stages, p.microbatches, p.microbatch_size, p.dp_degree,
+                                 wsparse);
+}
+inline void check_log_budget(const ModelSpec& m, const ParallelPlan& p, int64_t wsparse, const ClusterSpec& c) {
+  check(mlck_check_log_budget(m.token_dim, p.pp_stages, p.microbatches, p.microbatch_size, p.dp_degree, wsparse,
+                              c.cpu_mem_per_node, c.nodes));
+}
+
 // ---- device context -------------------------------------------------------
 class Context {
  public:
@@ -78,10 +119,44 @@ class Context {
   Context& operator=(const Context&) = delete;
   mlck_ctx* get() const { return h_; }
   void synchronize() const { check(mlck_ctx_synchronize(h_)); }
+  // SMs the hash kernel leaves to co-scheduled training work
+  void set_hash_reserve(int sms) const { check(mlck_ctx_set_hash_reserve(h_, sms)); }
+  // The context the scalar codec forms use when none is given (device 0).
+  static Context& default_context() {
+    thread_local Context c(0);
+    return c;
+  }
 
  private:
   mlck_ctx* h_ = nullptr;
 };
+
+// ---- codecs (tensor.hpp:99-183): the reference's scalar forms, computed by
+// the device codec kernels (bit-identical to the bulk paths) ---------------
+inline float quantize_value(Context& ctx, float x, int compute_bytes) {
+  float y = 0.0f;
+  check(mlck_quantize_values(ctx.get(), &x, &y, 1, compute_bytes));
+  return y;
+}
+inline uint16_t pack_reduced(Context& ctx, float x, int ebits, int mbits) {
+  uint16_t c = 0;
+  check(mlck_pack_reduced_values(ctx.get(), &x, &c, 1, ebits, mbits));
+  return c;
+}
+inline float unpack_reduced(Context& ctx, uint16_t code, int ebits, int mbits) {
+  float y = 0.0f;
+  check(mlck_unpack_reduced_values(ctx.get(), &code, &y, 1, ebits, mbits));
+  return y;
+}
+inline float quantize_value(float x, int compute_bytes) {
+  return quantize_value(Context::default_context(), x, compute_bytes);
+}
+inline uint16_t pack_reduced(float x, int ebits, int mbits) {
+  return pack_reduced(Context::default_context(), x, ebits, mbits);
+}
+inline float unpack_reduced(uint16_t code, int ebits, int mbits) {
+  return unpack_reduced(Context::default_context(), code, ebits, mbits);
+}
 
 // Host view of one operator (OperatorState, engine.hpp:33-45).
 struct OperatorState {
@@ -280,11 +355,11 @@ struct ParsedRecord {
 
 inline ParsedRecord parse_record(const DeviceBlob& blob, const PrecisionPlan& plan) {
   mlck_record_info info{};
-  std::vector<mlck_entry_info> ents(1 << 16);
   uint32_t n = 0;
   const int cb = static_cast<int>(plan.compute_bytes);
-  check(mlck_parse_record(blob.get(), cb, &info, ents.data(),
-                          static_cast<uint32_t>(ents.size()), &n));
+  check(mlck_parse_record(blob.get(), cb, &info, nullptr, 0, &n));
+  std::vector<mlck_entry_info> ents(n);
+  check(mlck_parse_record(blob.get(), cb, &info, ents.data(), n, &n));
   ParsedRecord pr;
   pr.iteration = info.iteration;
   pr.slot = info.slot;
@@ -375,6 +450,43 @@ struct SparseCheckpoint {
     return ck;
   }
 };
+
+// ---- conversion_plan (recovery.hpp:112-137) -------------------------------
+struct ConversionStep {
+  uint32_t record_index = 0;
+  uint64_t replay_iteration = 0;
+  std::vector<uint32_t> activating;
+};
+struct ConversionPlan {
+  uint64_t window_start = 0;
+  std::vector<ConversionStep> steps;
+};
+inline ConversionPlan conversion_plan(const SparseCheckpoint& ckpt, const PrecisionPlan& plan) {
+  ConversionPlan cp;
+  cp.window_start = ckpt.window_start;
+  if (ckpt.blobs.size() < ckpt.wsparse)  // the reference's ckpt.blobs.at(k)
+    throw std::out_of_range("vector::_M_range_check: __n (which is " + std::to_string(ckpt.blobs.size()) +
+                            ") >= this->size() (which is " + std::to_string(ckpt.blobs.size()) + ")");
+  std::vector<mlck_blob*> hs;
+  for (uint32_t k = 0; k < ckpt.wsparse; ++k) hs.push_back(ckpt.blobs[k].get());
+  std::vector<uint64_t> counts(hs.size());
+  uint64_t total = 0;
+  const int cb = static_cast<int>(plan.compute_bytes);
+  check(mlck_conversion_plan(hs.data(), static_cast<uint32_t>(hs.size()), cb, nullptr, 0, counts.data(), &total));
+  std::vector<uint32_t> ids(total);
+  check(mlck_conversion_plan(hs.data(), static_cast<uint32_t>(hs.size()), cb, ids.data(), total, counts.data(),
+                             &total));
+  uint64_t at = 0;
+  for (uint32_t k = 0; k < ckpt.wsparse; ++k) {
+    ConversionStep st;
+    st.record_index = k;
+    st.replay_iteration = ckpt.window_start + k + 1;
+    st.activating.assign(ids.begin() + static_cast<long>(at), ids.begin() + static_cast<long>(at + counts[k]));
+    at += counts[k];
+    cp.steps.push_back(std::move(st));
+  }
+  return cp;
+}
 
 // "One persisted checkpoint and another in flight, garbage-collecting the
 // oldest after persisting a new one".  Records go to the window
@@ -561,6 +673,10 @@ class UpstreamLog {
     return out;
   }
   void sync() const { check(mlck_log_sync(h_)); }
+  // ASYNC mode: put() leaves the producer stream free; the caller fences the
+  // stream that will overwrite a logged source (mlck_b200.h, mlck_log_put)
+  void set_async(bool on) const { check(mlck_log_set_async(h_, on ? 1 : 0)); }
+  void fence(void* stream = nullptr) const { check(mlck_log_fence(h_, stream)); }
 
  private:
   mlck_log* h_ = nullptr;
@@ -568,6 +684,43 @@ class UpstreamLog {
 
 inline void gc_logs(UpstreamLog& log, uint64_t persisted_window_start) {
   check(mlck_gc_logs(log.get(), persisted_window_start));
+}
+
+// ---- localized_recover(engine, segment, ckpt, logs, target) ----------------
+// (recovery.hpp:240-289) with the reference's own scope vocabulary: the
+// failed stage range of one pipeline (RecoverySegment, recovery.hpp:29-41)
+// and Engine::stage_of_op (stage_of_ops above).  The boundary tensors the
+// segment consumes must be in `logs` (checked per replayed iteration and
+// micro-batch, "upstream log missing entry: ..."); the optimizer steps come
+// from the gradient log.
+struct RecoverySegment {
+  int32_t pipeline = 0;
+  int32_t stage_lo = 0;
+  int32_t stage_hi = 0;
+  std::optional<int32_t> upstream_log_owner;
+  std::optional<int32_t> downstream_log_owner;
+};
+inline LocalizedRecoveryResult localized_recover(DeviceState& out, const RecoverySegment& seg,
+                                                 const SparseCheckpoint& ckpt, const UpstreamLog& logs,
+                                                 GradientLog* grads, const std::vector<int32_t>& stage_of_op,
+                                                 const ParallelPlan& plan, uint64_t data_seed,
+                                                 uint64_t target_iteration, const OptimizerConfig& oc = {}) {
+  if (stage_of_op.size() != out.op_count()) throw std::invalid_argument("stage_of_op: one entry per operator");
+  std::vector<mlck_blob*> hs;
+  for (const auto& b : ckpt.blobs) hs.push_back(b.get());
+  const mlck_optimizer o = oc.abi();
+  check(mlck_localized_recover_segment(out.get(), seg.stage_lo, seg.stage_hi, stage_of_op.data(), plan.pp_stages,
+                                       hs.data(), static_cast<uint32_t>(hs.size()), ckpt.window_start, ckpt.wsparse,
+                                       data_seed, logs.get(),
+                                       static_cast<uint32_t>(plan.dp_degree * plan.microbatches),
+                                       grads ? grads->get() : nullptr, target_iteration, &o));
+  LocalizedRecoveryResult r;
+  uint64_t it = 0, seed = 0;
+  check(mlck_state_get_meta(out.get(), &it, &seed));
+  r.iteration = it;
+  for (uint32_t id = 0; id < out.op_count(); ++id)
+    if (stage_of_op[id] >= seg.stage_lo && stage_of_op[id] <= seg.stage_hi) r.ops.emplace(id, out.op(id));
+  return r;
 }
 
 }  // namespace moelab_b200

@@ -432,3 +432,9 @@ float mlo_synth_value(uint64_t seed, uint64_t stream, uint64_t index, float lo, 
 void mlo_synth_fill(uint64_t seed, uint64_t stream, float lo, float hi, float* out, size_t n) {
   for (size_t i = 0; i < n; ++i) out[i] = mlo_synth_value(seed, stream, i, lo, hi);
 }
+
+/* elements [first, first + n) of the stream (chunked checks of big operators) */
+void mlo_synth_fill_range(uint64_t seed, uint64_t stream, float lo, float hi, float* out, uint64_t first,
+                          size_t n) {
+  for (size_t i = 0; i < n; ++i) out[i] = mlo_synth_value(seed, stream, first + i, lo, hi);
+}

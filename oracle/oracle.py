@@ -128,6 +128,8 @@ class Oracle:
         L.mlo_synth_value.restype = C.c_float
         L.mlo_synth_value.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_float, C.c_float]
         L.mlo_synth_fill.argtypes = [C.c_uint64, C.c_uint64, C.c_float, C.c_float, f32p, C.c_size_t]
+        L.mlo_synth_fill_range.argtypes = [C.c_uint64, C.c_uint64, C.c_float, C.c_float, f32p, C.c_uint64,
+                                           C.c_size_t]
 
     # ---- primitives
     def fnv1a64(self, data, seed: int = 0xcbf29ce484222325) -> int:
@@ -262,9 +264,9 @@ class Oracle:
         self.lib.mlo_init_master(seed, op_id, token_dim, _ptr(out, f32p), n)
         return out
 
-    def synth(self, seed, stream, lo, hi, n) -> np.ndarray:
+    def synth(self, seed, stream, lo, hi, n, first=0) -> np.ndarray:
         out = np.empty(n, dtype=np.float32)
-        self.lib.mlo_synth_fill(seed, stream, lo, hi, _ptr(out, f32p), n)
+        self.lib.mlo_synth_fill_range(seed, stream, lo, hi, _ptr(out, f32p), first, n)
         return out
 
 
@@ -359,12 +361,18 @@ class Reference:
         L.mlr_gc_logs.argtypes = [C.c_void_p, C.c_uint64]
         L.mlr_log_at.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint8,
                                  C.c_char_p, C.c_size_t]
+        L.mlr_conversion_plan.restype = C.c_int64
+        L.mlr_conversion_plan.argtypes = [C.c_uint64, C.c_uint32, C.POINTER(u8p), u64p, C.c_uint32, C.c_int64,
+                                          u32p, C.c_size_t, u64p, u64p, C.c_char_p, C.c_size_t]
+        L.mlr_check_log_budget.argtypes = [cp, C.c_int64, C.c_double, C.c_int32, C.c_char_p, C.c_size_t]
         L.mlr_upstream_log_bytes.restype = C.c_int64
         L.mlr_upstream_log_bytes.argtypes = [cp, C.c_int64]
         L.mlr_fnv1a64.restype = C.c_uint64
         L.mlr_fnv1a64.argtypes = [u8p, C.c_size_t, C.c_uint64]
         L.mlr_quantize_value.argtypes = [C.c_float, C.c_int, f32p, C.c_char_p, C.c_size_t]
         L.mlr_quantize_array.argtypes = [f32p, C.c_size_t, C.c_int, f32p, C.c_char_p, C.c_size_t]
+        L.mlr_pack_array.argtypes = [f32p, C.c_size_t, C.c_int, C.c_int, C.POINTER(C.c_uint16)]
+        L.mlr_unpack_array.argtypes = [C.POINTER(C.c_uint16), C.c_size_t, C.c_int, C.c_int, f32p]
         L.mlr_pack_reduced.restype = C.c_uint16
         L.mlr_pack_reduced.argtypes = [C.c_float, C.c_int, C.c_int]
         L.mlr_unpack_reduced.restype = C.c_float
@@ -554,6 +562,49 @@ def ref_localized_recover(ref: Reference, cfg: MlrConfig, window_start: int, wsp
     out = np.empty(n, dtype=np.uint8)
     ref.lib.mlr_localized_recover(*args, _ptr(out, u8p), n, err, 1024)
     return out.tobytes()
+
+
+def ref_conversion_plan(ref: Reference, window_start: int, wsparse: int, blobs: list, compute_bytes: int):
+    """conversion_plan (recovery.hpp:123-137): [(record_index, replay_iteration, activating ids)]."""
+    bufs = [np.frombuffer(bytes(b), dtype=np.uint8) for b in blobs]
+    ptrs = (u8p * max(1, len(bufs)))(*[_ptr(b, u8p) for b in bufs])
+    sizes = np.array([b.size for b in bufs] or [0], dtype=np.uint64)
+    n = max(1, wsparse)
+    counts = np.zeros(n, dtype=np.uint64)
+    its = np.zeros(n, dtype=np.uint64)
+    ids = np.zeros(1 << 16, dtype=np.uint32)
+    err = ref._err()
+    tot = ref.lib.mlr_conversion_plan(window_start, wsparse, ptrs, _ptr(sizes, u64p), len(bufs), compute_bytes,
+                                      _ptr(ids, u32p), ids.size, _ptr(counts, u64p), _ptr(its, u64p), err, 1024)
+    if tot < 0:
+        raise RefError(err.value.decode())
+    out, at = [], 0
+    for k in range(wsparse):
+        c = int(counts[k])
+        out.append((k, int(its[k]), [int(x) for x in ids[at:at + c]]))
+        at += c
+    return out
+
+
+def ref_pack_reduced(ref: Reference, x: np.ndarray, ebits: int, mbits: int) -> np.ndarray:
+    """pack_reduced (tensor.hpp:127-151) over float32 bits as they are (no
+    float -> double round trip: signalling-NaN payloads survive)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty(x.size, dtype=np.uint16)
+    ref.lib.mlr_pack_array(_ptr(x, f32p), x.size, ebits, mbits, out.ctypes.data_as(C.POINTER(C.c_uint16)))
+    return out
+
+
+def ref_unpack_reduced(ref: Reference, codes: np.ndarray, ebits: int, mbits: int) -> np.ndarray:
+    c = np.ascontiguousarray(codes, dtype=np.uint16)
+    out = np.empty(c.size, dtype=np.float32)
+    ref.lib.mlr_unpack_array(c.ctypes.data_as(C.POINTER(C.c_uint16)), c.size, ebits, mbits, _ptr(out, f32p))
+    return out
+
+
+def ref_check_log_budget(ref: Reference, cfg: MlrConfig, wsparse: int, cpu_mem_per_node: float, nodes: int):
+    err = ref._err()
+    ref._check(ref.lib.mlr_check_log_budget(C.byref(cfg), wsparse, cpu_mem_per_node, nodes, err, 1024), err)
 
 
 def ref_check_coverage(ref: Reference, wsparse: int, blobs: list, op_count: int, compute_bytes: int):

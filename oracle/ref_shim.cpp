@@ -358,6 +358,47 @@ int64_t mlr_localized_recover(const mlr_config* c, uint64_t window_start, uint32
   return size;
 }
 
+// conversion_plan(ckpt, plan) (recovery.hpp:123-137): counts[k] = the
+// activating ids of step k, concatenated into ids (cap entries); returns the
+// total, -1 on error.
+int64_t mlr_conversion_plan(uint64_t window_start, uint32_t wsparse, const uint8_t* const* blobs,
+                            const uint64_t* sizes, uint32_t n_blobs, int64_t compute_bytes, uint32_t* ids,
+                            size_t cap, uint64_t* counts, uint64_t* replay_iterations, char* err, size_t ecap) {
+  int64_t total = -1;
+  guarded(err, ecap, [&] {
+    SparseCheckpoint ckpt;
+    ckpt.window_start = window_start;
+    ckpt.wsparse = wsparse;
+    for (uint32_t k = 0; k < n_blobs; ++k) ckpt.blobs.emplace_back(blobs[k], blobs[k] + sizes[k]);
+    PrecisionPlan plan;
+    plan.compute_bytes = compute_bytes;
+    const ConversionPlan cp = conversion_plan(ckpt, plan);
+    size_t w = 0;
+    for (size_t k = 0; k < cp.steps.size(); ++k) {
+      counts[k] = cp.steps[k].activating.size();
+      replay_iterations[k] = cp.steps[k].replay_iteration;
+      for (uint32_t id : cp.steps[k].activating) {
+        if (w < cap) ids[w] = id;
+        ++w;
+      }
+    }
+    total = static_cast<int64_t>(w);
+  });
+  return total;
+}
+
+// check_log_budget(model, plan, wsparse, cluster) (recovery.hpp:308-317).
+int mlr_check_log_budget(const mlr_config* c, int64_t wsparse, double cpu_mem_per_node, int32_t nodes,
+                         char* err, size_t ecap) {
+  return guarded(err, ecap, [&] {
+    const EngineConfig cfg = to_cfg(c);
+    ClusterSpec cl;
+    cl.cpu_mem_per_node = cpu_mem_per_node;
+    cl.nodes = nodes;
+    check_log_budget(cfg.model, cfg.parallel, wsparse, cl);
+  });
+}
+
 // SparseCheckpoint::check_coverage (snapshot.hpp:322-334).
 int mlr_check_coverage(uint32_t wsparse, const uint8_t* const* blobs, const uint64_t* sizes,
                        uint32_t n_blobs, uint64_t op_count, int64_t compute_bytes, char* err,
@@ -425,6 +466,9 @@ void mlr_unpack_array(const uint16_t* codes, size_t n, int ebits, int mbits, flo
   for (size_t i = 0; i < n; ++i) out[i] = unpack_reduced(codes[i], ebits, mbits);
 }
 uint16_t mlr_pack_reduced(float x, int ebits, int mbits) { return pack_reduced(x, ebits, mbits); }
+void mlr_pack_array(const float* x, size_t n, int ebits, int mbits, uint16_t* out) {
+  for (size_t i = 0; i < n; ++i) out[i] = pack_reduced(x[i], ebits, mbits);
+}
 float mlr_unpack_reduced(uint16_t c, int ebits, int mbits) { return unpack_reduced(c, ebits, mbits); }
 
 int mlr_optimizer_step_adam(float* master, float* m, float* v, uint64_t* step, const float* grad,
@@ -551,6 +595,136 @@ double mlr_time_replay(uint32_t threads, uint64_t params, uint32_t steps, double
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (seconds) *seconds = secs;
   return static_cast<double>(threads) * params * steps / secs;
+}
+
+// Reference conversion on a window of the configs[3] shape, scaled: one
+// layer of `experts` experts of expert_params, NE ne_params, G gate_params,
+// W = wsparse with o_active Full operators per slot (generate_schedule on
+// the id order, schedule.hpp:153-172), records captured the reference's way
+// (capture_windows, verify.hpp:63-84) by `threads` independent engines
+// (SPEC.md:192).  Times, per thread, after one warm-up:
+//   [0] sparse_to_dense_convert(engine, ckpt)  (recovery.hpp:180-227, its
+//       recompute replay included);
+//   [1] the merge + logged-gradient replay the GPU kernel implements:
+//       parse_record of every record, then each operator's Full payload
+//       stepped with optimizer_step_adam on its W-k logged gradients.
+// secs[0..1] = wall seconds of each (all threads at once); returns the
+// Adam element-steps of one window per thread; *blob_bytes = its records.
+double mlr_time_convert(uint32_t threads, int32_t experts, int64_t expert_params, int64_t ne_params,
+                        int64_t gate_params, uint32_t wsparse, uint32_t o_active, double* secs,
+                        uint64_t* blob_bytes) {
+  struct Shard {
+    std::unique_ptr<Engine> eng;
+    SparseCheckpoint ckpt;
+    std::vector<std::vector<std::vector<float>>> grads;  // [iteration k][op]
+  };
+  std::vector<Shard> shards(threads);
+  double steps = 0;
+  uint64_t bytes = 0;
+  auto build = [&](uint32_t t) {
+    mlr_config c{};
+    c.layers = 1;
+    c.experts_per_layer = experts;
+    c.top_k = 2;
+    c.token_dim = 4;
+    c.expert_hidden = 4;
+    c.nonexpert_hidden = 4;
+    c.residual = 1;
+    c.expert_params = expert_params;
+    c.nonexpert_params = ne_params;
+    c.gate_params = gate_params;
+    c.compute_bytes = 2;
+    c.pp_stages = c.dp_degree = 1;
+    c.microbatches = 2;
+    c.microbatch_size = 4;
+    c.global_batch = 8;
+    c.lr = 1e-3f;
+    c.beta1 = 0.9f;
+    c.beta2 = 0.999f;
+    c.eps = 1e-8f;
+    c.seed = 5 + t;
+    Shard& sh = shards[t];
+    sh.eng = std::make_unique<Engine>(to_cfg(&c));
+    std::vector<uint32_t> ordered(sh.eng->operators().size());
+    for (uint32_t i = 0; i < ordered.size(); ++i) ordered[i] = i;
+    const SparseSchedule sched = generate_schedule(ordered, wsparse, o_active, OrderingScheme::HardCount);
+    sh.ckpt.window_start = 0;
+    sh.ckpt.wsparse = wsparse;
+    const PrecisionPlan& plan = sh.eng->config().precision;
+    for (uint32_t k = 0; k < wsparse; ++k) {  // state k -> slot k of window 0
+      sh.ckpt.add_record(take_sparse_snapshot(*sh.eng, sched.slots[k], k), plan);
+      // the iteration's weight gradients (the logged-replay input): the
+      // beta1 = 0, lr = 0 probe of a clone
+      mlr_config pc = c;
+      pc.beta1 = 0.0f;
+      pc.lr = 0.0f;
+      Engine probe(to_cfg(&pc));
+      probe.mutable_state() = sh.eng->state();
+      for (auto& op : probe.mutable_state().ops) std::fill(op.m.begin(), op.m.end(), 0.0f);
+      probe.run_iteration();
+      std::vector<std::vector<float>> g;
+      for (const auto& op : probe.state().ops) g.push_back(op.m);
+      sh.grads.push_back(std::move(g));
+      sh.eng->run_iteration();
+    }
+  };
+  {
+    std::vector<std::thread> ts;
+    for (uint32_t t = 0; t < threads; ++t) ts.emplace_back(build, t);
+    for (auto& th : ts) th.join();
+  }
+  {
+    const auto& sh = shards[0];
+    for (const auto& b : sh.ckpt.blobs) bytes += b.size();
+    const auto ops = sh.eng->operators();
+    for (uint32_t k = 0; k < wsparse; ++k) {
+      const ParsedRecord pr = parse_record(sh.ckpt.blobs[k], sh.eng->config().precision);
+      for (const auto& [id, p] : pr.record.entries)
+        if (p.mode == SnapshotMode::Full) steps += static_cast<double>(p.master.size()) * (wsparse - k);
+    }
+  }
+  auto convert = [&](uint32_t t) {
+    Shard& sh = shards[t];
+    Engine scratch(sh.eng->config());
+    const TrainState st = sparse_to_dense_convert(scratch, sh.ckpt);
+    (void)st;
+  };
+  auto replay = [&](uint32_t t) {
+    Shard& sh = shards[t];
+    const PrecisionPlan& plan = sh.eng->config().precision;
+    const OptimizerConfig oc = sh.eng->config().optimizer;
+    std::vector<OperatorState> ops(sh.eng->operators().size());
+    std::vector<uint32_t> slot_of(ops.size(), 0);
+    for (uint32_t k = 0; k < wsparse; ++k) {
+      const ParsedRecord pr = parse_record(sh.ckpt.blobs[k], plan);
+      for (const auto& [id, p] : pr.record.entries)
+        if (p.mode == SnapshotMode::Full) {
+          ops[id].master = p.master;
+          ops[id].m = p.m;
+          ops[id].v = p.v;
+          ops[id].step = p.step;
+          slot_of[id] = k;
+        }
+    }
+    for (uint32_t id = 0; id < ops.size(); ++id) {
+      for (uint32_t k = slot_of[id]; k < wsparse; ++k)
+        optimizer_step_adam(ops[id].master, ops[id].m, ops[id].v, ops[id].step, sh.grads[k][id], oc);
+      ops[id].refresh_compute(static_cast<int>(plan.compute_bytes));
+    }
+  };
+  auto timed = [&](auto&& fn) {
+    std::vector<std::thread> ts;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint32_t t = 0; t < threads; ++t) ts.emplace_back(fn, t);
+    for (auto& th : ts) th.join();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  };
+  timed(convert);  // warm-up
+  secs[0] = timed(convert);
+  timed(replay);
+  secs[1] = timed(replay);
+  if (blob_bytes) *blob_bytes = bytes;
+  return steps;
 }
 
 }  // extern "C"

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <string>
 #include <tuple>
@@ -68,8 +69,40 @@ struct mlck_ctx {
   int cur = 0;
   uint32_t* fnv_scratch = nullptr;
   size_t fnv_words = 0;
-  unsigned long long* results = nullptr;  // device [64]
-  unsigned long long* host_results = nullptr;  // pinned [64]
+  // record verification (parse_record's checksum) alternates between two
+  // side streams, each with its own look-back scratch, so one record's hash
+  // fills the SMs the previous one leaves as it drains, and the ctx stream
+  // stays free for the walk and the conversion replay
+  cudaStream_t vside[2] = {};
+  cudaEvent_t ev_vside[2] = {}, ev_vmain = nullptr;
+  uint32_t* vscratch[2] = {};
+  size_t vwords[2] = {};
+  uint32_t* vscratch_for(int i, uint64_t n) {
+    const size_t need = fnv_scratch_words(n);
+    if (need > vwords[i]) {
+      MLCK_CUDA(cudaStreamSynchronize(vside[i]));
+      if (vscratch[i]) MLCK_CUDA(cudaFree(vscratch[i]));
+      vwords[i] = align_up(std::max<size_t>(need, 4096), 1024);
+      MLCK_CUDA(cudaMalloc(&vscratch[i], vwords[i] * 4));
+      MLCK_CUDA(cudaMemsetAsync(vscratch[i], 0, vwords[i] * 4, vside[i]));
+    }
+    return vscratch[i];
+  }
+  // SMs the hash kernel leaves free (mlck_ctx_set_hash_reserve)
+  int hash_reserve = 0;
+  unsigned long long* results = nullptr;       // device [results_cap]
+  unsigned long long* host_results = nullptr;  // pinned [results_cap]
+  size_t results_cap = 0;
+  // grows both result arrays to >= n words (the stream is idle or synchronized)
+  void results_for(size_t n) {
+    if (n <= results_cap) return;
+    MLCK_CUDA(cudaStreamSynchronize(stream));
+    if (results) MLCK_CUDA(cudaFree(results));
+    if (host_results) MLCK_CUDA(cudaFreeHost(host_results));
+    results_cap = align_up(std::max<size_t>(n, 64), 64);
+    MLCK_CUDA(cudaMalloc(&results, results_cap * 8));
+    MLCK_CUDA(cudaMallocHost(&host_results, results_cap * 8));
+  }
   cudaEvent_t ev[16] = {};
   // Optional per-kernel timing (CUDA events on the launch stream), read back
   // with mlck_ctx_timings() -- the benchmark's roofline denominator.
@@ -168,12 +201,14 @@ struct mlck_ctx {
   // word in the scratch header; checked after the stream synchronizes.
   bool watchdog_seen = false;
   void read_watchdog() {
-    if (!fnv_scratch) return;
-    uint32_t w = 0;
-    MLCK_CUDA(cudaMemcpy(&w, fnv_scratch + fnv_sticky_word(), 4, cudaMemcpyDeviceToHost));
-    if (w) {
-      MLCK_CUDA(cudaMemset(fnv_scratch + fnv_sticky_word(), 0, 4));
-      watchdog_seen = true;
+    for (uint32_t* sc : {fnv_scratch, vscratch[0], vscratch[1]}) {
+      if (!sc) continue;
+      uint32_t w = 0;
+      MLCK_CUDA(cudaMemcpy(&w, sc + fnv_sticky_word(), 4, cudaMemcpyDeviceToHost));
+      if (w) {
+        MLCK_CUDA(cudaMemset(sc + fnv_sticky_word(), 0, 4));
+        watchdog_seen = true;
+      }
     }
   }
   void check_watchdog() {  // the stream is synchronized
@@ -199,7 +234,11 @@ struct mlck_ctx {
   }
   uint32_t next_epoch() {
     if (++fnv_epoch == 0) {  // wrapped: clear stale tags once
-      MLCK_CUDA(cudaMemsetAsync(fnv_scratch, 0, fnv_words * 4, stream));
+      MLCK_CUDA(cudaStreamSynchronize(stream));
+      for (int i = 0; i < 2; ++i) MLCK_CUDA(cudaStreamSynchronize(vside[i]));
+      if (fnv_scratch) MLCK_CUDA(cudaMemset(fnv_scratch, 0, fnv_words * 4));
+      for (int i = 0; i < 2; ++i)
+        if (vscratch[i]) MLCK_CUDA(cudaMemset(vscratch[i], 0, vwords[i] * 4));
       fnv_epoch = 1;
     }
     return fnv_epoch;
@@ -401,7 +440,7 @@ void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool traile
     uint32_t* scratch = ctx->fnv_scratch_for(body);
     const int tf = ctx->tbegin("pack_fnv");
     launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream,
-               nullptr, nullptr, &g);
+               nullptr, nullptr, &g, ctx->hash_reserve);
     ctx->tend(tf);
     ctx->launches += 1;
     return;
@@ -435,7 +474,7 @@ void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool traile
     uint32_t* scratch = ctx->fnv_scratch_for(body);
     const int tf = ctx->tbegin("fnv");
     launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream, nullptr,
-               nullptr, nullptr, 0, &reps);
+               nullptr, nullptr, ctx->hash_reserve, &reps);
     ctx->tend(tf);
     ctx->launches += 2;
     return;
@@ -463,7 +502,7 @@ void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool traile
     uint32_t* scratch = ctx->fnv_scratch_for(body);
     const int tf = ctx->tbegin("fnv");
     launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream, nullptr,
-               nullptr, nullptr, mlck_ctx::kPushSms);
+               nullptr, nullptr, std::max(mlck_ctx::kPushSms, ctx->hash_reserve));
     ctx->tend(tf);
     ctx->launches += 3;
     MLCK_CUDA(cudaEventRecord(ctx->ev_pushed[0], ctx->side[0]));
@@ -492,7 +531,8 @@ void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool traile
     uint32_t* scratch = ctx->fnv_scratch_for(body);
     auto hash = [&] {
       const int tf = ctx->tbegin("fnv");
-      launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream);
+      launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream, nullptr,
+                 nullptr, nullptr, ctx->hash_reserve);
       ctx->tend(tf);
       MLCK_CUDA(cudaEventRecord(ctx->ev_hashed, ctx->stream));
     };
@@ -548,7 +588,8 @@ void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool traile
     t.n = d.n;
     uint32_t* scratch = ctx->fnv_scratch_for(body);
     const int tf = ctx->tbegin("fnv");
-    launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream);
+    launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream, nullptr,
+               nullptr, nullptr, ctx->hash_reserve);
     ctx->tend(tf);
     ctx->launches += 1;
   }
@@ -656,92 +697,140 @@ std::string walk_error(const WalkResult& r) {
   }
 }
 
-// Verifies and walks n blobs with one FNV launch per blob and one walk
-// launch, one synchronization.  errors[k] empty when blob k parsed.
-std::vector<Parsed> parse_blobs(mlck_ctx* ctx, mlck_blob* const* blobs, uint32_t n, int cb,
-                                std::vector<std::string>& errors) {
-  errors.assign(n, std::string());
-  std::vector<Parsed> out(n);
-  if (n == 0) return out;
-  if (n > 32) throw_invalid("parse: at most 32 records per call");
-  // device scratch: results + per-blob walk outputs + entry tables
-  const uint32_t cap_entries = 1u << 16;
-  // entry tables live in a per-call device allocation
-  std::vector<uint8_t> checksum_ok(n, 0);
-  std::vector<unsigned long long> computed(n), stored(n);
+// parse_record over n device records in three phases, so the caller can
+// overlap its own work with the checksum pass:
+//   verify_begin: one FNV launch per record (trailer check, snapshot.hpp:
+//     156-163), alternating between the ctx stream and vside; nothing waits;
+//   walk: the header / entry walk of every record of >= 8 bytes (bounds
+//     checked, so a corrupt record walks harmlessly) on the ctx stream, which
+//     is synchronized -- entry tables sized from the records' own op counts;
+//   verify_end: the ctx stream joins vside; errors[k] in the reference's
+//     order: "container truncated" (< 8 bytes), "container checksum
+//     mismatch", then the walk's magic / version / truncation error.
+struct ParseJob {
+  mlck_ctx* ctx = nullptr;
+  mlck_blob* const* blobs = nullptr;
+  uint32_t n = 0;
+  int cb = 2;
+  std::vector<Parsed> out;
+  std::vector<std::string> walk_err;
+};
+
+void verify_begin(ParseJob& j) {
+  mlck_ctx* ctx = j.ctx;
+  const uint32_t n = j.n;
+  ctx->results_for(2 * static_cast<size_t>(n));
+  MLCK_CUDA(cudaEventRecord(ctx->ev_vmain, ctx->stream));  // the records are complete
+  for (int i = 0; i < 2; ++i) MLCK_CUDA(cudaStreamWaitEvent(ctx->vside[i], ctx->ev_vmain, 0));
+  uint32_t launched = 0;
   for (uint32_t k = 0; k < n; ++k) {
-    const mlck_blob* b = blobs[k];
-    if (b->size < 8) {
-      errors[k] = "container truncated";
-      continue;
-    }
+    const mlck_blob* b = j.blobs[k];
+    if (b->size < 8) continue;
+    const int side = static_cast<int>(launched++ & 1u);
+    cudaStream_t st = ctx->vside[side];
+    uint32_t* scratch = ctx->vscratch_for(side, b->size - 8);
     TrailerDsts none{};
-    uint32_t* scratch = ctx->fnv_scratch_for(b->size - 8);
-    const int tf = ctx->tbegin("fnv_verify");
-    launch_fnv(b->dev, b->size - 8, kFnvOffset, scratch, ctx->next_epoch(), ctx->results + k, none,
-               ctx->stream);
-    ctx->tend(tf);
+    const int tf = ctx->tbegin("fnv_verify", st);
+    launch_fnv(b->dev, b->size - 8, kFnvOffset, scratch, ctx->next_epoch(), ctx->results + k, none, st,
+               nullptr, nullptr, nullptr, ctx->hash_reserve);
+    ctx->tend(tf, st);
     ctx->launches += 1;
-    MLCK_CUDA(cudaMemcpyAsync(ctx->results + 32 + k, b->dev + b->size - 8, 8,
-                              cudaMemcpyDeviceToDevice, ctx->stream));
+    MLCK_CUDA(cudaMemcpyAsync(ctx->results + n + k, b->dev + b->size - 8, 8, cudaMemcpyDeviceToDevice, st));
   }
-  MLCK_CUDA(cudaMemcpyAsync(ctx->host_results, ctx->results, 64 * 8, cudaMemcpyDeviceToHost,
+  for (int i = 0; i < 2; ++i) MLCK_CUDA(cudaEventRecord(ctx->ev_vside[i], ctx->vside[i]));
+}
+
+void walk_records(ParseJob& j) {
+  mlck_ctx* ctx = j.ctx;
+  j.out.assign(j.n, Parsed{});
+  j.walk_err.assign(j.n, std::string());
+  std::vector<uint32_t> idx;
+  for (uint32_t k = 0; k < j.n; ++k)
+    if (j.blobs[k]->size >= 8) idx.push_back(k);
+  std::vector<uint32_t> cap(j.n, 1024);
+  // pass 1 with 1024 entries per record; records with more run again with
+  // their own op count (the walk validates every entry either way)
+  for (int pass = 0; pass < 2 && !idx.empty(); ++pass) {
+    const size_t nj = idx.size();
+    const size_t res_bytes = align_up(nj * sizeof(WalkResult), 256);
+    std::vector<size_t> ent_off(nj + 1, 0);
+    for (size_t q = 0; q < nj; ++q) ent_off[q + 1] = ent_off[q] + align_up(cap[idx[q]] * sizeof(WalkEntry), 256);
+    uint8_t* dscratch = nullptr;
+    MLCK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dscratch), res_bytes + ent_off[nj], ctx->stream));
+    std::vector<WalkJob> jobs(nj);
+    for (size_t q = 0; q < nj; ++q) {
+      const mlck_blob* b = j.blobs[idx[q]];
+      jobs[q] = WalkJob{b->dev, b->size, j.cb, cap[idx[q]], reinterpret_cast<WalkEntry*>(dscratch + res_bytes + ent_off[q]),
+                        reinterpret_cast<WalkResult*>(dscratch) + q};
+    }
+    auto& stg = ctx->stage_for(nj * sizeof(WalkJob));
+    std::memcpy(stg.host, jobs.data(), nj * sizeof(WalkJob));
+    ctx->stage_upload(stg, nj * sizeof(WalkJob));
+    const int tw = ctx->tbegin("walk");
+    launch_walk(reinterpret_cast<const WalkJob*>(stg.dev), static_cast<int>(nj), ctx->stream);
+    ctx->tend(tw);
+    ctx->launches += 1;
+    std::vector<WalkResult> res(nj);
+    MLCK_CUDA(cudaMemcpyAsync(res.data(), dscratch, nj * sizeof(WalkResult), cudaMemcpyDeviceToHost, ctx->stream));
+    MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::vector<uint32_t> again;
+    for (size_t q = 0; q < nj; ++q) {
+      const uint32_t k = idx[q];
+      j.out[k].hdr = res[q];
+      if (res[q].status != kWalkOk) {
+        j.walk_err[k] = walk_error(res[q]);
+        continue;
+      }
+      if (res[q].n_entries > cap[k]) {
+        cap[k] = res[q].n_entries;
+        again.push_back(k);
+        continue;
+      }
+      j.out[k].entries.resize(res[q].n_entries);
+      MLCK_CUDA(cudaMemcpyAsync(j.out[k].entries.data(), dscratch + res_bytes + ent_off[q],
+                                res[q].n_entries * sizeof(WalkEntry), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    MLCK_CUDA(cudaFreeAsync(dscratch, ctx->stream));
+    MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+    idx.swap(again);
+  }
+}
+
+std::vector<std::string> verify_end(ParseJob& j) {
+  mlck_ctx* ctx = j.ctx;
+  const uint32_t n = j.n;
+  for (int i = 0; i < 2; ++i) MLCK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_vside[i], 0));
+  MLCK_CUDA(cudaMemcpyAsync(ctx->host_results, ctx->results, 2 * static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost,
                             ctx->stream));
   MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->check_watchdog();
-  std::vector<WalkJob> jobs;
-  std::vector<uint32_t> job_blob;
+  std::vector<std::string> errors(n);
   for (uint32_t k = 0; k < n; ++k) {
-    if (!errors[k].empty()) continue;
-    if (ctx->host_results[k] != ctx->host_results[32 + k]) {  // snapshot.hpp:158-163
+    if (j.blobs[k]->size < 8)
+      errors[k] = "container truncated";
+    else if (ctx->host_results[k] != ctx->host_results[n + k])  // snapshot.hpp:158-163
       errors[k] = "container checksum mismatch";
-      continue;
-    }
-    job_blob.push_back(k);
+    else
+      errors[k] = j.walk_err[k];
+    if (!errors[k].empty()) j.out[k].entries.clear();
   }
-  if (job_blob.empty()) return out;
-  const size_t nj = job_blob.size();
-  const size_t res_bytes = align_up(nj * sizeof(WalkResult), 256);
-  const size_t ent_bytes = static_cast<size_t>(cap_entries) * sizeof(WalkEntry);
-  uint8_t* dscratch = nullptr;
-  MLCK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dscratch), res_bytes + nj * ent_bytes, ctx->stream));
-  for (size_t j = 0; j < nj; ++j) {
-    const mlck_blob* b = blobs[job_blob[j]];
-    WalkJob w;
-    w.blob = b->dev;
-    w.n = b->size;
-    w.compute_bytes = cb;
-    w.cap = cap_entries;
-    w.result = reinterpret_cast<WalkResult*>(dscratch) + j;
-    w.entries = reinterpret_cast<WalkEntry*>(dscratch + res_bytes + j * ent_bytes);
-    jobs.push_back(w);
-  }
-  auto& s = ctx->stage_for(nj * sizeof(WalkJob));
-  std::memcpy(s.host, jobs.data(), nj * sizeof(WalkJob));
-  ctx->stage_upload(s, nj * sizeof(WalkJob));
-  const int tw = ctx->tbegin("walk");
-  launch_walk(reinterpret_cast<const WalkJob*>(s.dev), static_cast<int>(nj), ctx->stream);
-  ctx->tend(tw);
-  ctx->launches += 1;
-  std::vector<WalkResult> res(nj);
-  MLCK_CUDA(cudaMemcpyAsync(res.data(), dscratch, nj * sizeof(WalkResult), cudaMemcpyDeviceToHost,
-                            ctx->stream));
-  MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
-  for (size_t j = 0; j < nj; ++j) {
-    const uint32_t k = job_blob[j];
-    out[k].hdr = res[j];
-    if (res[j].status != kWalkOk) {
-      errors[k] = walk_error(res[j]);
-      continue;
-    }
-    out[k].entries.resize(std::min(res[j].n_entries, cap_entries));
-    MLCK_CUDA(cudaMemcpyAsync(out[k].entries.data(), dscratch + res_bytes + j * ent_bytes,
-                              out[k].entries.size() * sizeof(WalkEntry), cudaMemcpyDeviceToHost,
-                              ctx->stream));
-  }
-  MLCK_CUDA(cudaFreeAsync(dscratch, ctx->stream));
-  MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
-  return out;
+  return errors;
+}
+
+// All three phases: verified and walked records; errors[k] empty when blob k parsed.
+std::vector<Parsed> parse_blobs(mlck_ctx* ctx, mlck_blob* const* blobs, uint32_t n, int cb,
+                                std::vector<std::string>& errors) {
+  ParseJob j;
+  j.ctx = ctx;
+  j.blobs = blobs;
+  j.n = n;
+  j.cb = cb;
+  errors.assign(n, std::string());
+  if (n == 0) return {};
+  verify_begin(j);
+  walk_records(j);
+  errors = verify_end(j);
+  return std::move(j.out);
 }
 
 }  // namespace
@@ -770,13 +859,17 @@ int mlck_ctx_create(int device, mlck_ctx** out) {
     c->stream = c->own;
     for (auto& s : c->stage) MLCK_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
     for (auto& sd : c->side) MLCK_CUDA(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      MLCK_CUDA(cudaStreamCreateWithPriority(&c->vside[i], cudaStreamNonBlocking, greatest));
+      MLCK_CUDA(cudaEventCreateWithFlags(&c->ev_vside[i], cudaEventDisableTiming));
+    }
+    MLCK_CUDA(cudaEventCreateWithFlags(&c->ev_vmain, cudaEventDisableTiming));
     for (cudaEvent_t* e : {&c->ev_packed, &c->ev_hashed})
       MLCK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (auto& e : c->ev_pushed) MLCK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : c->ev_piece) MLCK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : c->ev) MLCK_CUDA(cudaEventCreate(&e));
-    MLCK_CUDA(cudaMalloc(&c->results, 64 * 8));
-    MLCK_CUDA(cudaMallocHost(&c->host_results, 64 * 8));
+    c->results_for(64);
     // stream-ordered scratch (parse tables, staging) stays in the pool across
     // synchronizations instead of being returned to the OS every call
     cudaMemPool_t pool;
@@ -807,6 +900,13 @@ int mlck_ctx_destroy(mlck_ctx* c) {
     for (auto& e : c->ev_piece) cudaEventDestroy(e);
     cudaEventDestroy(c->ev_packed);
     cudaEventDestroy(c->ev_hashed);
+    for (int i = 0; i < 2; ++i) {
+      cudaStreamSynchronize(c->vside[i]);
+      cudaStreamDestroy(c->vside[i]);
+      cudaEventDestroy(c->ev_vside[i]);
+      if (c->vscratch[i]) cudaFree(c->vscratch[i]);
+    }
+    cudaEventDestroy(c->ev_vmain);
     if (c->fnv_scratch) cudaFree(c->fnv_scratch);
     if (c->patch) cudaFree(c->patch);
     cudaFree(c->results);
@@ -839,6 +939,13 @@ int mlck_ctx_set_replica_mode(mlck_ctx* c, int mode) {
                     "2 (fused pack+hash+push), 3 (SM push beside the hash), 4 (copy engines "
                     "after the hash) or 5 (hash-kernel stores)");
     c->replica_mode = mode;
+  });
+}
+
+int mlck_ctx_set_hash_reserve(mlck_ctx* c, int sms) {
+  return api([&] {
+    if (sms < 0) throw_invalid("hash reserve must be >= 0 SMs");
+    c->hash_reserve = sms;
   });
 }
 
@@ -1107,10 +1214,13 @@ int mlck_blob_replication(mlck_blob* b, uint32_t* done) {
     *done = 0;
     if (!b->written) return;
     const cudaError_t e = cudaEventQuery(b->written);
-    if (e == cudaSuccess)
-      *done = b->written_replicas;
-    else if (e != cudaErrorNotReady)
-      MLCK_CUDA(e);
+    if (e == cudaErrorNotReady) return;
+    MLCK_CUDA(e);
+    // a record whose hash the look-back watchdog cut short carries a poisoned
+    // trailer: it is not a replica of anything (the error, not a count)
+    b->ctx->activate();
+    b->ctx->check_watchdog();
+    *done = b->written_replicas;
   });
 }
 
@@ -1404,6 +1514,31 @@ int mlck_check_coverage(mlck_blob* const* blobs, uint32_t n, uint64_t op_count, 
   });
 }
 
+int mlck_conversion_plan(mlck_blob* const* blobs, uint32_t n, int cb, uint32_t* activating, uint64_t cap,
+                         uint64_t* counts, uint64_t* total) {
+  return api([&] {
+    if (total) *total = 0;
+    if (n == 0) return;
+    mlck_ctx* ctx = blobs[0]->ctx;
+    ctx->activate();
+    std::vector<std::string> errs;
+    auto p = parse_blobs(ctx, blobs, n, cb, errs);
+    uint64_t w = 0;
+    for (uint32_t k = 0; k < n; ++k) {  // recovery.hpp:127-134, in slot order
+      if (!errs[k].empty()) throw_runtime(errs[k]);
+      uint64_t c = 0;
+      for (const auto& e : p[k].entries)
+        if (e.mode == 0) {
+          if (activating && w < cap) activating[w] = e.id;
+          ++w;
+          ++c;
+        }
+      if (counts) counts[k] = c;
+    }
+    if (total) *total = w;
+  });
+}
+
 // ------------------------------------------------------------------ gradients
 int mlck_gradlog_create(mlck_ctx* ctx, uint32_t n_ops, const uint64_t* pc, uint32_t cap,
                         mlck_gradlog** out) {
@@ -1444,6 +1579,20 @@ int mlck_gradlog_put(mlck_gradlog* g, uint64_t it, uint32_t op, const float* hos
     MLCK_CUDA(cudaStreamSynchronize(g->ctx->stream));
   });
 }
+int mlck_gradlog_capture(mlck_gradlog* g, uint64_t it, uint32_t op, const float* src) {
+  return api([&] {
+    g->ctx->activate();
+    float* d = g->slot(it, op);
+    if (!g->P[op]) return;
+    if ((reinterpret_cast<uintptr_t>(src) & 15u) == 0) {  // slots are 256-byte aligned: SM copy at HBM speed
+      launch_copy16(d, src, 4 * g->P[op], g->ctx->stream);
+      g->ctx->launches += 1;
+    } else {
+      ce_copy(d, src, 4 * g->P[op], cudaMemcpyDeviceToDevice, g->ctx->stream);
+    }
+  });
+}
+uint64_t mlck_gradlog_bytes(const mlck_gradlog* g) { return g ? 4 * g->per_iter * g->cap : 0; }
 int mlck_gradlog_slot(mlck_gradlog* g, uint64_t it, uint32_t op, float** ptr) {
   return api([&] { *ptr = g->slot(it, op); });
 }
@@ -1554,12 +1703,43 @@ void convert_impl(mlck_state* out, mlck_blob* const* blobs, uint32_t n_blobs, ui
   }
   mlck_ctx* ctx = out->ctx;
   ctx->activate();
-  std::vector<std::string> errs;
   const uint32_t n_parse = (W == 1 && !localized) ? 1 : W;
-  auto parsed = parse_blobs(ctx, blobs, n_parse, out->cb, errs);
-  for (uint32_t k = 0; k < n_parse; ++k)  // recovery.hpp:163-171
-    if (!errs[k].empty())
-      throw_runtime("sparse checkpoint record (slot " + std::to_string(k) + "): " + errs[k]);
+  // The entry walk runs first (microseconds), then the records' checksums
+  // are verified on the two side streams while the host builds the replay
+  // table; the replay follows the verification (run concurrently, the
+  // ALU-bound hash and the issue-bound replay only slowed each other down:
+  // 13.0 ms vs 12.8 ms sequential, DESIGN 3.3).  Every error surfaces in the
+  // reference's order -- a record's parse error (checksum first) before
+  // anything the merge finds.
+  ParseJob job;
+  job.ctx = ctx;
+  job.blobs = blobs;
+  job.n = n_parse;
+  job.cb = out->cb;
+  walk_records(job);
+  verify_begin(job);
+  bool verified = false;
+  auto parse_errors = [&] {  // recovery.hpp:163-171
+    if (verified) return;
+    const auto errs = verify_end(job);
+    verified = true;
+    for (uint32_t k = 0; k < n_parse; ++k)
+      if (!errs[k].empty())
+        throw_runtime("sparse checkpoint record (slot " + std::to_string(k) + "): " + errs[k]);
+  };
+  for (uint32_t k = 0; k < n_parse; ++k)
+    if (blobs[k]->size < 8 || !job.walk_err[k].empty()) parse_errors();
+  const auto& parsed = job.out;
+  struct Finish {  // an exception below still joins the side streams
+    std::function<void()> f;
+    ~Finish() {
+      if (f) try { f(); } catch (...) {}
+    }
+  } join{[&] {
+    if (!verified) {
+      for (int i = 0; i < 2; ++i) cudaStreamWaitEvent(ctx->stream, ctx->ev_vside[i], 0);
+    }
+  }};
   auto in_scope = [&](uint32_t id) { return !localized || (id < scope->size() && (*scope)[id]); };
   // each operator's last Full payload in slot order (load_record overwrites)
   struct Src {
@@ -1569,10 +1749,15 @@ void convert_impl(mlck_state* out, mlck_blob* const* blobs, uint32_t n_blobs, ui
   std::vector<Src> src(out->n_ops);
   for (uint32_t k = 0; k < n_parse; ++k)
     for (const auto& e : parsed[k].entries) {
-      if (e.id >= out->n_ops) throw_runtime("conversion: record operator id out of range");
+      if (e.id >= out->n_ops) {
+        parse_errors();
+        throw_runtime("conversion: record operator id out of range");
+      }
       if (e.mode == 0 && in_scope(e.id)) {
-        if (e.param_count != out->P[e.id])
+        if (e.param_count != out->P[e.id]) {
+          parse_errors();
           throw_invalid("conversion: operator " + std::to_string(e.id) + " size mismatch");
+        }
         src[e.id] = {static_cast<int>(k), &e};
       }
     }
@@ -1583,16 +1768,15 @@ void convert_impl(mlck_state* out, mlck_blob* const* blobs, uint32_t n_blobs, ui
   const bool replay = localized || W > 1;
   if (replay)
     for (uint32_t id = 0; id < out->n_ops; ++id)
-      if (in_scope(id) && src[id].slot < 0)
+      if (in_scope(id) && src[id].slot < 0) {
+        parse_errors();
         throw_runtime(localized ? "localized recovery left operator " + std::to_string(id) + " frozen"  // 263-266
                                 : "conversion finished with frozen operator " + std::to_string(id));  // 222-225
+      }
   const uint64_t end = window_start + W + (localized && target > window_start + W ? target - window_start - W : 0);
   std::vector<uint64_t> new_step(out->n_ops, 0);
   for (uint32_t id = 0; id < out->n_ops; ++id) {
-    if (!in_scope(id)) continue;
-    out->present[id] = src[id].slot >= 0 ? 1 : 0;
-    out->has_full[id] = out->present[id];
-    if (src[id].slot < 0) continue;
+    if (!in_scope(id) || src[id].slot < 0) continue;
     const int k = src[id].slot;
     const WalkEntry& e = *src[id].e;
     adam::ConvOp c{};
@@ -1606,17 +1790,32 @@ void convert_impl(mlck_state* out, mlck_blob* const* blobs, uint32_t n_blobs, ui
     uint64_t stp = e.step;
     for (uint32_t s = 0; s < c.n_steps; ++s) {
       const uint64_t it = window_start + static_cast<uint64_t>(k) + 1 + s;
-      if (!g) throw_invalid("conversion: gradient log required for W > 1");
-      gptr.push_back(g->lookup(it, id));
+      if (!g) {
+        parse_errors();
+        throw_invalid("conversion: gradient log required for W > 1");
+      }
+      const float* gp = nullptr;
+      try {
+        gp = g->lookup(it, id);
+      } catch (...) {
+        parse_errors();
+        throw;
+      }
+      gptr.push_back(gp);
       stp += 1;
       bc.push_back(make_float2(bias_correction(o.b1, stp), bias_correction(o.b2, stp)));
     }
     new_step[id] = stp;
     ops.push_back(c);
   }
+  parse_errors();
   run_replay(ctx, ops, gptr, bc, o, out->cb);
   for (uint32_t id = 0; id < out->n_ops; ++id)
-    if (in_scope(id)) out->step[id] = new_step[id];
+    if (in_scope(id)) {
+      out->present[id] = src[id].slot >= 0 ? 1 : 0;
+      out->has_full[id] = out->present[id];
+      out->step[id] = new_step[id];
+    }
   if (!replay) {
     out->iteration = parsed[0].hdr.iteration;
     out->data_seed = parsed[0].hdr.data_seed;
@@ -1649,7 +1848,101 @@ int mlck_localized_recover(mlck_state* out, const uint32_t* scope_ids, uint32_t 
   });
 }
 
+int mlck_localized_recover_segment(mlck_state* out, int32_t lo, int32_t hi, const int32_t* stage_of_op,
+                                   int32_t n_stages, mlck_blob* const* blobs, uint32_t n_blobs,
+                                   uint64_t window_start, uint32_t W, uint64_t data_seed, mlck_log* log,
+                                   uint32_t n_gmb, mlck_gradlog* g, uint64_t target, const mlck_optimizer* opt) {
+  return api([&] {
+    if (n_stages < 1 || lo < 0 || hi < lo || hi >= n_stages)
+      throw_invalid("recovery segment: stages [" + std::to_string(lo) + ", " + std::to_string(hi) +
+                    "] outside 0.." + std::to_string(n_stages - 1));
+    if (n_blobs != W) throw_runtime("sparse checkpoint incomplete");  // recovery.hpp:250-251
+    // in_scope (recovery.hpp:253-256): Engine::stage_of_op in [stage_lo, stage_hi]
+    std::vector<uint8_t> scope(out->n_ops, 0);
+    for (uint32_t id = 0; id < out->n_ops; ++id) scope[id] = stage_of_op[id] >= lo && stage_of_op[id] <= hi;
+    // run_scoped reads the segment's boundary inputs from the log for every
+    // replayed iteration (engine.hpp:361-366 fwd, 393-400 bwd); the
+    // replay from logged weight gradients needs none of them, but a log that
+    // lacks one fails here as the reference's recovery would
+    const uint64_t end = std::max<uint64_t>(window_start + W, target);
+    if (lo > 0 || hi < n_stages - 1) {
+      if (!log) throw_invalid("localized recovery: the segment needs its neighbours' boundary log");
+      for (uint64_t it = window_start + 1; it <= end; ++it)
+        for (uint32_t b = 0; b < n_gmb; ++b) {
+          uint64_t nf = 0;
+          if (lo > 0 && mlck_log_get(log, it, b, static_cast<uint32_t>(lo - 1), 0, nullptr, 0, &nf) != 0)
+            throw_runtime(mlck_last_error());
+          if (hi < n_stages - 1 && mlck_log_get(log, it, b, static_cast<uint32_t>(hi), 1, nullptr, 0, &nf) != 0)
+            throw_runtime(mlck_last_error());
+        }
+    }
+    convert_impl(out, blobs, n_blobs, window_start, W, data_seed, g, opt, &scope, target);
+  });
+}
+
 // ------------------------------------------------------------------ codecs
+}  // extern "C"
+namespace {
+void check_format(int eb, int mb) {
+  if (eb < 2 || eb > 8 || mb < 1 || eb + mb > 15)
+    throw_invalid("reduced format: unsupported widths e" + std::to_string(eb) + "m" + std::to_string(mb));
+}
+// n host values through a device kernel: H2D, launch, D2H on the ctx stream
+template <typename In, typename Out, typename Launch>
+void host_roundtrip(mlck_ctx* ctx, const In* in, Out* out, uint64_t n, Launch launch) {
+  if (!n) return;
+  ctx->activate();
+  In* din = nullptr;
+  Out* dout = nullptr;
+  MLCK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&din), sizeof(In) * n, ctx->stream));
+  MLCK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dout), sizeof(Out) * n, ctx->stream));
+  MLCK_CUDA(cudaMemcpyAsync(din, in, sizeof(In) * n, cudaMemcpyHostToDevice, ctx->stream));
+  launch(din, dout);
+  ctx->launches += 1;
+  MLCK_CUDA(cudaMemcpyAsync(out, dout, sizeof(Out) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  MLCK_CUDA(cudaFreeAsync(din, ctx->stream));
+  MLCK_CUDA(cudaFreeAsync(dout, ctx->stream));
+  MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+}  // namespace
+extern "C" {
+
+int mlck_pack_reduced(mlck_ctx* ctx, const float* in, uint16_t* codes, uint64_t n, int eb, int mb) {
+  return api([&] {
+    check_format(eb, mb);
+    ctx->activate();
+    launch_pack_reduced(in, codes, n, eb, mb, ctx->stream);
+    ctx->launches += n ? 1 : 0;
+  });
+}
+int mlck_unpack_reduced(mlck_ctx* ctx, const uint16_t* codes, float* out, uint64_t n, int eb, int mb) {
+  return api([&] {
+    check_format(eb, mb);
+    ctx->activate();
+    launch_unpack_reduced(codes, out, n, eb, mb, ctx->stream);
+    ctx->launches += n ? 1 : 0;
+  });
+}
+int mlck_quantize_values(mlck_ctx* ctx, const float* in, float* out, uint64_t n, int cb) {
+  return api([&] {
+    if (cb != 1 && cb != 2 && cb != 4) throw_invalid("quantize: unsupported width " + std::to_string(cb));
+    host_roundtrip(ctx, in, out, n, [&](const float* di, float* dout) { launch_quantize(di, dout, n, cb, ctx->stream); });
+  });
+}
+int mlck_pack_reduced_values(mlck_ctx* ctx, const float* in, uint16_t* codes, uint64_t n, int eb, int mb) {
+  return api([&] {
+    check_format(eb, mb);
+    host_roundtrip(ctx, in, codes, n,
+                   [&](const float* di, uint16_t* dout) { launch_pack_reduced(di, dout, n, eb, mb, ctx->stream); });
+  });
+}
+int mlck_unpack_reduced_values(mlck_ctx* ctx, const uint16_t* codes, float* out, uint64_t n, int eb, int mb) {
+  return api([&] {
+    check_format(eb, mb);
+    host_roundtrip(ctx, codes, out, n,
+                   [&](const uint16_t* di, float* dout) { launch_unpack_reduced(di, dout, n, eb, mb, ctx->stream); });
+  });
+}
 int mlck_quantize(mlck_ctx* ctx, const float* in, float* out, uint64_t n, int cb) {
   return api([&] {
     if (cb != 1 && cb != 2 && cb != 4) throw_invalid("quantize: unsupported width " + std::to_string(cb));

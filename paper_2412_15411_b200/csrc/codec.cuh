@@ -100,6 +100,51 @@ __device__ __forceinline__ float decode_e4m3(uint8_t c) {
   return __uint_as_float(bits);
 }
 
+// ---- generic reduced formats (ebits exponent, mbits mantissa bits, IEEE-
+// style: exponent all-ones = inf/NaN), the reference's pack_reduced /
+// unpack_reduced for any width (tensor.hpp:127-183).  x is expected on the
+// target grid (it came out of quantize), so packing truncates; NaN keeps
+// only the quiet bit, finite values above the format saturate to inf's code.
+__device__ __forceinline__ uint16_t pack_generic(float x, int eb, int mb) {
+  const uint32_t bits = __float_as_uint(x);
+  const int bias = (1 << (eb - 1)) - 1;
+  const uint32_t sign = (bits >> 31) << (eb + mb);
+  const int e = static_cast<int>((bits >> 23) & 0xffu) - 127;
+  const uint32_t frac = bits & 0x7fffffu, emask = (1u << eb) - 1u;
+  if (e == 128) return static_cast<uint16_t>(sign | (emask << mb) | (frac ? 1u << (mb - 1) : 0u));
+  if ((bits & 0x7fffffffu) == 0) return static_cast<uint16_t>(sign);
+  if (e > bias) return static_cast<uint16_t>(sign | (emask << mb));
+  const int emin = 1 - bias;
+  if (e >= emin) return static_cast<uint16_t>(sign | (static_cast<uint32_t>(e + bias) << mb) | (frac >> (23 - mb)));
+  const int sh = 23 - mb + (emin - e);  // subnormal of the target
+  return static_cast<uint16_t>(sh > 31 ? sign : sign | (((1u << 23) | frac) >> sh));
+}
+__device__ __forceinline__ float unpack_generic(uint16_t c, int eb, int mb) {
+  const int bias = (1 << (eb - 1)) - 1;
+  const uint32_t emask = (1u << eb) - 1u, fmask = (1u << mb) - 1u;
+  const uint32_t sign = (static_cast<uint32_t>(c) >> (eb + mb)) << 31;
+  const uint32_t e = (c >> mb) & emask, f = c & fmask;
+  uint32_t bits;
+  if (e == 0) {
+    if (f == 0) {
+      bits = sign;
+    } else {  // normalise the subnormal
+      int ee = 1 - bias;
+      uint32_t m = f;
+      while (!(m & (1u << mb))) {
+        m <<= 1;
+        --ee;
+      }
+      bits = sign | (static_cast<uint32_t>(ee + 127) << 23) | ((m & fmask) << (23 - mb));
+    }
+  } else if (e == emask) {
+    bits = sign | 0x7f800000u | (f << (23 - mb));
+  } else {
+    bits = sign | (static_cast<uint32_t>(static_cast<int>(e) - bias + 127) << 23) | (f << (23 - mb));
+  }
+  return __uint_as_float(bits);
+}
+
 // Writes the code of x at element i of a code array of width cb.
 __device__ __forceinline__ void store_code(void* codes, uint64_t i, float x, int cb) {
   if (cb == 2) static_cast<uint16_t*>(codes)[i] = encode_half(x);

@@ -41,6 +41,8 @@
 
 #include <cuda.h>
 
+#include <cstddef>
+
 #include "mlck_common.cuh"
 #include "pack.cuh"
 
@@ -97,6 +99,7 @@ constexpr uint32_t kSpinLimit = 1u << 24;  // watchdog: never hang the GPU
 struct Scratch {
   unsigned long long* status;  // [n_chunks * kStatusStride] epoch-tagged words
   uint32_t epoch;              // this launch's tag (>= 1)
+  unsigned long long* ticket;  // next chunk to hand out (zeroed per launch)
   unsigned long long* accum;   // sum of chunk terms (inverse-power frame)
   uint32_t* finished;          // completed-CTA counter
   uint32_t* ulast;             // low byte of the final hash
@@ -484,9 +487,9 @@ __device__ __forceinline__ uint32_t look_back2_warp(const Scratch& scr, int64_t 
 constexpr int kGranules = kThreadBytes / 16;  // 8
 struct alignas(1024) Shared {
   uint4 data[kSlots][kComputeThreads * kGranules];  // 1024-byte aligned rows (TMA swizzle atoms)
-  uint4 spill[kSlots][kComputeThreads];
   unsigned long long mbar[kSlots][kComputeWarps];  // the slot's bytes landed (per warp; [s][0] under TMA)
   unsigned long long res[kSlots];                  // look-back result of the slot's round
+  int64_t next[kSlots];                            // the slot's next chunk (ticket), -1 = none
   uint32_t wmap[kSlots][32];    // warp maps of the round (compute -> look-back)
   uint32_t wstart[kSlots][32];  // warp start bits (look-back -> compute)
   unsigned long long red[32];
@@ -494,10 +497,14 @@ struct alignas(1024) Shared {
   uint2 wfrag[2][4][32];        // mma_pass B fragments: [data | automaton][k-block][lane]
   unsigned long long kpos[32][4];  // mma_pass epilogue weights per lane
 #endif
+  // last: only the gather variant uses it, the others launch without it (a
+  // co-scheduled kernel -- the conversion replay -- gets the 24 KiB)
+  uint4 spill[kSlots][kComputeThreads];
 };
 // + 1 KiB of slack: the kernel aligns Shared to 1 KiB inside its dynamic
 // shared memory (the TMA swizzle pattern is anchored to 1 KiB boundaries)
 constexpr size_t kSmemBytes = sizeof(Shared) + 1024;
+constexpr size_t kSmemBytesNoSpill = offsetof(Shared, spill) + 1024;
 static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
 static_assert(sizeof(uint4) * kComputeThreads * kGranules % 1024 == 0, "slots keep the swizzle alignment");
 

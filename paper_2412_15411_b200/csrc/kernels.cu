@@ -175,8 +175,7 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
           lap.mark(2);
           // ---- refill (thread-private granules: no CTA barrier needed); the
           // bytes land while the other slots take their turns
-          const int64_t nx = chunk[s] + stride;
-          chunk[s] = nx < n_chunks ? nx : -1;
+          chunk[s] = sh.next[s];  // the ticket the look-back warp took in round 3
           rnd[s] = 0;
           st[s] = 0;
           par ^= 1u << s;
@@ -297,12 +296,26 @@ __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t se
       lb[0] = now;
     }
   };
-  if (tmap && lane == 0) tma_load_chunk(sh, s, tmap, chunk, n / kThreadBytes);
-  for (; chunk < n_chunks; chunk += stride) {
+  if (tmap && lane == 0 && chunk >= 0) tma_load_chunk(sh, s, tmap, chunk, n / kThreadBytes);
+  while (chunk >= 0) {
     uint32_t word = 0;  // the chunk's status bits as published
+    int64_t next = -1;
     for (int r = 0; r < kRounds; ++r) {
       mark(5);
       bar_sync(bar_pub(s), kBarThreads);
+      if (r == kRounds - 1) {
+        // the slot's next chunk: a ticket taken now, in the order the slots
+        // reach their last round, so a CTA's chunks rise in its turn order and
+        // every chunk's predecessors are already held by running CTAs (no
+        // co-residency needed); handed to the compute warps with this round's
+        // result
+        if (lane == 0) {
+          const unsigned long long t = atomicAdd(scr.ticket, 1ull);
+          sh.next[s] = t < static_cast<unsigned long long>(n_chunks) ? static_cast<int64_t>(t) : -1;
+        }
+        __syncwarp();
+        next = sh.next[s];
+      }
       const uint32_t wm = lane < kComputeWarps ? sh.wmap[s][lane] : 0u;
       mark(1);
       uint32_t ctot;
@@ -327,8 +340,9 @@ __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t se
     }
     if (tmap) {  // the compute warps are done with the bytes: load the slot's next chunk
       bar_sync(bar_pub(s), kBarThreads);
-      if (lane == 0 && chunk + stride < n_chunks) tma_load_chunk(sh, s, tmap, chunk + stride, n / kThreadBytes);
+      if (lane == 0 && next >= 0) tma_load_chunk(sh, s, tmap, next, n / kThreadBytes);
     }
+    chunk = next;
   }
   mark(5);
   if (kProf && lane == 0) {
@@ -358,18 +372,23 @@ __global__ void __launch_bounds__(fnv::kThreads, 1)
   mma_tables(sh, tid);
 #endif
   __syncthreads();
-  // Slot-major chunk order: generation g of slot s on CTA i is chunk
-  // (g*kSlots + s)*G + i, so the compute warps' turn order is the chunk order
-  // and a chunk's predecessors publish on the same turn (same slot, lower
-  // CTAs) or an earlier one.  Needs all G CTAs co-resident: G <= SM count at
-  // one CTA per SM (launch_fnv).
-  const int64_t G = gridDim.x, stride = kSlots * G;
+  // Chunks are handed out by a ticket counter: a CTA takes its first kSlots
+  // chunks at once when it starts, then one per slot as the slot reaches its
+  // last round (fnv_lookback).  Tickets rise in the CTA's turn order and only
+  // running CTAs hold them, so every chunk's look-back waits on chunks that
+  // are already being hashed: any grid size, any co-scheduled work.
+  if (tid == 0) {
+    const unsigned long long t0 = atomicAdd(scr.ticket, static_cast<unsigned long long>(kSlots));
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s)
+      sh.next[s] = t0 + s < static_cast<unsigned long long>(n_chunks) ? static_cast<int64_t>(t0 + s) : -1;
+  }
+  __syncthreads();
+  const int64_t stride = 0;
   int64_t first[kSlots];
 #pragma unroll
-  for (int s = 0; s < kSlots; ++s) {
-    const int64_t c = s * G + blockIdx.x;
-    first[s] = c < n_chunks ? c : -1;
-  }
+  for (int s = 0; s < kSlots; ++s) first[s] = sh.next[s];
+  __syncthreads();  // sh.next is rewritten by the look-back warps from here on
   uint64_t acc = 0;
   const bool tma = !kGather && use_tma;
   if (compute_warp(warp) >= 0) {
@@ -377,7 +396,7 @@ __global__ void __launch_bounds__(fnv::kThreads, 1)
   } else {
 #pragma unroll
     for (int s = 0; s < kSlots; ++s)
-      if (warp == lookback_warp(s) && first[s] >= 0)
+      if (warp == lookback_warp(s))
         fnv_lookback<kProf>(sh, s, seed, scr, first[s], n_chunks, stride, tma ? &tmap : nullptr, n);
   }
   // CTA sum -> global accumulator; the last CTA finishes the hash
@@ -404,8 +423,11 @@ __global__ void __launch_bounds__(fnv::kThreads, 1)
       const uint32_t err = atomicAdd(scr.error, 0u);
       if (err) atomicOr(scr.sticky, 1u);  // reported by the host at its next synchronization
       *scr.result = err ? 0ull : h;
+      // a hash the watchdog cut short is not the record's: poison the trailer
+      // so every copy fails parse_record's checksum instead of carrying it
+      const uint64_t tr = err ? ~h : h;
       for (int r = 0; r < trailer.n; ++r)
-        for (int b = 0; b < 8; ++b) trailer.p[r][b] = static_cast<uint8_t>(h >> (8 * b));
+        for (int b = 0; b < 8; ++b) trailer.p[r][b] = static_cast<uint8_t>(tr >> (8 * b));
     }
   }
 }
@@ -427,7 +449,7 @@ void init_constants() {
 }
 
 uint64_t fnv_chunks(uint64_t n) { return div_up(n, fnv::kChunk); }
-// [256 B header: finished u32 @8, accum u64 @16, ulast u32 @24, error u32
+// [256 B header: chunk ticket u64 @0, finished u32 @8, accum u64 @16, ulast u32 @24, error u32
 //  @28, sticky watchdog u32 @32 (not cleared per launch)] [status: n_chunks
 //  words of 8 B at a 256 B stride]
 size_t fnv_scratch_words(uint64_t n) { return (256 + fnv_chunks(n) * fnv::kStatusStride * 8) / 4; }
@@ -441,6 +463,7 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
                 int reserve_sms, const pack::Dsts* copies) {
   const uint64_t n_chunks = fnv_chunks(n);
   fnv::Scratch scr;
+  scr.ticket = reinterpret_cast<unsigned long long*>(scratch);
   scr.finished = scratch + 2;
   scr.accum = reinterpret_cast<unsigned long long*>(scratch + 4);
   scr.ulast = scratch + 6;
@@ -457,7 +480,8 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
     launch_fnv_empty(seed, result, trailer, stream);
     return;
   }
-  // one CTA per SM, all co-resident (the slot-major chunk order relies on it)
+  // one CTA per SM (its shared memory holds kSlots chunks); tickets make any
+  // grid size correct, reserve_sms leaves SMs to co-scheduled work
   static int sms_of[64] = {0};
   int dev = 0;
   MLCK_CUDA(cudaGetDevice(&dev));
@@ -473,7 +497,7 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
     if (per_sm < 1) throw Error(kCuda, "fnv_kernel does not fit on an SM");
     MLCK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  const uint64_t grid = std::min<uint64_t>(n_chunks, static_cast<uint64_t>(std::max(1, sms - reserve_sms)));
+  const uint64_t grid = std::min<uint64_t>(div_up(n_chunks, fnv::kSlots), static_cast<uint64_t>(std::max(1, sms - reserve_sms)));
   fnv::Gather g{};
   if (gather) {
     g.segs = gather->segs;
@@ -518,22 +542,9 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
   const bool pf = prof || trace;
   auto k = gather ? (pf ? fnv_kernel<true, true> : fnv_kernel<false, true>)
                   : (pf ? fnv_kernel<true, false> : fnv_kernel<false, false>);
-  // Hash kernels of this process never overlap on a device: each needs all
-  // its CTAs resident (slot-major look-back), and two grids interleaved on
-  // the SMs could each leave CTAs unscheduled.  Every launch waits for the
-  // previous one on the device, whichever context issued it.
-  static std::mutex order_mu;
-  static cudaEvent_t last_of[64] = {};
-  std::lock_guard<std::mutex> lock(order_mu);
-  cudaEvent_t& last = last_of[dev & 63];
-  if (last)
-    MLCK_CUDA(cudaStreamWaitEvent(stream, last, 0));
-  else
-    MLCK_CUDA(cudaEventCreateWithFlags(&last, cudaEventDisableTiming));
-  k<<<static_cast<unsigned>(grid), fnv::kThreads, fnv::kSmemBytes, stream>>>(
+  k<<<static_cast<unsigned>(grid), fnv::kThreads, gather ? fnv::kSmemBytes : fnv::kSmemBytesNoSpill, stream>>>(
       data, n, seed, scr, static_cast<int64_t>(n_chunks), trailer, g, tmap, use_tma);
   MLCK_CUDA(cudaGetLastError());
-  MLCK_CUDA(cudaEventRecord(last, stream));
 }
 
 namespace {
@@ -736,7 +747,28 @@ unsigned grid_for(uint64_t n) {
   const uint64_t b = div_up(n, 256);
   return static_cast<unsigned>(b < 148ull * 32 ? (b ? b : 1) : 148ull * 32);
 }
+__global__ void pack_generic_kernel(const float* in, uint16_t* out, uint64_t n, int eb, int mb) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = codec::pack_generic(in[i], eb, mb);
+}
+__global__ void unpack_generic_kernel(const uint16_t* in, float* out, uint64_t n, int eb, int mb) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = codec::unpack_generic(in[i], eb, mb);
+}
 }  // namespace
+
+void launch_pack_reduced(const float* in, uint16_t* codes, uint64_t n, int eb, int mb, cudaStream_t stream) {
+  if (!n) return;
+  pack_generic_kernel<<<grid_for(n), 256, 0, stream>>>(in, codes, n, eb, mb);
+  MLCK_CUDA(cudaGetLastError());
+}
+void launch_unpack_reduced(const uint16_t* codes, float* out, uint64_t n, int eb, int mb, cudaStream_t stream) {
+  if (!n) return;
+  unpack_generic_kernel<<<grid_for(n), 256, 0, stream>>>(codes, out, n, eb, mb);
+  MLCK_CUDA(cudaGetLastError());
+}
 
 void launch_quantize(const float* in, float* out, uint64_t n, int cb, cudaStream_t stream) {
   if (!n) return;

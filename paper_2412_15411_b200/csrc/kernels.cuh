@@ -80,6 +80,8 @@ void launch_adam_arrays(float* w, float* m, float* v, const float* g, uint64_t n
 void launch_quantize(const float* in, float* out, uint64_t n, int cb, cudaStream_t stream);
 void launch_encode(const float* in, void* codes, uint64_t n, int cb, cudaStream_t stream);
 void launch_decode(const void* codes, float* out, uint64_t n, int cb, cudaStream_t stream);
+void launch_pack_reduced(const float* in, uint16_t* codes, uint64_t n, int eb, int mb, cudaStream_t stream);
+void launch_unpack_reduced(const uint16_t* codes, float* out, uint64_t n, int eb, int mb, cudaStream_t stream);
 uint64_t synth_key(uint64_t seed, uint64_t stream);
 void launch_synth(float* out, uint64_t n, uint64_t seed, uint64_t stream_id, float lo, float hi,
                   cudaStream_t stream);

@@ -56,6 +56,8 @@ struct mlck_log {
   std::map<uint64_t, uint64_t> free_list;  // off -> size
   cudaStream_t side = nullptr;
   cudaEvent_t ev = nullptr;
+  cudaEvent_t copied = nullptr;  // recorded on `side` after every copy
+  bool async = false;            // false: the ctx stream waits for each copy (src reusable)
 
   uint64_t alloc(uint64_t bytes) {
     bytes = align_up(bytes ? bytes : 16, 256);
@@ -127,6 +129,7 @@ int mlck_log_create(mlck_ctx* ctx, int kind, int device, uint64_t capacity, mlck
     MLCK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     MLCK_CUDA(cudaStreamCreateWithPriority(&l->side, cudaStreamNonBlocking, lo));  // lowest
     MLCK_CUDA(cudaEventCreateWithFlags(&l->ev, cudaEventDisableTiming));
+    MLCK_CUDA(cudaEventCreateWithFlags(&l->copied, cudaEventDisableTiming));
     l->free_list[0] = l->cap;
     *out = l;
   });
@@ -148,6 +151,7 @@ int mlck_log_create_external(mlck_ctx* ctx, void* device_base, uint64_t capacity
     MLCK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     MLCK_CUDA(cudaStreamCreateWithPriority(&l->side, cudaStreamNonBlocking, lo));  // lowest
     MLCK_CUDA(cudaEventCreateWithFlags(&l->ev, cudaEventDisableTiming));
+    MLCK_CUDA(cudaEventCreateWithFlags(&l->copied, cudaEventDisableTiming));
     l->free_list[0] = l->cap;
     *out = l;
   });
@@ -169,6 +173,7 @@ int mlck_log_destroy(mlck_log* l) {
     }
     cudaStreamDestroy(l->side);
     cudaEventDestroy(l->ev);
+    cudaEventDestroy(l->copied);
     delete l;
   });
 }
@@ -203,6 +208,28 @@ int mlck_log_put(mlck_log* l, uint64_t it, uint32_t mb, uint32_t boundary, uint8
       }
     }
     l->entries[k] = {off, n};
+    MLCK_CUDA(cudaEventRecord(l->copied, l->side));
+    // ordered mode: later work on the ctx stream may overwrite src
+    if (!l->async) MLCK_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), l->copied, 0));
+  });
+}
+
+int mlck_log_set_async(mlck_log* l, int async) {
+  return log_api([&] { l->async = async != 0; });
+}
+
+int mlck_log_fence(mlck_log* l, void* stream) {
+  return log_api([&] {
+    MLCK_CUDA(cudaSetDevice(l->ctx_device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (!st) {
+      void* cs = nullptr;
+      int dev = 0;
+      mlck_ctx_device_stream_(l->ctx, &dev, &cs);
+      st = static_cast<cudaStream_t>(cs);
+    }
+    MLCK_CUDA(cudaEventRecord(l->copied, l->side));
+    MLCK_CUDA(cudaStreamWaitEvent(st, l->copied, 0));
   });
 }
 
@@ -274,6 +301,27 @@ int mlck_gc_logs(mlck_log* l, uint64_t persisted_window_start) {
         ++it;
       }
     }
+  });
+}
+
+// ---- log storage budget (recovery.hpp:296-317) ---------------------------
+int64_t mlck_upstream_log_bytes(int32_t token_dim, int32_t pp_stages, int32_t microbatches,
+                                int64_t microbatch_size, int32_t dp_degree, int64_t wsparse) {
+  const int64_t boundaries = pp_stages > 1 ? pp_stages - 1 : 0;
+  const int64_t per_tensor = microbatch_size * token_dim * static_cast<int64_t>(sizeof(float));
+  const int64_t entries_per_iter = 2 * boundaries * microbatches * dp_degree;
+  return 2 * wsparse * entries_per_iter * per_tensor;  // live window + the one being persisted
+}
+
+int mlck_check_log_budget(int32_t token_dim, int32_t pp_stages, int32_t microbatches, int64_t microbatch_size,
+                          int32_t dp_degree, int64_t wsparse, double cpu_mem_per_node, int32_t nodes) {
+  return log_api([&] {
+    if (cpu_mem_per_node <= 0) return;
+    const int64_t need = mlck_upstream_log_bytes(token_dim, pp_stages, microbatches, microbatch_size, dp_degree, wsparse);
+    const double have = cpu_mem_per_node * nodes;
+    if (static_cast<double>(need) > have)
+      throw_invalid("upstream log budget exceeded: need " + std::to_string(need) + " bytes of host memory, budget " +
+                    std::to_string(static_cast<int64_t>(have)));
   });
 }
 

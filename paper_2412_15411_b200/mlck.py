@@ -26,6 +26,8 @@ u8p = C.POINTER(C.c_uint8)
 f32p = C.POINTER(C.c_float)
 u32p = C.POINTER(C.c_uint32)
 u64p = C.POINTER(C.c_uint64)
+u16p = C.POINTER(C.c_uint16)
+i32p = C.POINTER(C.c_int32)
 vp = C.c_void_p
 
 
@@ -161,6 +163,24 @@ def lib():
             "mlck_host_free_pinned": (C.c_int, [vp, vp]),
             "mlck_memcpy_h2d": (C.c_int, [vp, vp, vp, C.c_uint64]),
             "mlck_memcpy_d2h": (C.c_int, [vp, vp, vp, C.c_uint64]),
+            "mlck_ctx_set_hash_reserve": (C.c_int, [vp, C.c_int]),
+            "mlck_gradlog_capture": (C.c_int, [vp, C.c_uint64, C.c_uint32, vp]),
+            "mlck_gradlog_bytes": (C.c_uint64, [vp]),
+            "mlck_conversion_plan": (C.c_int, [C.POINTER(vp), C.c_uint32, C.c_int, u32p, C.c_uint64, u64p, u64p]),
+            "mlck_localized_recover_segment": (C.c_int, [vp, C.c_int32, C.c_int32, i32p, C.c_int32, C.POINTER(vp),
+                                                         C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64, vp,
+                                                         C.c_uint32, vp, C.c_uint64, C.POINTER(Optimizer)]),
+            "mlck_log_set_async": (C.c_int, [vp, C.c_int]),
+            "mlck_log_fence": (C.c_int, [vp, vp]),
+            "mlck_upstream_log_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32,
+                                                    C.c_int64]),
+            "mlck_check_log_budget": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.c_int64,
+                                                C.c_double, C.c_int32]),
+            "mlck_pack_reduced": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_int, C.c_int]),
+            "mlck_unpack_reduced": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_int, C.c_int]),
+            "mlck_quantize_values": (C.c_int, [vp, f32p, f32p, C.c_uint64, C.c_int]),
+            "mlck_pack_reduced_values": (C.c_int, [vp, f32p, u16p, C.c_uint64, C.c_int, C.c_int]),
+            "mlck_unpack_reduced_values": (C.c_int, [vp, u16p, f32p, C.c_uint64, C.c_int, C.c_int]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -227,6 +247,29 @@ class Context:
         SMs overlapped with the hash; 2: fused gather+store+hash kernel; 0:
         pack-kernel stores, then hash; 4: copy engines after the hash."""
         check(lib().mlck_ctx_set_replica_mode(self.h, mode))
+
+    def set_hash_reserve(self, sms: int):
+        """SMs the hash kernel leaves to co-scheduled work (0 = all SMs)."""
+        check(lib().mlck_ctx_set_hash_reserve(self.h, sms))
+
+    # ---- codecs: the reference's scalar forms (tensor.hpp:99-183) on device
+    def quantize_values(self, x, compute_bytes: int) -> np.ndarray:
+        x = np.ascontiguousarray(np.atleast_1d(x), dtype=np.float32)
+        out = np.empty_like(x)
+        check(lib().mlck_quantize_values(self.h, _ptr(x, f32p), _ptr(out, f32p), x.size, compute_bytes))
+        return out
+
+    def pack_reduced_values(self, x, ebits: int, mbits: int) -> np.ndarray:
+        x = np.ascontiguousarray(np.atleast_1d(x), dtype=np.float32)
+        out = np.empty(x.size, dtype=np.uint16)
+        check(lib().mlck_pack_reduced_values(self.h, _ptr(x, f32p), _ptr(out, u16p), x.size, ebits, mbits))
+        return out
+
+    def unpack_reduced_values(self, codes, ebits: int, mbits: int) -> np.ndarray:
+        c = np.ascontiguousarray(np.atleast_1d(codes), dtype=np.uint16)
+        out = np.empty(c.size, dtype=np.float32)
+        check(lib().mlck_unpack_reduced_values(self.h, _ptr(c, u16p), _ptr(out, f32p), c.size, ebits, mbits))
+        return out
 
     def fastmath_check(self, n_div: int, seed: int = 1) -> tuple[int, int]:
         """(division, sqrt) mismatches of the replay's spelled-out fast paths."""
@@ -535,9 +578,10 @@ def dense_checkpoint(state: DeviceState, out: Blob | None = None) -> Blob:
 def parse_record(blob: Blob, compute_bytes: int):
     """parse_record (snapshot.hpp:153-197): (header dict, entry dicts)."""
     info = RecordInfo()
-    cap = 1 << 16
-    ents = (EntryInfo * cap)()
     n = C.c_uint32()
+    check(lib().mlck_parse_record(blob.h, compute_bytes, C.byref(info), None, 0, C.byref(n)))
+    cap = max(1, n.value)
+    ents = (EntryInfo * cap)()
     check(lib().mlck_parse_record(blob.h, compute_bytes, C.byref(info), ents, cap, C.byref(n)))
     header = dict(kind=info.kind, iteration=info.iteration, window_start=info.window_start,
                   wsparse=info.wsparse, slot=info.slot, data_seed=info.data_seed)
@@ -597,6 +641,14 @@ class GradLog:
     def fill_synthetic(self, first_iteration: int, n_iterations: int, seed: int):
         check(lib().mlck_gradlog_fill_synthetic(self.h, first_iteration, n_iterations, seed))
 
+    def capture(self, iteration: int, op: int, device_src: int):
+        """Copy a trainer-owned device gradient into the log (ctx stream)."""
+        check(lib().mlck_gradlog_capture(self.h, iteration, op, device_src))
+
+    @property
+    def nbytes(self) -> int:
+        return int(lib().mlck_gradlog_bytes(self.h))
+
 
 def sparse_to_dense_convert(out: DeviceState, blobs, window_start: int, wsparse: int, data_seed: int,
                             gradlog: GradLog | None, opt: Optimizer | None = None):
@@ -617,6 +669,54 @@ def localized_recover(out: DeviceState, scope, blobs, window_start: int, wsparse
     opt = opt or Optimizer.adam()
     check(lib().mlck_localized_recover(out.h, _ptr(ids, u32p), ids.size, arr, len(blobs), window_start, wsparse,
                                        data_seed, gradlog.h if gradlog else None, target_iteration, C.byref(opt)))
+
+
+def localized_recover_segment(out: DeviceState, stage_lo: int, stage_hi: int, stage_of_op, n_stages: int, blobs,
+                              window_start: int, wsparse: int, data_seed: int, log: "UpstreamLog | None",
+                              n_global_microbatches: int, gradlog: GradLog | None, target_iteration: int,
+                              opt: Optimizer | None = None):
+    """localized_recover(engine, RecoverySegment{stage_lo, stage_hi}, ckpt, logs,
+    target) (recovery.hpp:240-244): the scope is Engine::stage_of_op in the
+    segment's stage range; the boundary inputs it consumes must be in `log`."""
+    st = np.ascontiguousarray(np.array(list(stage_of_op), dtype=np.int32))
+    arr = (vp * max(1, len(blobs)))(*[b.h for b in blobs])
+    opt = opt or Optimizer.adam()
+    check(lib().mlck_localized_recover_segment(out.h, stage_lo, stage_hi, _ptr(st, i32p), n_stages, arr, len(blobs),
+                                               window_start, wsparse, data_seed, log.h if log else None,
+                                               n_global_microbatches, gradlog.h if gradlog else None,
+                                               target_iteration, C.byref(opt)))
+
+
+def conversion_plan(blobs, window_start: int, compute_bytes: int):
+    """conversion_plan (recovery.hpp:123-137): [(record_index, replay_iteration,
+    activating ids)] -- step k loads record k, replays window_start + k + 1."""
+    arr = (vp * max(1, len(blobs)))(*[b.h for b in blobs])
+    counts = np.zeros(max(1, len(blobs)), dtype=np.uint64)
+    total = C.c_uint64()
+    check(lib().mlck_conversion_plan(arr, len(blobs), compute_bytes, None, 0, _ptr(counts, u64p), C.byref(total)))
+    ids = np.zeros(max(1, total.value), dtype=np.uint32)
+    check(lib().mlck_conversion_plan(arr, len(blobs), compute_bytes, _ptr(ids, u32p), ids.size,
+                                     _ptr(counts, u64p), C.byref(total)))
+    out, at = [], 0
+    for k in range(len(blobs)):
+        c = int(counts[k])
+        out.append((k, window_start + k + 1, [int(x) for x in ids[at:at + c]]))
+        at += c
+    return out
+
+
+def upstream_log_bytes(token_dim: int, pp_stages: int, microbatches: int, microbatch_size: int, dp_degree: int,
+                       wsparse: int) -> int:
+    """upstream_log_bytes (recovery.hpp:296-304)."""
+    return int(lib().mlck_upstream_log_bytes(token_dim, pp_stages, microbatches, microbatch_size, dp_degree,
+                                             wsparse))
+
+
+def check_log_budget(token_dim: int, pp_stages: int, microbatches: int, microbatch_size: int, dp_degree: int,
+                     wsparse: int, cpu_mem_per_node: float, nodes: int):
+    """check_log_budget (recovery.hpp:308-317): ValueError when the host budget cannot hold the logs."""
+    check(lib().mlck_check_log_budget(token_dim, pp_stages, microbatches, microbatch_size, dp_degree, wsparse,
+                                      cpu_mem_per_node, nodes))
 
 
 def optimizer_step_adam(ctx: Context, master: int, m: int, v: int, step: int, grad: int, n: int,
@@ -694,3 +794,11 @@ class UpstreamLog:
 
     def sync(self):
         check(lib().mlck_log_sync(self.h))
+
+    def set_async(self, on: bool):
+        """ASYNC mode: put() does not order the ctx stream after the copy;
+        fence() the stream that will overwrite a logged source."""
+        check(lib().mlck_log_set_async(self.h, 1 if on else 0))
+
+    def fence(self, stream: int | None = None):
+        check(lib().mlck_log_fence(self.h, stream))

@@ -151,6 +151,43 @@ int main(int argc, char** argv) {
   } catch (const std::runtime_error& e) {
     std::cout << "ERR runtime_error: " << e.what() << "\n";
   }
+  // conversion_plan (recovery.hpp:123-137)
+  {
+    const ConversionPlan cp = conversion_plan(ckpt, plan);
+    std::cout << "PLAN " << cp.window_start;
+    for (const auto& st : cp.steps) {
+      std::cout << " " << st.record_index << ":" << st.replay_iteration << ":";
+      for (size_t i = 0; i < st.activating.size(); ++i) std::cout << (i ? "," : "") << st.activating[i];
+    }
+    std::cout << "\n";
+  }
+  // scalar codecs (tensor.hpp:99-183), the reference's known answers
+  std::cout << "CODEC " << quantize_value(ctx, 65520.0f, 2) << " " << quantize_value(ctx, 300.0f, 1) << " "
+            << pack_reduced(ctx, 1.0f, 5, 10) << " " << unpack_reduced(ctx, 0x3c00, 5, 10) << " "
+            << pack_reduced(1.5f, 4, 3) << " " << unpack_reduced(static_cast<uint16_t>(0x77), 4, 3) << "\n";
+  try {
+    (void)quantize_value(ctx, 1.0f, 3);
+  } catch (const std::invalid_argument& e) {
+    std::cout << "ERR invalid_argument: " << e.what() << "\n";
+  }
+  // log budget (recovery.hpp:296-317): configs[4] needs 38.65 GB
+  {
+    ModelSpec m;
+    m.token_dim = 2048;
+    ParallelPlan pp;
+    pp.pp_stages = 4;
+    pp.dp_degree = 2;
+    pp.microbatches = 8;
+    pp.microbatch_size = 4096;
+    ClusterSpec cl;
+    cl.cpu_mem_per_node = 1e9;
+    std::cout << "LOGBYTES " << upstream_log_bytes(m, pp, 6) << "\n";
+    try {
+      check_log_budget(m, pp, 6, cl);
+    } catch (const std::invalid_argument& e) {
+      std::cout << "ERR invalid_argument: " << e.what() << "\n";
+    }
+  }
   std::cout << "OK\n";
   return 0;
 }

@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 from golden_cases import load_case
+from oracle.oracle import ref_conversion_plan
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "tests", "cpp", "_build", "shim_parity")
@@ -48,7 +49,7 @@ def test_shim_binary_exists():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,w", [("verify_toy", 3), ("six_op_cb1", 3), ("toy_sgd", 0)])
-def test_cpp_shim_window_matches_reference(tmp_path, name, w):
+def test_cpp_shim_window_matches_reference(tmp_path, reference, name, w):
     if not os.path.exists(BIN):
         pytest.fail("tests/cpp/_build/shim_parity not built")
     c = load_case(name)
@@ -70,3 +71,13 @@ def test_cpp_shim_window_matches_reference(tmp_path, name, w):
     assert "SAVED same 1 durable_persisted 0" in out
     assert f"RING before 0 after {w} in_flight 0" in out
     assert (tmp_path / "window" / f"window_{w}_slot_0.mlck").read_bytes() == c.blob(w)
+    # conversion_plan, scalar codecs and the log budget through the C++ shim
+    plan_line = next(x for x in out.splitlines() if x.startswith("PLAN "))
+    want = [f"{k}:{it}:" + ",".join(str(i) for i in ids)
+            for k, it, ids in ref_conversion_plan(reference, w, c.W, c.window_blobs(w), c.compute_bytes)]
+    assert plan_line.split()[1:] == [str(w)] + want
+    assert "CODEC inf 240 15360 1 " in out  # tensor.hpp: fp16 overflow, E4M3 saturation, 0x3c00
+    assert "ERR invalid_argument: quantize: unsupported width 3" in out
+    assert "LOGBYTES 38654705664" in out
+    assert "ERR invalid_argument: upstream log budget exceeded: need 38654705664 bytes of host memory, " \
+           "budget 1000000000" in out
