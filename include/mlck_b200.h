@@ -94,6 +94,20 @@ int mlck_ctx_set_replica_mode(mlck_ctx* ctx, int mode);
  * a snapshot); 0 = all SMs.  The kernel hands chunks out by ticket, so any
  * grid is correct -- this only trades hash throughput for room. */
 int mlck_ctx_set_hash_reserve(mlck_ctx* ctx, int sms);
+/* Witnessed verification (default on).  A record the hash kernel writes
+ * keeps, beside its blob, the low byte of the FNV state at every 32-byte
+ * segment start (3 % of the record).  parse_record / check_coverage /
+ * conversion re-hash such a record without the look-back rounds: each row
+ * runs the automaton from its witnessed starts and each segment's end state
+ * must equal the next witnessed start -- if all do, the starts are the true
+ * ones and the sum is exactly FNV-1a-64 of the bytes in memory; if one does
+ * not (stale witness, changed bytes) the record is re-hashed from scratch.
+ * The result is the exact checksum either way, and the witness is not part
+ * of the record (the MLCK wire format is unchanged).  Records from files,
+ * host bytes or peers have no witness.  used / fallbacks count witnessed verifications
+ * and those that fell back. */
+int mlck_ctx_set_witness(mlck_ctx* ctx, int on);
+int mlck_ctx_witness_stats(mlck_ctx* ctx, uint64_t* used, uint64_t* fallbacks);
 int mlck_ctx_timings(mlck_ctx* ctx, char* labels_csv, uint64_t labels_cap, float* ms,
                      uint32_t cap, uint32_t* n);
 
@@ -133,6 +147,9 @@ int mlck_blob_destroy(mlck_blob* b);
 int mlck_blob_from_host(mlck_ctx* ctx, const uint8_t* bytes, uint64_t n, mlck_blob** out);
 uint64_t mlck_blob_size(const mlck_blob* b);
 void* mlck_blob_device_ptr(const mlck_blob* b);
+/* Device pointer of the blob's witness (u32 per 128-byte row of the body),
+ * NULL when it has none for its current record. */
+void* mlck_blob_witness_ptr(const mlck_blob* b);
 int mlck_blob_to_host(const mlck_blob* b, uint8_t* host, uint64_t cap);
 /* Replica targets written by the same pack kernel as the local copy: a
  * device pointer of >= capacity bytes (local HBM, or a peer buffer opened

@@ -90,6 +90,10 @@ struct mlck_ctx {
   }
   // SMs the hash kernel leaves free (mlck_ctx_set_hash_reserve)
   int hash_reserve = 0;
+  // records keep the hash kernel's segment starts (a witness) and are
+  // re-verified against it (fnv.cuh); counters for tests and the bench
+  bool witness = true;
+  uint64_t witness_used = 0, witness_fallbacks = 0;
   unsigned long long* results = nullptr;       // device [results_cap]
   unsigned long long* host_results = nullptr;  // pinned [results_cap]
   size_t results_cap = 0;
@@ -274,6 +278,10 @@ struct mlck_blob {
   // and in every replica (mlck_blob_replication polls it)
   cudaEvent_t written = nullptr;
   uint32_t written_replicas = 0;
+  // the segment starts of the last record's hash (fnv.cuh, witness): valid
+  // for a body of witness_n bytes when witness_n == size - 8
+  uint32_t* witness = nullptr;
+  uint64_t witness_cap = 0, witness_n = ~0ull;
 
   void reserve(uint64_t n) {
     if (n <= cap) return;
@@ -281,7 +289,24 @@ struct mlck_blob {
     if (dev) MLCK_CUDA(cudaFree(dev));
     cap = align_up(n, kAlign);
     dev_malloc(reinterpret_cast<void**>(&dev), cap);
+    witness_n = ~0ull;
+    if (ctx->witness) reserve_witness(cap);  // with the record buffer: never inside a snapshot
   }
+  void reserve_witness(uint64_t body) {
+    const uint64_t words = fnv_witness_words(body) + 1;
+    if (words <= witness_cap) return;
+    MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (witness) MLCK_CUDA(cudaFree(witness));
+    witness_cap = align_up(words, 1024);
+    dev_malloc(reinterpret_cast<void**>(&witness), 4 * witness_cap);
+  }
+  uint32_t* witness_for(uint64_t body) {
+    witness_n = ~0ull;
+    if (!ctx->witness) return nullptr;
+    reserve_witness(body);
+    return witness;
+  }
+  bool has_witness() const { return witness && size >= 8 && witness_n == size - 8; }
 };
 
 struct mlck_gradlog {
@@ -362,6 +387,7 @@ struct SegmentBuilder {
 // `trailer`): the blob body is [0, builder.pos), the trailer at pos.
 void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer);
 void run_pack(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
+  out->witness_n = ~0ull;
   run_pack_impl(ctx, b, out, trailer);
   if (!out->written) MLCK_CUDA(cudaEventCreateWithFlags(&out->written, cudaEventDisableTiming));
   MLCK_CUDA(cudaEventRecord(out->written, ctx->stream));  // every path ends with the pushes joined
@@ -439,8 +465,10 @@ void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool traile
     t.n = d.n;
     uint32_t* scratch = ctx->fnv_scratch_for(body);
     const int tf = ctx->tbegin("pack_fnv");
+    uint32_t* wit = out->witness_for(body);
     launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream,
-               nullptr, nullptr, &g, ctx->hash_reserve);
+               nullptr, nullptr, &g, ctx->hash_reserve, nullptr, wit);
+    if (wit) out->witness_n = body;
     ctx->tend(tf);
     ctx->launches += 1;
     return;
@@ -473,8 +501,10 @@ void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool traile
     t.n = d.n;
     uint32_t* scratch = ctx->fnv_scratch_for(body);
     const int tf = ctx->tbegin("fnv");
+    uint32_t* wit = out->witness_for(body);
     launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream, nullptr,
-               nullptr, nullptr, ctx->hash_reserve, &reps);
+               nullptr, nullptr, ctx->hash_reserve, &reps, wit);
+    if (wit) out->witness_n = body;
     ctx->tend(tf);
     ctx->launches += 2;
     return;
@@ -501,8 +531,10 @@ void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool traile
     t.n = d.n;
     uint32_t* scratch = ctx->fnv_scratch_for(body);
     const int tf = ctx->tbegin("fnv");
+    uint32_t* wit = out->witness_for(body);
     launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream, nullptr,
-               nullptr, nullptr, std::max(mlck_ctx::kPushSms, ctx->hash_reserve));
+               nullptr, nullptr, std::max(mlck_ctx::kPushSms, ctx->hash_reserve), nullptr, wit);
+    if (wit) out->witness_n = body;
     ctx->tend(tf);
     ctx->launches += 3;
     MLCK_CUDA(cudaEventRecord(ctx->ev_pushed[0], ctx->side[0]));
@@ -531,8 +563,10 @@ void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool traile
     uint32_t* scratch = ctx->fnv_scratch_for(body);
     auto hash = [&] {
       const int tf = ctx->tbegin("fnv");
+      uint32_t* wit = out->witness_for(body);
       launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream, nullptr,
-                 nullptr, nullptr, ctx->hash_reserve);
+                 nullptr, nullptr, ctx->hash_reserve, nullptr, wit);
+      if (wit) out->witness_n = body;
       ctx->tend(tf);
       MLCK_CUDA(cudaEventRecord(ctx->ev_hashed, ctx->stream));
     };
@@ -588,8 +622,10 @@ void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool traile
     t.n = d.n;
     uint32_t* scratch = ctx->fnv_scratch_for(body);
     const int tf = ctx->tbegin("fnv");
+    uint32_t* wit = out->witness_for(body);
     launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream, nullptr,
-               nullptr, nullptr, ctx->hash_reserve);
+               nullptr, nullptr, ctx->hash_reserve, nullptr, wit);
+    if (wit) out->witness_n = body;
     ctx->tend(tf);
     ctx->launches += 1;
   }
@@ -719,7 +755,8 @@ struct ParseJob {
 void verify_begin(ParseJob& j) {
   mlck_ctx* ctx = j.ctx;
   const uint32_t n = j.n;
-  ctx->results_for(2 * static_cast<size_t>(n));
+  ctx->results_for(3 * static_cast<size_t>(n));
+  MLCK_CUDA(cudaMemsetAsync(ctx->results + 2 * static_cast<size_t>(n), 0, 8 * static_cast<size_t>(n), ctx->stream));
   MLCK_CUDA(cudaEventRecord(ctx->ev_vmain, ctx->stream));  // the records are complete
   for (int i = 0; i < 2; ++i) MLCK_CUDA(cudaStreamWaitEvent(ctx->vside[i], ctx->ev_vmain, 0));
   uint32_t launched = 0;
@@ -730,10 +767,18 @@ void verify_begin(ParseJob& j) {
     cudaStream_t st = ctx->vside[side];
     uint32_t* scratch = ctx->vscratch_for(side, b->size - 8);
     TrailerDsts none{};
-    const int tf = ctx->tbegin("fnv_verify", st);
-    launch_fnv(b->dev, b->size - 8, kFnvOffset, scratch, ctx->next_epoch(), ctx->results + k, none, st,
-               nullptr, nullptr, nullptr, ctx->hash_reserve);
-    ctx->tend(tf, st);
+    if (ctx->witness && b->has_witness()) {  // exact re-hash against the record's witness (fnv.cuh)
+      const int tf = ctx->tbegin("fnv_witness", st);
+      launch_fnv_witness(b->dev, b->size - 8, kFnvOffset, b->witness, scratch, ctx->results + k,
+                         ctx->results + 2 * static_cast<size_t>(n) + k, st);
+      ctx->tend(tf, st);
+      ctx->witness_used += 1;
+    } else {
+      const int tf = ctx->tbegin("fnv_verify", st);
+      launch_fnv(b->dev, b->size - 8, kFnvOffset, scratch, ctx->next_epoch(), ctx->results + k, none, st,
+                 nullptr, nullptr, nullptr, ctx->hash_reserve);
+      ctx->tend(tf, st);
+    }
     ctx->launches += 1;
     MLCK_CUDA(cudaMemcpyAsync(ctx->results + n + k, b->dev + b->size - 8, 8, cudaMemcpyDeviceToDevice, st));
   }
@@ -800,10 +845,33 @@ std::vector<std::string> verify_end(ParseJob& j) {
   mlck_ctx* ctx = j.ctx;
   const uint32_t n = j.n;
   for (int i = 0; i < 2; ++i) MLCK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_vside[i], 0));
-  MLCK_CUDA(cudaMemcpyAsync(ctx->host_results, ctx->results, 2 * static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost,
+  MLCK_CUDA(cudaMemcpyAsync(ctx->host_results, ctx->results, 3 * static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost,
                             ctx->stream));
   MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->check_watchdog();
+  // a witness that does not match its record's bytes: hash the record from
+  // scratch (the witness path computed nothing usable)
+  std::vector<uint32_t> redo;
+  for (uint32_t k = 0; k < n; ++k)
+    if (ctx->host_results[2 * static_cast<size_t>(n) + k]) redo.push_back(k);
+  if (!redo.empty()) {
+    std::vector<unsigned long long> full(n, 0);
+    for (uint32_t k : redo) {
+      const mlck_blob* b = j.blobs[k];
+      TrailerDsts none{};
+      uint32_t* scratch = ctx->fnv_scratch_for(b->size - 8);
+      const int tf = ctx->tbegin("fnv_verify");
+      launch_fnv(b->dev, b->size - 8, kFnvOffset, scratch, ctx->next_epoch(), ctx->results + k, none, ctx->stream,
+                 nullptr, nullptr, nullptr, ctx->hash_reserve);
+      ctx->tend(tf);
+      ctx->launches += 1;
+      ctx->witness_fallbacks += 1;
+    }
+    MLCK_CUDA(cudaMemcpyAsync(ctx->host_results, ctx->results, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->check_watchdog();
+  }
   std::vector<std::string> errors(n);
   for (uint32_t k = 0; k < n; ++k) {
     if (j.blobs[k]->size < 8)
@@ -939,6 +1007,16 @@ int mlck_ctx_set_replica_mode(mlck_ctx* c, int mode) {
                     "2 (fused pack+hash+push), 3 (SM push beside the hash), 4 (copy engines "
                     "after the hash) or 5 (hash-kernel stores)");
     c->replica_mode = mode;
+  });
+}
+
+int mlck_ctx_set_witness(mlck_ctx* c, int on) {
+  return api([&] { c->witness = on != 0; });
+}
+int mlck_ctx_witness_stats(mlck_ctx* c, uint64_t* used, uint64_t* fallbacks) {
+  return api([&] {
+    if (used) *used = c->witness_used;
+    if (fallbacks) *fallbacks = c->witness_fallbacks;
   });
 }
 
@@ -1160,6 +1238,7 @@ int mlck_blob_destroy(mlck_blob* b) {
     b->ctx->activate();
     cudaStreamSynchronize(b->ctx->stream);
     if (b->dev) cudaFree(b->dev);
+    if (b->witness) cudaFree(b->witness);
     if (b->written) cudaEventDestroy(b->written);
     delete b;
   });
@@ -1178,6 +1257,7 @@ int mlck_blob_from_host(mlck_ctx* ctx, const uint8_t* bytes, uint64_t n, mlck_bl
 }
 uint64_t mlck_blob_size(const mlck_blob* b) { return b ? b->size : 0; }
 void* mlck_blob_device_ptr(const mlck_blob* b) { return b ? b->dev : nullptr; }
+void* mlck_blob_witness_ptr(const mlck_blob* b) { return b && b->has_witness() ? b->witness : nullptr; }
 int mlck_blob_to_host(const mlck_blob* b, uint8_t* host, uint64_t cap) {
   return api([&] {
     if (cap < b->size) throw_invalid("blob_to_host: buffer too small");

@@ -100,6 +100,7 @@ struct Scratch {
   unsigned long long* status;  // [n_chunks * kStatusStride] epoch-tagged words
   uint32_t epoch;              // this launch's tag (>= 1)
   unsigned long long* ticket;  // next chunk to hand out (zeroed per launch)
+  uint32_t* witness;           // null, or the segment starts of every 128-byte row (written)
   unsigned long long* accum;   // sum of chunk terms (inverse-power frame)
   uint32_t* finished;          // completed-CTA counter
   uint32_t* ulast;             // low byte of the final hash
@@ -490,6 +491,7 @@ struct alignas(1024) Shared {
   unsigned long long mbar[kSlots][kComputeWarps];  // the slot's bytes landed (per warp; [s][0] under TMA)
   unsigned long long res[kSlots];                  // look-back result of the slot's round
   int64_t next[kSlots];                            // the slot's next chunk (ticket), -1 = none
+  uint32_t* witness;                               // Scratch::witness (read at the final pass)
   uint32_t wmap[kSlots][32];    // warp maps of the round (compute -> look-back)
   uint32_t wstart[kSlots][32];  // warp start bits (look-back -> compute)
   unsigned long long red[32];
@@ -676,6 +678,20 @@ __device__ __forceinline__ void load_thread_gather(Shared& sh, int slot, int t, 
   *phase = ph;
 }
 
+__device__ __forceinline__ void write_thread_rows(uint4* rows, int t, const uint32_t (&w)[kThreadWords]) {
+#pragma unroll
+  for (int q = 0; q < kGranules; ++q) rows[granule(t, q)] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+}
+__device__ __forceinline__ void read_thread_rows(const uint4* rows, int t, uint32_t (&w)[kThreadWords]) {
+#pragma unroll
+  for (int q = 0; q < kGranules; ++q) {
+    const uint4 v = rows[granule(t, q)];
+    w[4 * q] = v.x;
+    w[4 * q + 1] = v.y;
+    w[4 * q + 2] = v.z;
+    w[4 * q + 3] = v.w;
+  }
+}
 __device__ __forceinline__ void write_thread(Shared& sh, int slot, int t, const uint32_t (&w)[kThreadWords]) {
 #pragma unroll
   for (int q = 0; q < kGranules; ++q)
@@ -722,21 +738,27 @@ __device__ __forceinline__ void mma_u8(int (&c)[4], uint32_t a0, uint32_t a1, ui
 __host__ __device__ constexpr int mma_segment(int kb, int k) {
   return 32 * kb + 8 * ((k & 15) >> 2) + ((k >> 4) << 2) + (k & 3);
 }
-// One pass over the warp's 32 threads' words of the slot (after __syncwarp).
-__device__ __forceinline__ void mma_pass(const Shared& sh, int slot, int warp, int lane, int tab,
-                                         int (&acc)[2][4]) {
+// One pass over the warp's 32 threads' words of a chunk's rows (after
+// __syncwarp); wfrag = the B fragment tables.
+__device__ __forceinline__ void mma_pass_rows(const uint4* rows, const uint2 (*wfrag)[4][32], int warp, int lane,
+                                              int tab, int (&acc)[2][4]) {
   const int g = lane >> 2, q = lane & 3, t0 = 32 * warp + 2 * q;
 #pragma unroll
   for (int kb = 0; kb < 4; ++kb) {
-    const uint4 lo = sh.data[slot][granule(t0 + 8 * kb, g)];
-    const uint4 hi = sh.data[slot][granule(t0 + 8 * kb + 1, g)];
-    const uint2 b = sh.wfrag[tab][kb][lane];
+    const uint4 lo = rows[granule(t0 + 8 * kb, g)];
+    const uint4 hi = rows[granule(t0 + 8 * kb + 1, g)];
+    const uint2 b = wfrag[tab][kb][lane];
     mma_u8(acc[0], lo.x, lo.y, hi.x, hi.y, b.x, b.y);
     mma_u8(acc[1], lo.z, lo.w, hi.z, hi.w, b.x, b.y);
   }
 }
+__device__ __forceinline__ void mma_pass(const Shared& sh, int slot, int warp, int lane, int tab,
+                                         int (&acc)[2][4]) {
+  mma_pass_rows(sh.data[slot], sh.wfrag, warp, lane, tab, acc);
+}
 // Tables (once per CTA): B fragments and epilogue weights.
-__device__ __forceinline__ void mma_tables(Shared& sh, int tid) {
+template <typename S>
+__device__ __forceinline__ void mma_tables(S& sh, int tid) {
   if (tid < 2 * 4 * 32) {
     const int tab = tid >> 7, kb = (tid >> 5) & 3, lane = tid & 31, n = lane >> 2, q = lane & 3;
     uint32_t b[2] = {0, 0};
@@ -754,7 +776,8 @@ __device__ __forceinline__ void mma_tables(Shared& sh, int tid) {
   }
 }
 // The warp's sum_p P^(E_w - p) d_p (this lane's share) from the accumulators.
-__device__ __forceinline__ uint64_t mma_epilogue(const Shared& sh, int lane, const int (&acc)[2][4]) {
+template <typename S>
+__device__ __forceinline__ uint64_t mma_epilogue(const S& sh, int lane, const int (&acc)[2][4]) {
   uint64_t t = 0;
 #pragma unroll
   for (int rb = 0; rb < 2; ++rb) {
@@ -779,6 +802,38 @@ __device__ __forceinline__ void automaton_and(uint32_t (&w)[kThreadWords], uint3
     bd = ((bd ^ y) & ~M) * 0xb3u;
   }
 }
+// automaton_and that also returns the state after each segment's last
+// byte (byte lane i = segment i): the witness check of fnv_witness_kernel.
+__device__ __forceinline__ uint32_t automaton_and_ends(uint32_t (&w)[kThreadWords], uint32_t st) {
+  constexpr uint32_t M = 0x00ff00ffu;
+  uint32_t ac = st & M, bd = st & ~M;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t y = w[k];
+    w[k] = ((ac & M) | (bd & ~M)) & y;
+    ac = ((ac ^ y) & M) * 0xb3u;
+    bd = ((bd ^ y) & ~M) * 0xb3u;
+  }
+  return (ac & M) | (bd & ~M);
+}
+
+// ---- verification against a witness.  A record hashed by fnv_kernel can
+// keep the low byte of the hash at the start of every 32-byte segment (the
+// segment starts its look-back resolved; one u32 per 128-byte row, byte i =
+// segment i).  Re-hashing the record then needs no rounds and no look-back:
+// every row runs the automaton from its witnessed starts, the two dot
+// products follow on the tensor cores, and each segment's end state is
+// compared with the next segment's witnessed start.  If every comparison
+// holds the witnessed starts are the true ones (induction from the seed's
+// low byte), so the sum is exactly FNV-1a-64 of the bytes now in memory;
+// if one fails (a stale witness, bytes changed) the caller hashes the
+// record with fnv_kernel.  Either way the result is the exact hash.
+struct WitnessShared {
+  uint4 data[kComputeThreads * kGranules];  // the chunk, rows in the granule swizzle
+  uint2 wfrag[2][4][32];
+  unsigned long long kpos[32][4];
+  unsigned long long red[kComputeWarps];
+};
 #endif
 
 __device__ __forceinline__ void read_thread_unaligned(const Shared& sh, int slot, int t, uint32_t ph,

@@ -131,6 +131,12 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
             mma_pass(sh, s, warp, lane, 1, mac);  // the u & b vector, weights -2 P^(...)
             acc += mma_epilogue(sh, lane, mac) * (pinv_t * chunk_weight(chunk[s]));
           }
+          {  // the row's segment starts, for later verification (fnv_witness_kernel);
+             // the pointer comes from shared memory, not a live register
+            uint32_t* const wp = *reinterpret_cast<uint32_t* volatile*>(&sh.witness);
+            const uint64_t row = static_cast<uint64_t>(chunk[s]) * kComputeThreads + tid;
+            if (wp && row * kThreadBytes < n) wp[row] = st[s];
+          }
           lap.mark(6);
 #else
           // ---- final pass: the real recurrence from each segment's start
@@ -378,6 +384,7 @@ __global__ void __launch_bounds__(fnv::kThreads, 1)
   // running CTAs hold them, so every chunk's look-back waits on chunks that
   // are already being hashed: any grid size, any co-scheduled work.
   if (tid == 0) {
+    sh.witness = scr.witness;
     const unsigned long long t0 = atomicAdd(scr.ticket, static_cast<unsigned long long>(kSlots));
 #pragma unroll
     for (int s = 0; s < kSlots; ++s)
@@ -432,6 +439,126 @@ __global__ void __launch_bounds__(fnv::kThreads, 1)
   }
 }
 
+// Re-hash of a record against its witness (fnv.cuh, WitnessShared).
+// Persistent: one CTA per SM walks chunks blockIdx.x, +gridDim.x, ... with
+// the next chunk's rows in flight (cp.async into the other buffer) while the
+// current one is hashed; rows are thread-private, so warps only meet at the
+// tensor-core passes (__syncwarp).  *bad <- 1 when a witnessed start
+// disagrees with the automaton (the caller then runs fnv_kernel).
+__device__ uint2 g_wfrag[2][4][32];             // mma_pass B fragments (init_constants)
+__device__ unsigned long long g_kpos[32][4];    // mma_epilogue weights
+__constant__ unsigned long long c_pinv_warp[fnv::kComputeWarps];  // P^-(4096 (w + 1))
+
+__device__ __forceinline__ void witness_load_row(uint4* rows, int tid, const uint8_t* data, uint64_t n, uint64_t p) {
+  using namespace fnv;
+  if (p + kThreadBytes <= n) {
+#pragma unroll
+    for (int q = 0; q < kGranules; ++q) cp_async16(&rows[granule(tid, q)], data + p + 16 * q);
+  } else {  // the record's last, partial row (zeros past n add nothing), or past the end
+    for (int q = 0; q < kGranules; ++q) {
+      uint32_t v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t x = 0;
+        for (int b = 0; b < 4; ++b) {
+          const uint64_t o = p + 16 * q + 4 * i + b;
+          x |= (o < n ? static_cast<uint32_t>(data[o]) : 0u) << (8 * b);
+        }
+        v[i] = x;
+      }
+      rows[granule(tid, q)] = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+constexpr int kWitnessBufs = 3;  // chunks in flight per SM (load ~2x the hash time of one)
+struct WitnessSmem {
+  uint4 data[kWitnessBufs][fnv::kComputeThreads * fnv::kGranules];
+  uint2 wfrag[2][4][32];
+  unsigned long long kpos[32][4];
+  unsigned long long red[fnv::kComputeWarps];
+};
+
+__global__ void __launch_bounds__(fnv::kComputeThreads, 1)
+    fnv_witness_kernel(const uint8_t* data, uint64_t n, uint64_t seed, const uint32_t* witness, fnv::Scratch scr,
+                       unsigned long long* bad, int64_t n_chunks) {
+  using namespace fnv;
+  extern __shared__ __align__(16) unsigned char smem_w[];
+  WitnessSmem& sh = *reinterpret_cast<WitnessSmem*>(smem_w);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint64_t n_seg = (n + 31) / 32;
+  if (tid < 2 * 4 * 32) (&sh.wfrag[0][0][0])[tid] = (&g_wfrag[0][0][0])[tid];
+  if (tid < 32 * 4) (&sh.kpos[0][0])[tid] = (&g_kpos[0][0])[tid];
+  const uint64_t pinv_w = c_pinv_warp[warp];
+  int64_t chunk = blockIdx.x;
+#pragma unroll
+  for (int b = 0; b < kWitnessBufs - 1; ++b) {  // the first chunks' rows in flight
+    const int64_t c = chunk + b * static_cast<int64_t>(gridDim.x);
+    if (c < n_chunks)
+      witness_load_row(sh.data[b], tid, data, n, (static_cast<uint64_t>(c) * kComputeThreads + tid) * kThreadBytes);
+    else
+      asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  __syncthreads();  // tables
+  uint64_t acc = 0;
+  bool ok = true;
+  for (int buf = 0; chunk < n_chunks; chunk += gridDim.x, buf = buf + 1 == kWitnessBufs ? 0 : buf + 1) {
+    const int64_t nx = chunk + (kWitnessBufs - 1) * static_cast<int64_t>(gridDim.x);
+    const int nb = buf == 0 ? kWitnessBufs - 1 : buf - 1;  // the buffer hashed last turn
+    if (nx < n_chunks)  // later chunks' rows land while this one is hashed
+      witness_load_row(sh.data[nb], tid, data, n, (static_cast<uint64_t>(nx) * kComputeThreads + tid) * kThreadBytes);
+    else
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    const uint64_t row = static_cast<uint64_t>(chunk) * kComputeThreads + tid;
+    uint32_t st = 0, expect = 0, check = 0;
+    if (row * kThreadBytes < n) {
+      st = __ldg(witness + row);
+      const uint64_t seg0 = 4 * row;
+      const uint32_t next = seg0 + 4 < n_seg ? (__ldg(witness + row + 1) & 0xffu) : 0u;
+      expect = (st >> 8) | (next << 24);  // segment i ends where segment i+1 starts
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (seg0 + i + 1 < n_seg) check |= 0xffu << (8 * i);
+      if (row == 0 && (st & 0xffu) != (seed & 0xffu)) ok = false;
+    }
+    asm volatile("cp.async.wait_group %0;" ::"n"(kWitnessBufs - 1) : "memory");  // this chunk's rows (own copies)
+    uint4* rows = sh.data[buf];
+    uint32_t w[kThreadWords];
+    read_thread_rows(rows, tid, w);
+    interleave(w);
+    write_thread_rows(rows, tid, w);
+    __syncwarp();
+    int mac[2][4] = {};
+    mma_pass_rows(rows, sh.wfrag, warp, lane, 0, mac);  // the data vector
+    const uint32_t ends = automaton_and_ends(w, st);
+    if ((ends ^ expect) & check) ok = false;
+    __syncwarp();  // every lane has read the data words
+    write_thread_rows(rows, tid, w);
+    __syncwarp();
+    mma_pass_rows(rows, sh.wfrag, warp, lane, 1, mac);  // the u & b vector, weights -2 P^(...)
+    acc += mma_epilogue(sh, lane, mac) * (pinv_w * chunk_weight(chunk));
+    __syncwarp();  // the buffer is refilled two chunks on
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (__any_sync(0xffffffffu, !ok) && lane == 0) atomicExch(bad, 1ull);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) sh.red[warp] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t sum = 0;
+    for (int q = 0; q < kComputeWarps; ++q) sum += sh.red[q];
+    atomicAdd(scr.accum, static_cast<unsigned long long>(sum));
+    __threadfence();
+    if (atomicAdd(scr.finished, 1u) + 1 == gridDim.x) {
+      __threadfence();
+      const uint64_t total = atomicAdd(scr.accum, 0ull);
+      *scr.result = pow_p(n) * (total + seed);
+    }
+  }
+}
+
 }  // namespace
 
 void init_constants() {
@@ -446,6 +573,33 @@ void init_constants() {
     }
   }
   MLCK_CUDA(cudaMemcpyToSymbol(fnv::c_wchunk, t, sizeof(t)));
+  // the witness kernel's tensor-core tables (fnv.cuh mma_tables, once)
+  static uint2 wf[2][4][32];
+  static unsigned long long kp[32][4], pw[fnv::kComputeWarps];
+  for (int tab = 0; tab < 2; ++tab)
+    for (int kb = 0; kb < 4; ++kb)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int nn = lane >> 2, q = lane & 3;
+        uint32_t b[2] = {0, 0};
+        for (int h = 0; h < 2; ++h)
+          for (int e = 0; e < 4; ++e) {
+            const int seg = fnv::mma_segment(kb, 16 * h + 4 * q + e);
+            uint64_t wgt = fnv::pow_u64(fnv::kPrime, 32ull * (127 - seg));
+            if (tab) wgt *= ~1ull;
+            b[h] |= static_cast<uint32_t>((wgt >> (8 * nn)) & 0xffu) << (8 * e);
+          }
+        wf[tab][kb][lane] = make_uint2(b[0], b[1]);
+      }
+  for (int lane = 0; lane < 32; ++lane)
+    for (int m = 0; m < 4; ++m) {
+      const int g = lane >> 2, q = lane & 3;
+      kp[lane][m] = fnv::pow_u64(fnv::kPrime, 32 - (4 * g + m)) << (16 * q);
+    }
+  for (int w = 0; w < fnv::kComputeWarps; ++w)
+    pw[w] = fnv::pow_u64(fnv::kPrimeInv, static_cast<uint64_t>(fnv::kThreadBytes) * 32 * (w + 1));
+  MLCK_CUDA(cudaMemcpyToSymbol(g_wfrag, wf, sizeof(wf)));
+  MLCK_CUDA(cudaMemcpyToSymbol(g_kpos, kp, sizeof(kp)));
+  MLCK_CUDA(cudaMemcpyToSymbol(c_pinv_warp, pw, sizeof(pw)));
 }
 
 uint64_t fnv_chunks(uint64_t n) { return div_up(n, fnv::kChunk); }
@@ -460,9 +614,10 @@ uint32_t fnv_sticky_word() { return 8; }
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
                 unsigned long long* prof, unsigned long long* trace, const FnvGather* gather,
-                int reserve_sms, const pack::Dsts* copies) {
+                int reserve_sms, const pack::Dsts* copies, uint32_t* witness) {
   const uint64_t n_chunks = fnv_chunks(n);
-  fnv::Scratch scr;
+  fnv::Scratch scr{};
+  scr.witness = witness;
   scr.ticket = reinterpret_cast<unsigned long long*>(scratch);
   scr.finished = scratch + 2;
   scr.accum = reinterpret_cast<unsigned long long*>(scratch + 4);
@@ -582,6 +737,35 @@ void launch_fnv_empty(uint64_t seed, unsigned long long* result, const TrailerDs
   fnv_empty_kernel<<<1, 1, 0, stream>>>(seed, result, trailer);
   MLCK_CUDA(cudaGetLastError());
 }
+
+void launch_fnv_witness(const uint8_t* data, uint64_t n, uint64_t seed, const uint32_t* witness, uint32_t* scratch,
+                        unsigned long long* result, unsigned long long* bad, cudaStream_t stream) {
+  MLCK_CUDA(cudaMemsetAsync(scratch, 0, 32, stream));
+  MLCK_CUDA(cudaMemsetAsync(bad, 0, 8, stream));
+  if (n == 0) {
+    launch_fnv_empty(seed, result, TrailerDsts{}, stream);
+    return;
+  }
+  static int sms_of[64] = {0};
+  int dev = 0;
+  MLCK_CUDA(cudaGetDevice(&dev));
+  int& sms = sms_of[dev & 63];
+  if (!sms) {
+    MLCK_CUDA(cudaFuncSetAttribute(fnv_witness_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(sizeof(WitnessSmem))));
+    MLCK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  fnv::Scratch scr{};
+  scr.finished = scratch + 2;
+  scr.accum = reinterpret_cast<unsigned long long*>(scratch + 4);
+  scr.result = result;
+  const int64_t n_chunks = static_cast<int64_t>(fnv_chunks(n));
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_chunks, sms));
+  fnv_witness_kernel<<<grid, fnv::kComputeThreads, sizeof(WitnessSmem), stream>>>(data, n, seed, witness, scr, bad,
+                                                                                  n_chunks);
+  MLCK_CUDA(cudaGetLastError());
+}
+
 
 // ---------------------------------------------------------------- pack (K1)
 void launch_pack(const pack::Segment* segs, int n_segs, uint64_t total, const pack::Dsts& d,

@@ -62,7 +62,14 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
                 unsigned long long* prof = nullptr, unsigned long long* trace = nullptr,
                 const FnvGather* gather = nullptr, int reserve_sms = 0,
-                const pack::Dsts* copies = nullptr);  // non-gather: also store the bytes to these
+                const pack::Dsts* copies = nullptr,  // non-gather: also store the bytes to these
+                uint32_t* witness = nullptr);        // non-null: the rows' segment starts (fnv.cuh)
+// Exact re-hash of n bytes against the witness fnv_kernel left (one u32 per
+// 128-byte row); *bad = 1 when the witness does not match the bytes (the
+// caller then hashes with launch_fnv).  scratch as launch_fnv's.
+void launch_fnv_witness(const uint8_t* data, uint64_t n, uint64_t seed, const uint32_t* witness, uint32_t* scratch,
+                        unsigned long long* result, unsigned long long* bad, cudaStream_t stream);
+inline uint64_t fnv_witness_words(uint64_t n) { return (n + 127) / 128; }
 // Copy `bytes` from src to every dst with `ctas` CTAs of one SM each.
 void launch_push(const uint8_t* src, uint64_t bytes, const pack::Dsts& d, int ctas, cudaStream_t stream);
 void launch_fnv_empty(uint64_t seed, unsigned long long* result, const TrailerDsts& trailer,

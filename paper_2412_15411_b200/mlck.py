@@ -165,6 +165,9 @@ def lib():
             "mlck_memcpy_d2h": (C.c_int, [vp, vp, vp, C.c_uint64]),
             "mlck_ctx_set_hash_reserve": (C.c_int, [vp, C.c_int]),
             "mlck_gradlog_capture": (C.c_int, [vp, C.c_uint64, C.c_uint32, vp]),
+            "mlck_ctx_set_witness": (C.c_int, [vp, C.c_int]),
+            "mlck_ctx_witness_stats": (C.c_int, [vp, u64p, u64p]),
+            "mlck_blob_witness_ptr": (vp, [vp]),
             "mlck_gradlog_bytes": (C.c_uint64, [vp]),
             "mlck_conversion_plan": (C.c_int, [C.POINTER(vp), C.c_uint32, C.c_int, u32p, C.c_uint64, u64p, u64p]),
             "mlck_localized_recover_segment": (C.c_int, [vp, C.c_int32, C.c_int32, i32p, C.c_int32, C.POINTER(vp),
@@ -247,6 +250,16 @@ class Context:
         SMs overlapped with the hash; 2: fused gather+store+hash kernel; 0:
         pack-kernel stores, then hash; 4: copy engines after the hash."""
         check(lib().mlck_ctx_set_replica_mode(self.h, mode))
+
+    def set_witness(self, on: bool):
+        """Witnessed re-verification of records this context hashed (default on)."""
+        check(lib().mlck_ctx_set_witness(self.h, 1 if on else 0))
+
+    def witness_stats(self) -> tuple[int, int]:
+        """(witnessed verifications, of which fell back to a full hash)."""
+        u, f = C.c_uint64(), C.c_uint64()
+        check(lib().mlck_ctx_witness_stats(self.h, C.byref(u), C.byref(f)))
+        return u.value, f.value
 
     def set_hash_reserve(self, sms: int):
         """SMs the hash kernel leaves to co-scheduled work (0 = all SMs)."""
@@ -509,6 +522,11 @@ class Blob:
     def device_ptr(self) -> int:
         return int(lib().mlck_blob_device_ptr(self.h) or 0)
 
+    @property
+    def witness_ptr(self) -> int:
+        """Device pointer of the record's witness (0 when it has none)."""
+        return int(lib().mlck_blob_witness_ptr(self.h) or 0)
+
     def to_host(self) -> bytes:
         out = np.empty(self.size, dtype=np.uint8)
         check(lib().mlck_blob_to_host(self.h, _ptr(out, u8p), out.size))
@@ -656,7 +674,7 @@ def sparse_to_dense_convert(out: DeviceState, blobs, window_start: int, wsparse:
     arr = (vp * max(1, len(blobs)))(*[b.h for b in blobs])
     opt = opt or Optimizer.adam()
     check(lib().mlck_sparse_to_dense_convert(out.h, arr, len(blobs), window_start, wsparse, data_seed,
-                                             gradlog.h if gradlog else None, C.byref(opt)))
+                                             gradlog.h if gradlog is not None else None, C.byref(opt)))
 
 
 def localized_recover(out: DeviceState, scope, blobs, window_start: int, wsparse: int, data_seed: int,
@@ -668,7 +686,7 @@ def localized_recover(out: DeviceState, scope, blobs, window_start: int, wsparse
     arr = (vp * max(1, len(blobs)))(*[b.h for b in blobs])
     opt = opt or Optimizer.adam()
     check(lib().mlck_localized_recover(out.h, _ptr(ids, u32p), ids.size, arr, len(blobs), window_start, wsparse,
-                                       data_seed, gradlog.h if gradlog else None, target_iteration, C.byref(opt)))
+                                       data_seed, gradlog.h if gradlog is not None else None, target_iteration, C.byref(opt)))
 
 
 def localized_recover_segment(out: DeviceState, stage_lo: int, stage_hi: int, stage_of_op, n_stages: int, blobs,
@@ -682,8 +700,8 @@ def localized_recover_segment(out: DeviceState, stage_lo: int, stage_hi: int, st
     arr = (vp * max(1, len(blobs)))(*[b.h for b in blobs])
     opt = opt or Optimizer.adam()
     check(lib().mlck_localized_recover_segment(out.h, stage_lo, stage_hi, _ptr(st, i32p), n_stages, arr, len(blobs),
-                                               window_start, wsparse, data_seed, log.h if log else None,
-                                               n_global_microbatches, gradlog.h if gradlog else None,
+                                               window_start, wsparse, data_seed, log.h if log is not None else None,
+                                               n_global_microbatches, gradlog.h if gradlog is not None else None,
                                                target_iteration, C.byref(opt)))
 
 
