@@ -299,6 +299,56 @@ int mlck_localized_recover(mlck_state* out, const uint32_t* scope_ids, uint32_t 
                            uint32_t wsparse, uint64_t data_seed, mlck_gradlog* g,
                            uint64_t target_iteration, const mlck_optimizer* opt);
 
+/* ---- the miniature MoE trainer on the GPU (moelab::Engine, engine.hpp:
+ * 150-730): the recompute half of conversion / recovery and
+ * a GPU producer of the boundary log and of the weight-gradient log. ------
+ * EngineConfig's model / parallel / optimizer / precision fields
+ * (engine.hpp:96-124, core.hpp:66-191); params < 0 = derived from the toy
+ * dimensions.  Operator ids as ModelSpec::operators (layer-major, E experts,
+ * NE, gate).  A state (mlck_state) of the engine's param_counts holds the
+ * operators; its data_seed is the data stream's seed. */
+typedef struct mlck_engine mlck_engine;
+typedef struct {
+  int32_t layers, experts_per_layer, top_k, shared_experts;
+  int32_t token_dim, expert_hidden, nonexpert_hidden, residual;
+  int64_t expert_params, nonexpert_params, gate_params;
+  int32_t pp_stages, dp_degree, microbatches, compute_bytes;
+  int64_t microbatch_size;
+  mlck_optimizer optimizer;
+} mlck_engine_config;
+int mlck_engine_create(mlck_ctx* ctx, const mlck_engine_config* cfg, mlck_engine** out);
+int mlck_engine_destroy(mlck_engine* e);
+uint32_t mlck_engine_op_count(const mlck_engine* e);
+int mlck_engine_param_counts(const mlck_engine* e, uint64_t* out);
+int32_t mlck_engine_stage_of_op(const mlck_engine* e, uint32_t id);
+/* Engine::run_iteration(modes, log) (engine.hpp:189-207) on `st`:
+ * forward + backward of every micro-batch, Adam / SGD on the active
+ * operators, st's iteration + 1.  frozen: n_ops flags (NULL = all active).
+ * log_out (may be NULL): the sender-side boundary copies of the iteration.
+ * grads_out (may be NULL): the active operators' weight gradients land in
+ * its slots of the new iteration -- the zero-copy capture the logged-
+ * gradient conversion replays. */
+int mlck_engine_run_iteration(mlck_engine* e, mlck_state* st, const uint8_t* frozen, mlck_log* log_out,
+                              mlck_gradlog* grads_out);
+/* Engine::replay_scoped_iteration (engine.hpp:214-222): stages
+ * [stage_lo, stage_hi] of `ops` at `iteration`, boundary inputs from log_in
+ * ("upstream log missing entry: ..."), updates of the active in-scope ops. */
+int mlck_engine_replay_scoped_iteration(mlck_engine* e, mlck_state* ops, uint64_t iteration, int32_t stage_lo,
+                                        int32_t stage_hi, const uint8_t* frozen, mlck_log* log_in);
+/* sparse_to_dense_convert (recovery.hpp:180-227) with the reference's own
+ * replay: each window iteration re-run forward + backward, frozen operators
+ * without weight gradients.  Errors as mlck_sparse_to_dense_convert. */
+int mlck_sparse_to_dense_convert_recompute(mlck_engine* e, mlck_state* out, mlck_blob* const* blobs,
+                                           uint32_t n_blobs, uint64_t window_start, uint32_t wsparse,
+                                           uint64_t data_seed);
+/* localized_recover(engine, RecoverySegment{stage_lo, stage_hi}, ckpt,
+ * logs, target) (recovery.hpp:240-289) by recompute: only the segment's
+ * stages run, boundary tensors from `logs`; in-scope operators of `out`. */
+int mlck_localized_recover_recompute(mlck_engine* e, mlck_state* out, int32_t stage_lo, int32_t stage_hi,
+                                     mlck_blob* const* blobs, uint32_t n_blobs, uint64_t window_start,
+                                     uint32_t wsparse, uint64_t data_seed, mlck_log* logs,
+                                     uint64_t target_iteration);
+
 /* ---- K4: upstream boundary log (LogKey/UpstreamLog, engine.hpp:55-94) ----
  * kind 0: pinned host ring (copy engine, side stream); kind 1: device ring
  * on `device` (peer HBM over NVLink when device != ctx device). */
@@ -329,7 +379,8 @@ int mlck_log_fence(mlck_log* l, void* stream);
 /* UpstreamLog::at (engine.hpp:71-79): "upstream log missing entry: ..." */
 int mlck_log_get(mlck_log* l, uint64_t iteration, uint32_t micro_batch, uint32_t boundary,
                  uint8_t direction, float* host_out, uint64_t cap_floats, uint64_t* n_floats);
-/* Device-side copy of an entry into dst (replay input). */
+/* Device-side copy of an entry into dst (replay input), ordered on the ctx
+ * stream after the work queued there (no host synchronization). */
 int mlck_log_get_device(mlck_log* l, uint64_t iteration, uint32_t micro_batch, uint32_t boundary,
                         uint8_t direction, float* device_dst, uint64_t cap_floats,
                         uint64_t* n_floats);

@@ -686,6 +686,45 @@ inline void gc_logs(UpstreamLog& log, uint64_t persisted_window_start) {
   check(mlck_gc_logs(log.get(), persisted_window_start));
 }
 
+// ---- the miniature MoE trainer on the GPU (engine.hpp:150-730) ----------------
+// EngineConfig's fields as the C ABI's mlck_engine_config (params < 0 =
+// derived).  run_iteration produces the boundary log and the weight-gradient
+// log (zero-copy: the gradients land in the log's slots); the recompute
+// conversion / localized recovery replay iterations by forward + backward.
+class Engine {
+ public:
+  Engine(Context& ctx, const mlck_engine_config& cfg) : ctx_(&ctx) { check(mlck_engine_create(ctx.get(), &cfg, &h_)); }
+  ~Engine() {
+    if (h_) mlck_engine_destroy(h_);
+  }
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+  mlck_engine* get() const { return h_; }
+  std::vector<uint64_t> param_counts() const {
+    std::vector<uint64_t> p(mlck_engine_op_count(h_));
+    check(mlck_engine_param_counts(h_, p.data()));
+    return p;
+  }
+  int32_t stage_of_op(uint32_t id) const { return mlck_engine_stage_of_op(h_, id); }
+  // Engine::run_iteration(modes, log) (engine.hpp:189-207); frozen: n_ops flags or empty
+  void run_iteration(DeviceState& st, const std::vector<uint8_t>& frozen = {}, UpstreamLog* log = nullptr,
+                     GradientLog* grads = nullptr) {
+    check(mlck_engine_run_iteration(h_, st.get(), frozen.empty() ? nullptr : frozen.data(),
+                                    log ? log->get() : nullptr, grads ? grads->get() : nullptr));
+  }
+  // sparse_to_dense_convert(engine, ckpt) with the reference's recompute replay
+  void sparse_to_dense_convert(DeviceState& out, const SparseCheckpoint& ckpt, uint64_t data_seed) {
+    std::vector<mlck_blob*> hs;
+    for (const auto& b : ckpt.blobs) hs.push_back(b.get());
+    check(mlck_sparse_to_dense_convert_recompute(h_, out.get(), hs.data(), static_cast<uint32_t>(hs.size()),
+                                                 ckpt.window_start, ckpt.wsparse, data_seed));
+  }
+
+ private:
+  Context* ctx_;
+  mlck_engine* h_ = nullptr;
+};
+
 // ---- localized_recover(engine, segment, ckpt, logs, target) ----------------
 // (recovery.hpp:240-289) with the reference's own scope vocabulary: the
 // failed stage range of one pipeline (RecoverySegment, recovery.hpp:29-41)

@@ -19,6 +19,7 @@
 #include <cuda.h>
 
 #include "../../include/mlck_b200.h"
+#include "engine.cuh"
 #include "kernels.cuh"
 
 using namespace mlck;
@@ -1707,10 +1708,10 @@ namespace {
 // pointers and bias corrections.
 void run_replay(mlck_ctx* ctx, std::vector<adam::ConvOp>& ops, const std::vector<const float*>& gptr,
                 const std::vector<float2>& bc, const adam::Opt& o, int cb) {
-  uint64_t units = 0;
+  uint64_t units = 0;  // CTAs: each operator's units round up to whole CTAs
   for (auto& op : ops) {
     op.unit_begin = units;
-    units += div_up(op.P, 4);
+    units += div_up(div_up(op.P, 4), static_cast<uint64_t>(replay_cta_threads()));
   }
   const size_t ob = ops.size() * sizeof(adam::ConvOp);
   const size_t go = align_up(ob, 16), gb = gptr.size() * sizeof(float*);
@@ -2154,6 +2155,380 @@ int mlck_memcpy_d2h(mlck_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
   return api([&] {
     ctx->activate();
     MLCK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  });
+}
+
+}  // extern "C"
+
+// =========================================================================
+// the GPU toy trainer (engine.cuh): run_iteration / replay_scoped_iteration
+// and the recompute conversion / localized recovery
+// =========================================================================
+struct mlck_engine {
+  mlck_ctx* ctx = nullptr;
+  toy::Dims m{};
+  uint32_t n_ops = 0;
+  std::vector<uint64_t> P;
+  mlck_optimizer opt{};
+  float inv_tokens = 1.0f;
+  // device scratch for a scope of every layer
+  float *in_acts = nullptr, *targets = nullptr, *grad_in = nullptr, *fwd_out = nullptr, *bwd_out = nullptr;
+  float *cache = nullptr, *work = nullptr, *terms = nullptr;
+  void** codes_dev = nullptr;     // [n_ops] code pointers of the state in use
+  uint8_t* active_dev = nullptr;  // [n_ops]
+  float** grads_dev = nullptr;    // [n_ops] gradient destinations
+  float* grads_own = nullptr;     // sum P floats: replay gradients (no log)
+  std::vector<uint64_t> grads_off;
+
+  int32_t layer_of(uint32_t id) const { return static_cast<int32_t>(id / m.ops_per_layer()); }
+  int32_t stage_of_op(uint32_t id) const { return m.stage_of_layer(layer_of(id)); }
+};
+
+namespace {
+
+void engine_free(mlck_engine* e) {
+  for (void* p : {static_cast<void*>(e->in_acts), static_cast<void*>(e->targets), static_cast<void*>(e->grad_in),
+                  static_cast<void*>(e->fwd_out), static_cast<void*>(e->bwd_out), static_cast<void*>(e->cache),
+                  static_cast<void*>(e->work), static_cast<void*>(e->terms), static_cast<void*>(e->codes_dev),
+                  static_cast<void*>(e->active_dev), static_cast<void*>(e->grads_dev),
+                  static_cast<void*>(e->grads_own)})
+    if (p) cudaFree(p);
+}
+
+// Optimizer steps of the listed operators with the gradients at gptr (one
+// step each): Engine::apply_updates (engine.hpp:699-728), then codes refresh.
+void apply_updates_ptrs(mlck_state* st, const std::vector<uint32_t>& ids, const std::vector<const float*>& gp,
+                        const mlck_optimizer* opt) {
+  const adam::Opt o = to_opt(opt);
+  std::vector<adam::ConvOp> ops;
+  std::vector<const float*> gptr;
+  std::vector<float2> bc;
+  for (size_t k = 0; k < ids.size(); ++k) {
+    const uint32_t id = ids[k];
+    adam::ConvOp c{};
+    c.src = reinterpret_cast<const uint8_t*>(st->master(id));
+    c.dst = st->master(id);
+    c.codes = st->codes(id);
+    c.P = st->P[id];
+    c.n_steps = 1;
+    c.grad_base = static_cast<uint32_t>(gptr.size());
+    c.bc_base = static_cast<uint32_t>(bc.size());
+    gptr.push_back(gp[k]);
+    const uint64_t s1 = st->step[id] + 1;
+    bc.push_back(make_float2(bias_correction(o.b1, s1), bias_correction(o.b2, s1)));
+    st->step[id] = s1;
+    ops.push_back(c);
+  }
+  run_replay(st->ctx, ops, gptr, bc, o, st->cb);
+}
+
+// run_scoped (engine.hpp:332-417) + apply_updates over [lo, hi]: frozen[id]
+// = no weight gradient, no update.  grads[id]: where an active operator's
+// gradient goes (null = the engine's own buffer).
+void engine_step(mlck_engine* e, mlck_state* st, uint64_t it, int32_t lo, int32_t hi,
+                 const std::vector<uint8_t>& frozen, mlck_log* log_in, mlck_log* log_out,
+                 const std::vector<float*>* grads) {
+  mlck_ctx* ctx = e->ctx;
+  const toy::Dims& m = e->m;
+  if (st->n_ops != e->n_ops) throw_invalid("engine: state has " + std::to_string(st->n_ops) + " operators, model " +
+                                           std::to_string(e->n_ops));
+  int32_t llo = m.layers, lhi = -1;
+  for (int32_t l = 0; l < m.layers; ++l)
+    if (m.stage_of_layer(l) >= lo && m.stage_of_layer(l) <= hi) {
+      llo = std::min(llo, l);
+      lhi = std::max(lhi, l);
+    }
+  if (lhi < llo) throw_runtime("stage range covers no layers");  // engine.hpp:349-350
+  const int64_t T = m.tokens(), row = m.mb * m.d;
+  const uint32_t n_gmb = static_cast<uint32_t>(m.dp) * static_cast<uint32_t>(m.M);
+  cudaStream_t s = ctx->stream;
+  // scope inputs: the data stream, or the upstream stage's logged activations
+  if (lo == 0) {
+    toy::launch_stream(e->in_acts, m, st->data_seed, it, 0, s);
+    ctx->launches += 1;
+  } else {
+    for (uint32_t g = 0; g < n_gmb; ++g) {
+      uint64_t nf = 0;
+      if (!log_in) throw_invalid("engine: stages above 0 need a boundary log");
+      if (mlck_log_get_device(log_in, it, g, static_cast<uint32_t>(lo - 1), 0, e->in_acts + g * row, row, &nf) != 0)
+        throw_runtime(mlck_last_error());
+    }
+  }
+  if (hi == m.stages - 1) {
+    toy::launch_stream(e->targets, m, st->data_seed, it, 1, s);
+    ctx->launches += 1;
+  } else {
+    for (uint32_t g = 0; g < n_gmb; ++g) {
+      uint64_t nf = 0;
+      if (!log_in) throw_invalid("engine: stages below the last need a boundary log");
+      if (mlck_log_get_device(log_in, it, g, static_cast<uint32_t>(hi), 1, e->grad_in + g * row, row, &nf) != 0)
+        throw_runtime(mlck_last_error());
+    }
+  }
+  // per-operator tables: code pointers, active flags, gradient destinations
+  std::vector<const void*> codes(e->n_ops);
+  std::vector<uint8_t> active(e->n_ops, 0);
+  std::vector<float*> gdst(e->n_ops, nullptr);
+  std::vector<uint32_t> upd;
+  std::vector<const float*> upd_g;
+  for (uint32_t id = 0; id < e->n_ops; ++id) {
+    codes[id] = st->codes(id);
+    const int32_t sg = e->stage_of_op(id);
+    if (sg < lo || sg > hi || frozen[id]) continue;
+    active[id] = 1;
+    gdst[id] = grads && (*grads)[id] ? (*grads)[id] : e->grads_own + e->grads_off[id];
+    MLCK_CUDA(cudaMemsetAsync(gdst[id], 0, 4 * e->P[id], s));  // parameters the toy model never reads: 0
+    upd.push_back(id);
+    upd_g.push_back(gdst[id]);
+  }
+  const size_t tb = 8 * static_cast<size_t>(e->n_ops);
+  auto& stg = ctx->stage_for(3 * tb);
+  std::memcpy(stg.host, codes.data(), tb);
+  std::memcpy(stg.host + tb, gdst.data(), tb);
+  std::memcpy(stg.host + 2 * tb, active.data(), e->n_ops);
+  ctx->stage_upload(stg, 2 * tb + e->n_ops);
+  MLCK_CUDA(cudaMemcpyAsync(e->codes_dev, stg.dev, tb, cudaMemcpyDeviceToDevice, s));
+  MLCK_CUDA(cudaMemcpyAsync(e->grads_dev, stg.dev + tb, tb, cudaMemcpyDeviceToDevice, s));
+  MLCK_CUDA(cudaMemcpyAsync(e->active_dev, stg.dev + 2 * tb, e->n_ops, cudaMemcpyDeviceToDevice, s));
+  toy::ScopeArgs a{};
+  a.m = m;
+  a.layer_lo = llo;
+  a.layer_hi = lhi;
+  a.stage_lo = lo;
+  a.stage_hi = hi;
+  a.codes = e->codes_dev;
+  a.active = e->active_dev;
+  a.in_acts = e->in_acts;
+  a.targets = e->targets;
+  a.grad_in = e->grad_in;
+  a.fwd_out = log_out ? e->fwd_out : nullptr;
+  a.bwd_out = log_out ? e->bwd_out : nullptr;
+  a.cache = e->cache;
+  a.work = e->work;
+  a.terms = e->terms;
+  a.inv_tokens = e->inv_tokens;
+  toy::launch_scope(a, s);
+  ctx->launches += 1;
+  for (int32_t l = llo; l <= lhi; ++l) {
+    toy::launch_reduce(a, l, e->grads_dev, s);
+    ctx->launches += 1;
+  }
+  if (log_out)  // sender-side boundary copies (engine.hpp:383-385, 407-409)
+    for (int32_t b = lo; b < hi; ++b)
+      for (uint32_t g = 0; g < n_gmb; ++g) {
+        const int64_t at = ((b - lo) * T + static_cast<int64_t>(g) * m.mb) * m.d;
+        if (mlck_log_put(log_out, it, g, static_cast<uint32_t>(b), 0, e->fwd_out + at, row) != 0 ||
+            mlck_log_put(log_out, it, g, static_cast<uint32_t>(b), 1, e->bwd_out + at, row) != 0)
+          throw_runtime(mlck_last_error());
+      }
+  if (!upd.empty()) apply_updates_ptrs(st, upd, upd_g, &e->opt);
+}
+
+// load_record (recovery.hpp:144-161): Full payloads replace the operator's
+// state (refresh_compute); compute-only payloads set the codes of operators
+// still frozen.
+void load_record_dev(mlck_state* st, mlck_blob* b, const Parsed& pr, const std::vector<uint8_t>& scope) {
+  cudaStream_t s = st->ctx->stream;
+  for (const auto& en : pr.entries) {
+    const uint32_t id = en.id;
+    if (id >= st->n_ops) throw_runtime("conversion: record operator id out of range");
+    if (!scope[id]) continue;
+    if (en.param_count != st->P[id]) throw_invalid("conversion: operator " + std::to_string(id) + " size mismatch");
+    const uint64_t P = en.param_count;
+    if (en.mode == 0) {
+      if (P) {
+        ce_copy(st->master(id), b->dev + en.payload_offset, 12 * P, cudaMemcpyDeviceToDevice, s);
+        launch_encode(st->master(id), st->codes(id), P, st->cb, s);
+        st->ctx->launches += 1;
+      }
+      st->step[id] = en.step;
+      st->has_full[id] = 1;
+      st->present[id] = 1;
+    } else if (!st->has_full[id]) {
+      if (P) ce_copy(st->codes(id), b->dev + en.payload_offset, static_cast<uint64_t>(st->cb) * P,
+                     cudaMemcpyDeviceToDevice, s);
+      st->present[id] = 1;
+    }
+  }
+}
+
+void convert_recompute(mlck_engine* e, mlck_state* out, mlck_blob* const* blobs, uint32_t n, uint64_t a,
+                       uint32_t W, uint64_t data_seed, const int32_t* seg, mlck_log* logs, uint64_t target) {
+  const bool localized = seg != nullptr;
+  if (n != W) {
+    if (localized) throw_runtime("sparse checkpoint incomplete");
+    throw_runtime("sparse checkpoint incomplete: " + std::to_string(n) + " of " + std::to_string(W) + " records");
+  }
+  mlck_ctx* ctx = e->ctx;
+  ctx->activate();
+  if (out->n_ops != e->n_ops) throw_invalid("engine: state / model operator count mismatch");
+  const int32_t lo = localized ? seg[0] : 0, hi = localized ? seg[1] : e->m.stages - 1;
+  std::vector<uint8_t> scope(e->n_ops, 0);
+  for (uint32_t id = 0; id < e->n_ops; ++id) scope[id] = e->stage_of_op(id) >= lo && e->stage_of_op(id) <= hi;
+  std::vector<std::string> errs;
+  const uint32_t n_parse = (W == 1 && !localized) ? 1 : W;
+  auto parsed = parse_blobs(ctx, blobs, n_parse, out->cb, errs);
+  for (uint32_t k = 0; k < n_parse; ++k)  // recovery.hpp:163-171
+    if (!errs[k].empty()) throw_runtime("sparse checkpoint record (slot " + std::to_string(k) + "): " + errs[k]);
+  for (uint32_t id = 0; id < e->n_ops; ++id)
+    if (scope[id]) out->has_full[id] = 0;
+  if (!localized && W == 1) {  // recovery.hpp:190-200
+    load_record_dev(out, blobs[0], parsed[0], scope);
+    out->iteration = parsed[0].hdr.iteration;
+    out->data_seed = parsed[0].hdr.data_seed;
+    return;
+  }
+  out->iteration = a;
+  out->data_seed = data_seed;
+  std::vector<uint8_t> frozen(e->n_ops, 1);
+  uint64_t it = a;
+  for (uint32_t k = 0; k < W; ++k) {
+    load_record_dev(out, blobs[k], parsed[k], scope);
+    for (uint32_t id = 0; id < e->n_ops; ++id)
+      if (scope[id] && out->has_full[id]) frozen[id] = 0;
+    it = a + k + 1;
+    engine_step(e, out, it, lo, hi, frozen, localized ? logs : nullptr, nullptr, nullptr);
+    out->iteration = it;
+  }
+  for (uint32_t id = 0; id < e->n_ops; ++id)
+    if (scope[id] && !out->has_full[id])
+      throw_runtime(localized ? "localized recovery left operator " + std::to_string(id) + " frozen"  // 263-266
+                              : "conversion finished with frozen operator " + std::to_string(id));  // 222-225
+  while (localized && it < target) {  // the lost iterations after the window (recovery.hpp:269-273)
+    it += 1;
+    engine_step(e, out, it, lo, hi, frozen, logs, nullptr, nullptr);
+    out->iteration = it;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int mlck_engine_create(mlck_ctx* ctx, const mlck_engine_config* c, mlck_engine** out) {
+  return api([&] {
+    if (c->layers < 1 || c->experts_per_layer < 1 || c->token_dim < 1 || c->pp_stages < 1 || c->dp_degree < 1 ||
+        c->microbatches < 1 || c->microbatch_size < 1)
+      throw_invalid("engine: every dimension must be >= 1");
+    if (c->top_k + c->shared_experts > c->experts_per_layer)  // engine.hpp:111-112
+      throw_invalid("engine: top_k + shared_experts > experts_per_layer");
+    if (c->pp_stages > c->layers) throw_invalid("engine: more pipeline stages than layers");
+    if (c->compute_bytes != 1 && c->compute_bytes != 2 && c->compute_bytes != 4)
+      throw_invalid("quantize: unsupported width " + std::to_string(c->compute_bytes));
+    ctx->activate();
+    auto* e = new mlck_engine();
+    e->ctx = ctx;
+    toy::Dims& m = e->m;
+    m.layers = c->layers;
+    m.E = c->experts_per_layer;
+    m.top_k = c->top_k;
+    m.shared = c->shared_experts;
+    m.d = c->token_dim;
+    m.he = c->expert_hidden;
+    m.hn = c->nonexpert_hidden;
+    m.residual = c->residual;
+    m.stages = c->pp_stages;
+    m.dp = c->dp_degree;
+    m.M = c->microbatches;
+    m.mb = c->microbatch_size;
+    m.cb = c->compute_bytes;
+    // ModelSpec::derived_*_params (core.hpp:86-100)
+    m.pe = c->expert_params >= 0 ? c->expert_params : toy::Dims::mlp_live(m.d, m.he);
+    m.pn = c->nonexpert_params >= 0 ? c->nonexpert_params : toy::Dims::mlp_live(m.d, m.hn);
+    m.pg = c->gate_params >= 0 ? c->gate_params : m.g_live();
+    if (m.pe < m.e_live() || m.pn < m.ne_live() || m.pg < m.g_live())
+      throw_invalid("engine: explicit parameter counts below the toy model's");
+    e->opt = c->optimizer;
+    e->n_ops = static_cast<uint32_t>(m.layers) * static_cast<uint32_t>(m.ops_per_layer());
+    uint64_t tot = 0;
+    for (uint32_t id = 0; id < e->n_ops; ++id) {
+      const uint32_t j = id % m.ops_per_layer();
+      const uint64_t p = j < static_cast<uint32_t>(m.E) ? m.pe : j == static_cast<uint32_t>(m.E) ? m.pn : m.pg;
+      e->P.push_back(p);
+      e->grads_off.push_back(tot);
+      tot += align_up(p, 64);
+    }
+    e->inv_tokens = 1.0f / static_cast<float>(m.tokens());  // engine.hpp:341-342
+    const int64_t T = m.tokens(), d = m.d;
+    const toy::CacheLayout L(m);
+    const toy::TermLayout TL(m);
+    const int64_t hmax = std::max<int64_t>(1, std::max(m.he, m.hn));
+    auto alloc = [&](auto** p, uint64_t bytes) { dev_malloc(reinterpret_cast<void**>(p), std::max<uint64_t>(bytes, 256)); };
+    alloc(&e->in_acts, 4 * T * d);
+    alloc(&e->targets, 4 * T * d);
+    alloc(&e->grad_in, 4 * T * d);
+    alloc(&e->fwd_out, 4 * T * d * std::max(1, m.stages - 1));
+    alloc(&e->bwd_out, 4 * T * d * std::max(1, m.stages - 1));
+    alloc(&e->cache, 4 * T * m.layers * L.stride);
+    alloc(&e->work, 4 * T * (4 * d + 2 * m.nsel() + 2 * hmax));
+    alloc(&e->terms, 4 * T * m.layers * TL.stride);
+    alloc(&e->codes_dev, 8 * e->n_ops);
+    alloc(&e->active_dev, e->n_ops);
+    alloc(&e->grads_dev, 8 * e->n_ops);
+    alloc(&e->grads_own, 4 * tot);
+    *out = e;
+  });
+}
+
+int mlck_engine_destroy(mlck_engine* e) {
+  return api([&] {
+    if (!e) return;
+    e->ctx->activate();
+    cudaStreamSynchronize(e->ctx->stream);
+    engine_free(e);
+    delete e;
+  });
+}
+
+uint32_t mlck_engine_op_count(const mlck_engine* e) { return e ? e->n_ops : 0; }
+int mlck_engine_param_counts(const mlck_engine* e, uint64_t* out) {
+  return api([&] { std::copy(e->P.begin(), e->P.end(), out); });
+}
+int32_t mlck_engine_stage_of_op(const mlck_engine* e, uint32_t id) {
+  return e && id < e->n_ops ? e->stage_of_op(id) : -1;
+}
+
+int mlck_engine_run_iteration(mlck_engine* e, mlck_state* st, const uint8_t* frozen, mlck_log* log_out,
+                              mlck_gradlog* grads_out) {
+  return api([&] {
+    e->ctx->activate();
+    const uint64_t it = st->iteration + 1;
+    std::vector<uint8_t> fz(e->n_ops, 0);
+    if (frozen) fz.assign(frozen, frozen + e->n_ops);
+    std::vector<float*> gd(e->n_ops, nullptr);
+    if (grads_out) {
+      if (grads_out->n_ops != e->n_ops) throw_invalid("gradient log: operator count mismatch");
+      for (uint32_t id = 0; id < e->n_ops; ++id)
+        if (!fz[id]) gd[id] = grads_out->slot(it, id);  // zero-copy capture
+    }
+    engine_step(e, st, it, 0, e->m.stages - 1, fz, nullptr, log_out, &gd);
+    st->iteration = it;
+  });
+}
+
+int mlck_engine_replay_scoped_iteration(mlck_engine* e, mlck_state* ops, uint64_t it, int32_t lo, int32_t hi,
+                                        const uint8_t* frozen, mlck_log* log_in) {
+  return api([&] {
+    if (lo < 0 || hi < lo || hi >= e->m.stages) throw_invalid("replay: stage range out of bounds");
+    e->ctx->activate();
+    std::vector<uint8_t> fz(e->n_ops, 0);
+    if (frozen) fz.assign(frozen, frozen + e->n_ops);
+    engine_step(e, ops, it, lo, hi, fz, log_in, nullptr, nullptr);
+  });
+}
+
+int mlck_sparse_to_dense_convert_recompute(mlck_engine* e, mlck_state* out, mlck_blob* const* blobs, uint32_t n,
+                                           uint64_t a, uint32_t W, uint64_t data_seed) {
+  return api([&] { convert_recompute(e, out, blobs, n, a, W, data_seed, nullptr, nullptr, 0); });
+}
+
+int mlck_localized_recover_recompute(mlck_engine* e, mlck_state* out, int32_t lo, int32_t hi,
+                                     mlck_blob* const* blobs, uint32_t n, uint64_t a, uint32_t W,
+                                     uint64_t data_seed, mlck_log* logs, uint64_t target) {
+  return api([&] {
+    if (lo < 0 || hi < lo || hi >= e->m.stages) throw_invalid("recovery segment: stage range out of bounds");
+    const int32_t seg[2] = {lo, hi};
+    convert_recompute(e, out, blobs, n, a, W, data_seed, seg, logs, target);
   });
 }
 

@@ -867,11 +867,13 @@ void launch_walk(const WalkJob* jobs, int n_jobs, cudaStream_t stream) {
 void launch_replay(const adam::ConvOp* ops, int n_ops, const float* const* gptr, const float2* bc,
                    const adam::Opt& o, int cb, uint64_t total_units, cudaStream_t stream) {
   if (total_units == 0) return;
-  const uint64_t blocks = div_up(total_units, adam::kReplayThreads);
+  const uint64_t blocks = total_units;  // total_units counts CTAs (run_replay)
   adam::replay_kernel<<<static_cast<unsigned>(blocks), adam::kReplayThreads, 0, stream>>>(ops, n_ops, gptr, bc, o,
                                                                                         cb, total_units);
   MLCK_CUDA(cudaGetLastError());
 }
+
+int replay_cta_threads() { return adam::kReplayThreads; }
 
 void launch_fastmath_check(uint64_t n, uint64_t seed, unsigned long long* counts, cudaStream_t stream) {
   adam::fastmath_check_kernel<<<148 * 8, 256, 0, stream>>>(n, seed, counts);

@@ -80,6 +80,9 @@ void launch_pack(const pack::Segment* segs, int n_segs, uint64_t total, const pa
 void launch_walk(const WalkJob* jobs, int n_jobs, cudaStream_t stream);
 void launch_replay(const adam::ConvOp* ops, int n_ops, const float* const* gptr, const float2* bc,
                    const adam::Opt& o, int cb, uint64_t total_units, cudaStream_t stream);
+// Threads per replay CTA (launch_replay's total_units counts CTAs: each
+// operator's 4-element units round up to whole CTAs).
+int replay_cta_threads();
 // Self-check of the replay kernel's spelled-out IEEE fast paths (adam.cuh).
 void launch_fastmath_check(uint64_t n, uint64_t seed, unsigned long long* counts, cudaStream_t stream);
 void launch_adam_arrays(float* w, float* m, float* v, const float* g, uint64_t n,

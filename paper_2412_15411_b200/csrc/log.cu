@@ -249,9 +249,21 @@ static int log_get_impl(mlck_log* l, const Key& k, float* out, uint64_t cap, uin
     if (!out) return;
     if (cap < it->second.n_floats) throw_invalid("log get: buffer too small");
     MLCK_CUDA(cudaSetDevice(l->ctx_device));
-    MLCK_CUDA(cudaStreamSynchronize(l->side));
     const uint64_t bytes = 4 * it->second.n_floats;
-    if (l->kind == 0 && !device_out) {
+    if (device_out) {
+      // stream-ordered on the ctx stream (after the entry's copy landed): the
+      // destination may still be read by work queued before this call
+      void* cs = nullptr;
+      int dev = 0;
+      mlck_ctx_device_stream_(l->ctx, &dev, &cs);
+      MLCK_CUDA(cudaEventRecord(l->copied, l->side));
+      MLCK_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(cs), l->copied, 0));
+      MLCK_CUDA(cudaMemcpyAsync(out, l->base + it->second.off, bytes, cudaMemcpyDefault,
+                                static_cast<cudaStream_t>(cs)));
+      return;
+    }
+    MLCK_CUDA(cudaStreamSynchronize(l->side));
+    if (l->kind == 0) {
       std::memcpy(out, l->base + it->second.off, bytes);
     } else {
       MLCK_CUDA(cudaMemcpy(out, l->base + it->second.off, bytes, cudaMemcpyDefault));

@@ -53,6 +53,26 @@ class Optimizer(C.Structure):
         return cls(1, lr, 0.9, 0.999, 1e-8)
 
 
+class EngineConfig(C.Structure):
+    """EngineConfig (engine.hpp:96-124; core.hpp:66-191): params < 0 = derived."""
+    _fields_ = [("layers", C.c_int32), ("experts_per_layer", C.c_int32), ("top_k", C.c_int32),
+                ("shared_experts", C.c_int32), ("token_dim", C.c_int32), ("expert_hidden", C.c_int32),
+                ("nonexpert_hidden", C.c_int32), ("residual", C.c_int32), ("expert_params", C.c_int64),
+                ("nonexpert_params", C.c_int64), ("gate_params", C.c_int64), ("pp_stages", C.c_int32),
+                ("dp_degree", C.c_int32), ("microbatches", C.c_int32), ("compute_bytes", C.c_int32),
+                ("microbatch_size", C.c_int64), ("optimizer", Optimizer)]
+
+    @classmethod
+    def from_dict(cls, c: dict) -> "EngineConfig":
+        opt = Optimizer(int(c.get("optimizer_kind", 0)), c.get("lr", 1e-3), c.get("beta1", 0.9),
+                        c.get("beta2", 0.999), c.get("eps", 1e-8))
+        return cls(c["layers"], c["experts_per_layer"], c["top_k"], c.get("shared_experts", 0), c["token_dim"],
+                   c["expert_hidden"], c["nonexpert_hidden"], int(c.get("residual", 1)),
+                   int(c.get("expert_params", -1)), int(c.get("nonexpert_params", -1)),
+                   int(c.get("gate_params", -1)), c["pp_stages"], c["dp_degree"], c["microbatches"],
+                   int(c["compute_bytes"]), c["microbatch_size"], opt)
+
+
 class RecordInfo(C.Structure):
     _fields_ = [("kind", C.c_uint8), ("iteration", C.c_uint64), ("window_start", C.c_uint64),
                 ("wsparse", C.c_uint32), ("slot", C.c_uint32), ("data_seed", C.c_uint64),
@@ -166,6 +186,17 @@ def lib():
             "mlck_ctx_set_hash_reserve": (C.c_int, [vp, C.c_int]),
             "mlck_gradlog_capture": (C.c_int, [vp, C.c_uint64, C.c_uint32, vp]),
             "mlck_ctx_set_witness": (C.c_int, [vp, C.c_int]),
+            "mlck_engine_create": (C.c_int, [vp, C.POINTER(EngineConfig), C.POINTER(vp)]),
+            "mlck_engine_destroy": (C.c_int, [vp]),
+            "mlck_engine_op_count": (C.c_uint32, [vp]),
+            "mlck_engine_param_counts": (C.c_int, [vp, u64p]),
+            "mlck_engine_stage_of_op": (C.c_int32, [vp, C.c_uint32]),
+            "mlck_engine_run_iteration": (C.c_int, [vp, vp, u8p, vp, vp]),
+            "mlck_engine_replay_scoped_iteration": (C.c_int, [vp, vp, C.c_uint64, C.c_int32, C.c_int32, u8p, vp]),
+            "mlck_sparse_to_dense_convert_recompute": (C.c_int, [vp, vp, C.POINTER(vp), C.c_uint32, C.c_uint64,
+                                                                 C.c_uint32, C.c_uint64]),
+            "mlck_localized_recover_recompute": (C.c_int, [vp, vp, C.c_int32, C.c_int32, C.POINTER(vp), C.c_uint32,
+                                                           C.c_uint64, C.c_uint32, C.c_uint64, vp, C.c_uint64]),
             "mlck_ctx_witness_stats": (C.c_int, [vp, u64p, u64p]),
             "mlck_blob_witness_ptr": (vp, [vp]),
             "mlck_gradlog_bytes": (C.c_uint64, [vp]),
@@ -820,3 +851,73 @@ class UpstreamLog:
 
     def fence(self, stream: int | None = None):
         check(lib().mlck_log_fence(self.h, stream))
+
+
+class Engine:
+    """The miniature MoE trainer on the GPU (moelab::Engine, engine.hpp:150-730):
+    run_iteration (producer of the boundary and gradient logs) and the
+    recompute replay of conversion / localized recovery."""
+
+    def __init__(self, ctx: Context, cfg: "EngineConfig | dict"):
+        self.ctx = ctx
+        self.cfg = cfg if isinstance(cfg, EngineConfig) else EngineConfig.from_dict(cfg)
+        self.h = vp()
+        check(lib().mlck_engine_create(ctx.h, C.byref(self.cfg), C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            lib().mlck_engine_destroy(self.h)
+            self.h = vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def op_count(self) -> int:
+        return int(lib().mlck_engine_op_count(self.h))
+
+    def param_counts(self) -> list:
+        out = np.zeros(self.op_count, dtype=np.uint64)
+        check(lib().mlck_engine_param_counts(self.h, _ptr(out, u64p)))
+        return [int(x) for x in out]
+
+    def stage_of_op(self, i: int) -> int:
+        return int(lib().mlck_engine_stage_of_op(self.h, i))
+
+    @staticmethod
+    def _flags(frozen, n):
+        if frozen is None:
+            return None, None
+        f = np.zeros(n, dtype=np.uint8)
+        for i in frozen:
+            f[i] = 1
+        return f, _ptr(f, u8p)
+
+    def run_iteration(self, st: DeviceState, frozen=None, log: "UpstreamLog | None" = None,
+                      gradlog: GradLog | None = None):
+        keep, fp = self._flags(frozen, self.op_count)
+        check(lib().mlck_engine_run_iteration(self.h, st.h, fp, log.h if log is not None else None,
+                                              gradlog.h if gradlog is not None else None))
+
+    def replay_scoped_iteration(self, ops: DeviceState, iteration: int, stage_lo: int, stage_hi: int, frozen=None,
+                                log: "UpstreamLog | None" = None):
+        keep, fp = self._flags(frozen, self.op_count)
+        check(lib().mlck_engine_replay_scoped_iteration(self.h, ops.h, iteration, stage_lo, stage_hi, fp,
+                                                        log.h if log is not None else None))
+
+    def sparse_to_dense_convert(self, out: DeviceState, blobs, window_start: int, wsparse: int, data_seed: int):
+        """sparse_to_dense_convert (recovery.hpp:180-227) with the recompute replay."""
+        arr = (vp * max(1, len(blobs)))(*[b.h for b in blobs])
+        check(lib().mlck_sparse_to_dense_convert_recompute(self.h, out.h, arr, len(blobs), window_start, wsparse,
+                                                           data_seed))
+
+    def localized_recover(self, out: DeviceState, stage_lo: int, stage_hi: int, blobs, window_start: int,
+                          wsparse: int, data_seed: int, log: "UpstreamLog | None", target_iteration: int):
+        """localized_recover (recovery.hpp:240-289) by recompute from the boundary log."""
+        arr = (vp * max(1, len(blobs)))(*[b.h for b in blobs])
+        check(lib().mlck_localized_recover_recompute(self.h, out.h, stage_lo, stage_hi, arr, len(blobs),
+                                                     window_start, wsparse, data_seed,
+                                                     log.h if log is not None else None, target_iteration))

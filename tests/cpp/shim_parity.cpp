@@ -188,6 +188,46 @@ int main(int argc, char** argv) {
       std::cout << "ERR invalid_argument: " << e.what() << "\n";
     }
   }
+  // the compiled gradient source: the GPU trainer runs the window itself,
+  // its weight gradients landing in the gradient log (no copy); both
+  // conversions rebuild its state bit for bit
+  if (argc == 3 && n_ops == 18) {  // verify_toy: 3 layers x (4 experts + NE + gate)
+    mlck_engine_config ec{};
+    ec.layers = 3;
+    ec.experts_per_layer = 4;
+    ec.top_k = 2;
+    ec.token_dim = 4;
+    ec.expert_hidden = 4;
+    ec.nonexpert_hidden = 4;
+    ec.residual = 1;
+    ec.expert_params = ec.nonexpert_params = ec.gate_params = -1;
+    ec.pp_stages = 3;
+    ec.dp_degree = 1;
+    ec.microbatches = 2;
+    ec.microbatch_size = 4;
+    ec.compute_bytes = static_cast<int32_t>(cb);
+    ec.optimizer = oc.abi();
+    Engine eng(ctx, ec);
+    DeviceState run(ctx, P, static_cast<int>(cb));
+    for (uint32_t i = 0; i < n_ops; ++i) run.set_op(i, conv.op(i));
+    run.set_meta(conv.iteration(), data_seed);
+    const uint64_t ws2 = conv.iteration();
+    SparseCheckpoint win;
+    win.window_start = ws2;
+    win.wsparse = W;
+    GradientLog g2(ctx, P, W + 1);
+    UpstreamLog blog(ctx, 1 << 20);
+    for (uint32_t k = 0; k < W; ++k) {
+      win.add_record(take_sparse_snapshot(run, slots[k], k), plan);
+      eng.run_iteration(run, {}, &blog, &g2);
+    }
+    DeviceState a(ctx, P, static_cast<int>(cb)), b(ctx, P, static_cast<int>(cb));
+    eng.sparse_to_dense_convert(a, win, data_seed);
+    sparse_to_dense_convert(b, win, &g2, data_seed, oc);
+    const auto want = run.serialize_state();
+    std::cout << "ENGINE recompute " << (a.serialize_state() == want) << " logged " << (b.serialize_state() == want)
+              << " log_entries " << blog.size() << "\n";
+  }
   std::cout << "OK\n";
   return 0;
 }
