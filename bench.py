@@ -661,6 +661,8 @@ def run_ours(args, d: Dist):
 
     dev = d.local
     ctx = mlck.Context(dev)
+    ctx.set_hash_async(bool(args.hash_async))
+    ctx.set_hash_reserve(args.hash_reserve)
     wl = pick_workload(args, d.world)
     pcs, cb, W = wl["param_counts"], wl["cb"], wl["W"]
     slots = schedule(wl)
@@ -1007,6 +1009,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-log", action="store_true")
+    ap.add_argument("--hash-async", type=int, default=1, help="trailer hash off the pack's critical path (1/0)")
+    ap.add_argument("--hash-reserve", type=int, default=0, help="SMs the hash kernel leaves to the next pack")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the N=1 same-workload leg, gradient-log capture and interference keys")
     args = ap.parse_args()

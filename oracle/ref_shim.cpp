@@ -21,6 +21,7 @@
 
 #include "moelab/recovery.hpp"
 #include "moelab/schedule.hpp"
+#include "moelab/sim.hpp"
 #include "moelab/snapshot.hpp"
 #include "moelab/verify.hpp"
 
@@ -385,6 +386,55 @@ int64_t mlr_conversion_plan(uint64_t window_start, uint32_t wsparse, const uint8
     total = static_cast<int64_t>(w);
   });
   return total;
+}
+
+// run_simulation (sim.hpp:246-597) for the sparse policy with Poisson
+// failures: out[] = wsparse, t_iter, iterations, failures, useful, stall,
+// recovery, idle, wall, ettr, overhead_s_per_iter, recovery_recompute_s,
+// max_recovery_event_s, mean_recovery_event_s, checkpoint_never_persisted.
+int mlr_run_simulation_sparse(int32_t layers, int32_t experts, int64_t expert_params, int64_t nonexpert_params,
+                              int64_t gate_params, int64_t tokens_per_sample, int32_t nodes, double pcie,
+                              double replication_bw, int32_t pp_stages, int32_t microbatches, int64_t global_batch,
+                              const double* t_stage, int32_t n_stage, double t_sync, double t_update,
+                              double t_iter_override, int32_t upstream_logging, int32_t savings, double mtbf,
+                              double horizon, double t_restart, double detection_delay, int32_t replication_r,
+                              uint64_t seed, double* out, char* err, size_t ecap) {
+  return guarded(err, ecap, [&] {
+    SimConfig cfg;
+    cfg.model.layers = layers;
+    cfg.model.experts_per_layer = experts;
+    cfg.model.top_k = 1;
+    cfg.model.expert_params = expert_params;
+    cfg.model.nonexpert_params = nonexpert_params;
+    cfg.model.gate_params = gate_params;
+    cfg.model.tokens_per_sample = tokens_per_sample;
+    cfg.cluster.nodes = nodes;
+    cfg.cluster.pcie_bandwidth = pcie;
+    cfg.cluster.replication_bandwidth = replication_bw;
+    cfg.parallel.pp_stages = pp_stages;
+    cfg.parallel.microbatches = microbatches;
+    cfg.parallel.global_batch = global_batch;
+    cfg.profile.t_stage.assign(t_stage, t_stage + n_stage);
+    cfg.profile.t_sync = t_sync;
+    cfg.profile.t_update = t_update;
+    cfg.profile.t_iter_override = t_iter_override;
+    cfg.policy.kind = PolicyKind::Sparse;
+    cfg.policy.upstream_logging = upstream_logging != 0;
+    cfg.policy.conversion_compute_savings = savings != 0;
+    cfg.failures.kind = FailureProcess::Kind::Poisson;
+    cfg.failures.mtbf = mtbf;
+    cfg.horizon = horizon;
+    cfg.t_restart = t_restart;
+    cfg.detection_delay = detection_delay;
+    cfg.replication_r = replication_r;
+    cfg.seed = seed;
+    const Metrics m = run_simulation(cfg);
+    const double v[] = {m.wsparse_or_interval, m.t_iter, static_cast<double>(m.iterations),
+                        static_cast<double>(m.failures), m.useful_s, m.stall_s, m.recovery_s, m.idle_s, m.wall_s,
+                        m.ettr, m.overhead_s_per_iter, m.recovery_recompute_s, m.max_recovery_event_s,
+                        m.mean_recovery_event_s, m.checkpoint_never_persisted ? 1.0 : 0.0};
+    std::memcpy(out, v, sizeof(v));
+  });
 }
 
 // check_log_budget(model, plan, wsparse, cluster) (recovery.hpp:308-317).

@@ -91,6 +91,33 @@ struct mlck_ctx {
   }
   // SMs the hash kernel leaves free (mlck_ctx_set_hash_reserve)
   int hash_reserve = 0;
+  // Asynchronous trailer hash (mlck_ctx_set_hash_async, default on): the
+  // default transport's FNV kernel runs on hstream after the pack, so the
+  // next pack (next slot, another blob) need not wait for it -- the hash is
+  // off the snapshot's critical path, as PAPER.md's overlap intends.  Every
+  // reader of a record waits for its `written` event; the raw helpers and
+  // synchronize join all hashes (join_hash).
+  bool hash_async = true;
+  cudaStream_t hstream = nullptr;
+  cudaEvent_t ev_packed_h = nullptr, ev_hash_last = nullptr;
+  bool hash_pending = false;
+  uint32_t* hscratch = nullptr;
+  size_t hwords = 0;
+  unsigned long long* hresult = nullptr;
+  uint32_t* hscratch_for(uint64_t n) {
+    const size_t need = fnv_scratch_words(n);
+    if (need > hwords) {
+      MLCK_CUDA(cudaStreamSynchronize(hstream));
+      if (hscratch) MLCK_CUDA(cudaFree(hscratch));
+      hwords = align_up(std::max<size_t>(need, 4096), 1024);
+      MLCK_CUDA(cudaMalloc(&hscratch, hwords * 4));
+      MLCK_CUDA(cudaMemsetAsync(hscratch, 0, hwords * 4, hstream));
+    }
+    return hscratch;
+  }
+  void join_hash() {
+    if (hash_pending) MLCK_CUDA(cudaStreamWaitEvent(stream, ev_hash_last, 0));
+  }
   // records keep the hash kernel's segment starts (a witness) and are
   // re-verified against it (fnv.cuh); counters for tests and the bench
   bool witness = true;
@@ -206,7 +233,7 @@ struct mlck_ctx {
   // word in the scratch header; checked after the stream synchronizes.
   bool watchdog_seen = false;
   void read_watchdog() {
-    for (uint32_t* sc : {fnv_scratch, vscratch[0], vscratch[1]}) {
+    for (uint32_t* sc : {fnv_scratch, vscratch[0], vscratch[1], hscratch}) {
       if (!sc) continue;
       uint32_t w = 0;
       MLCK_CUDA(cudaMemcpy(&w, sc + fnv_sticky_word(), 4, cudaMemcpyDeviceToHost));
@@ -241,6 +268,8 @@ struct mlck_ctx {
     if (++fnv_epoch == 0) {  // wrapped: clear stale tags once
       MLCK_CUDA(cudaStreamSynchronize(stream));
       for (int i = 0; i < 2; ++i) MLCK_CUDA(cudaStreamSynchronize(vside[i]));
+      MLCK_CUDA(cudaStreamSynchronize(hstream));
+      if (hscratch) MLCK_CUDA(cudaMemset(hscratch, 0, hwords * 4));
       if (fnv_scratch) MLCK_CUDA(cudaMemset(fnv_scratch, 0, fnv_words * 4));
       for (int i = 0; i < 2; ++i)
         if (vscratch[i]) MLCK_CUDA(cudaMemset(vscratch[i], 0, vwords[i] * 4));
@@ -286,6 +315,7 @@ struct mlck_blob {
 
   void reserve(uint64_t n) {
     if (n <= cap) return;
+    ctx->join_hash();
     MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
     if (dev) MLCK_CUDA(cudaFree(dev));
     cap = align_up(n, kAlign);
@@ -296,6 +326,7 @@ struct mlck_blob {
   void reserve_witness(uint64_t body) {
     const uint64_t words = fnv_witness_words(body) + 1;
     if (words <= witness_cap) return;
+    ctx->join_hash();
     MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
     if (witness) MLCK_CUDA(cudaFree(witness));
     witness_cap = align_up(words, 1024);
@@ -386,15 +417,17 @@ struct SegmentBuilder {
 
 // Uploads the segment table + meta, launches pack (and the FNV trailer when
 // `trailer`): the blob body is [0, builder.pos), the trailer at pos.
-void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer);
+cudaStream_t run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer);
 void run_pack(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
+  // the blob's previous record may still be read by its asynchronous hash
+  if (out->written) MLCK_CUDA(cudaStreamWaitEvent(ctx->stream, out->written, 0));
   out->witness_n = ~0ull;
-  run_pack_impl(ctx, b, out, trailer);
+  const cudaStream_t last = run_pack_impl(ctx, b, out, trailer);
   if (!out->written) MLCK_CUDA(cudaEventCreateWithFlags(&out->written, cudaEventDisableTiming));
-  MLCK_CUDA(cudaEventRecord(out->written, ctx->stream));  // every path ends with the pushes joined
+  MLCK_CUDA(cudaEventRecord(out->written, last));  // every path ends with the pushes joined
   out->written_replicas = static_cast<uint32_t>(out->replicas.size());
 }
-void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
+cudaStream_t run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
   const uint64_t body = b.pos;
   const uint64_t total = body + (trailer ? 8 : 0);
   out->reserve(total);
@@ -472,7 +505,7 @@ void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool traile
     if (wit) out->witness_n = body;
     ctx->tend(tf);
     ctx->launches += 1;
-    return;
+    return ctx->stream;
   }
   int mode = ctx->replica_mode;
   if (mode == -1) {  // auto: 0 when every replica is in this GPU's HBM, else 1
@@ -508,7 +541,7 @@ void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool traile
     if (wit) out->witness_n = body;
     ctx->tend(tf);
     ctx->launches += 2;
-    return;
+    return ctx->stream;
   }
   if (trailer && mode == 3 && !out->replicas.empty() && body) {
     // pack the local record; push it to the replicas with SM stores from
@@ -540,7 +573,7 @@ void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool traile
     ctx->launches += 3;
     MLCK_CUDA(cudaEventRecord(ctx->ev_pushed[0], ctx->side[0]));
     MLCK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_pushed[0], 0));  // record complete everywhere
-    return;
+    return ctx->stream;
   }
   if (trailer && (mode == 1 || mode == 4) && !out->replicas.empty() && body) {
     // pack the local record in pieces; the copy engines push each piece to
@@ -611,25 +644,40 @@ void run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool traile
       MLCK_CUDA(cudaEventRecord(ctx->ev_pushed[r % mlck_ctx::kPushStreams], ctx->side[r % mlck_ctx::kPushStreams]));
       MLCK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_pushed[r % mlck_ctx::kPushStreams], 0));  // record complete everywhere
     }
-    return;
+    return ctx->stream;
   }
   const int tp = ctx->tbegin("pack");
   launch_pack(segs, n_segs, body, d, ctx->stream);
   ctx->tend(tp);
   ctx->launches += body ? 1 : 0;
-  if (trailer) {
-    TrailerDsts t{};
-    for (int r = 0; r < d.n; ++r) t.p[r] = d.p[r] + body;
-    t.n = d.n;
-    uint32_t* scratch = ctx->fnv_scratch_for(body);
-    const int tf = ctx->tbegin("fnv");
-    uint32_t* wit = out->witness_for(body);
-    launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream, nullptr,
-               nullptr, nullptr, ctx->hash_reserve, nullptr, wit);
-    if (wit) out->witness_n = body;
-    ctx->tend(tf);
-    ctx->launches += 1;
+  if (!trailer) return ctx->stream;
+  TrailerDsts t{};
+  for (int r = 0; r < d.n; ++r) t.p[r] = d.p[r] + body;
+  t.n = d.n;
+  uint32_t* wit = out->witness_for(body);
+  cudaStream_t hs = ctx->stream;
+  uint32_t* scratch = nullptr;
+  unsigned long long* res = ctx->results;
+  if (ctx->hash_async) {  // the hash follows this pack on hstream; the ctx stream moves on
+    MLCK_CUDA(cudaEventRecord(ctx->ev_packed_h, ctx->stream));
+    MLCK_CUDA(cudaStreamWaitEvent(ctx->hstream, ctx->ev_packed_h, 0));
+    hs = ctx->hstream;
+    scratch = ctx->hscratch_for(body);
+    res = ctx->hresult;
+  } else {
+    scratch = ctx->fnv_scratch_for(body);
   }
+  const int tf = ctx->tbegin("fnv", hs);
+  launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), res, t, hs, nullptr, nullptr, nullptr,
+             ctx->hash_reserve, nullptr, wit);
+  if (wit) out->witness_n = body;
+  ctx->tend(tf, hs);
+  ctx->launches += 1;
+  if (ctx->hash_async) {
+    MLCK_CUDA(cudaEventRecord(ctx->ev_hash_last, ctx->hstream));
+    ctx->hash_pending = true;
+  }
+  return hs;
 }
 
 void build_state_image(const mlck_state* st, SegmentBuilder& b) {
@@ -753,9 +801,16 @@ struct ParseJob {
   std::vector<std::string> walk_err;
 };
 
+// the records' asynchronous hashes (trailer, witness) have landed
+void wait_written(mlck_ctx* ctx, mlck_blob* const* blobs, uint32_t n) {
+  for (uint32_t k = 0; k < n; ++k)
+    if (blobs[k]->written) MLCK_CUDA(cudaStreamWaitEvent(ctx->stream, blobs[k]->written, 0));
+}
+
 void verify_begin(ParseJob& j) {
   mlck_ctx* ctx = j.ctx;
   const uint32_t n = j.n;
+  wait_written(ctx, j.blobs, n);
   ctx->results_for(3 * static_cast<size_t>(n));
   MLCK_CUDA(cudaMemsetAsync(ctx->results + 2 * static_cast<size_t>(n), 0, 8 * static_cast<size_t>(n), ctx->stream));
   MLCK_CUDA(cudaEventRecord(ctx->ev_vmain, ctx->stream));  // the records are complete
@@ -788,6 +843,7 @@ void verify_begin(ParseJob& j) {
 
 void walk_records(ParseJob& j) {
   mlck_ctx* ctx = j.ctx;
+  wait_written(ctx, j.blobs, j.n);
   j.out.assign(j.n, Parsed{});
   j.walk_err.assign(j.n, std::string());
   std::vector<uint32_t> idx;
@@ -933,6 +989,10 @@ int mlck_ctx_create(int device, mlck_ctx** out) {
       MLCK_CUDA(cudaEventCreateWithFlags(&c->ev_vside[i], cudaEventDisableTiming));
     }
     MLCK_CUDA(cudaEventCreateWithFlags(&c->ev_vmain, cudaEventDisableTiming));
+    MLCK_CUDA(cudaStreamCreateWithFlags(&c->hstream, cudaStreamNonBlocking));
+    MLCK_CUDA(cudaEventCreateWithFlags(&c->ev_packed_h, cudaEventDisableTiming));
+    MLCK_CUDA(cudaEventCreateWithFlags(&c->ev_hash_last, cudaEventDisableTiming));
+    MLCK_CUDA(cudaMalloc(&c->hresult, 64));
     for (cudaEvent_t* e : {&c->ev_packed, &c->ev_hashed})
       MLCK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (auto& e : c->ev_pushed) MLCK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -976,6 +1036,12 @@ int mlck_ctx_destroy(mlck_ctx* c) {
       if (c->vscratch[i]) cudaFree(c->vscratch[i]);
     }
     cudaEventDestroy(c->ev_vmain);
+    cudaStreamSynchronize(c->hstream);
+    cudaStreamDestroy(c->hstream);
+    cudaEventDestroy(c->ev_packed_h);
+    cudaEventDestroy(c->ev_hash_last);
+    if (c->hscratch) cudaFree(c->hscratch);
+    cudaFree(c->hresult);
     if (c->fnv_scratch) cudaFree(c->fnv_scratch);
     if (c->patch) cudaFree(c->patch);
     cudaFree(c->results);
@@ -987,6 +1053,7 @@ int mlck_ctx_destroy(mlck_ctx* c) {
 
 int mlck_ctx_set_stream(mlck_ctx* c, void* stream) {
   return api([&] {
+    c->join_hash();
     MLCK_CUDA(cudaStreamSynchronize(c->stream));
     c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own;
   });
@@ -994,6 +1061,7 @@ int mlck_ctx_set_stream(mlck_ctx* c, void* stream) {
 int mlck_ctx_synchronize(mlck_ctx* c) {
   return api([&] {
     c->activate();
+    c->join_hash();
     MLCK_CUDA(cudaStreamSynchronize(c->stream));
     c->check_watchdog();
   });
@@ -1021,6 +1089,13 @@ int mlck_ctx_witness_stats(mlck_ctx* c, uint64_t* used, uint64_t* fallbacks) {
   });
 }
 
+int mlck_ctx_set_hash_async(mlck_ctx* c, int on) {
+  return api([&] {
+    c->join_hash();
+    c->hash_async = on != 0;
+  });
+}
+
 int mlck_ctx_set_hash_reserve(mlck_ctx* c, int sms) {
   return api([&] {
     if (sms < 0) throw_invalid("hash reserve must be >= 0 SMs");
@@ -1040,6 +1115,7 @@ int mlck_ctx_timings(mlck_ctx* c, char* labels, uint64_t labels_cap, float* ms, 
                      uint32_t* n) {
   return api([&] {
     c->activate();
+    c->join_hash();
     MLCK_CUDA(cudaStreamSynchronize(c->stream));
     std::string csv;
     const uint32_t cnt = static_cast<uint32_t>(c->timed.size());
@@ -1237,6 +1313,7 @@ int mlck_blob_destroy(mlck_blob* b) {
   return api([&] {
     if (!b) return;
     b->ctx->activate();
+    if (b->written) cudaEventSynchronize(b->written);
     cudaStreamSynchronize(b->ctx->stream);
     if (b->dev) cudaFree(b->dev);
     if (b->witness) cudaFree(b->witness);
@@ -1263,6 +1340,7 @@ int mlck_blob_to_host(const mlck_blob* b, uint8_t* host, uint64_t cap) {
   return api([&] {
     if (cap < b->size) throw_invalid("blob_to_host: buffer too small");
     b->ctx->activate();
+    if (b->written) MLCK_CUDA(cudaStreamWaitEvent(b->ctx->stream, b->written, 0));
     if (b->size)
       ce_copy(host, b->dev, b->size, cudaMemcpyDeviceToHost, b->ctx->stream);
     MLCK_CUDA(cudaStreamSynchronize(b->ctx->stream));
@@ -1337,6 +1415,7 @@ struct File {
 int mlck_blob_save(mlck_blob* b, const char* path, uint64_t* written) {
   return api([&] {
     b->ctx->activate();
+    if (b->written) MLCK_CUDA(cudaStreamWaitEvent(b->ctx->stream, b->written, 0));
     File file(path, "wb");
     if (!file.f) throw_runtime(std::string("persist: cannot open ") + path);
     IoStage io;
@@ -1477,6 +1556,7 @@ int mlck_fastmath_check(mlck_ctx* ctx, uint64_t n_div, uint64_t seed, uint64_t* 
 int mlck_fnv1a64(mlck_ctx* ctx, const void* ptr, uint64_t n, uint64_t seed, uint64_t* out) {
   return api([&] {
     ctx->activate();
+    ctx->join_hash();
     TrailerDsts none{};
     uint32_t* scratch = ctx->fnv_scratch_for(n);
     launch_fnv(static_cast<const uint8_t*>(ptr), n, seed, scratch, ctx->next_epoch(), ctx->results,
@@ -1546,6 +1626,7 @@ int mlck_read_entry(mlck_blob* b, const mlck_entry_info* e, int cb, float* maste
   return api([&] {
     mlck_ctx* ctx = b->ctx;
     ctx->activate();
+    if (b->written) MLCK_CUDA(cudaStreamWaitEvent(ctx->stream, b->written, 0));
     const uint64_t P = e->param_count;
     const uint8_t* src = b->dev + e->payload_offset;
     if (e->mode == 0) {
@@ -2104,6 +2185,7 @@ int mlck_enable_peer_access(mlck_ctx* ctx, int peer) {
 // ------------------------------------------------------------------ timing / memory
 int mlck_event_record(mlck_ctx* ctx, int slot) {
   return api([&] {
+    ctx->join_hash();
     if (slot < 0 || slot >= 16) throw_invalid("event slot out of range");
     MLCK_CUDA(cudaEventRecord(ctx->ev[slot], ctx->stream));
   });
@@ -2123,6 +2205,7 @@ int mlck_device_alloc(mlck_ctx* ctx, uint64_t bytes, void** ptr) {
 int mlck_device_free(mlck_ctx* ctx, void* ptr) {
   return api([&] {
     ctx->activate();
+    ctx->join_hash();
     MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
     MLCK_CUDA(cudaFree(ptr));
   });
@@ -2130,6 +2213,7 @@ int mlck_device_free(mlck_ctx* ctx, void* ptr) {
 int mlck_device_memset(mlck_ctx* ctx, void* ptr, int value, uint64_t bytes) {
   return api([&] {
     ctx->activate();
+    ctx->join_hash();
     MLCK_CUDA(cudaMemsetAsync(ptr, value, bytes, ctx->stream));
   });
 }
@@ -2148,12 +2232,14 @@ int mlck_host_free_pinned(mlck_ctx* ctx, void* ptr) {
 int mlck_memcpy_h2d(mlck_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
   return api([&] {
     ctx->activate();
+    ctx->join_hash();
     MLCK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
   });
 }
 int mlck_memcpy_d2h(mlck_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
   return api([&] {
     ctx->activate();
+    ctx->join_hash();
     MLCK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   });
 }

@@ -186,6 +186,7 @@ def lib():
             "mlck_ctx_set_hash_reserve": (C.c_int, [vp, C.c_int]),
             "mlck_gradlog_capture": (C.c_int, [vp, C.c_uint64, C.c_uint32, vp]),
             "mlck_ctx_set_witness": (C.c_int, [vp, C.c_int]),
+            "mlck_ctx_set_hash_async": (C.c_int, [vp, C.c_int]),
             "mlck_engine_create": (C.c_int, [vp, C.POINTER(EngineConfig), C.POINTER(vp)]),
             "mlck_engine_destroy": (C.c_int, [vp]),
             "mlck_engine_op_count": (C.c_uint32, [vp]),
@@ -291,6 +292,10 @@ class Context:
         u, f = C.c_uint64(), C.c_uint64()
         check(lib().mlck_ctx_witness_stats(self.h, C.byref(u), C.byref(f)))
         return u.value, f.value
+
+    def set_hash_async(self, on: bool):
+        """Trailer hash on a side stream after the pack (default on)."""
+        check(lib().mlck_ctx_set_hash_async(self.h, 1 if on else 0))
 
     def set_hash_reserve(self, sms: int):
         """SMs the hash kernel leaves to co-scheduled work (0 = all SMs)."""
