@@ -488,6 +488,7 @@ def bench_logging(ctx, d, mlck, iterations=3):
     ctx.synchronize()
     base_ms = ctx.event_ms(4, 5)
     host = mlck.UpstreamLog(ctx, cap, kind=0)
+    host.set_async(True)  # the producer does not wait for the copies (it does not reuse src here)
     for mb in range(m):
         host.put(2000, mb, 1, 0, src[mb & 1], entry_floats)
         host.put(2000, mb, 1, 1, src[(mb + 1) & 1], entry_floats)
@@ -496,7 +497,7 @@ def bench_logging(ctx, d, mlck, iterations=3):
     host.sync()
     with_ms = ctx.event_ms(4, 5)
     host.close()
-    out["overlap"] = {"producer": "quantize kernel stream, 16 x 2 GiB HBM", "producer_kernel_ms": base_ms,
+    out["overlap"] = {"producer": "quantize kernel stream, 16 x 2 GiB HBM (log in async mode)", "producer_kernel_ms": base_ms,
                       "with_host_logging_ms": with_ms, "slowdown": with_ms / base_ms - 1}
     dev.close()
     if opened:
@@ -663,6 +664,7 @@ def run_ours(args, d: Dist):
     ctx = mlck.Context(dev)
     ctx.set_hash_async(bool(args.hash_async))
     ctx.set_hash_reserve(args.hash_reserve)
+    ctx.set_convert_overlap(args.convert_overlap)
     wl = pick_workload(args, d.world)
     pcs, cb, W = wl["param_counts"], wl["cb"], wl["W"]
     slots = schedule(wl)
@@ -1009,7 +1011,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-log", action="store_true")
-    ap.add_argument("--hash-async", type=int, default=1, help="trailer hash off the pack's critical path (1/0)")
+    ap.add_argument("--hash-async", type=int, default=0, help="trailer hash off the pack's critical path (1/0)")
+    ap.add_argument("--convert-overlap", type=int, default=0, help="SMs verifying beside the conversion replay")
     ap.add_argument("--hash-reserve", type=int, default=0, help="SMs the hash kernel leaves to the next pack")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the N=1 same-workload leg, gradient-log capture and interference keys")

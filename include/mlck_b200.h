@@ -94,7 +94,7 @@ int mlck_ctx_set_replica_mode(mlck_ctx* ctx, int mode);
  * a snapshot); 0 = all SMs.  The kernel hands chunks out by ticket, so any
  * grid is correct -- this only trades hash throughput for room. */
 int mlck_ctx_set_hash_reserve(mlck_ctx* ctx, int sms);
-/* Asynchronous trailer hash (default on): with replicas in this GPU's HBM
+/* Asynchronous trailer hash (default off): with replicas in this GPU's HBM
  * (transport 0) the FNV kernel of a record runs on a side stream after its
  * pack, so the next snapshot's pack (another blob) starts without waiting
  * for it -- the hash leaves the snapshot's critical path.
@@ -102,6 +102,11 @@ int mlck_ctx_set_hash_reserve(mlck_ctx* ctx, int sms);
  * the next snapshot into the same blob) waits for its hash; synchronize,
  * event_record and the memcpy / memset helpers join all pending hashes. */
 int mlck_ctx_set_hash_async(mlck_ctx* ctx, int on);
+/* Conversion / localized recovery of witnessed records: verify them on
+ * `witness_sms` SMs while the replay runs on the rest (0 = verify first,
+ * then replay; the default).  Errors keep the reference's order either way;
+ * on an error `out`'s operator arrays are unspecified. */
+int mlck_ctx_set_convert_overlap(mlck_ctx* ctx, int witness_sms);
 /* Witnessed verification (default on).  A record the hash kernel writes
  * keeps, beside its blob, the low byte of the FNV state at every 32-byte
  * segment start (3 % of the record).  parse_record / check_coverage /

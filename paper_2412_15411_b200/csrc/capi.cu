@@ -97,7 +97,10 @@ struct mlck_ctx {
   // off the snapshot's critical path, as PAPER.md's overlap intends.  Every
   // reader of a record waits for its `written` event; the raw helpers and
   // synchronize join all hashes (join_hash).
-  bool hash_async = true;
+  bool hash_async = false;
+  // conversion: the records' witnessed verification on `convert_overlap`
+  // SMs beside the replay (0 = verification first, then the replay)
+  int convert_overlap = 0;
   cudaStream_t hstream = nullptr;
   cudaEvent_t ev_packed_h = nullptr, ev_hash_last = nullptr;
   bool hash_pending = false;
@@ -793,6 +796,7 @@ std::string walk_error(const WalkResult& r) {
 //     order: "container truncated" (< 8 bytes), "container checksum
 //     mismatch", then the walk's magic / version / truncation error.
 struct ParseJob {
+  int witness_ctas = 0;  // 0 = one per SM
   mlck_ctx* ctx = nullptr;
   mlck_blob* const* blobs = nullptr;
   uint32_t n = 0;
@@ -826,7 +830,7 @@ void verify_begin(ParseJob& j) {
     if (ctx->witness && b->has_witness()) {  // exact re-hash against the record's witness (fnv.cuh)
       const int tf = ctx->tbegin("fnv_witness", st);
       launch_fnv_witness(b->dev, b->size - 8, kFnvOffset, b->witness, scratch, ctx->results + k,
-                         ctx->results + 2 * static_cast<size_t>(n) + k, st);
+                         ctx->results + 2 * static_cast<size_t>(n) + k, st, j.witness_ctas);
       ctx->tend(tf, st);
       ctx->witness_used += 1;
     } else {
@@ -1086,6 +1090,13 @@ int mlck_ctx_witness_stats(mlck_ctx* c, uint64_t* used, uint64_t* fallbacks) {
   return api([&] {
     if (used) *used = c->witness_used;
     if (fallbacks) *fallbacks = c->witness_fallbacks;
+  });
+}
+
+int mlck_ctx_set_convert_overlap(mlck_ctx* c, int witness_sms) {
+  return api([&] {
+    if (witness_sms < 0) throw_invalid("convert overlap: SM count must be >= 0");
+    c->convert_overlap = witness_sms;
   });
 }
 
@@ -1879,6 +1890,10 @@ void convert_impl(mlck_state* out, mlck_blob* const* blobs, uint32_t n_blobs, ui
   job.n = n_parse;
   job.cb = out->cb;
   walk_records(job);
+  // the witnessed verification can run on a few SMs beside the replay
+  bool all_witnessed = ctx->witness && ctx->convert_overlap > 0;
+  for (uint32_t k = 0; k < n_parse && all_witnessed; ++k) all_witnessed = blobs[k]->has_witness();
+  if (all_witnessed) job.witness_ctas = ctx->convert_overlap;
   verify_begin(job);
   bool verified = false;
   auto parse_errors = [&] {  // recovery.hpp:163-171
@@ -1970,8 +1985,13 @@ void convert_impl(mlck_state* out, mlck_blob* const* blobs, uint32_t n_blobs, ui
     new_step[id] = stp;
     ops.push_back(c);
   }
-  parse_errors();
-  run_replay(ctx, ops, gptr, bc, o, out->cb);
+  if (all_witnessed) {  // replay beside the verification; its errors still come first
+    run_replay(ctx, ops, gptr, bc, o, out->cb);
+    parse_errors();
+  } else {
+    parse_errors();
+    run_replay(ctx, ops, gptr, bc, o, out->cb);
+  }
   for (uint32_t id = 0; id < out->n_ops; ++id)
     if (in_scope(id)) {
       out->present[id] = src[id].slot >= 0 ? 1 : 0;

@@ -739,7 +739,7 @@ void launch_fnv_empty(uint64_t seed, unsigned long long* result, const TrailerDs
 }
 
 void launch_fnv_witness(const uint8_t* data, uint64_t n, uint64_t seed, const uint32_t* witness, uint32_t* scratch,
-                        unsigned long long* result, unsigned long long* bad, cudaStream_t stream) {
+                        unsigned long long* result, unsigned long long* bad, cudaStream_t stream, int ctas) {
   MLCK_CUDA(cudaMemsetAsync(scratch, 0, 32, stream));
   MLCK_CUDA(cudaMemsetAsync(bad, 0, 8, stream));
   if (n == 0) {
@@ -760,7 +760,7 @@ void launch_fnv_witness(const uint8_t* data, uint64_t n, uint64_t seed, const ui
   scr.accum = reinterpret_cast<unsigned long long*>(scratch + 4);
   scr.result = result;
   const int64_t n_chunks = static_cast<int64_t>(fnv_chunks(n));
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_chunks, sms));
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_chunks, ctas > 0 ? std::min(ctas, sms) : sms));
   fnv_witness_kernel<<<grid, fnv::kComputeThreads, sizeof(WitnessSmem), stream>>>(data, n, seed, witness, scr, bad,
                                                                                   n_chunks);
   MLCK_CUDA(cudaGetLastError());

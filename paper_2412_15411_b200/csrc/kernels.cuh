@@ -68,7 +68,7 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
 // 128-byte row); *bad = 1 when the witness does not match the bytes (the
 // caller then hashes with launch_fnv).  scratch as launch_fnv's.
 void launch_fnv_witness(const uint8_t* data, uint64_t n, uint64_t seed, const uint32_t* witness, uint32_t* scratch,
-                        unsigned long long* result, unsigned long long* bad, cudaStream_t stream);
+                        unsigned long long* result, unsigned long long* bad, cudaStream_t stream, int ctas = 0);
 inline uint64_t fnv_witness_words(uint64_t n) { return (n + 127) / 128; }
 // Copy `bytes` from src to every dst with `ctas` CTAs of one SM each.
 void launch_push(const uint8_t* src, uint64_t bytes, const pack::Dsts& d, int ctas, cudaStream_t stream);

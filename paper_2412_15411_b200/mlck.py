@@ -187,6 +187,7 @@ def lib():
             "mlck_gradlog_capture": (C.c_int, [vp, C.c_uint64, C.c_uint32, vp]),
             "mlck_ctx_set_witness": (C.c_int, [vp, C.c_int]),
             "mlck_ctx_set_hash_async": (C.c_int, [vp, C.c_int]),
+            "mlck_ctx_set_convert_overlap": (C.c_int, [vp, C.c_int]),
             "mlck_engine_create": (C.c_int, [vp, C.POINTER(EngineConfig), C.POINTER(vp)]),
             "mlck_engine_destroy": (C.c_int, [vp]),
             "mlck_engine_op_count": (C.c_uint32, [vp]),
@@ -293,8 +294,12 @@ class Context:
         check(lib().mlck_ctx_witness_stats(self.h, C.byref(u), C.byref(f)))
         return u.value, f.value
 
+    def set_convert_overlap(self, witness_sms: int):
+        """Witnessed verification on `witness_sms` SMs beside the conversion replay (0 = sequential)."""
+        check(lib().mlck_ctx_set_convert_overlap(self.h, witness_sms))
+
     def set_hash_async(self, on: bool):
-        """Trailer hash on a side stream after the pack (default on)."""
+        """Trailer hash on a side stream after the pack (default off)."""
         check(lib().mlck_ctx_set_hash_async(self.h, 1 if on else 0))
 
     def set_hash_reserve(self, sms: int):

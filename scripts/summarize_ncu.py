@@ -13,7 +13,7 @@ import sys
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OUT = os.path.join(ROOT, "gpurun_out")
+OUT = os.environ.get("NCU_OUT") or os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 
 METRICS = [
@@ -71,7 +71,7 @@ def main():
     if os.path.exists(os.path.join(OUT, "launches.csv")):
         summary["launch_list"] = launch_shares(os.path.join(OUT, "launches.csv"))
     kernels = {}
-    for k in ("fnv_kernel", "pack_kernel", "replay_kernel"):
+    for k in ("fnv_kernel", "pack_kernel", "replay_kernel", "fnv_witness_kernel", "scope_kernel"):
         rep = os.path.join(OUT, f"prof_{k}.ncu-rep")
         if os.path.exists(rep):
             m = raw_metrics(rep)
@@ -87,7 +87,7 @@ def main():
     with open(os.path.join(PROF, f"{rnd}_ncu_summary.json"), "w") as fh:
         json.dump(summary, fh, indent=1, default=str)
     lines = [f"# ncu summary ({rnd})", "",
-             "Command: `python bench.py --steps 2 --warmup 3 --no-cpu` (scripts/profile.sh); "
+             "Command: `python bench.py --steps 2 --warmup 3 --no-cpu --no-extras` (scripts/profile.sh); "
              "launch list = `--metrics gpu__time_duration.sum --clock-control none` (cold-cache, serialised); "
              "full captures = `--set full --clock-control none`, one launch each.", "",
              "## Launch list: share of device time", "", "| kernel | launches | total ms | share |",
