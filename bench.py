@@ -665,6 +665,8 @@ def run_ours(args, d: Dist):
     ctx.set_hash_async(bool(args.hash_async))
     ctx.set_hash_reserve(args.hash_reserve)
     ctx.set_convert_overlap(args.convert_overlap)
+    if args.replica_mode != -1:
+        ctx.set_replica_mode(args.replica_mode)
     wl = pick_workload(args, d.world)
     pcs, cb, W = wl["param_counts"], wl["cb"], wl["W"]
     slots = schedule(wl)
@@ -1013,6 +1015,7 @@ def main():
     ap.add_argument("--no-log", action="store_true")
     ap.add_argument("--hash-async", type=int, default=0, help="trailer hash off the pack's critical path (1/0)")
     ap.add_argument("--convert-overlap", type=int, default=0, help="SMs verifying beside the conversion replay")
+    ap.add_argument("--replica-mode", type=int, default=-1, help="snapshot transport (-1 auto, 0-6)")
     ap.add_argument("--hash-reserve", type=int, default=0, help="SMs the hash kernel leaves to the next pack")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the N=1 same-workload leg, gradient-log capture and interference keys")

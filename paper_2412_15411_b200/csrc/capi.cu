@@ -651,8 +651,8 @@ cudaStream_t run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, boo
   }
   const int tp = ctx->tbegin("pack");
   launch_pack(segs, n_segs, body, d, ctx->stream);
-  ctx->tend(tp);
   ctx->launches += body ? 1 : 0;
+  ctx->tend(tp);
   if (!trailer) return ctx->stream;
   TrailerDsts t{};
   for (int r = 0; r < d.n; ++r) t.p[r] = d.p[r] + body;
@@ -1808,15 +1808,17 @@ void run_replay(mlck_ctx* ctx, std::vector<adam::ConvOp>& ops, const std::vector
   const size_t ob = ops.size() * sizeof(adam::ConvOp);
   const size_t go = align_up(ob, 16), gb = gptr.size() * sizeof(float*);
   const size_t bo = align_up(go + gb, 16), bb = bc.size() * sizeof(float2);
-  auto& s = ctx->stage_for(bo + bb + 16);
+  const size_t so = align_up(bo + bb, 16), sb = bc.size() * sizeof(adam::StepConst);
+  auto& s = ctx->stage_for(so + sb + 16);  // the StepConst table is filled on the device
   std::memcpy(s.host, ops.data(), ob);
   std::memcpy(s.host + go, gptr.data(), gb);
   std::memcpy(s.host + bo, bc.data(), bb);
   ctx->stage_upload(s, bo + bb);
   const int tr = ctx->tbegin("replay");
   launch_replay(reinterpret_cast<const adam::ConvOp*>(s.dev), static_cast<int>(ops.size()),
-                reinterpret_cast<const float* const*>(s.dev + go),
-                reinterpret_cast<const float2*>(s.dev + bo), o, cb, units, ctx->stream);
+                reinterpret_cast<const float* const*>(s.dev + go), reinterpret_cast<const float2*>(s.dev + bo),
+                static_cast<uint32_t>(bc.size()), reinterpret_cast<adam::StepConst*>(s.dev + so), o, cb, units,
+                ctx->stream);
   ctx->tend(tr);
   ctx->launches += units ? 1 : 0;
 }

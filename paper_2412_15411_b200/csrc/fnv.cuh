@@ -828,12 +828,7 @@ __device__ __forceinline__ uint32_t automaton_and_ends(uint32_t (&w)[kThreadWord
 // low byte), so the sum is exactly FNV-1a-64 of the bytes now in memory;
 // if one fails (a stale witness, bytes changed) the caller hashes the
 // record with fnv_kernel.  Either way the result is the exact hash.
-struct WitnessShared {
-  uint4 data[kComputeThreads * kGranules];  // the chunk, rows in the granule swizzle
-  uint2 wfrag[2][4][32];
-  unsigned long long kpos[32][4];
-  unsigned long long red[kComputeWarps];
-};
+// (fnv_witness_kernel in kernels.cu)
 #endif
 
 __device__ __forceinline__ void read_thread_unaligned(const Shared& sh, int slot, int t, uint32_t ph,

@@ -439,77 +439,89 @@ __global__ void __launch_bounds__(fnv::kThreads, 1)
   }
 }
 
-// Re-hash of a record against its witness (fnv.cuh, WitnessShared).
-// Persistent: one CTA per SM walks chunks blockIdx.x, +gridDim.x, ... with
-// the next chunk's rows in flight (cp.async into the other buffer) while the
-// current one is hashed; rows are thread-private, so warps only meet at the
-// tensor-core passes (__syncwarp).  *bad <- 1 when a witnessed start
-// disagrees with the automaton (the caller then runs fnv_kernel).
+// The thread's own row from global bytes, zeros past n (the record's last,
+// partial row and rows past the end -- the tensor map covers full rows only).
+__device__ __forceinline__ void witness_row_bytes(uint4* rows, int tid, const uint8_t* data, uint64_t n, uint64_t p) {
+  using namespace fnv;
+  for (int q = 0; q < kGranules; ++q) {
+    uint32_t v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t x = 0;
+      for (int b = 0; b < 4; ++b) {
+        const uint64_t o = p + 16 * q + 4 * i + b;
+        x |= (o < n ? static_cast<uint32_t>(data[o]) : 0u) << (8 * b);
+      }
+      v[i] = x;
+    }
+    rows[granule(tid, q)] = make_uint4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+constexpr int kWitnessBufs = 3;  // chunks in flight per SM
+struct WitnessSmem {
+  uint4 data[kWitnessBufs][fnv::kComputeThreads * fnv::kGranules];  // 1 KiB-aligned rows (TMA swizzle)
+  uint2 wfrag[2][4][32];
+  unsigned long long kpos[32][4];
+  unsigned long long red[fnv::kComputeWarps];
+  unsigned long long mbar[kWitnessBufs];
+};
+constexpr size_t kWitnessSmem = sizeof(WitnessSmem) + 1024;
+
+// One chunk's full rows into buffer b by the tensor map (two 256-row boxes,
+// one mbarrier phase); rows at or past rows_full are the threads'.
+__device__ __forceinline__ void witness_tma_chunk(WitnessSmem& sh, int b, const CUtensorMap* map, int64_t chunk,
+                                                  uint64_t rows_full) {
+  using namespace fnv;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const uint64_t row0 = static_cast<uint64_t>(chunk) * kComputeThreads;
+  int boxes = 0;
+#pragma unroll
+  for (int x = 0; x < kComputeThreads / kTmaBoxRows; ++x) boxes += row0 + kTmaBoxRows * x < rows_full;
+  mbar_arrive_expect_tx(&sh.mbar[b], boxes * kTmaBoxRows * kThreadBytes);
+  for (int x = 0; x < boxes; ++x)
+    tma_load_rows(&sh.data[b][kGranules * kTmaBoxRows * x], map, static_cast<int32_t>(row0 + kTmaBoxRows * x),
+                  &sh.mbar[b]);
+}
+
+// Re-hash of a record against its witness (fnv.cuh, automaton_and_ends).
+// Persistent: one CTA per SM walks chunks blockIdx.x, +gridDim.x, ...; a
+// thread issues the tensor-map loads of the chunks three turns ahead, so
+// the compute warps only read shared memory.  *bad <- 1 when a witnessed
+// start disagrees with the automaton (the caller then runs fnv_kernel).
 __device__ uint2 g_wfrag[2][4][32];             // mma_pass B fragments (init_constants)
 __device__ unsigned long long g_kpos[32][4];    // mma_epilogue weights
 __constant__ unsigned long long c_pinv_warp[fnv::kComputeWarps];  // P^-(4096 (w + 1))
 
-__device__ __forceinline__ void witness_load_row(uint4* rows, int tid, const uint8_t* data, uint64_t n, uint64_t p) {
-  using namespace fnv;
-  if (p + kThreadBytes <= n) {
-#pragma unroll
-    for (int q = 0; q < kGranules; ++q) cp_async16(&rows[granule(tid, q)], data + p + 16 * q);
-  } else {  // the record's last, partial row (zeros past n add nothing), or past the end
-    for (int q = 0; q < kGranules; ++q) {
-      uint32_t v[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        uint32_t x = 0;
-        for (int b = 0; b < 4; ++b) {
-          const uint64_t o = p + 16 * q + 4 * i + b;
-          x |= (o < n ? static_cast<uint32_t>(data[o]) : 0u) << (8 * b);
-        }
-        v[i] = x;
-      }
-      rows[granule(tid, q)] = make_uint4(v[0], v[1], v[2], v[3]);
-    }
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-constexpr int kWitnessBufs = 3;  // chunks in flight per SM (load ~2x the hash time of one)
-struct WitnessSmem {
-  uint4 data[kWitnessBufs][fnv::kComputeThreads * fnv::kGranules];
-  uint2 wfrag[2][4][32];
-  unsigned long long kpos[32][4];
-  unsigned long long red[fnv::kComputeWarps];
-};
-
 __global__ void __launch_bounds__(fnv::kComputeThreads, 1)
     fnv_witness_kernel(const uint8_t* data, uint64_t n, uint64_t seed, const uint32_t* witness, fnv::Scratch scr,
-                       unsigned long long* bad, int64_t n_chunks) {
+                       unsigned long long* bad, int64_t n_chunks, const __grid_constant__ CUtensorMap tmap,
+                       uint64_t rows_full) {
   using namespace fnv;
-  extern __shared__ __align__(16) unsigned char smem_w[];
-  WitnessSmem& sh = *reinterpret_cast<WitnessSmem*>(smem_w);
+  extern __shared__ __align__(1024) unsigned char smem_w[];
+  WitnessSmem& sh = *reinterpret_cast<WitnessSmem*>(smem_w + ((1024u - (smem_addr(smem_w) & 1023u)) & 1023u));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t n_seg = (n + 31) / 32;
+  const int64_t G = gridDim.x;
   if (tid < 2 * 4 * 32) (&sh.wfrag[0][0][0])[tid] = (&g_wfrag[0][0][0])[tid];
   if (tid < 32 * 4) (&sh.kpos[0][0])[tid] = (&g_kpos[0][0])[tid];
+  if (tid == 0)
+    for (int b = 0; b < kWitnessBufs; ++b) mbar_init(&sh.mbar[b], 1);
   const uint64_t pinv_w = c_pinv_warp[warp];
+  __syncthreads();  // tables, barriers
   int64_t chunk = blockIdx.x;
-#pragma unroll
-  for (int b = 0; b < kWitnessBufs - 1; ++b) {  // the first chunks' rows in flight
-    const int64_t c = chunk + b * static_cast<int64_t>(gridDim.x);
-    if (c < n_chunks)
-      witness_load_row(sh.data[b], tid, data, n, (static_cast<uint64_t>(c) * kComputeThreads + tid) * kThreadBytes);
-    else
-      asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  __syncthreads();  // tables
+  if (tid == 0)
+    for (int b = 0; b < kWitnessBufs; ++b)
+      if (chunk + b * G < n_chunks) witness_tma_chunk(sh, b, &tmap, chunk + b * G, rows_full);
   uint64_t acc = 0;
   bool ok = true;
-  for (int buf = 0; chunk < n_chunks; chunk += gridDim.x, buf = buf + 1 == kWitnessBufs ? 0 : buf + 1) {
-    const int64_t nx = chunk + (kWitnessBufs - 1) * static_cast<int64_t>(gridDim.x);
-    const int nb = buf == 0 ? kWitnessBufs - 1 : buf - 1;  // the buffer hashed last turn
-    if (nx < n_chunks)  // later chunks' rows land while this one is hashed
-      witness_load_row(sh.data[nb], tid, data, n, (static_cast<uint64_t>(nx) * kComputeThreads + tid) * kThreadBytes);
-    else
-      asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int i = 0, buf = 0; chunk < n_chunks; ++i, chunk += G, buf = buf + 1 == kWitnessBufs ? 0 : buf + 1) {
+    if (i > 0) {  // every thread is done with last turn's buffer: refill it three chunks on
+      __syncthreads();
+      const int pb = buf == 0 ? kWitnessBufs - 1 : buf - 1;
+      const int64_t nx = chunk + (kWitnessBufs - 1) * G;
+      if (tid == 0 && nx < n_chunks) witness_tma_chunk(sh, pb, &tmap, nx, rows_full);
+    }
     const uint64_t row = static_cast<uint64_t>(chunk) * kComputeThreads + tid;
     uint32_t st = 0, expect = 0, check = 0;
     if (row * kThreadBytes < n) {
@@ -518,12 +530,13 @@ __global__ void __launch_bounds__(fnv::kComputeThreads, 1)
       const uint32_t next = seg0 + 4 < n_seg ? (__ldg(witness + row + 1) & 0xffu) : 0u;
       expect = (st >> 8) | (next << 24);  // segment i ends where segment i+1 starts
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (seg0 + i + 1 < n_seg) check |= 0xffu << (8 * i);
+      for (int q = 0; q < 4; ++q)
+        if (seg0 + q + 1 < n_seg) check |= 0xffu << (8 * q);
       if (row == 0 && (st & 0xffu) != (seed & 0xffu)) ok = false;
     }
-    asm volatile("cp.async.wait_group %0;" ::"n"(kWitnessBufs - 1) : "memory");  // this chunk's rows (own copies)
     uint4* rows = sh.data[buf];
+    mbar_wait(&sh.mbar[buf], static_cast<uint32_t>(i / kWitnessBufs) & 1u);
+    if (row >= rows_full) witness_row_bytes(rows, tid, data, n, row * kThreadBytes);
     uint32_t w[kThreadWords];
     read_thread_rows(rows, tid, w);
     interleave(w);
@@ -538,9 +551,7 @@ __global__ void __launch_bounds__(fnv::kComputeThreads, 1)
     __syncwarp();
     mma_pass_rows(rows, sh.wfrag, warp, lane, 1, mac);  // the u & b vector, weights -2 P^(...)
     acc += mma_epilogue(sh, lane, mac) * (pinv_w * chunk_weight(chunk));
-    __syncwarp();  // the buffer is refilled two chunks on
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
   if (__any_sync(0xffffffffu, !ok) && lane == 0) atomicExch(bad, 1ull);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -611,6 +622,34 @@ size_t fnv_scratch_words(uint64_t n) { return (256 + fnv_chunks(n) * fnv::kStatu
 uint64_t fnv_chunk_bytes() { return fnv::kChunk; }
 uint32_t fnv_sticky_word() { return 8; }
 
+// The bytes [data, data + n) as a [n / 128 rows x 128 bytes] tensor map (the
+// full rows only), 256-row boxes landing in the 128-byte swizzle the FNV
+// kernels' shared-memory rows use.  False when the TMA cannot serve it.
+bool make_row_tmap(const uint8_t* data, uint64_t n, CUtensorMap* tmap) {
+  std::memset(tmap, 0, sizeof(*tmap));
+  const uint64_t rows = n / fnv::kThreadBytes;
+  if (rows == 0 || (reinterpret_cast<uintptr_t>(data) & 15u) != 0 || rows >= (1ull << 31)) return false;
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q{};
+    MLCK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,
+                                      &q));
+    if (q != cudaDriverEntryPointSuccess || !encode) throw Error(kCuda, "cuTensorMapEncodeTiled unavailable");
+  }
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(fnv::kThreadBytes), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(fnv::kThreadBytes)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(fnv::kThreadBytes), static_cast<cuuint32_t>(fnv::kTmaBoxRows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(data), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(kCuda, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return true;
+}
+
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
                 unsigned long long* prof, unsigned long long* trace, const FnvGather* gather,
@@ -670,30 +709,7 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
   // the record as a [n / 128 rows x 128 bytes] tensor, loaded in 256-row
   // boxes in the 128-byte swizzle the shared-memory rows use
   CUtensorMap tmap;
-  std::memset(&tmap, 0, sizeof(tmap));
-  int use_tma = 0;
-  const uint64_t rows = n / fnv::kThreadBytes;
-  if (!gather && rows > 0 && (reinterpret_cast<uintptr_t>(data) & 15u) == 0 && rows < (1ull << 31)) {
-    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static Encode encode = nullptr;
-    if (!encode) {
-      cudaDriverEntryPointQueryResult q{};
-      MLCK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode),
-                                        cudaEnableDefault, &q));
-      if (q != cudaDriverEntryPointSuccess || !encode) throw Error(kCuda, "cuTensorMapEncodeTiled unavailable");
-    }
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(fnv::kThreadBytes), static_cast<cuuint64_t>(rows)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(fnv::kThreadBytes)};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(fnv::kThreadBytes), static_cast<cuuint32_t>(fnv::kTmaBoxRows)};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(data), dims, strides,
-                              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw Error(kCuda, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
-    use_tma = 1;
-  }
+  const int use_tma = !gather && make_row_tmap(data, n, &tmap) ? 1 : 0;
   const bool pf = prof || trace;
   auto k = gather ? (pf ? fnv_kernel<true, true> : fnv_kernel<false, true>)
                   : (pf ? fnv_kernel<true, false> : fnv_kernel<false, false>);
@@ -752,17 +768,19 @@ void launch_fnv_witness(const uint8_t* data, uint64_t n, uint64_t seed, const ui
   int& sms = sms_of[dev & 63];
   if (!sms) {
     MLCK_CUDA(cudaFuncSetAttribute(fnv_witness_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(sizeof(WitnessSmem))));
+                                   static_cast<int>(kWitnessSmem)));
     MLCK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
+  CUtensorMap tmap;
+  const uint64_t rows_full = make_row_tmap(data, n, &tmap) ? n / fnv::kThreadBytes : 0;
   fnv::Scratch scr{};
   scr.finished = scratch + 2;
   scr.accum = reinterpret_cast<unsigned long long*>(scratch + 4);
   scr.result = result;
   const int64_t n_chunks = static_cast<int64_t>(fnv_chunks(n));
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_chunks, ctas > 0 ? std::min(ctas, sms) : sms));
-  fnv_witness_kernel<<<grid, fnv::kComputeThreads, sizeof(WitnessSmem), stream>>>(data, n, seed, witness, scr, bad,
-                                                                                  n_chunks);
+  fnv_witness_kernel<<<grid, fnv::kComputeThreads, kWitnessSmem, stream>>>(data, n, seed, witness, scr, bad,
+                                                                           n_chunks, tmap, rows_full);
   MLCK_CUDA(cudaGetLastError());
 }
 
@@ -864,12 +882,16 @@ void launch_walk(const WalkJob* jobs, int n_jobs, cudaStream_t stream) {
 }
 
 // ---------------------------------------------------------------- replay (K3)
-void launch_replay(const adam::ConvOp* ops, int n_ops, const float* const* gptr, const float2* bc,
-                   const adam::Opt& o, int cb, uint64_t total_units, cudaStream_t stream) {
+void launch_replay(const adam::ConvOp* ops, int n_ops, const float* const* gptr, const float2* bc, uint32_t n_bc,
+                   adam::StepConst* steps, const adam::Opt& o, int cb, uint64_t total_units, cudaStream_t stream) {
   if (total_units == 0) return;
+  if (n_bc) {
+    adam::replay_steps_kernel<<<(n_bc + 127) / 128, 128, 0, stream>>>(bc, steps, n_bc);
+    MLCK_CUDA(cudaGetLastError());
+  }
   const uint64_t blocks = total_units;  // total_units counts CTAs (run_replay)
-  adam::replay_kernel<<<static_cast<unsigned>(blocks), adam::kReplayThreads, 0, stream>>>(ops, n_ops, gptr, bc, o,
-                                                                                        cb, total_units);
+  adam::replay_kernel<<<static_cast<unsigned>(blocks), adam::kReplayThreads, 0, stream>>>(ops, n_ops, gptr, bc, steps,
+                                                                                        o, cb, total_units);
   MLCK_CUDA(cudaGetLastError());
 }
 

@@ -78,8 +78,10 @@ void launch_fnv_empty(uint64_t seed, unsigned long long* result, const TrailerDs
 void launch_pack(const pack::Segment* segs, int n_segs, uint64_t total, const pack::Dsts& d,
                  cudaStream_t stream, uint64_t lo = 0);
 void launch_walk(const WalkJob* jobs, int n_jobs, cudaStream_t stream);
-void launch_replay(const adam::ConvOp* ops, int n_ops, const float* const* gptr, const float2* bc,
-                   const adam::Opt& o, int cb, uint64_t total_units, cudaStream_t stream);
+// (bc: the host's bias corrections per (operator, step); steps: device
+// scratch of n_bc StepConst the launch fills first)
+void launch_replay(const adam::ConvOp* ops, int n_ops, const float* const* gptr, const float2* bc, uint32_t n_bc,
+                   adam::StepConst* steps, const adam::Opt& o, int cb, uint64_t total_units, cudaStream_t stream);
 // Threads per replay CTA (launch_replay's total_units counts CTAs: each
 // operator's 4-element units round up to whole CTAs).
 int replay_cta_threads();

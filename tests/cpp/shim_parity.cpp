@@ -227,6 +227,36 @@ int main(int argc, char** argv) {
     const auto want = run.serialize_state();
     std::cout << "ENGINE recompute " << (a.serialize_state() == want) << " logged " << (b.serialize_state() == want)
               << " log_entries " << blog.size() << "\n";
+    // localized_recover(engine, RecoverySegment, ckpt, logs, target) for the
+    // middle stage, boundary entries from the trainer's own log
+    ModelSpec ms;
+    ms.layers = 3;
+    ms.experts_per_layer = 4;
+    ms.token_dim = 4;
+    ParallelPlan pp;
+    pp.pp_stages = 3;
+    pp.dp_degree = 1;
+    pp.microbatches = 2;
+    pp.microbatch_size = 4;
+    const std::vector<int32_t> sop = stage_of_ops(ms, pp);
+    RecoverySegment seg;
+    seg.stage_lo = seg.stage_hi = 1;
+    DeviceState rec(ctx, P, static_cast<int>(cb));
+    const LocalizedRecoveryResult lr =
+        localized_recover(rec, seg, win, blog, &g2, sop, pp, data_seed, ws2 + W, oc);
+    bool same = lr.iteration == ws2 + W && !lr.ops.empty();
+    for (const auto& [id, op] : lr.ops) {
+      const OperatorState want_op = run.op(id);
+      same = same && op.step == want_op.step && op.master == want_op.master && op.m == want_op.m && op.v == want_op.v;
+    }
+    std::cout << "SEGMENT ops " << lr.ops.size() << " same " << same << "\n";
+    UpstreamLog empty_log(ctx, 1 << 16);
+    try {
+      DeviceState rec2(ctx, P, static_cast<int>(cb));
+      (void)localized_recover(rec2, seg, win, empty_log, &g2, sop, pp, data_seed, ws2 + W, oc);
+    } catch (const std::runtime_error& e) {
+      std::cout << "ERR runtime_error: " << e.what() << "\n";
+    }
   }
   std::cout << "OK\n";
   return 0;

@@ -81,5 +81,7 @@ def test_cpp_shim_window_matches_reference(tmp_path, reference, name, w):
     assert "LOGBYTES 38654705664" in out
     if name == "verify_toy":  # the GPU trainer as the gradient source: both conversions exact
         assert "ENGINE recompute 1 logged 1 log_entries " in out
+        assert "SEGMENT ops 6 same 1" in out  # stage 1 of 3: one layer's 4 experts + NE + gate
+        assert "ERR runtime_error: upstream log missing entry: iteration " in out
     assert "ERR invalid_argument: upstream log budget exceeded: need 38654705664 bytes of host memory, " \
            "budget 1000000000" in out

@@ -1,4 +1,4 @@
-"""Witnessed re-verification (mlck_ctx_set_witness, fnv.cuh WitnessShared):
+"""Witnessed re-verification (mlck_ctx_set_witness, fnv.cuh automaton_and_ends, kernels.cu fnv_witness_kernel):
 a record the hash kernel wrote keeps its segment starts, and parse_record /
 check_coverage / conversion re-hash it against them.  The checksum must be
 the exact FNV-1a-64 of the bytes in memory whatever happened to the record
