@@ -360,8 +360,13 @@ __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t se
 // Persistent CTAs (one per SM, kSlots chunks in flight each).  The CTA that
 // finishes last combines the terms and writes the trailer (serialize_record
 // appends the checksum, snapshot.hpp:142).
+#ifdef MLCK_FNV_MAXREG
+#define MLCK_FNV_BOUNDS __maxnreg__(MLCK_FNV_MAXREG)
+#else
+#define MLCK_FNV_BOUNDS __launch_bounds__(fnv::kThreads, 1)
+#endif
 template <bool kProf, bool kGather>
-__global__ void __launch_bounds__(fnv::kThreads, 1)
+__global__ void MLCK_FNV_BOUNDS
     fnv_kernel(const uint8_t* data, uint64_t n, uint64_t seed, fnv::Scratch scr, int64_t n_chunks,
                TrailerDsts trailer, fnv::Gather gth, const __grid_constant__ CUtensorMap tmap, int use_tma) {
   using namespace fnv;
