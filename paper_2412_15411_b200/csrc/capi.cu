@@ -418,6 +418,101 @@ struct SegmentBuilder {
   }
 };
 
+// ---- fused snapshot plan (replica mode 2) --------------------------------
+// The allocation holding p (driver: cuMemGetAddressRange); false when the
+// pointer is not device memory the driver knows.
+bool alloc_range(const void* p, uint64_t* base, uint64_t* bytes) {
+  using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static Fn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", reinterpret_cast<void**>(&fn), cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    cudaGetLastError();
+    if (!fn) return false;
+  }
+  CUdeviceptr b = 0;
+  size_t n = 0;
+  if (fn(&b, &n, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return false;
+  *base = static_cast<uint64_t>(b);
+  *bytes = static_cast<uint64_t>(n);
+  return true;
+}
+
+struct FusedPlan {
+  std::vector<std::pair<uint64_t, uint64_t>> src;  // source allocations (base, bytes); the patch map follows
+  std::vector<FnvRun> runs;
+  std::vector<int64_t> patch;  // chunks gathered whole into the patch buffer
+};
+
+// Record chunks as runs of whole chunks inside one payload span (loaded by
+// TMA from the span's allocation, shifted by the span's misalignment
+// against the record's rows) and single patch chunks (everything else: the
+// headers, entry boundaries, the record's partial last chunk).  False when
+// the record does not suit the fused kernel (too many allocations or mostly
+// patch chunks): the caller packs instead.
+bool plan_fused(const SegmentBuilder& b, uint64_t body, FusedPlan* fp) {
+  const uint64_t cb = fnv_chunk_bytes(), n_chunks = fnv_chunks(body);
+  const uint64_t win = cb + 128;  // the rows a shifted chunk lands
+  size_t k = 0;
+  for (uint64_t c = 0; c < n_chunks;) {
+    const uint64_t lo = c * cb;
+    while (k + 1 < b.segs.size() && b.segs[k].dst + b.segs[k].len <= lo) ++k;
+    const pack::Segment& g = b.segs[k];
+    // whole chunks of the span from c on (the last chunk of the record is partial: patch)
+    uint64_t c_end = std::min((g.dst + g.len) / cb, body / cb);
+    int map = -1;
+    uint64_t off = 0;
+    if (!b.is_meta[k] && g.dst <= lo && c_end > c) {
+      const uint64_t src = reinterpret_cast<uint64_t>(g.src) + (lo - g.dst);
+      for (size_t m = 0; m < fp->src.size() && map < 0; ++m)
+        if (src >= fp->src[m].first && src < fp->src[m].first + fp->src[m].second) map = static_cast<int>(m);
+      if (map < 0) {
+        uint64_t base = 0, bytes = 0;
+        if (alloc_range(g.src, &base, &bytes) && base % 16 == 0 && src >= base && src < base + bytes) {
+          if (fp->src.size() + 1 >= static_cast<size_t>(kFnvMaxSrc)) return false;
+          fp->src.emplace_back(base, bytes);
+          map = static_cast<int>(fp->src.size()) - 1;
+        }
+      }
+      if (map >= 0) {
+        off = src - fp->src[map].first;
+        // every chunk's window (512 rows + the overhang row) inside the allocation's rows
+        const uint64_t rows_end = fp->src[map].second / 128 * 128;
+        while (c_end > c && off + (c_end - 1 - c) * cb + win > rows_end) --c_end;
+        if (c_end == c) map = -1;
+      }
+    }
+    if (map >= 0) {
+      fp->runs.push_back(FnvRun{static_cast<int64_t>(c), static_cast<int64_t>(c_end),
+                                static_cast<int64_t>(off / 128), map, static_cast<int32_t>(off % 128)});
+      c = c_end;
+    } else {
+      fp->patch.push_back(static_cast<int64_t>(c));
+      ++c;
+    }
+  }
+  const int patch_map = static_cast<int>(fp->src.size());
+  // patch chunks as one-chunk runs of the patch map, merged in chunk order
+  std::vector<FnvRun> all;
+  all.reserve(fp->runs.size() + fp->patch.size());
+  size_t r = 0;
+  for (size_t j = 0; j < fp->patch.size(); ++j) {
+    while (r < fp->runs.size() && fp->runs[r].c0 < fp->patch[j]) all.push_back(fp->runs[r++]);
+    all.push_back(FnvRun{fp->patch[j], fp->patch[j] + 1, static_cast<int64_t>(j * (cb / 128)), patch_map, 0});
+  }
+  while (r < fp->runs.size()) all.push_back(fp->runs[r++]);
+  fp->runs.swap(all);
+  return fp->patch.size() * 4 <= n_chunks + 4;
+}
+
+bool fused_mode(const mlck_ctx* ctx, const mlck_blob* out) {
+  (void)out;
+  return ctx->replica_mode == 2;
+}
+
 // Uploads the segment table + meta, launches pack (and the FNV trailer when
 // `trailer`): the blob body is [0, builder.pos), the trailer at pos.
 cudaStream_t run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer);
@@ -441,23 +536,14 @@ cudaStream_t run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, boo
   out->size = total;
   const size_t seg_bytes = b.segs.size() * sizeof(pack::Segment);
   const size_t meta_off = align_up(seg_bytes, 16);
-  const bool fused = trailer && body && ctx->replica_mode == 2;
-  // fused: chunk -> first segment table, and the windows that straddle a
-  // segment boundary or the record end (pre-gathered by launch_patch)
-  const uint64_t n_chunks = fused ? fnv_chunks(body) : 0;
-  const uint64_t cb = fused ? fnv_chunk_bytes() : 1;
-  std::vector<uint64_t> win;
-  if (fused) {
-    for (size_t k = 1; k < b.segs.size(); ++k)
-      if (b.segs[k].dst % 128) win.push_back(b.segs[k].dst / 128 * 128);
-    if (body % 128) win.push_back(body / 128 * 128);
-    std::sort(win.begin(), win.end());
-    win.erase(std::unique(win.begin(), win.end()), win.end());
-  }
-  const size_t cs_off = align_up(meta_off + b.meta.size(), 16);
-  const size_t pf_off = align_up(cs_off + 4 * n_chunks, 16);
-  const size_t po_off = align_up(pf_off + 4 * (n_chunks + 1), 16);
-  const size_t stage_bytes = fused ? po_off + 8 * win.size() : meta_off + b.meta.size();
+  // fused (mode 2, or auto with local copies): the FNV kernel loads the
+  // chunks from their sources by TMA and stores them to the record and its
+  // replicas -- no pack pass
+  FusedPlan fp;
+  const bool fused = trailer && body >= 128 && fused_mode(ctx, out) && plan_fused(b, body, &fp);
+  const size_t runs_off = align_up(meta_off + b.meta.size(), 16);
+  const size_t pl_off = runs_off + sizeof(FnvRun) * fp.runs.size();
+  const size_t stage_bytes = fused ? pl_off + 8 * fp.patch.size() : meta_off + b.meta.size();
   auto& s = ctx->stage_for(stage_bytes);
   for (size_t i = 0; i < b.segs.size(); ++i)
     if (b.is_meta[i])
@@ -465,16 +551,8 @@ cudaStream_t run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, boo
   std::memcpy(s.host, b.segs.data(), seg_bytes);
   std::memcpy(s.host + meta_off, b.meta.data(), b.meta.size());
   if (fused) {
-    auto* cs = reinterpret_cast<uint32_t*>(s.host + cs_off);
-    auto* pf = reinterpret_cast<uint32_t*>(s.host + pf_off);
-    uint32_t k = 0, w = 0;
-    for (uint64_t c = 0; c <= n_chunks; ++c) {
-      while (k + 1 < b.segs.size() && b.segs[k].dst + b.segs[k].len <= c * cb) ++k;
-      while (w < win.size() && win[w] < c * cb) ++w;
-      if (c < n_chunks) cs[c] = k;
-      pf[c] = w;
-    }
-    std::memcpy(s.host + po_off, win.data(), 8 * win.size());
+    std::memcpy(s.host + runs_off, fp.runs.data(), sizeof(FnvRun) * fp.runs.size());
+    std::memcpy(s.host + pl_off, fp.patch.data(), 8 * fp.patch.size());
   }
   ctx->stage_upload(s, stage_bytes);
   pack::Dsts d{};
@@ -484,27 +562,28 @@ cudaStream_t run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, boo
   const auto* segs = reinterpret_cast<const pack::Segment*>(s.dev);
   const int n_segs = static_cast<int>(b.segs.size());
   if (fused) {
-    // one pass: gather from the arena, store to the record and every replica
-    // (NVLink stores for peers), hash, append the trailer everywhere
-    uint8_t* patch = ctx->patch_for(128 * win.size());
-    launch_patch(segs, n_segs, reinterpret_cast<const uint64_t*>(s.dev + po_off), win.size(), body, patch,
-                 ctx->stream);
-    ctx->launches += win.empty() ? 0 : 1;
-    FnvGather g{segs,
-                n_segs,
-                reinterpret_cast<const uint32_t*>(s.dev + cs_off),
-                reinterpret_cast<const uint32_t*>(s.dev + pf_off),
-                reinterpret_cast<const uint64_t*>(s.dev + po_off),
-                patch,
-                d};
+    uint8_t* patch = ctx->patch_for(fnv_chunk_bytes() * std::max<size_t>(fp.patch.size(), 1));
+    launch_patch_chunks(segs, n_segs, reinterpret_cast<const int64_t*>(s.dev + pl_off), fp.patch.size(), body, patch,
+                        ctx->stream);
+    ctx->launches += fp.patch.empty() ? 0 : 1;
+    FnvFused f{};
+    f.runs = reinterpret_cast<const FnvRun*>(s.dev + runs_off);
+    f.n_runs = static_cast<int>(fp.runs.size());
+    f.n_src = static_cast<int>(fp.src.size()) + 1;
+    for (size_t m = 0; m < fp.src.size(); ++m) {
+      f.src[m] = reinterpret_cast<const uint8_t*>(fp.src[m].first);
+      f.src_bytes[m] = fp.src[m].second;
+    }
+    f.src[fp.src.size()] = patch;
+    f.src_bytes[fp.src.size()] = fnv_chunk_bytes() * std::max<size_t>(fp.patch.size(), 1);
     TrailerDsts t{};
     for (int r = 0; r < d.n; ++r) t.p[r] = d.p[r] + body;
     t.n = d.n;
     uint32_t* scratch = ctx->fnv_scratch_for(body);
     const int tf = ctx->tbegin("pack_fnv");
     uint32_t* wit = out->witness_for(body);
-    launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream,
-               nullptr, nullptr, &g, ctx->hash_reserve, nullptr, wit);
+    launch_fnv(out->dev, body, kFnvOffset, scratch, ctx->next_epoch(), ctx->results, t, ctx->stream, nullptr,
+               nullptr, &f, ctx->hash_reserve, &d, wit);
     if (wit) out->witness_n = body;
     ctx->tend(tf);
     ctx->launches += 1;
@@ -521,7 +600,7 @@ cudaStream_t run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, boo
     }
     cudaGetLastError();
   }
-  if (trailer && mode == 5 && !out->replicas.empty() && body) {
+  if (trailer && mode == 5 && !out->replicas.empty() && body >= 128) {
     // pack the local record; the FNV kernel stores the replicas from the
     // bytes it stages in shared memory (coalesced warp stores) and appends
     // the trailer to every copy -- no second read of the record

@@ -484,13 +484,18 @@ __device__ __forceinline__ uint32_t look_back2_warp(const Scratch& scr, int64_t 
 // TMA 128-byte swizzle: granule q of row t sits at 16 * (8t + (q ^ (t & 7))),
 // so a tensor-map load lands the chunk in place and the lanes of a
 // quarter-warp hit 8 distinct bank groups for every access pattern below.
-// An unaligned gather's ninth source granule goes to `spill`.
+// A slot holds kComputeThreads + 8 rows: a fused snapshot lands a source
+// window shifted by 0-127 bytes against the record's rows, one row longer
+// (one more 1 KiB swizzle atom).
 constexpr int kGranules = kThreadBytes / 16;  // 8
+constexpr int kSlotRows = kComputeThreads + 8;
 struct alignas(1024) Shared {
-  uint4 data[kSlots][kComputeThreads * kGranules];  // 1024-byte aligned rows (TMA swizzle atoms)
+  uint4 data[kSlots][kSlotRows * kGranules];       // 1024-byte aligned rows (TMA swizzle atoms)
   unsigned long long mbar[kSlots][kComputeWarps];  // the slot's bytes landed (per warp; [s][0] under TMA)
   unsigned long long res[kSlots];                  // look-back result of the slot's round
+  unsigned long long sres[kSlots];                 // copies: the TMA stores have read the slot's rows
   int64_t next[kSlots];                            // the slot's next chunk (ticket), -1 = none
+  uint32_t shift[kSlots];                          // fused: the landed window's byte shift (0-127)
   uint32_t* witness;                               // Scratch::witness (read at the final pass)
   uint32_t wmap[kSlots][32];    // warp maps of the round (compute -> look-back)
   uint32_t wstart[kSlots][32];  // warp start bits (look-back -> compute)
@@ -499,45 +504,42 @@ struct alignas(1024) Shared {
   uint2 wfrag[2][4][32];        // mma_pass B fragments: [data | automaton][k-block][lane]
   unsigned long long kpos[32][4];  // mma_pass epilogue weights per lane
 #endif
-  // last: only the gather variant uses it, the others launch without it (a
-  // co-scheduled kernel -- the conversion replay -- gets the 24 KiB)
-  uint4 spill[kSlots][kComputeThreads];
 };
 // + 1 KiB of slack: the kernel aligns Shared to 1 KiB inside its dynamic
 // shared memory (the TMA swizzle pattern is anchored to 1 KiB boundaries)
 constexpr size_t kSmemBytes = sizeof(Shared) + 1024;
-constexpr size_t kSmemBytesNoSpill = offsetof(Shared, spill) + 1024;
 static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
-static_assert(sizeof(uint4) * kComputeThreads * kGranules % 1024 == 0, "slots keep the swizzle alignment");
+static_assert(sizeof(uint4) * kSlotRows * kGranules % 1024 == 0, "slots keep the swizzle alignment");
 
 __device__ __forceinline__ int granule(int t, int q) { return kGranules * t + (q ^ (t & 7)); }
-// granule q (0..8) of thread t's gather window: 8 = the spill granule
-__device__ __forceinline__ uint4* window_granule(Shared& sh, int slot, int t, int q) {
-  return q < kGranules ? &sh.data[slot][granule(t, q)] : &sh.spill[slot][t];
-}
-__device__ __forceinline__ const uint4* window_granule(const Shared& sh, int slot, int t, int q) {
-  return q < kGranules ? &sh.data[slot][granule(t, q)] : &sh.spill[slot][t];
-}
 
-// Fused snapshot (pack + hash + push): the kernel gathers the record from
-// its segment list instead of reading a packed record, writes the bytes to
-// the record and every replica (peer pointers: NVLink stores), and hashes
-// them.  chunk_seg[c] = the segment holding byte c * kChunk.
-// Thread windows (128 record bytes at 128-aligned offsets) that straddle a
-// segment boundary or the record end are pre-gathered into `patch` (128
-// bytes each, aligned; patch_off sorted, patch_first[c] = first patch of
-// chunk c), so every window is one aligned or unaligned 16-byte async copy
-// stream -- no byte-serial loads on the hash's critical path.
-struct Gather {
-  const pack::Segment* segs;
-  int n_segs;
-  const uint32_t* chunk_seg;
-  const uint32_t* patch_first;
-  const uint64_t* patch_off;
-  const uint8_t* patch;
-  uint8_t* dst[pack::kMaxDst];
-  int n_dst;
+// ---- copies (fused snapshot, replicas) ---------------------------------------
+// The hash kernel can also write the bytes it hashes: every chunk's rows go
+// from shared memory to up to pack::kMaxDst destinations by TMA tensor
+// stores (record-row maps; rows past the last full row are clipped and the
+// partial last row is stored by its thread), and, for a fused snapshot,
+// arrive from the record's sources instead of the record: chunk c of run r
+// is rows row0 + 512 (c - c0) ... of source map `map`, shifted by `delta`
+// bytes (a source is not 128-aligned against the record), rows 512-519 of
+// the slot taking the window's overhang.  Chunks that straddle segments
+// (headers, entry boundaries, the record's partial last chunk) are
+// pre-gathered whole into a patch buffer, which is one more source map.
+constexpr int kMaxSrc = 6;
+struct Run {
+  int64_t c0, c1;  // record chunks [c0, c1)
+  int64_t row0;    // source row of chunk c0
+  int32_t map, delta;
 };
+struct Copy {
+  CUtensorMap src[kMaxSrc][2];      // [map][0]: 256-row boxes, [map][1]: 8-row boxes
+  CUtensorMap dst[pack::kMaxDst];   // record-row maps of the destinations (256-row boxes)
+  uint8_t* dst_ptr[pack::kMaxDst];  // the same, for the partial last row
+  int n_dst;                        // 0: hash only
+  const Run* runs;                  // fused: sorted by c0, covering every chunk; null otherwise
+  int n_runs;
+};
+
+
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -612,6 +614,65 @@ __device__ __forceinline__ void tma_load_rows(void* dst, const CUtensorMap* map,
       "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(row), "r"(smem_addr(mbar))
       : "memory");
 }
+// Tensor-map store of `rows` x 128 bytes of swizzled rows at src to record
+// row `row` (rows past the tensor are clipped); bulk async-group.
+__device__ __forceinline__ void tma_store_rows(const CUtensorMap* map, int32_t row, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(0), "r"(row), "r"(smem_addr(src))
+               : "memory");
+}
+__device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// Fused snapshot: chunk `chunk` of run `r` into `slot` (one thread; one
+// mbarrier arrival with the byte count): 512 source rows, plus the 8-row atom
+// of the overhang when the window is shifted.
+__device__ __forceinline__ void tma_load_src(Shared& sh, int slot, const Copy& cp, const Run& r, int64_t chunk) {
+  unsigned long long* mb = &sh.mbar[slot][0];
+  const uint32_t delta = static_cast<uint32_t>(r.delta);
+  const int32_t row = static_cast<int32_t>(r.row0 + static_cast<int64_t>(kComputeThreads) * (chunk - r.c0));
+  sh.shift[slot] = delta;  // released to the waiters by the arrival below
+  fence_async_shared();
+  mbar_arrive_expect_tx(mb, (kComputeThreads + (delta ? 8 : 0)) * kThreadBytes);
+  const CUtensorMap* m = &cp.src[r.map][0];
+  for (int b = 0; b < kComputeThreads / 256; ++b)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_addr(&sh.data[slot][kGranules * 256 * b])),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(0), "r"(row + 256 * b), "r"(smem_addr(mb))
+        : "memory");
+  if (delta)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_addr(&sh.data[slot][kGranules * kComputeThreads])),
+        "l"(reinterpret_cast<uint64_t>(&cp.src[r.map][1])), "r"(0), "r"(row + kComputeThreads), "r"(smem_addr(mb))
+        : "memory");
+}
+// The run holding record chunk c (warp-collective: a 32-ary search over the
+// run starts, one load per lane per level).
+__device__ __forceinline__ Run find_run(const Copy& cp, int64_t c) {
+  const int lane = threadIdx.x & 31;
+  int lo = 0, hi = cp.n_runs;
+  while (hi - lo > 1) {
+    const int step = (hi - lo + 31) / 32;
+    const int i = lo + lane * step;
+    const unsigned m = __ballot_sync(0xffffffffu, i < hi && cp.runs[i].c0 <= c);
+    lo += (31 - __clz(m)) * step;  // lane 0's run starts at or before c
+    hi = min(hi, lo + step);
+  }
+  return cp.runs[lo];
+}
+// The slot's chunk out to every destination (one thread; the caller waits
+// for the TMA to have read the rows before the compute warps rewrite them).
+__device__ __forceinline__ void tma_store_chunk(const Shared& sh, int slot, const Copy& cp, int64_t chunk,
+                                                uint64_t rows_full) {
+  const uint64_t row0 = static_cast<uint64_t>(chunk) * kComputeThreads;
+  for (int d = 0; d < cp.n_dst; ++d)
+    for (int b = 0; b < kComputeThreads / 256; ++b)
+      if (row0 + 256 * b < rows_full)
+        tma_store_rows(&cp.dst[d], static_cast<int32_t>(row0 + 256 * b), &sh.data[slot][kGranules * 256 * b]);
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
 // The chunk of `slot` by one thread: the 256-row boxes that start inside the
 // map's rows_full full rows (the compute threads write the rest), one
 // mbarrier arrival with their byte count.
@@ -643,39 +704,6 @@ __device__ __forceinline__ void load_thread(Shared& sh, int slot, int t, const u
   } else {
     load_thread_bytes(sh, slot, t, [&](int i) -> uint32_t { return p + i < n ? data[p + i] : 0u; });
   }
-}
-
-// Gather variant: the thread's 128 record bytes -- from the patch buffer for
-// a straddling window, else the aligned source window in its segment (9
-// granules; *phase = source misalignment, undone when the round-0 turn reads
-// them); zeros past the record end.
-__device__ __forceinline__ void load_thread_gather(Shared& sh, int slot, int t, const Gather& g, uint64_t n,
-                                                   int64_t chunk, uint32_t* phase) {
-  const uint64_t p = static_cast<uint64_t>(chunk) * kChunk + static_cast<uint64_t>(t) * kThreadBytes;
-  *phase = 0;
-  uint4* dst = sh.data[slot];
-  if (p >= n) {
-#pragma unroll
-    for (int q = 0; q < kGranules; ++q) dst[granule(t, q)] = make_uint4(0, 0, 0, 0);
-    mbar_arrive(&sh.mbar[slot][t >> 5]);
-    return;
-  }
-  const uint8_t* src = nullptr;
-  for (uint32_t j = g.patch_first[chunk], e = g.patch_first[chunk + 1]; j < e; ++j)
-    if (g.patch_off[j] == p) src = g.patch + static_cast<uint64_t>(kThreadBytes) * j;
-  uint32_t ph = 0;
-  if (!src) {  // inside one segment (the host patched every other window)
-    int s = static_cast<int>(g.chunk_seg[chunk]);
-    while (s + 1 < g.n_segs && g.segs[s].dst + g.segs[s].len <= p) ++s;
-    src = g.segs[s].src + (p - g.segs[s].dst);
-    ph = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(src) & 15u);
-    src -= ph;
-  }
-#pragma unroll
-  for (int q = 0; q < kGranules; ++q) cp_async16(dst + granule(t, q), src + 16 * q);
-  if (ph) cp_async16(window_granule(sh, slot, t, kGranules), src + 16 * kGranules);
-  cp_async_arrive(&sh.mbar[slot][t >> 5]);
-  *phase = ph;
 }
 
 __device__ __forceinline__ void write_thread_rows(uint4* rows, int t, const uint32_t (&w)[kThreadWords]) {
@@ -831,17 +859,24 @@ __device__ __forceinline__ uint32_t automaton_and_ends(uint32_t (&w)[kThreadWord
 // (fnv_witness_kernel in kernels.cu)
 #endif
 
-__device__ __forceinline__ void read_thread_unaligned(const Shared& sh, int slot, int t, uint32_t ph,
-                                                     uint32_t (&w)[kThreadWords]) {
+// Record row t of a window landed `delta` bytes into the slot (0 < delta <
+// 128): linear granules 8t + delta/16 ... + 8 of the swizzled rows (rows t
+// and t + 1; a quarter-warp's lanes still hit 8 bank groups), then a byte
+// funnel by delta % 16 (uniform over the chunk).
+__device__ __forceinline__ void read_thread_shifted(const Shared& sh, int slot, int t, uint32_t delta,
+                                                   uint32_t (&w)[kThreadWords]) {
+  const int a = static_cast<int>(delta >> 4);
   uint32_t x[kThreadWords + 4];
 #pragma unroll
   for (int q = 0; q <= kGranules; ++q) {
-    const uint4 v = *window_granule(sh, slot, t, q);
+    const int l = a + q, r = t + (l >> 3);
+    const uint4 v = sh.data[slot][granule(r, l & 7)];
     x[4 * q] = v.x;
     x[4 * q + 1] = v.y;
     x[4 * q + 2] = v.z;
     x[4 * q + 3] = v.w;
   }
+  const uint32_t ph = delta & 15u;
   const uint32_t sel = 0x3210u + 0x1111u * (ph & 3u);  // bytes (ph&3) .. (ph&3)+3 of a:b
   switch (ph >> 2) {
 #define MLCK_REALIGN(W)                                                      \
@@ -856,31 +891,6 @@ __device__ __forceinline__ void read_thread_unaligned(const Shared& sh, int slot
   }
 #pragma unroll
   for (int i = 0; i < kThreadWords; ++i) w[i] = x[i];
-}
-
-// Coalesced store of a warp's 4 KB of record bytes (thread t's 128 bytes in
-// its granules of `slot`, aligned): store q moves granules 32q .. 32q+31 of
-// the warp's region, 512 contiguous bytes per instruction, to every dst.
-__device__ __forceinline__ void store_warp_region(const Shared& sh, int slot, int t, const Gather& g,
-                                                  uint64_t warp_base, uint64_t n) {
-  const int lane = t & 31, t0 = t - lane;
-#pragma unroll
-  for (int q = 0; q < kGranules; ++q) {
-    const int G = 32 * q + lane;  // granule of the warp region, record order
-    const uint4 v = sh.data[slot][granule(t0 + G / kGranules, G % kGranules)];
-    const uint64_t off = warp_base + 16ull * G;
-    if (off + 16 <= n) {
-#pragma unroll
-      for (int d = 0; d < pack::kMaxDst; ++d)
-        if (d < g.n_dst) st_v4(g.dst[d] + off, v);
-    } else if (off < n) {  // the record's last partial granule
-      const uint32_t c[4] = {v.x, v.y, v.z, v.w};
-      for (uint64_t k = 0; off + k < n; ++k)
-#pragma unroll
-        for (int d = 0; d < pack::kMaxDst; ++d)
-          if (d < g.n_dst) g.dst[d][off + k] = static_cast<uint8_t>(c[k >> 2] >> (8 * (k & 3)));
-    }
-  }
 }
 
 }  // namespace fnv

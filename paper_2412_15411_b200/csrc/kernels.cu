@@ -23,6 +23,12 @@ using fnv::kSlots;
 // mbarrier res[s] (one arrival per round), so compute warps never wait for
 // each other -- a fast warp moves on to the next slot's turn.
 __device__ __forceinline__ int bar_pub(int s) { return 1 + s; }
+// Copies: STORE(s) -- the compute warps have the slot's record-aligned rows
+// in shared memory (the look-back warp then issues the TMA stores; the
+// compute warps wait on sres[s] before overwriting the rows); COMPUTE --
+// the compute warps alone (a shifted window is read before it is rewritten).
+__device__ __forceinline__ int bar_store(int s) { return 1 + fnv::kSlots + s; }
+constexpr int kBarCompute = 1 + 2 * fnv::kSlots;
 
 // Profile laps of one thread's clock (kProf only): consecutive buckets, so
 // they add up to the loop time.
@@ -49,7 +55,7 @@ template <bool kProf, bool kGather>
 __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* data, uint64_t n,
                                                 const fnv::Scratch& scr, int64_t n_chunks,
                                                 const int64_t (&first)[kSlots], int64_t stride,
-                                                const fnv::Gather& gth, bool tma) {
+                                                const fnv::Copy& cp, bool tma) {
   using namespace fnv;
   // TMA mode: the slot's look-back warp loads whole chunks through the tensor
   // map; rows at or past the last full 128-byte row are written here
@@ -66,9 +72,10 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
   bool pend[kSlots];
   uint32_t st[kSlots];    // segment start bits, byte i = segment i
   uint32_t keep[kSlots];  // pending round: lane exclusive map [0,3), segment maps 0..kSegs-2 above
-  uint32_t ph[kSlots];    // kGather: source misalignment of the slot's bytes
   uint32_t par = 0;       // data mbarrier phase parity per slot
   uint32_t rpar = 0;      // result mbarrier phase parity per slot
+  uint32_t spar = 0;      // copies: store mbarrier phase parity per slot
+  const bool copy = cp.n_dst > 0;
   uint64_t acc = 0;
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
@@ -77,13 +84,7 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
     pend[s] = false;
     st[s] = 0;
     keep[s] = 0;
-    ph[s] = 0;
-    if (chunk[s] >= 0 && !tma) {
-      if (kGather)
-        load_thread_gather(sh, s, tid, gth, n, chunk[s], &ph[s]);
-      else
-        load_thread(sh, s, tid, data, n, chunk[s]);
-    }
+    if (chunk[s] >= 0 && !tma) load_thread(sh, s, tid, data, n, chunk[s]);
   }
   (void)warp;
   // [0] rounds, [1] waits for look-back results, [2] final passes, [3] other
@@ -188,10 +189,7 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
           if (tma) {
             bar_arrive(bar_pub(s), kBarThreads);  // done with the bytes: the look-back warp refills
           } else if (chunk[s] >= 0) {
-            if (kGather)
-              load_thread_gather(sh, s, tid, gth, n, chunk[s], &ph[s]);
-            else
-              load_thread(sh, s, tid, data, n, chunk[s]);
+            load_thread(sh, s, tid, data, n, chunk[s]);
           }
           lap.mark(4);
           continue;
@@ -201,7 +199,7 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
       if (rnd[s] == 0) {
         lap.mark(0);
         fnv::mbar_wait(&sh.mbar[s][tma ? 0 : warp], (par >> s) & 1u);
-        if (tma) {
+        if (tma && !kGather) {
           const uint64_t row = static_cast<uint64_t>(chunk[s]) * kComputeThreads + tid;
           if (row >= rows_full) {  // the partial last row, or zeros past the record
             const uint64_t p = row * kThreadBytes;
@@ -215,23 +213,37 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
         }
       }
       uint32_t w[kThreadWords];
-      if (kGather && rnd[s] == 0 && ph[s])
-        read_thread_unaligned(sh, s, tid, ph[s], w);
+      const uint32_t delta = kGather && rnd[s] == 0 ? sh.shift[s] : 0u;  // uniform over the chunk
+      if (delta)
+        read_thread_shifted(sh, s, tid, delta, w);
       else
         read_thread(sh, s, tid, w);
+      const bool store = copy && rnd[s] == 0;
       if (rnd[s] == 0) {
-        if (kGather) {  // fused pack: the gathered bytes go to the record and its replicas
-          write_thread(sh, s, tid, w);  // aligned, then out through coalesced warp stores
-          __syncwarp();
-          store_warp_region(sh, s, tid, gth,
-                            static_cast<uint64_t>(chunk[s]) * kChunk + static_cast<uint64_t>(tid - lane) * kThreadBytes, n);
-          __syncwarp();
-        } else if (gth.n_dst) {  // replica copies written from the landed bytes
-          store_warp_region(sh, s, tid, gth,
-                            static_cast<uint64_t>(chunk[s]) * kChunk + static_cast<uint64_t>(tid - lane) * kThreadBytes, n);
-          __syncwarp();  // the warp's granules are read before they are interleaved in place
+        if (delta) {  // every thread has read its window before the rows are rewritten aligned
+          bar_sync(kBarCompute, kComputeThreads);
+          write_thread(sh, s, tid, w);
+        }
+        if (store) {  // record-aligned rows in place: the look-back warp stores them
+          fence_async_shared();
+          bar_arrive(bar_store(s), kBarThreads);
+          const uint64_t row = static_cast<uint64_t>(chunk[s]) * kComputeThreads + tid;
+          if (row == rows_full && (n & (kThreadBytes - 1))) {  // the partial last row (TMA stores clip it)
+            const uint8_t* rb = reinterpret_cast<const uint8_t*>(sh.data[s]);
+            for (uint32_t k = 0; k < (n & (kThreadBytes - 1)); ++k) {
+              const uint8_t b = rb[16 * granule(tid, k >> 4) + (k & 15)];
+              for (int d = 0; d < cp.n_dst; ++d) cp.dst_ptr[d][rows_full * kThreadBytes + k] = b;
+            }
+          }
         }
         interleave(w);  // fresh bytes: interleave the segments once, in place
+        if (!store) write_thread(sh, s, tid, w);
+      } else if (copy && rnd[s] == 1) {
+        // copies: the rows stayed record-aligned for the TMA stores through
+        // round 0; interleaved in place now, once the stores have read them
+        interleave(w);
+        fnv::mbar_wait(&sh.sres[s], (spar >> s) & 1u);
+        spar ^= 1u << s;
         write_thread(sh, s, tid, w);
       }
 #if MLCK_FNV_PACKED_MAPS
@@ -283,10 +295,10 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
 // the slot it folds their warp maps into the chunk's map, publishes it,
 // looks back for the chunk's start bits and hands each warp its start.  Only
 // this slot's turns involve it, so the slots' look-backs run concurrently.
-template <bool kProf>
+template <bool kProf, bool kGather>
 __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t seed, const fnv::Scratch& scr,
                                              int64_t chunk, int64_t n_chunks, int64_t stride,
-                                             const CUtensorMap* tmap, uint64_t n) {
+                                             const CUtensorMap* tmap, uint64_t n, const fnv::Copy& cp) {
   using namespace fnv;
   const int lane = threadIdx.x & 31;
   const unsigned long long tag = static_cast<unsigned long long>(scr.epoch) << 32;
@@ -302,11 +314,28 @@ __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t se
       lb[0] = now;
     }
   };
-  if (tmap && lane == 0 && chunk >= 0) tma_load_chunk(sh, s, tmap, chunk, n / kThreadBytes);
+  const uint64_t rows_full = n / kThreadBytes;
+  const bool copy = cp.n_dst > 0;
+  if (kGather && chunk >= 0) {
+    const Run run = find_run(cp, chunk);
+    if (lane == 0) tma_load_src(sh, s, cp, run, chunk);
+  } else if (tmap && lane == 0 && chunk >= 0) {
+    tma_load_chunk(sh, s, tmap, chunk, rows_full);
+  }
   while (chunk >= 0) {
     uint32_t word = 0;  // the chunk's status bits as published
     int64_t next = -1;
+    Run nrun{};  // kGather: the run of the next chunk, looked up beside the last round
+    if (copy) {  // the compute warps have the rows aligned: out to every destination
+      bar_sync(bar_store(s), kBarThreads);
+      if (lane == 0) tma_store_chunk(sh, s, cp, chunk, rows_full);
+      __syncwarp();
+    }
     for (int r = 0; r < kRounds; ++r) {
+      if (copy && r == 1 && lane == 0) {  // round 1 rewrites the rows: once the stores have read them
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        mbar_arrive(&sh.sres[s]);
+      }
       mark(5);
       bar_sync(bar_pub(s), kBarThreads);
       if (r == kRounds - 1) {
@@ -321,6 +350,7 @@ __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t se
         }
         __syncwarp();
         next = sh.next[s];
+        if (kGather && next >= 0) nrun = find_run(cp, next);
       }
       const uint32_t wm = lane < kComputeWarps ? sh.wmap[s][lane] : 0u;
       mark(1);
@@ -344,12 +374,18 @@ __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t se
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.res[s]);  // release: wstart is visible to the waiters
     }
-    if (tmap) {  // the compute warps are done with the bytes: load the slot's next chunk
+    if (kGather || tmap) {  // the compute warps are done with the bytes: load the slot's next chunk
       bar_sync(bar_pub(s), kBarThreads);
-      if (lane == 0 && next >= 0) tma_load_chunk(sh, s, tmap, next, n / kThreadBytes);
+      if (lane == 0 && next >= 0) {
+        if (kGather)
+          tma_load_src(sh, s, cp, nrun, next);
+        else
+          tma_load_chunk(sh, s, tmap, next, rows_full);
+      }
     }
     chunk = next;
   }
+  if (copy && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
   mark(5);
   if (kProf && lane == 0) {
     for (int b = 1; b <= 5; ++b) atomicAdd(scr.prof + 7 + b, static_cast<unsigned long long>(lb[b]));
@@ -368,7 +404,8 @@ __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t se
 template <bool kProf, bool kGather>
 __global__ void MLCK_FNV_BOUNDS
     fnv_kernel(const uint8_t* data, uint64_t n, uint64_t seed, fnv::Scratch scr, int64_t n_chunks,
-               TrailerDsts trailer, fnv::Gather gth, const __grid_constant__ CUtensorMap tmap, int use_tma) {
+               TrailerDsts trailer, const __grid_constant__ fnv::Copy cp, const __grid_constant__ CUtensorMap tmap,
+               int use_tma) {
   using namespace fnv;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1 KiB-aligned rows whatever the base of the dynamic window
@@ -376,8 +413,9 @@ __global__ void MLCK_FNV_BOUNDS
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0)
     for (int s = 0; s < kSlots; ++s) {
-      for (int w = 0; w < kComputeWarps; ++w) mbar_init(&sh.mbar[s][w], use_tma ? 1 : 32);
+      for (int w = 0; w < kComputeWarps; ++w) mbar_init(&sh.mbar[s][w], kGather || use_tma ? 1 : 32);
       mbar_init(&sh.res[s], 1);
+      mbar_init(&sh.sres[s], 1);
     }
 #if MLCK_FNV_MMA
   mma_tables(sh, tid);
@@ -402,14 +440,15 @@ __global__ void MLCK_FNV_BOUNDS
   for (int s = 0; s < kSlots; ++s) first[s] = sh.next[s];
   __syncthreads();  // sh.next is rewritten by the look-back warps from here on
   uint64_t acc = 0;
-  const bool tma = !kGather && use_tma;
+  const bool tma = kGather || use_tma;  // chunks land by TMA (from the sources under kGather)
   if (compute_warp(warp) >= 0) {
-    acc = fnv_compute<kProf, kGather>(sh, data, n, scr, n_chunks, first, stride, gth, tma);
+    acc = fnv_compute<kProf, kGather>(sh, data, n, scr, n_chunks, first, stride, cp, tma);
   } else {
 #pragma unroll
     for (int s = 0; s < kSlots; ++s)
       if (warp == lookback_warp(s))
-        fnv_lookback<kProf>(sh, s, seed, scr, first[s], n_chunks, stride, tma ? &tmap : nullptr, n);
+        fnv_lookback<kProf, kGather>(sh, s, seed, scr, first[s], n_chunks, stride,
+                                     !kGather && use_tma ? &tmap : nullptr, n, cp);
   }
   // CTA sum -> global accumulator; the last CTA finishes the hash
 #pragma unroll
@@ -630,10 +669,9 @@ uint32_t fnv_sticky_word() { return 8; }
 // The bytes [data, data + n) as a [n / 128 rows x 128 bytes] tensor map (the
 // full rows only), 256-row boxes landing in the 128-byte swizzle the FNV
 // kernels' shared-memory rows use.  False when the TMA cannot serve it.
-bool make_row_tmap(const uint8_t* data, uint64_t n, CUtensorMap* tmap) {
-  std::memset(tmap, 0, sizeof(*tmap));
-  const uint64_t rows = n / fnv::kThreadBytes;
-  if (rows == 0 || (reinterpret_cast<uintptr_t>(data) & 15u) != 0 || rows >= (1ull << 31)) return false;
+// `rows` x 128-byte rows at data as a tensor map with `box_rows`-row boxes in
+// the 128-byte swizzle of the FNV kernels' shared-memory rows.
+void encode_rows(const uint8_t* data, uint64_t rows, uint32_t box_rows, CUtensorMap* tmap) {
   using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -646,18 +684,24 @@ bool make_row_tmap(const uint8_t* data, uint64_t n, CUtensorMap* tmap) {
   }
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(fnv::kThreadBytes), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(fnv::kThreadBytes)};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(fnv::kThreadBytes), static_cast<cuuint32_t>(fnv::kTmaBoxRows)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(fnv::kThreadBytes), box_rows};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode(tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(data), dims, strides, box,
                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(kCuda, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+bool make_row_tmap(const uint8_t* data, uint64_t n, CUtensorMap* tmap) {
+  std::memset(tmap, 0, sizeof(*tmap));
+  const uint64_t rows = n / fnv::kThreadBytes;
+  if (rows == 0 || (reinterpret_cast<uintptr_t>(data) & 15u) != 0 || rows >= (1ull << 31)) return false;
+  encode_rows(data, rows, fnv::kTmaBoxRows, tmap);
   return true;
 }
 
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
-                unsigned long long* prof, unsigned long long* trace, const FnvGather* gather,
+                unsigned long long* prof, unsigned long long* trace, const FnvFused* fused,
                 int reserve_sms, const pack::Dsts* copies, uint32_t* witness) {
   const uint64_t n_chunks = fnv_chunks(n);
   fnv::Scratch scr{};
@@ -697,51 +741,72 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
     MLCK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   const uint64_t grid = std::min<uint64_t>(div_up(n_chunks, fnv::kSlots), static_cast<uint64_t>(std::max(1, sms - reserve_sms)));
-  fnv::Gather g{};
-  if (gather) {
-    g.segs = gather->segs;
-    g.n_segs = gather->n_segs;
-    g.chunk_seg = gather->chunk_seg;
-    g.patch_first = gather->patch_first;
-    g.patch_off = gather->patch_off;
-    g.patch = gather->patch;
-    g.n_dst = gather->dsts.n;
-    for (int d = 0; d < gather->dsts.n; ++d) g.dst[d] = gather->dsts.p[d];
-  } else if (copies) {
-    g.n_dst = copies->n;
-    for (int d = 0; d < copies->n; ++d) g.dst[d] = copies->p[d];
+  // copies: TMA stores of every hashed chunk; fused: chunks from the sources
+  static_assert(sizeof(FnvRun) == sizeof(fnv::Run) && kFnvMaxSrc == fnv::kMaxSrc, "FnvRun mirrors fnv::Run");
+  fnv::Copy cp;
+  std::memset(&cp, 0, sizeof(cp));
+  if (copies && copies->n > 0) {
+    if (n < fnv::kThreadBytes || (reinterpret_cast<uintptr_t>(data) & 15u))
+      throw_invalid("hash copies need a 16-byte aligned record of at least one row");
+    cp.n_dst = copies->n;
+    for (int d = 0; d < copies->n; ++d) {
+      if (reinterpret_cast<uintptr_t>(copies->p[d]) & 15u) throw_invalid("copy destinations must be 16-byte aligned");
+      make_row_tmap(copies->p[d], n, &cp.dst[d]);
+      cp.dst_ptr[d] = copies->p[d];
+    }
+  }
+  if (fused) {
+    if (!cp.n_dst) throw_invalid("a fused snapshot stores to at least the record");
+    if (fused->n_src < 1 || fused->n_src > fnv::kMaxSrc) throw_invalid("fused snapshot: 1-6 source maps");
+    for (int m = 0; m < fused->n_src; ++m) {
+      const uint64_t rows = fused->src_bytes[m] / fnv::kThreadBytes;
+      if ((reinterpret_cast<uintptr_t>(fused->src[m]) & 15u) || rows == 0 || rows >= (1ull << 31))
+        throw_invalid("fused snapshot: a source map must be 16-byte aligned, 128 B .. 256 GiB");
+      encode_rows(fused->src[m], rows, fnv::kTmaBoxRows, &cp.src[m][0]);
+      encode_rows(fused->src[m], rows, 8, &cp.src[m][1]);
+    }
+    cp.runs = reinterpret_cast<const fnv::Run*>(fused->runs);
+    cp.n_runs = fused->n_runs;
   }
   // the record as a [n / 128 rows x 128 bytes] tensor, loaded in 256-row
   // boxes in the 128-byte swizzle the shared-memory rows use
   CUtensorMap tmap;
-  const int use_tma = !gather && make_row_tmap(data, n, &tmap) ? 1 : 0;
+  const int use_tma = !fused && make_row_tmap(data, n, &tmap) ? 1 : 0;
+  if (cp.n_dst && !fused && !use_tma) throw_invalid("hash copies need the record's tensor map");
   const bool pf = prof || trace;
-  auto k = gather ? (pf ? fnv_kernel<true, true> : fnv_kernel<false, true>)
-                  : (pf ? fnv_kernel<true, false> : fnv_kernel<false, false>);
-  k<<<static_cast<unsigned>(grid), fnv::kThreads, gather ? fnv::kSmemBytes : fnv::kSmemBytesNoSpill, stream>>>(
-      data, n, seed, scr, static_cast<int64_t>(n_chunks), trailer, g, tmap, use_tma);
+  auto k = fused ? (pf ? fnv_kernel<true, true> : fnv_kernel<false, true>)
+                 : (pf ? fnv_kernel<true, false> : fnv_kernel<false, false>);
+  k<<<static_cast<unsigned>(grid), fnv::kThreads, fnv::kSmemBytes, stream>>>(
+      data, n, seed, scr, static_cast<int64_t>(n_chunks), trailer, cp, tmap, use_tma);
   MLCK_CUDA(cudaGetLastError());
 }
 
 namespace {
-// The straddling windows of a fused snapshot (fnv::Gather): block j gathers
-// the 128 record bytes at offs[j] (zeros past the record end).
-__global__ void patch_kernel(const pack::Segment* __restrict__ segs, int n_segs,
-                             const uint64_t* __restrict__ offs, uint64_t n, uint8_t* __restrict__ out) {
-  const uint64_t pos = offs[blockIdx.x] + threadIdx.x;
-  uint8_t b = 0;
+// The straddling chunks of a fused snapshot: block (x, j) gathers 4 KiB of
+// chunk chunks[j], 16 bytes per thread (zeros past the record end).
+__global__ void patch_chunks_kernel(const pack::Segment* __restrict__ segs, int n_segs,
+                                    const int64_t* __restrict__ chunks, uint64_t n, uint8_t* __restrict__ out) {
+  const uint64_t off = 4096ull * blockIdx.x + 16ull * threadIdx.x;
+  const uint64_t pos = static_cast<uint64_t>(chunks[blockIdx.y]) * fnv::kChunk + off;
+  uint32_t v[4] = {0, 0, 0, 0};
   if (pos < n) {
-    const int s = pack::find_segment(segs, n_segs, pos);
-    b = segs[s].src[pos - segs[s].dst];
+    int s = pack::find_segment(segs, n_segs, pos);
+    for (int k = 0; k < 16 && pos + k < n; ++k) {
+      while (segs[s].dst + segs[s].len <= pos + k) ++s;
+      v[k >> 2] |= static_cast<uint32_t>(segs[s].src[pos + k - segs[s].dst]) << (8 * (k & 3));
+    }
   }
-  out[static_cast<uint64_t>(blockIdx.x) * fnv::kThreadBytes + threadIdx.x] = b;
+  *reinterpret_cast<uint4*>(out + static_cast<uint64_t>(blockIdx.y) * fnv::kChunk + off) =
+      make_uint4(v[0], v[1], v[2], v[3]);
 }
 }  // namespace
 
-void launch_patch(const pack::Segment* segs, int n_segs, const uint64_t* offs, uint64_t n_win, uint64_t n,
-                  uint8_t* out, cudaStream_t stream) {
-  if (!n_win) return;
-  patch_kernel<<<static_cast<unsigned>(n_win), fnv::kThreadBytes, 0, stream>>>(segs, n_segs, offs, n, out);
+void launch_patch_chunks(const pack::Segment* segs, int n_segs, const int64_t* chunks, uint64_t n_patch, uint64_t n,
+                         uint8_t* out, cudaStream_t stream) {
+  if (!n_patch) return;
+  static_assert(fnv::kChunk % 4096 == 0, "4 KiB blocks");
+  patch_chunks_kernel<<<dim3(fnv::kChunk / 4096, static_cast<unsigned>(n_patch)), 256, 0, stream>>>(
+      segs, n_segs, chunks, n, out);
   MLCK_CUDA(cudaGetLastError());
 }
 

@@ -38,20 +38,26 @@ struct WalkJob {
   WalkResult* result;
 };
 
-// Fused snapshot: the FNV kernel gathers the record from `segs` (chunk_seg[c]
-// = segment holding byte c * fnv_chunk_bytes()), writes it to every dst and
-// hashes it in the same pass.
-struct FnvGather {
-  const pack::Segment* segs;
-  int n_segs;
-  const uint32_t* chunk_seg;
-  const uint32_t* patch_first;  // [n_chunks + 1]
-  const uint64_t* patch_off;    // sorted 128-aligned window offsets
-  const uint8_t* patch;         // 128 bytes per window (launch_patch)
-  pack::Dsts dsts;
+// Fused snapshot: the FNV kernel loads the record's chunks from its sources
+// by TMA (runs: chunks [c0, c1) are rows row0 + 512 (c - c0) ... of source
+// `map`, shifted by `delta` bytes; map n_src = the patch buffer of the chunks
+// that straddle segments), hashes them and stores them to every copies dst.
+struct FnvRun {
+  int64_t c0, c1, row0;
+  int32_t map, delta;
 };
-void launch_patch(const pack::Segment* segs, int n_segs, const uint64_t* offs, uint64_t n_win, uint64_t n,
-                  uint8_t* out, cudaStream_t stream);
+constexpr int kFnvMaxSrc = 6;  // source maps per launch, the patch buffer included
+struct FnvFused {
+  const FnvRun* runs;  // device, sorted by c0, covering every chunk
+  int n_runs;
+  const uint8_t* src[kFnvMaxSrc];  // source allocations (16-byte aligned), the patch buffer last
+  uint64_t src_bytes[kFnvMaxSrc];
+  int n_src;
+};
+// The straddling chunks of a fused snapshot: chunk chunks[j] of the record
+// (bytes from `segs`, zeros past n) to out + j * fnv_chunk_bytes().
+void launch_patch_chunks(const pack::Segment* segs, int n_segs, const int64_t* chunks, uint64_t n_patch, uint64_t n,
+                         uint8_t* out, cudaStream_t stream);
 
 void init_constants();
 uint64_t fnv_chunk_bytes();
@@ -61,8 +67,8 @@ size_t fnv_scratch_words(uint64_t n);
 void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratch, uint32_t epoch,
                 unsigned long long* result, const TrailerDsts& trailer, cudaStream_t stream,
                 unsigned long long* prof = nullptr, unsigned long long* trace = nullptr,
-                const FnvGather* gather = nullptr, int reserve_sms = 0,
-                const pack::Dsts* copies = nullptr,  // non-gather: also store the bytes to these
+                const FnvFused* fused = nullptr, int reserve_sms = 0,
+                const pack::Dsts* copies = nullptr,  // also store the hashed bytes to these (TMA)
                 uint32_t* witness = nullptr);        // non-null: the rows' segment starts (fnv.cuh)
 // Exact re-hash of n bytes against the witness fnv_kernel left (one u32 per
 // 128-byte row); *bad = 1 when the witness does not match the bytes (the
