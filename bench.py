@@ -338,8 +338,8 @@ def cpu_baseline_full(wl):
 
 
 def AUTO_TRANSPORT(world):
-    """What replica mode -1 (auto) picks: 0 for local replicas (N=1), 1 for peers."""
-    return 0 if world == 1 else 1
+    """What replica mode -1 (auto) picks: 2 (fused) for local replicas (N=1), 1 for peers."""
+    return 2 if world == 1 else 1
 
 
 METRIC = "snapshot+replicate GB/s/GPU and sparse-to-dense conversion time vs HBM/NVLink roofline"
@@ -627,7 +627,7 @@ def bench_interference(ctx, mlck, st, blobs, slots, dev, gemms=200):
 # --------------------------------------------------------------------------
 def bench_snapshot_n1(ctx, mlck, wl, args):
     """Snapshot steps of `wl` on one GPU: one record buffer + a replica in a
-    second HBM buffer (transport 0), records rotating through the slots."""
+    second HBM buffer (auto transport: the fused kernel), records rotating through the slots."""
     pcs, cb, W = wl["param_counts"], wl["cb"], wl["W"]
     slots = schedule(wl)
     sizes = [record_bytes(wl, sl) for sl in slots]
@@ -653,7 +653,7 @@ def bench_snapshot_n1(ctx, mlck, wl, args):
     ctx.synchronize()
     ms = ctx.event_ms(0, 1)
     total = sum(sizes[i % W] for i in range(args.steps))
-    out = {"workload": wl["name"], "n_gpus": 1, "replica_target": "second HBM buffer (transport 0)",
+    out = {"workload": wl["name"], "n_gpus": 1, "replica_target": "second HBM buffer (auto transport 2, fused)",
            "ms_per_step": ms / args.steps, "value": total / (ms / 1000) / GB, "unit": "GB/s",
            "record_bytes_per_slot": sizes}
     st.close()
@@ -735,8 +735,9 @@ def run_ours(args, d: Dist):
     transport = args.replica_mode if args.replica_mode != -1 else AUTO_TRANSPORT(d.world)  # the timed transport
 
     # ---- per-kernel breakdown (CUDA events around each launch) of the timed
-    # configuration -- N=1, transport 0: the pack kernel writes the record and
-    # its local replica, then the FNV kernel hashes; N>1, transport 1: pack
+    # configuration -- N=1, transport 2: one fused FNV kernel loads the
+    # record's chunks from the state arena, hashes them and stores the record
+    # and its local replica; N>1, transport 1: pack
     # kernel, then the copy engines push to the ring peers while the FNV
     # kernel hashes -- plus every other transport as a whole-step ablation.
     hbm_peak, peak_kind = peaks()
@@ -809,9 +810,12 @@ def run_ours(args, d: Dist):
                 "frac": ach / hbm_peak, "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
                 "per_launch_bytes": kd["bytes_per_launch"],
                 "compute_side": ncu_pipes("fnv_kernel"),
-                "note": "dominant kernel of the step (the pack kernel alone: kernels['pack']); it is bound by the "
-                        "integer ALU work of the FNV automaton and its per-round look-back latency, not by HBM "
-                        "(compute_side: issue / pipe utilisation from the committed ncu capture; DESIGN.md 3.2)"}
+                "note": ("the step's one kernel (fused: TMA loads from the sources, hash, TMA stores of the record and "
+                         "its replica; achieved = payload read + record and replica writes per launch)" if fused_ms else
+                         "dominant kernel of the step (the pack kernel alone: kernels['pack'])") +
+                        "; bound by the integer ALU work of the FNV automaton and its per-round look-back latency, "
+                        "not by HBM (compute_side: issue / pipe utilisation from the committed ncu capture; "
+                        "DESIGN.md 3.2)"}
     if d.world > 1:
         nv_peak = 782.0  # one copy engine, GPU->peer (scripts/micro/push.cu on this pool)
         egress = r * bytes_local / (ms_local / 1000) / GB

@@ -80,15 +80,19 @@ uint64_t mlck_ctx_kernel_launches(mlck_ctx* ctx);
  * fnv_verify, walk, replay).  mlck_ctx_timings synchronizes, returns the
  * labels as CSV and the durations (ms) recorded since the last read. */
 int mlck_ctx_set_timing(mlck_ctx* ctx, int on);
-/* Snapshot transport.  -1 (default) auto: 0 when every replica is in this
- * GPU's HBM, else 1.  1: pack kernel, then copy engines push the record
- * while the FNV kernel hashes it.  5: pack kernel, then the FNV kernel
- * stores the replicas from the bytes it stages (no second read).  3: pack
- * kernel, then a push kernel on reserved SMs stores the record to the
- * replicas while the FNV kernel hashes it on the other SMs.  2: one fused
- * kernel gathers the record from the state arena, stores it to the blob and
- * every replica and hashes it.  0: the pack kernel stores the replicas, then
- * the FNV kernel.  4: copy engines after the hash (no overlap). */
+/* Snapshot transport.  -1 (default) auto: 2 when every replica is in this
+ * GPU's HBM, else 1.  2: one fused kernel -- the FNV kernel loads the
+ * record's chunks straight from their sources (the state arena, the codes;
+ * TMA, shifted windows), hashes them and stores them to the blob and every
+ * replica by TMA (chunks that straddle segments are pre-gathered; a record
+ * whose payload spans more than 5 allocations, or is mostly straddling
+ * chunks, takes transport 0).  1: pack kernel, then copy engines push the
+ * record while the FNV kernel hashes it.  5: pack kernel, then the FNV
+ * kernel stores the replicas from the bytes it stages (no second read).
+ * 3: pack kernel, then a push kernel on reserved SMs stores the record to
+ * the replicas while the FNV kernel hashes it on the other SMs.  0: the pack
+ * kernel stores the replicas, then the FNV kernel.  4: copy engines after
+ * the hash (no overlap). */
 int mlck_ctx_set_replica_mode(mlck_ctx* ctx, int mode);
 /* SMs the hash kernel leaves to co-scheduled work (training kernels beside
  * a snapshot); 0 = all SMs.  The kernel hands chunks out by ticket, so any

@@ -508,9 +508,20 @@ bool plan_fused(const SegmentBuilder& b, uint64_t body, FusedPlan* fp) {
   return fp->patch.size() * 4 <= n_chunks + 4;
 }
 
-bool fused_mode(const mlck_ctx* ctx, const mlck_blob* out) {
-  (void)out;
-  return ctx->replica_mode == 2;
+// The transport of a record (mlck_ctx_set_replica_mode): auto (-1) is the
+// fused kernel (2) when every replica is in this GPU's HBM, else the pack
+// kernel with copy-engine pushes to the peers (1).
+int resolve_mode(const mlck_ctx* ctx, const mlck_blob* out) {
+  if (ctx->replica_mode != -1) return ctx->replica_mode;
+  for (auto& r : out->replicas) {
+    cudaPointerAttributes a{};
+    if (ctx->is_ipc(r.first) || cudaPointerGetAttributes(&a, r.first) != cudaSuccess ||
+        a.type != cudaMemoryTypeDevice || a.device != ctx->device) {
+      cudaGetLastError();
+      return 1;
+    }
+  }
+  return 2;
 }
 
 // Uploads the segment table + meta, launches pack (and the FNV trailer when
@@ -540,7 +551,7 @@ cudaStream_t run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, boo
   // chunks from their sources by TMA and stores them to the record and its
   // replicas -- no pack pass
   FusedPlan fp;
-  const bool fused = trailer && body >= 128 && fused_mode(ctx, out) && plan_fused(b, body, &fp);
+  const bool fused = trailer && body >= 128 && resolve_mode(ctx, out) == 2 && plan_fused(b, body, &fp);
   const size_t runs_off = align_up(meta_off + b.meta.size(), 16);
   const size_t pl_off = runs_off + sizeof(FnvRun) * fp.runs.size();
   const size_t stage_bytes = fused ? pl_off + 8 * fp.patch.size() : meta_off + b.meta.size();
@@ -589,17 +600,7 @@ cudaStream_t run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, boo
     ctx->launches += 1;
     return ctx->stream;
   }
-  int mode = ctx->replica_mode;
-  if (mode == -1) {  // auto: 0 when every replica is in this GPU's HBM, else 1
-    mode = 0;
-    for (auto& r : out->replicas) {
-      cudaPointerAttributes a{};
-      if (ctx->is_ipc(r.first) || cudaPointerGetAttributes(&a, r.first) != cudaSuccess ||
-          a.type != cudaMemoryTypeDevice || a.device != ctx->device)
-        mode = 1;
-    }
-    cudaGetLastError();
-  }
+  const int mode = resolve_mode(ctx, out);  // 2 fell through: the record did not suit the fused kernel
   if (trailer && mode == 5 && !out->replicas.empty() && body >= 128) {
     // pack the local record; the FNV kernel stores the replicas from the
     // bytes it stages in shared memory (coalesced warp stores) and appends
