@@ -450,6 +450,8 @@ int mlck_decode_compute(mlck_ctx* ctx, const void* device_codes, float* device_o
 /* ---- multi-GPU replica placement (CUDA IPC over NVLink) ------------------ */
 int mlck_ipc_export(mlck_ctx* ctx, void* device_ptr, uint8_t handle[64]);
 int mlck_ipc_open(mlck_ctx* ctx, const uint8_t handle[64], void** device_ptr);
+/* Closes a mapping mlck_ipc_open returned; pending snapshots finish first,
+ * and every blob of the ctx drops the replicas registered inside it. */
 int mlck_ipc_close(mlck_ctx* ctx, void* device_ptr);
 int mlck_enable_peer_access(mlck_ctx* ctx, int peer_device);
 

@@ -51,6 +51,7 @@ struct mlck_ctx {
   // device ranges opened through CUDA IPC (another GPU's memory: pointer
   // attributes report the mapping device, not the owner)
   std::vector<std::pair<uint64_t, uint64_t>> ipc_ranges;
+  std::vector<mlck_blob*> blobs;  // live blobs (mlck_ipc_close drops replicas inside a closed mapping)
   bool is_ipc(const void* p) const {
     const uint64_t a = reinterpret_cast<uint64_t>(p);
     for (const auto& r : ipc_ranges)
@@ -1397,6 +1398,7 @@ int mlck_blob_create(mlck_ctx* ctx, uint64_t capacity, mlck_blob** out) {
     auto* b = new mlck_blob();
     b->ctx = ctx;
     b->reserve(std::max<uint64_t>(capacity, kAlign));
+    ctx->blobs.push_back(b);
     *out = b;
   });
 }
@@ -1409,6 +1411,8 @@ int mlck_blob_destroy(mlck_blob* b) {
     if (b->dev) cudaFree(b->dev);
     if (b->witness) cudaFree(b->witness);
     if (b->written) cudaEventDestroy(b->written);
+    auto& v = b->ctx->blobs;
+    v.erase(std::remove(v.begin(), v.end(), b), v.end());
     delete b;
   });
 }
@@ -1421,6 +1425,7 @@ int mlck_blob_from_host(mlck_ctx* ctx, const uint8_t* bytes, uint64_t n, mlck_bl
     if (n) MLCK_CUDA(cudaMemcpyAsync(b->dev, bytes, n, cudaMemcpyHostToDevice, ctx->stream));
     MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
     b->size = n;
+    ctx->blobs.push_back(b);
     *out = b;
   });
 }
@@ -1563,6 +1568,7 @@ int mlck_blob_load(mlck_ctx* ctx, const char* path, mlck_blob** out) {
       delete b;
       throw;
     }
+    ctx->blobs.push_back(b);
     *out = b;
   });
 }
@@ -2268,7 +2274,23 @@ int mlck_ipc_close(mlck_ctx* ctx, void* ptr) {
     ctx->activate();
     const uint64_t a = reinterpret_cast<uint64_t>(ptr);
     auto& v = ctx->ipc_ranges;
+    uint64_t end = a;
+    for (const auto& r : v)
+      if (r.first == a) end = r.first + r.second;
     v.erase(std::remove_if(v.begin(), v.end(), [&](const auto& r) { return r.first == a; }), v.end());
+    // no blob keeps a replica inside the closed mapping (its next record
+    // would be stored to unmapped memory): in-flight writes finish first
+    ctx->join_hash();
+    MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (mlck_blob* b : ctx->blobs) {
+      auto& reps = b->replicas;
+      reps.erase(std::remove_if(reps.begin(), reps.end(),
+                                [&](const auto& r) {
+                                  const uint64_t p = reinterpret_cast<uint64_t>(r.first);
+                                  return p >= a && p < end;
+                                }),
+                 reps.end());
+    }
     MLCK_CUDA(cudaIpcCloseMemHandle(ptr));
   });
 }

@@ -75,6 +75,12 @@ constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
 #ifndef MLCK_FNV_NOSHIFT
 #define MLCK_FNV_NOSHIFT 1
 #endif
+// MLCK_FNV_WARP_STORES: copies leave by per-warp TMA stores of 32 rows in
+// round 0 (1) or by the look-back warp's whole-chunk stores, the rows
+// interleaved in round 1 (0).
+#ifndef MLCK_FNV_WARP_STORES
+#define MLCK_FNV_WARP_STORES 0
+#endif
 constexpr int kSlots = MLCK_FNV_SLOTS;         // chunks in flight per CTA
 constexpr int kComputeWarps = MLCK_FNV_WARPS;  // + one look-back warp per slot
 constexpr int kWarps = kComputeWarps + kSlots;
@@ -494,6 +500,7 @@ struct alignas(1024) Shared {
   unsigned long long mbar[kSlots][kComputeWarps];  // the slot's bytes landed (per warp; [s][0] under TMA)
   unsigned long long res[kSlots];                  // look-back result of the slot's round
   unsigned long long sres[kSlots];                 // copies: the TMA stores have read the slot's rows
+  unsigned long long rd[kSlots][kComputeWarps];    // fused: warp w - 1 has read its window (overhang)
   int64_t next[kSlots];                            // the slot's next chunk (ticket), -1 = none
   uint32_t shift[kSlots];                          // fused: the landed window's byte shift (0-127)
   uint32_t* witness;                               // Scratch::witness (read at the final pass)
@@ -606,21 +613,46 @@ __device__ __forceinline__ void load_thread_bytes(Shared& sh, int slot, int t, B
 
 // Tensor-map load of `rows` x 128 bytes starting at record row `row` into
 // swizzled rows at dst (rows past the tensor arrive as zeros).
+// MLCK_FNV_L2HINT: TMA loads and stores of the streamed bytes carry an
+// L2 evict-first policy (the look-back words and tables stay resident).
+#ifndef MLCK_FNV_L2HINT
+#define MLCK_FNV_L2HINT 0
+#endif
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void tma_load_rows(void* dst, const CUtensorMap* map, int32_t row,
                                               unsigned long long* mbar) {
+#if MLCK_FNV_L2HINT
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(row), "r"(smem_addr(mbar)), "l"(l2_evict_first())
+      : "memory");
+#else
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
           "r"(smem_addr(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(row), "r"(smem_addr(mbar))
       : "memory");
+#endif
 }
 // Tensor-map store of `rows` x 128 bytes of swizzled rows at src to record
 // row `row` (rows past the tensor are clipped); bulk async-group.
 __device__ __forceinline__ void tma_store_rows(const CUtensorMap* map, int32_t row, const void* src) {
+#if MLCK_FNV_L2HINT
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::
+                   "l"(reinterpret_cast<uint64_t>(map)),
+               "r"(0), "r"(row), "r"(smem_addr(src)), "l"(l2_evict_first())
+               : "memory");
+#else
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
                "r"(0), "r"(row), "r"(smem_addr(src))
                : "memory");
+#endif
 }
 __device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // Fused snapshot: chunk `chunk` of run `r` into `slot` (one thread; one
@@ -633,19 +665,9 @@ __device__ __forceinline__ void tma_load_src(Shared& sh, int slot, const Copy& c
   sh.shift[slot] = delta;  // released to the waiters by the arrival below
   fence_async_shared();
   mbar_arrive_expect_tx(mb, (kComputeThreads + (delta ? 8 : 0)) * kThreadBytes);
-  const CUtensorMap* m = &cp.src[r.map][0];
   for (int b = 0; b < kComputeThreads / 256; ++b)
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
-            "r"(smem_addr(&sh.data[slot][kGranules * 256 * b])),
-        "l"(reinterpret_cast<uint64_t>(m)), "r"(0), "r"(row + 256 * b), "r"(smem_addr(mb))
-        : "memory");
-  if (delta)
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
-            "r"(smem_addr(&sh.data[slot][kGranules * kComputeThreads])),
-        "l"(reinterpret_cast<uint64_t>(&cp.src[r.map][1])), "r"(0), "r"(row + kComputeThreads), "r"(smem_addr(mb))
-        : "memory");
+    tma_load_rows(&sh.data[slot][kGranules * 256 * b], &cp.src[r.map][0], row + 256 * b, mb);
+  if (delta) tma_load_rows(&sh.data[slot][kGranules * kComputeThreads], &cp.src[r.map][1], row + kComputeThreads, mb);
 }
 // The run holding record chunk c (warp-collective: a 32-ary search over the
 // run starts, one load per lane per level).

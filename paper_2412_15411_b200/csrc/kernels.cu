@@ -25,10 +25,8 @@ using fnv::kSlots;
 __device__ __forceinline__ int bar_pub(int s) { return 1 + s; }
 // Copies: STORE(s) -- the compute warps have the slot's record-aligned rows
 // in shared memory (the look-back warp then issues the TMA stores; the
-// compute warps wait on sres[s] before overwriting the rows); COMPUTE --
-// the compute warps alone (a shifted window is read before it is rewritten).
+// compute warps wait on sres[s] before overwriting the rows in round 1).
 __device__ __forceinline__ int bar_store(int s) { return 1 + fnv::kSlots + s; }
-constexpr int kBarCompute = 1 + 2 * fnv::kSlots;
 
 // Profile laps of one thread's clock (kProf only): consecutive buckets, so
 // they add up to the loop time.
@@ -75,6 +73,7 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
   uint32_t par = 0;       // data mbarrier phase parity per slot
   uint32_t rpar = 0;      // result mbarrier phase parity per slot
   uint32_t spar = 0;      // copies: store mbarrier phase parity per slot
+  uint32_t rdpar = 0;     // fused: neighbour-read mbarrier phase parity per slot
   const bool copy = cp.n_dst > 0;
   uint64_t acc = 0;
 #pragma unroll
@@ -213,20 +212,46 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
         }
       }
       uint32_t w[kThreadWords];
+#ifdef MLCK_FUSED_NOSHIFT  // development A/B only (wrong bytes): the cost of the shifted read
+      const uint32_t delta = 0u;
+#else
       const uint32_t delta = kGather && rnd[s] == 0 ? sh.shift[s] : 0u;  // uniform over the chunk
+#endif
       if (delta)
         read_thread_shifted(sh, s, tid, delta, w);
       else
         read_thread(sh, s, tid, w);
       const bool store = copy && rnd[s] == 0;
       if (rnd[s] == 0) {
-        if (delta) {  // every thread has read its window before the rows are rewritten aligned
-          bar_sync(kBarCompute, kComputeThreads);
+        if (delta) {
+          // every window is read before its rows are rewritten aligned: the
+          // warp's lanes (syncwarp) and the previous warp's last lane, whose
+          // window overhangs into this warp's first row (a handshake with
+          // the neighbour, not a barrier over all compute warps)
+          __syncwarp();
+          if (lane == 0 && warp + 1 < kComputeWarps) mbar_arrive(&sh.rd[s][warp + 1]);
+          if (warp > 0) fnv::mbar_wait(&sh.rd[s][warp], (rdpar >> s) & 1u);
+          rdpar ^= 1u << s;
           write_thread(sh, s, tid, w);
         }
-        if (store) {  // record-aligned rows in place: the look-back warp stores them
+        if (store) {  // record-aligned rows in place: out to every destination
           fence_async_shared();
+#if MLCK_FNV_WARP_STORES
+          // each warp stores its own 32 rows (4 KiB) and waits until the TMA
+          // has read them: no hand-off, the rows are interleaved right after
+          __syncwarp();
+          if (lane == 0) {
+            const uint64_t r0 = static_cast<uint64_t>(chunk[s]) * kComputeThreads + 32 * warp;
+            if (r0 < rows_full) {
+              for (int d = 0; d < cp.n_dst; ++d)
+                tma_store_rows(&cp.dst[d], static_cast<int32_t>(r0), &sh.data[s][kGranules * 32 * warp]);
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
+          }
+#else
           bar_arrive(bar_store(s), kBarThreads);
+#endif
           const uint64_t row = static_cast<uint64_t>(chunk[s]) * kComputeThreads + tid;
           if (row == rows_full && (n & (kThreadBytes - 1))) {  // the partial last row (TMA stores clip it)
             const uint8_t* rb = reinterpret_cast<const uint8_t*>(sh.data[s]);
@@ -237,8 +262,14 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
           }
         }
         interleave(w);  // fresh bytes: interleave the segments once, in place
+#if MLCK_FNV_WARP_STORES
+        __syncwarp();  // lane 0 saw the TMA read the warp's rows
+        write_thread(sh, s, tid, w);
+      } else if (false) {
+#else
         if (!store) write_thread(sh, s, tid, w);
       } else if (copy && rnd[s] == 1) {
+#endif
         // copies: the rows stayed record-aligned for the TMA stores through
         // round 0; interleaved in place now, once the stores have read them
         interleave(w);
@@ -278,6 +309,7 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
       lap.mark(0);
     }
   }
+  if (copy && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
   if (kProf && tid == 0) {
     lap.mark(3);
     atomicAdd(scr.prof + 2, static_cast<unsigned long long>(lap.t[0]));
@@ -326,13 +358,13 @@ __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t se
     uint32_t word = 0;  // the chunk's status bits as published
     int64_t next = -1;
     Run nrun{};  // kGather: the run of the next chunk, looked up beside the last round
-    if (copy) {  // the compute warps have the rows aligned: out to every destination
+    if (copy && !MLCK_FNV_WARP_STORES) {  // the compute warps have the rows aligned: out to every destination
       bar_sync(bar_store(s), kBarThreads);
       if (lane == 0) tma_store_chunk(sh, s, cp, chunk, rows_full);
       __syncwarp();
     }
     for (int r = 0; r < kRounds; ++r) {
-      if (copy && r == 1 && lane == 0) {  // round 1 rewrites the rows: once the stores have read them
+      if (copy && !MLCK_FNV_WARP_STORES && r == 1 && lane == 0) {  // round 1 rewrites the rows: once read
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         mbar_arrive(&sh.sres[s]);
       }
@@ -416,6 +448,7 @@ __global__ void MLCK_FNV_BOUNDS
       for (int w = 0; w < kComputeWarps; ++w) mbar_init(&sh.mbar[s][w], kGather || use_tma ? 1 : 32);
       mbar_init(&sh.res[s], 1);
       mbar_init(&sh.sres[s], 1);
+      for (int w = 0; w < kComputeWarps; ++w) mbar_init(&sh.rd[s][w], 1);
     }
 #if MLCK_FNV_MMA
   mma_tables(sh, tid);
@@ -751,7 +784,7 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
     cp.n_dst = copies->n;
     for (int d = 0; d < copies->n; ++d) {
       if (reinterpret_cast<uintptr_t>(copies->p[d]) & 15u) throw_invalid("copy destinations must be 16-byte aligned");
-      make_row_tmap(copies->p[d], n, &cp.dst[d]);
+      encode_rows(copies->p[d], n / fnv::kThreadBytes, MLCK_FNV_WARP_STORES ? 32 : fnv::kTmaBoxRows, &cp.dst[d]);
       cp.dst_ptr[d] = copies->p[d];
     }
   }
@@ -767,6 +800,9 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
     }
     cp.runs = reinterpret_cast<const fnv::Run*>(fused->runs);
     cp.n_runs = fused->n_runs;
+#ifdef MLCK_FUSED_NOSTORE  // development A/B only (no record written): the cost of the TMA stores
+    cp.n_dst = 0;
+#endif
   }
   // the record as a [n / 128 rows x 128 bytes] tensor, loaded in 256-row
   // boxes in the 128-byte swizzle the shared-memory rows use

@@ -113,10 +113,15 @@ def _worker(rank, world, port, q):
                     ok, msg = False, f"mode {mode}: rank {rank} replica {j} of rank {src} differs"
             dist.barrier()
         ctx.set_replica_mode(-1)
-        blob.clear_replicas()
-        blob.close()
+        dist.barrier()  # every peer is done reading its inbound buffers
+        # closing the mappings drops the blob's replicas inside them: the next
+        # record stays local instead of storing to unmapped memory
         for p in opened:
             ctx.ipc_close(p)
+        mlck.snapshot_record(st, active, compute_only, 1, 1, 36, 4, blob)
+        if blob.to_host() != ref or blob.replication() != 0:
+            ok, msg = False, f"rank {rank}: replicas inside a closed IPC mapping were kept"
+        blob.close()
         dist.barrier()
     except Exception as e:  # report, do not hang the other ranks' queue reads
         ok, msg = False, f"rank {rank}, mode {cur_mode}: {type(e).__name__}: {e}"
