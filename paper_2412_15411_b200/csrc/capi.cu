@@ -1889,7 +1889,7 @@ void run_replay(mlck_ctx* ctx, std::vector<adam::ConvOp>& ops, const std::vector
   uint64_t units = 0;  // CTAs: each operator's units round up to whole CTAs
   for (auto& op : ops) {
     op.unit_begin = units;
-    units += div_up(div_up(op.P, 4), static_cast<uint64_t>(replay_cta_threads()));
+    units += div_up(div_up(op.P, static_cast<uint64_t>(replay_unit_elems())), static_cast<uint64_t>(replay_cta_threads()));
   }
   const size_t ob = ops.size() * sizeof(adam::ConvOp);
   const size_t go = align_up(ob, 16), gb = gptr.size() * sizeof(float*);

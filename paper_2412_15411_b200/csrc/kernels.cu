@@ -1002,6 +1002,7 @@ void launch_replay(const adam::ConvOp* ops, int n_ops, const float* const* gptr,
 }
 
 int replay_cta_threads() { return adam::kReplayThreads; }
+int replay_unit_elems() { return adam::kReplayVec; }
 
 void launch_fastmath_check(uint64_t n, uint64_t seed, unsigned long long* counts, cudaStream_t stream) {
   adam::fastmath_check_kernel<<<148 * 8, 256, 0, stream>>>(n, seed, counts);

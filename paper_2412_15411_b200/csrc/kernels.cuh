@@ -90,6 +90,7 @@ void launch_replay(const adam::ConvOp* ops, int n_ops, const float* const* gptr,
                    adam::StepConst* steps, const adam::Opt& o, int cb, uint64_t total_units, cudaStream_t stream);
 // Threads per replay CTA (launch_replay's total_units counts CTAs: each
 // operator's 4-element units round up to whole CTAs).
+int replay_unit_elems();  // consecutive elements per replay thread
 int replay_cta_threads();
 // Self-check of the replay kernel's spelled-out IEEE fast paths (adam.cuh).
 void launch_fastmath_check(uint64_t n, uint64_t seed, unsigned long long* counts, cudaStream_t stream);
