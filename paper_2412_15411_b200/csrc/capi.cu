@@ -328,7 +328,7 @@ struct mlck_blob {
     if (ctx->witness) reserve_witness(cap);  // with the record buffer: never inside a snapshot
   }
   void reserve_witness(uint64_t body) {
-    const uint64_t words = fnv_witness_words(body) + 1;
+    const uint64_t words = fnv_witness_words(body) + 1 + 520;  // + the verifier's bulk over-read of a chunk
     if (words <= witness_cap) return;
     ctx->join_hash();
     MLCK_CUDA(cudaStreamSynchronize(ctx->stream));

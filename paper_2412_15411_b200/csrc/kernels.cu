@@ -536,41 +536,34 @@ __device__ __forceinline__ void witness_row_bytes(uint4* rows, int tid, const ui
 }
 
 constexpr int kWitnessBufs = 3;  // chunks in flight per SM
+// the chunk's witness words and the next chunk's first (a 16-byte multiple)
+constexpr int kWitnessWords = fnv::kComputeThreads + 4;
 struct WitnessSmem {
   uint4 data[kWitnessBufs][fnv::kComputeThreads * fnv::kGranules];  // 1 KiB-aligned rows (TMA swizzle)
+  uint32_t wit[kWitnessBufs][kWitnessWords];                         // the rows' witnessed starts
   uint2 wfrag[2][4][32];
   unsigned long long kpos[32][4];
   unsigned long long red[fnv::kComputeWarps];
-  unsigned long long mbar[kWitnessBufs];
+  unsigned long long full[kWitnessBufs];   // the chunk's rows and witness words landed
+  unsigned long long empty[kWitnessBufs];  // every compute warp is done with the buffer
 };
 constexpr size_t kWitnessSmem = sizeof(WitnessSmem) + 1024;
-
-// One chunk's full rows into buffer b by the tensor map (two 256-row boxes,
-// one mbarrier phase); rows at or past rows_full are the threads'.
-__device__ __forceinline__ void witness_tma_chunk(WitnessSmem& sh, int b, const CUtensorMap* map, int64_t chunk,
-                                                  uint64_t rows_full) {
-  using namespace fnv;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  const uint64_t row0 = static_cast<uint64_t>(chunk) * kComputeThreads;
-  int boxes = 0;
-#pragma unroll
-  for (int x = 0; x < kComputeThreads / kTmaBoxRows; ++x) boxes += row0 + kTmaBoxRows * x < rows_full;
-  mbar_arrive_expect_tx(&sh.mbar[b], boxes * kTmaBoxRows * kThreadBytes);
-  for (int x = 0; x < boxes; ++x)
-    tma_load_rows(&sh.data[b][kGranules * kTmaBoxRows * x], map, static_cast<int32_t>(row0 + kTmaBoxRows * x),
-                  &sh.mbar[b]);
-}
+constexpr int kWitnessThreads = fnv::kComputeThreads + 32;  // + the producer warp
 
 // Re-hash of a record against its witness (fnv.cuh, automaton_and_ends).
-// Persistent: one CTA per SM walks chunks blockIdx.x, +gridDim.x, ...; a
-// thread issues the tensor-map loads of the chunks three turns ahead, so
-// the compute warps only read shared memory.  *bad <- 1 when a witnessed
-// start disagrees with the automaton (the caller then runs fnv_kernel).
+// Persistent and warp-specialized: one CTA per SM walks chunks blockIdx.x,
+// +gridDim.x, ...; its producer warp keeps kWitnessBufs chunks in flight --
+// the rows by tensor-map loads, the witness words by a bulk copy, one
+// mbarrier per buffer -- and refills a buffer once all compute warps have
+// released it, so compute warps never wait on each other or on a global
+// load.  *bad <- 1 when a witnessed start disagrees with the automaton (the
+// caller then runs fnv_kernel).  The witness array holds >= kWitnessWords
+// words past the record's last chunk start (mlck_blob::reserve_witness).
 __device__ uint2 g_wfrag[2][4][32];             // mma_pass B fragments (init_constants)
 __device__ unsigned long long g_kpos[32][4];    // mma_epilogue weights
 __constant__ unsigned long long c_pinv_warp[fnv::kComputeWarps];  // P^-(4096 (w + 1))
 
-__global__ void __launch_bounds__(fnv::kComputeThreads, 1)
+__global__ void __launch_bounds__(kWitnessThreads, 1)
     fnv_witness_kernel(const uint8_t* data, uint64_t n, uint64_t seed, const uint32_t* witness, fnv::Scratch scr,
                        unsigned long long* bad, int64_t n_chunks, const __grid_constant__ CUtensorMap tmap,
                        uint64_t rows_full) {
@@ -583,56 +576,74 @@ __global__ void __launch_bounds__(fnv::kComputeThreads, 1)
   if (tid < 2 * 4 * 32) (&sh.wfrag[0][0][0])[tid] = (&g_wfrag[0][0][0])[tid];
   if (tid < 32 * 4) (&sh.kpos[0][0])[tid] = (&g_kpos[0][0])[tid];
   if (tid == 0)
-    for (int b = 0; b < kWitnessBufs; ++b) mbar_init(&sh.mbar[b], 1);
-  const uint64_t pinv_w = c_pinv_warp[warp];
+    for (int b = 0; b < kWitnessBufs; ++b) {
+      mbar_init(&sh.full[b], 1);
+      mbar_init(&sh.empty[b], kComputeWarps);
+    }
   __syncthreads();  // tables, barriers
-  int64_t chunk = blockIdx.x;
-  if (tid == 0)
-    for (int b = 0; b < kWitnessBufs; ++b)
-      if (chunk + b * G < n_chunks) witness_tma_chunk(sh, b, &tmap, chunk + b * G, rows_full);
   uint64_t acc = 0;
   bool ok = true;
-  for (int i = 0, buf = 0; chunk < n_chunks; ++i, chunk += G, buf = buf + 1 == kWitnessBufs ? 0 : buf + 1) {
-    if (i > 0) {  // every thread is done with last turn's buffer: refill it three chunks on
-      __syncthreads();
-      const int pb = buf == 0 ? kWitnessBufs - 1 : buf - 1;
-      const int64_t nx = chunk + (kWitnessBufs - 1) * G;
-      if (tid == 0 && nx < n_chunks) witness_tma_chunk(sh, pb, &tmap, nx, rows_full);
-    }
-    const uint64_t row = static_cast<uint64_t>(chunk) * kComputeThreads + tid;
-    uint32_t st = 0, expect = 0, check = 0;
-    if (row * kThreadBytes < n) {
-      st = __ldg(witness + row);
-      const uint64_t seg0 = 4 * row;
-      const uint32_t next = seg0 + 4 < n_seg ? (__ldg(witness + row + 1) & 0xffu) : 0u;
-      expect = (st >> 8) | (next << 24);  // segment i ends where segment i+1 starts
+  if (warp == kComputeWarps) {  // ---- producer
+    if (lane == 0)
+      for (int64_t i = 0, chunk = blockIdx.x; chunk < n_chunks; ++i, chunk += G) {
+        const int b = static_cast<int>(i % kWitnessBufs);
+        if (i >= kWitnessBufs) mbar_wait(&sh.empty[b], static_cast<uint32_t>(i / kWitnessBufs - 1) & 1u);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint64_t row0 = static_cast<uint64_t>(chunk) * kComputeThreads;
+        int boxes = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (seg0 + q + 1 < n_seg) check |= 0xffu << (8 * q);
-      if (row == 0 && (st & 0xffu) != (seed & 0xffu)) ok = false;
+        for (int x = 0; x < kComputeThreads / kTmaBoxRows; ++x) boxes += row0 + kTmaBoxRows * x < rows_full;
+        mbar_arrive_expect_tx(&sh.full[b], boxes * kTmaBoxRows * kThreadBytes + 4 * kWitnessWords);
+        for (int x = 0; x < boxes; ++x)
+          tma_load_rows(&sh.data[b][kGranules * kTmaBoxRows * x], &tmap, static_cast<int32_t>(row0 + kTmaBoxRows * x),
+                        &sh.full[b]);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_addr(&sh.wit[b][0])),
+            "l"(witness + row0), "r"(4 * kWitnessWords), "r"(smem_addr(&sh.full[b]))
+            : "memory");
+      }
+  } else {  // ---- compute warps
+    const uint64_t pinv_w = c_pinv_warp[warp];
+    for (int64_t i = 0, chunk = blockIdx.x; chunk < n_chunks; ++i, chunk += G) {
+      const int b = static_cast<int>(i % kWitnessBufs);
+      uint4* rows = sh.data[b];
+      mbar_wait(&sh.full[b], static_cast<uint32_t>(i / kWitnessBufs) & 1u);
+      const uint64_t row = static_cast<uint64_t>(chunk) * kComputeThreads + tid;
+      uint32_t st = 0, expect = 0, check = 0;
+      if (row * kThreadBytes < n) {
+        st = sh.wit[b][tid];
+        const uint64_t seg0 = 4 * row;
+        const uint32_t next = seg0 + 4 < n_seg ? (sh.wit[b][tid + 1] & 0xffu) : 0u;
+        expect = (st >> 8) | (next << 24);  // segment i ends where segment i+1 starts
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (seg0 + q + 1 < n_seg) check |= 0xffu << (8 * q);
+        if (row == 0 && (st & 0xffu) != (seed & 0xffu)) ok = false;
+      }
+      if (row >= rows_full) witness_row_bytes(rows, tid, data, n, row * kThreadBytes);
+      uint32_t w[kThreadWords];
+      read_thread_rows(rows, tid, w);
+      interleave(w);
+      write_thread_rows(rows, tid, w);
+      __syncwarp();
+      int mac[2][4] = {};
+      mma_pass_rows(rows, sh.wfrag, warp, lane, 0, mac);  // the data vector
+      const uint32_t ends = automaton_and_ends(w, st);
+      if ((ends ^ expect) & check) ok = false;
+      __syncwarp();  // every lane has read the data words
+      write_thread_rows(rows, tid, w);
+      __syncwarp();
+      mma_pass_rows(rows, sh.wfrag, warp, lane, 1, mac);  // the u & b vector, weights -2 P^(...)
+      acc += mma_epilogue(sh, lane, mac) * (pinv_w * chunk_weight(chunk));
+      __syncwarp();  // the warp's reads of the buffer are done
+      if (lane == 0) mbar_arrive(&sh.empty[b]);
     }
-    uint4* rows = sh.data[buf];
-    mbar_wait(&sh.mbar[buf], static_cast<uint32_t>(i / kWitnessBufs) & 1u);
-    if (row >= rows_full) witness_row_bytes(rows, tid, data, n, row * kThreadBytes);
-    uint32_t w[kThreadWords];
-    read_thread_rows(rows, tid, w);
-    interleave(w);
-    write_thread_rows(rows, tid, w);
-    __syncwarp();
-    int mac[2][4] = {};
-    mma_pass_rows(rows, sh.wfrag, warp, lane, 0, mac);  // the data vector
-    const uint32_t ends = automaton_and_ends(w, st);
-    if ((ends ^ expect) & check) ok = false;
-    __syncwarp();  // every lane has read the data words
-    write_thread_rows(rows, tid, w);
-    __syncwarp();
-    mma_pass_rows(rows, sh.wfrag, warp, lane, 1, mac);  // the u & b vector, weights -2 P^(...)
-    acc += mma_epilogue(sh, lane, mac) * (pinv_w * chunk_weight(chunk));
   }
   if (__any_sync(0xffffffffu, !ok) && lane == 0) atomicExch(bad, 1ull);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) sh.red[warp] = acc;
+  if (lane == 0 && warp < kComputeWarps) sh.red[warp] = acc;
   __syncthreads();
   if (tid == 0) {
     uint64_t sum = 0;
@@ -885,8 +896,8 @@ void launch_fnv_witness(const uint8_t* data, uint64_t n, uint64_t seed, const ui
   scr.result = result;
   const int64_t n_chunks = static_cast<int64_t>(fnv_chunks(n));
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_chunks, ctas > 0 ? std::min(ctas, sms) : sms));
-  fnv_witness_kernel<<<grid, fnv::kComputeThreads, kWitnessSmem, stream>>>(data, n, seed, witness, scr, bad,
-                                                                           n_chunks, tmap, rows_full);
+  fnv_witness_kernel<<<grid, kWitnessThreads, kWitnessSmem, stream>>>(data, n, seed, witness, scr, bad, n_chunks,
+                                                                      tmap, rows_full);
   MLCK_CUDA(cudaGetLastError());
 }
 
