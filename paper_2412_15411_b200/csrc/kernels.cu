@@ -658,6 +658,267 @@ __global__ void __launch_bounds__(kWitnessThreads, 1)
   }
 }
 
+
+// ---- the verifier on the 5th-generation tensor cores (tcgen05 + TMEM).
+// Per chunk, two 128 x 16 x 512 u8 MMAs do every dot product of the chunk:
+// A = the chunk's 512 rows as they sit in shared memory (M = the 128 byte
+// positions of a row, K = the row: the TMA's 128-byte-swizzled rows ARE the
+// canonical MN-major SWIZZLE_128B operand layout), B = the 8-bit limbs of
+// P^-(128 k) (and of -2 P^-(128 k)) for row k.  MMA 1 reads the bytes as
+// landed (natural order), MMA 2 the rows the compute warps overwrite with
+// u & b (interleaved order: byte 4j + s of a row = segment s, byte j).  The
+// accumulators (s32, < 2^26) go to TMEM; four warps fold a chunk's 128 x 8
+// limb sums with P^-(byte position) two chunks later.  Compute threads keep
+// only the automaton: no fragment loads, no mma.sync, one row write.
+#ifndef MLCK_WITNESS_TC
+#define MLCK_WITNESS_TC 1
+#endif
+constexpr int kTcThreads = fnv::kComputeThreads + 96;  // + the producer warp + one warp per MMA
+constexpr int kTcN = 16;                              // MMA N (limbs 0-7 used, 8-15 zero)
+constexpr uint32_t kTcCols = 128;                     // TMEM columns: [buffer][2 accumulators][16]
+struct WitnessTcSmem {
+  uint4 data[kWitnessBufs][fnv::kComputeThreads * fnv::kGranules];  // 1 KiB-aligned rows (TMA swizzle)
+  uint8_t wb[2][fnv::kComputeThreads][kTcN];                         // B: [data | -2][row k][limb n], 16 KiB
+  uint32_t wit[kWitnessBufs][kWitnessWords];
+  unsigned long long full[kWitnessBufs], empty[kWitnessBufs];        // producer <-> MMA / compute warps
+  unsigned long long mma1[kWitnessBufs], mma2[kWitnessBufs];         // MMA 1 / 2 complete
+  unsigned long long uab[kWitnessBufs], tfree[kWitnessBufs];         // u & b rows written / accumulators read
+  unsigned long long tail;                                           // the last chunk's partial rows written
+  unsigned long long red[32];
+  uint32_t tmem;
+  uint32_t abort;
+};
+constexpr size_t kWitnessTcSmem = sizeof(WitnessTcSmem) + 1024;
+__device__ uint8_t g_tcw[2][fnv::kComputeThreads][kTcN];  // B tables (init_constants)
+
+__device__ __forceinline__ bool mbar_try(unsigned long long* m, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(ok)
+               : "r"(fnv::smem_addr(m)), "r"(parity)
+               : "memory");
+  return ok != 0;
+}
+// A bounded wait: a protocol error ends the kernel with the record marked
+// unverified (the caller re-hashes it) instead of hanging the GPU.
+__device__ __forceinline__ bool mbar_wait_tc(unsigned long long* m, uint32_t parity, volatile uint32_t* abort) {
+  for (uint32_t n = 1;; ++n) {
+    if (mbar_try(m, parity)) return true;
+    if ((n & 255u) == 0 && (*abort || n > (1u << 24))) {
+      *abort = 1;
+      return false;
+    }
+  }
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+// shared-memory matrix descriptors (sm_100 layout: start >> 4 @0, LBO >> 4
+// @16, SBO >> 4 @32, version 1 @46, layout type @61)
+__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3fffu) | (static_cast<uint64_t>((lbo >> 4) & 0x3fffu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3fffu) << 32) | (1ull << 46) | (static_cast<uint64_t>(layout) << 61);
+}
+// kind::i8, u8 x u8 -> s32, A and B MN-major, N = 16, M = 128
+constexpr uint32_t kTcIdesc = (2u << 4) | (1u << 15) | (1u << 16) | ((kTcN >> 3) << 17) | ((128 >> 4) << 24);
+// D[tmem] (+)= A[128 x 512 rows at a] . B[512 x 16 at b]: 16 MMAs of K = 32
+__device__ __forceinline__ void tc_chunk_mma(uint32_t d_tmem, uint32_t a, uint32_t b) {
+#pragma unroll
+  for (int k = 0; k < fnv::kComputeThreads / 32; ++k) {
+    // A: SWIZZLE_128B MN-major, 8-row atoms 1 KiB apart, K-step = 32 rows (4 KiB)
+    const uint64_t da = tc_desc(a + 4096u * k, 0, 1024, 2);
+    // B: no swizzle, MN-major, core matrices of 8 rows x 16 B, 128 B apart along K
+    const uint64_t db = tc_desc(b + 512u * k, 128, 0, 0);
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }" ::"r"(d_tmem),
+        "l"(da), "l"(db), "r"(kTcIdesc), "r"(k)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tc_commit(unsigned long long* m) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(fnv::smem_addr(m))
+               : "memory");
+}
+// 8 columns of this warp's 32 TMEM lanes
+__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    fnv_witness_tc_kernel(const uint8_t* data, uint64_t n, uint64_t seed, const uint32_t* witness, fnv::Scratch scr,
+                          unsigned long long* bad, int64_t n_chunks, const __grid_constant__ CUtensorMap tmap,
+                          uint64_t rows_full) {
+  using namespace fnv;
+  extern __shared__ __align__(1024) unsigned char smem_t[];
+  WitnessTcSmem& sh = *reinterpret_cast<WitnessTcSmem*>(smem_t + ((1024u - (smem_addr(smem_t) & 1023u)) & 1023u));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint64_t n_seg = (n + 31) / 32;
+  const int64_t G = gridDim.x;
+  constexpr int kProducer = kComputeWarps, kMma = kComputeWarps + 1, kMma2 = kComputeWarps + 2;
+  {  // B tables
+    const uint4* src = reinterpret_cast<const uint4*>(&g_tcw[0][0][0]);
+    uint4* dst = reinterpret_cast<uint4*>(&sh.wb[0][0][0]);
+    for (int i = tid; i < static_cast<int>(sizeof(sh.wb) / 16); i += kTcThreads) dst[i] = src[i];
+  }
+  if (tid == 0) {
+    for (int b = 0; b < kWitnessBufs; ++b) {
+      mbar_init(&sh.full[b], 1);
+      mbar_init(&sh.empty[b], 1);
+      mbar_init(&sh.mma1[b], 1);
+      mbar_init(&sh.mma2[b], 1);
+      mbar_init(&sh.uab[b], kComputeWarps);
+      mbar_init(&sh.tfree[b], 4);
+    }
+    mbar_init(&sh.tail, kComputeWarps);
+    sh.abort = 0;
+  }
+  if (warp == kMma) {  // TMEM for 3 x 2 accumulators (one warp allocates and frees)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&sh.tmem)),
+                 "r"(kTcCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_async_shared();  // the B tables, for the tensor cores
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sh.tmem;
+  volatile uint32_t* abort = &sh.abort;
+  const int64_t my_chunks = blockIdx.x < n_chunks ? (n_chunks - 1 - blockIdx.x) / G + 1 : 0;
+  uint64_t acc = 0;
+  bool ok = true;
+  if (warp == kProducer) {  // ---- rows + witness words of every chunk, kWitnessBufs ahead
+    if (lane == 0)
+      for (int64_t i = 0; i < my_chunks; ++i) {
+        const int b = static_cast<int>(i % kWitnessBufs);
+        if (i >= kWitnessBufs && !mbar_wait_tc(&sh.empty[b], static_cast<uint32_t>(i / kWitnessBufs - 1) & 1u, abort))
+          break;
+        const uint64_t row0 = static_cast<uint64_t>(blockIdx.x + i * G) * kComputeThreads;
+        int boxes = 0;
+#pragma unroll
+        for (int x = 0; x < kComputeThreads / kTmaBoxRows; ++x) boxes += row0 + kTmaBoxRows * x < rows_full;
+        mbar_arrive_expect_tx(&sh.full[b], boxes * kTmaBoxRows * kThreadBytes + 4 * kWitnessWords);
+        for (int x = 0; x < boxes; ++x)
+          tma_load_rows(&sh.data[b][kGranules * kTmaBoxRows * x], &tmap, static_cast<int32_t>(row0 + kTmaBoxRows * x),
+                        &sh.full[b]);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_addr(&sh.wit[b][0])),
+            "l"(witness + row0), "r"(4 * kWitnessWords), "r"(smem_addr(&sh.full[b]))
+            : "memory");
+      }
+  } else if (warp == kMma) {  // ---- MMA 1 of every chunk, as soon as its bytes land
+    if (lane == 0)
+      for (int64_t i = 0; i < my_chunks; ++i) {
+        const int b = static_cast<int>(i % kWitnessBufs);
+        const uint32_t ph = static_cast<uint32_t>(i / kWitnessBufs) & 1u;
+        if (!mbar_wait_tc(&sh.full[b], ph, abort)) break;
+        if (i >= kWitnessBufs && !mbar_wait_tc(&sh.tfree[b], ph ^ 1u, abort)) break;  // chunk i-3 folded
+        const bool last = (static_cast<uint64_t>(blockIdx.x + i * G) + 1) * kComputeThreads > rows_full;
+        if (last && !mbar_wait_tc(&sh.tail, 0, abort)) break;  // the partial rows, written by their threads
+        tc_fence_after();
+        tc_chunk_mma(tmem + 2 * kTcN * b, smem_addr(&sh.data[b][0]), smem_addr(&sh.wb[0][0][0]));  // bytes as landed
+        tc_commit(&sh.mma1[b]);
+      }
+  } else if (warp == kMma2) {  // ---- MMA 2 of every chunk, once its u & b rows are written
+    if (lane == 0)
+      for (int64_t i = 0; i < my_chunks; ++i) {
+        const int b = static_cast<int>(i % kWitnessBufs);
+        const uint32_t ph = static_cast<uint32_t>(i / kWitnessBufs) & 1u;
+        // (uab follows mma1 of the same chunk, which followed the fold of chunk i-3)
+        if (!mbar_wait_tc(&sh.uab[b], ph, abort)) break;
+        tc_fence_after();
+        tc_chunk_mma(tmem + 2 * kTcN * b + kTcN, smem_addr(&sh.data[b][0]), smem_addr(&sh.wb[1][0][0]));
+        tc_commit(&sh.mma2[b]);
+        tc_commit(&sh.empty[b]);  // the rows are free for the producer
+      }
+  } else {  // ---- compute warps: the automaton; warps 0-3 fold the accumulators
+    const int m = 32 * (warp & 3) + lane;                                      // this lane's TMEM lane
+    const uint64_t w_nat = pow_u64(kPrimeInv, static_cast<uint64_t>(m));       // MMA 1: natural byte m
+    const uint64_t w_il = pow_u64(kPrimeInv, static_cast<uint64_t>(32 * (m & 3) + (m >> 2)));  // MMA 2: 4j+s
+    auto fold = [&](int64_t j) {
+      const int b = static_cast<int>(j % kWitnessBufs);
+      if (!mbar_wait_tc(&sh.mma2[b], static_cast<uint32_t>(j / kWitnessBufs) & 1u, abort)) return;
+      tc_fence_after();
+      uint32_t r0[8], r1[8];
+      const uint32_t t = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + 2 * kTcN * b;
+      tc_ld8(t, r0);
+      tc_ld8(t + kTcN, r1);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      uint64_t s0 = 0, s1 = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        s0 += static_cast<uint64_t>(r0[q]) << (8 * q);
+        s1 += static_cast<uint64_t>(r1[q]) << (8 * q);
+      }
+      acc += (s0 * w_nat + s1 * w_il) * chunk_weight(static_cast<int64_t>(blockIdx.x) + j * G);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.tfree[b]);
+    };
+    for (int64_t i = 0; i < my_chunks && !*abort; ++i) {
+      const int b = static_cast<int>(i % kWitnessBufs);
+      const uint32_t ph = static_cast<uint32_t>(i / kWitnessBufs) & 1u;
+      if (warp < 4 && i > 1) fold(i - 2);  // the sums of two chunks back, long done
+      if (!mbar_wait_tc(&sh.full[b], ph, abort)) break;
+      const int64_t chunk = blockIdx.x + i * G;
+      uint4* rows = sh.data[b];
+      const uint64_t row = static_cast<uint64_t>(chunk) * kComputeThreads + tid;
+      uint32_t st = 0, expect = 0, check = 0;
+      if (row * kThreadBytes < n) {
+        st = sh.wit[b][tid];
+        const uint64_t seg0 = 4 * row;
+        const uint32_t next = seg0 + 4 < n_seg ? (sh.wit[b][tid + 1] & 0xffu) : 0u;
+        expect = (st >> 8) | (next << 24);  // segment i ends where segment i+1 starts
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (seg0 + q + 1 < n_seg) check |= 0xffu << (8 * q);
+        if (row == 0 && (st & 0xffu) != (seed & 0xffu)) ok = false;
+      }
+      if ((static_cast<uint64_t>(chunk) + 1) * kComputeThreads > rows_full) {  // the partial rows: before MMA 1
+        if (row >= rows_full) witness_row_bytes(rows, tid, data, n, row * kThreadBytes);
+        fence_async_shared();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.tail);
+      }
+      uint32_t w[kThreadWords];
+      read_thread_rows(rows, tid, w);
+      interleave(w);
+      const uint32_t ends = automaton_and_ends(w, st);
+      if ((ends ^ expect) & check) ok = false;
+      if (!mbar_wait_tc(&sh.mma1[b], ph, abort)) break;  // MMA 1 has read the bytes
+      write_thread_rows(rows, tid, w);
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.uab[b]);
+    }
+    for (int64_t j = my_chunks > 2 ? my_chunks - 2 : 0; warp < 4 && j < my_chunks && !*abort; ++j) fold(j);
+  }
+  if (__any_sync(0xffffffffu, !ok) && lane == 0) atomicExch(bad, 1ull);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) sh.red[warp] = acc;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (*abort && tid == 0) atomicExch(bad, 1ull);  // a wait timed out: the sum is not the record's
+  if (warp == kMma)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTcCols) : "memory");
+  if (tid == 0) {
+    uint64_t sum = 0;
+    for (int q = 0; q < 4; ++q) sum += sh.red[q];
+    atomicAdd(scr.accum, static_cast<unsigned long long>(sum));
+    __threadfence();
+    if (atomicAdd(scr.finished, 1u) + 1 == gridDim.x) {
+      __threadfence();
+      const uint64_t total = atomicAdd(scr.accum, 0ull);
+      *scr.result = pow_p(n) * (total + seed);
+    }
+  }
+}
+
 }  // namespace
 
 void init_constants() {
@@ -696,6 +957,17 @@ void init_constants() {
     }
   for (int w = 0; w < fnv::kComputeWarps; ++w)
     pw[w] = fnv::pow_u64(fnv::kPrimeInv, static_cast<uint64_t>(fnv::kThreadBytes) * 32 * (w + 1));
+  // tcgen05 verifier B tables: limb n of P^-(128 k) and of -2 P^-(128 k)
+  static uint8_t tw[2][fnv::kComputeThreads][kTcN];
+  std::memset(tw, 0, sizeof(tw));
+  for (int k = 0; k < fnv::kComputeThreads; ++k) {
+    const uint64_t pk = fnv::pow_u64(fnv::kPrimeInv, 128ull * k);
+    for (int nn = 0; nn < 8; ++nn) {
+      tw[0][k][nn] = static_cast<uint8_t>(pk >> (8 * nn));
+      tw[1][k][nn] = static_cast<uint8_t>((pk * ~1ull) >> (8 * nn));
+    }
+  }
+  MLCK_CUDA(cudaMemcpyToSymbol(g_tcw, tw, sizeof(tw)));
   MLCK_CUDA(cudaMemcpyToSymbol(g_wfrag, wf, sizeof(wf)));
   MLCK_CUDA(cudaMemcpyToSymbol(g_kpos, kp, sizeof(kp)));
   MLCK_CUDA(cudaMemcpyToSymbol(c_pinv_warp, pw, sizeof(pw)));
@@ -886,6 +1158,8 @@ void launch_fnv_witness(const uint8_t* data, uint64_t n, uint64_t seed, const ui
   if (!sms) {
     MLCK_CUDA(cudaFuncSetAttribute(fnv_witness_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(kWitnessSmem)));
+    MLCK_CUDA(cudaFuncSetAttribute(fnv_witness_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(kWitnessTcSmem)));
     MLCK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   CUtensorMap tmap;
@@ -896,8 +1170,12 @@ void launch_fnv_witness(const uint8_t* data, uint64_t n, uint64_t seed, const ui
   scr.result = result;
   const int64_t n_chunks = static_cast<int64_t>(fnv_chunks(n));
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_chunks, ctas > 0 ? std::min(ctas, sms) : sms));
-  fnv_witness_kernel<<<grid, kWitnessThreads, kWitnessSmem, stream>>>(data, n, seed, witness, scr, bad, n_chunks,
-                                                                      tmap, rows_full);
+  if (MLCK_WITNESS_TC && rows_full > 0)  // the dot products on tcgen05 (the record's rows load by TMA)
+    fnv_witness_tc_kernel<<<grid, kTcThreads, kWitnessTcSmem, stream>>>(data, n, seed, witness, scr, bad, n_chunks,
+                                                                        tmap, rows_full);
+  else
+    fnv_witness_kernel<<<grid, kWitnessThreads, kWitnessSmem, stream>>>(data, n, seed, witness, scr, bad, n_chunks,
+                                                                        tmap, rows_full);
   MLCK_CUDA(cudaGetLastError());
 }
 
