@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.tfree[b]);
     };
-    for (int64_t i = 0; i < my_chunks && !*abort; ++i) {
+    for (int64_t i = 0; i < my_chunks; ++i) {  // (a timed-out wait breaks the loop)
       const int b = static_cast<int>(i % kWitnessBufs);
       const uint32_t ph = static_cast<uint32_t>(i / kWitnessBufs) & 1u;
       if (warp < 4 && i > 1) fold(i - 2);  // the sums of two chunks back, long done
@@ -872,9 +872,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint64_t seg0 = 4 * row;
         const uint32_t next = seg0 + 4 < n_seg ? (sh.wit[b][tid + 1] & 0xffu) : 0u;
         expect = (st >> 8) | (next << 24);  // segment i ends where segment i+1 starts
+        if (seg0 + 4 < n_seg) {
+          check = ~0u;
+        } else {  // the record's last row: no successor past the last segment
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (seg0 + q + 1 < n_seg) check |= 0xffu << (8 * q);
+          for (int q = 0; q < 4; ++q)
+            if (seg0 + q + 1 < n_seg) check |= 0xffu << (8 * q);
+        }
         if (row == 0 && (st & 0xffu) != (seed & 0xffu)) ok = false;
       }
       if ((static_cast<uint64_t>(chunk) + 1) * kComputeThreads > rows_full) {  // the partial rows: before MMA 1
