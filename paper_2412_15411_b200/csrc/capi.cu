@@ -552,7 +552,10 @@ cudaStream_t run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, boo
   // chunks from their sources by TMA and stores them to the record and its
   // replicas -- no pack pass
   FusedPlan fp;
-  const bool fused = trailer && body >= 128 && resolve_mode(ctx, out) == 2 && plan_fused(b, body, &fp);
+  // (TMA stores need 16-byte aligned destinations: the record is, a replica may not be)
+  bool aligned = (reinterpret_cast<uintptr_t>(out->dev) & 15u) == 0;
+  for (auto& r : out->replicas) aligned = aligned && (reinterpret_cast<uintptr_t>(r.first) & 15u) == 0;
+  const bool fused = trailer && body >= 128 && aligned && resolve_mode(ctx, out) == 2 && plan_fused(b, body, &fp);
   const size_t runs_off = align_up(meta_off + b.meta.size(), 16);
   const size_t pl_off = runs_off + sizeof(FnvRun) * fp.runs.size();
   const size_t stage_bytes = fused ? pl_off + 8 * fp.patch.size() : meta_off + b.meta.size();
@@ -602,7 +605,7 @@ cudaStream_t run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, boo
     return ctx->stream;
   }
   const int mode = resolve_mode(ctx, out);  // 2 fell through: the record did not suit the fused kernel
-  if (trailer && mode == 5 && !out->replicas.empty() && body >= 128) {
+  if (trailer && mode == 5 && !out->replicas.empty() && body >= 128 && aligned) {
     // pack the local record; the FNV kernel stores the replicas from the
     // bytes it stages in shared memory (coalesced warp stores) and appends
     // the trailer to every copy -- no second read of the record

@@ -220,6 +220,50 @@ def test_snapshot_large_replicas_vs_oracle(mk, ctx, oracle, mode):
     st.close()
 
 
+@pytest.mark.parametrize("reserve", [0, 144])
+def test_fused_snapshot_on_few_sms_and_unaligned_replicas(mk, ctx, oracle, reserve):
+    """The fused snapshot (transport 2: TMA loads from the arena, hash, TMA
+    stores) on all SMs and on 4 SMs (chunk tickets: any grid), with a replica
+    at an allocation's base and one 48 bytes into it (TMA store maps start
+    anywhere 16-byte aligned), every copy against the oracle's
+    serialize_record; ~60 MB records, entries at odd offsets.  Unaligned
+    replicas are refused by add_replica."""
+    pcs = [3_000_001, 4_999_999, 1_000_003, 333]
+    st = mk.DeviceState(ctx, pcs, 2)
+    st.fill_synthetic(seed=21, step=4)
+    st.set_meta(50, 9)
+    active, co = [1, 3], [0, 2]
+    ents = []
+    for i in range(len(pcs)):
+        P = pcs[i]
+        master = oracle.synth(21, 3 * i, -0.25, 0.25, P)
+        if i in active:
+            ents.append(dict(id=i, mode=0, param_count=P, step=4, master=master,
+                             m=oracle.synth(21, 3 * i + 1, -1e-3, 1e-3, P),
+                             v=oracle.synth(21, 3 * i + 2, 0.0, 1e-6, P)))
+        else:
+            ents.append(dict(id=i, mode=1, param_count=P, compute=oracle.quantize(master, 2)))
+    ref = oracle.serialize_record(dict(kind=1, iteration=50, window_start=48, wsparse=4, slot=2, data_seed=9),
+                                  ents, 2)
+    cap = len(ref) + 4096
+    ctx.set_replica_mode(2)
+    ctx.set_hash_reserve(reserve)
+    try:
+        for offset in (0, 48):
+            out = mk.Blob(ctx, cap)
+            buf = ctx.alloc(cap + 64)
+            out.add_replica(buf + offset, cap)
+            mk.snapshot_record(st, active, co, 2, 1, 48, 4, out)
+            assert out.to_host() == ref, (reserve, offset)
+            assert ctx.download(buf + offset, len(ref)) == ref, (reserve, offset)
+            out.close()
+            ctx.free(buf)
+    finally:
+        ctx.set_replica_mode(-1)
+        ctx.set_hash_reserve(0)
+        st.close()
+
+
 def test_replay_fast_paths_match_ieee_intrinsics(mk, ctx):
     """The conversion's hoisted-reciprocal division and spelled-out square root
     equal __fdiv_rn / __fsqrt_rn: 2^28 divisions over every exponent pair of
