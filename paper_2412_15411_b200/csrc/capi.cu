@@ -506,7 +506,7 @@ bool plan_fused(const SegmentBuilder& b, uint64_t body, FusedPlan* fp) {
   }
   while (r < fp->runs.size()) all.push_back(fp->runs[r++]);
   fp->runs.swap(all);
-  return fp->patch.size() * 4 <= n_chunks + 4;
+  return fp->patch.size() * 4 <= n_chunks + 4 && fp->patch.size() <= 65535;  // (patch grid: y <= 65535)
 }
 
 // The transport of a record (mlck_ctx_set_replica_mode): auto (-1) is the
