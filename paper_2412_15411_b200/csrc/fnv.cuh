@@ -75,12 +75,6 @@ constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
 #ifndef MLCK_FNV_NOSHIFT
 #define MLCK_FNV_NOSHIFT 1
 #endif
-// MLCK_FNV_WARP_STORES: copies leave by per-warp TMA stores of 32 rows in
-// round 0 (1) or by the look-back warp's whole-chunk stores, the rows
-// interleaved in round 1 (0).
-#ifndef MLCK_FNV_WARP_STORES
-#define MLCK_FNV_WARP_STORES 0
-#endif
 constexpr int kSlots = MLCK_FNV_SLOTS;         // chunks in flight per CTA
 constexpr int kComputeWarps = MLCK_FNV_WARPS;  // + one look-back warp per slot
 constexpr int kWarps = kComputeWarps + kSlots;

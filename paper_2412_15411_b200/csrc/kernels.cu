@@ -236,22 +236,7 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
         }
         if (store) {  // record-aligned rows in place: out to every destination
           fence_async_shared();
-#if MLCK_FNV_WARP_STORES
-          // each warp stores its own 32 rows (4 KiB) and waits until the TMA
-          // has read them: no hand-off, the rows are interleaved right after
-          __syncwarp();
-          if (lane == 0) {
-            const uint64_t r0 = static_cast<uint64_t>(chunk[s]) * kComputeThreads + 32 * warp;
-            if (r0 < rows_full) {
-              for (int d = 0; d < cp.n_dst; ++d)
-                tma_store_rows(&cp.dst[d], static_cast<int32_t>(r0), &sh.data[s][kGranules * 32 * warp]);
-              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            }
-          }
-#else
           bar_arrive(bar_store(s), kBarThreads);
-#endif
           const uint64_t row = static_cast<uint64_t>(chunk[s]) * kComputeThreads + tid;
           if (row == rows_full && (n & (kThreadBytes - 1))) {  // the partial last row (TMA stores clip it)
             const uint8_t* rb = reinterpret_cast<const uint8_t*>(sh.data[s]);
@@ -262,14 +247,8 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
           }
         }
         interleave(w);  // fresh bytes: interleave the segments once, in place
-#if MLCK_FNV_WARP_STORES
-        __syncwarp();  // lane 0 saw the TMA read the warp's rows
-        write_thread(sh, s, tid, w);
-      } else if (false) {
-#else
         if (!store) write_thread(sh, s, tid, w);
       } else if (copy && rnd[s] == 1) {
-#endif
         // copies: the rows stayed record-aligned for the TMA stores through
         // round 0; interleaved in place now, once the stores have read them
         interleave(w);
@@ -358,13 +337,13 @@ __device__ __forceinline__ void fnv_lookback(fnv::Shared& sh, int s, uint64_t se
     uint32_t word = 0;  // the chunk's status bits as published
     int64_t next = -1;
     Run nrun{};  // kGather: the run of the next chunk, looked up beside the last round
-    if (copy && !MLCK_FNV_WARP_STORES) {  // the compute warps have the rows aligned: out to every destination
+    if (copy) {  // the compute warps have the rows aligned: out to every destination
       bar_sync(bar_store(s), kBarThreads);
       if (lane == 0) tma_store_chunk(sh, s, cp, chunk, rows_full);
       __syncwarp();
     }
     for (int r = 0; r < kRounds; ++r) {
-      if (copy && !MLCK_FNV_WARP_STORES && r == 1 && lane == 0) {  // round 1 rewrites the rows: once read
+      if (copy && r == 1 && lane == 0) {  // round 1 rewrites the rows: once the stores have read them
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         mbar_arrive(&sh.sres[s]);
       }
@@ -1071,7 +1050,7 @@ void launch_fnv(const uint8_t* data, uint64_t n, uint64_t seed, uint32_t* scratc
     cp.n_dst = copies->n;
     for (int d = 0; d < copies->n; ++d) {
       if (reinterpret_cast<uintptr_t>(copies->p[d]) & 15u) throw_invalid("copy destinations must be 16-byte aligned");
-      encode_rows(copies->p[d], n / fnv::kThreadBytes, MLCK_FNV_WARP_STORES ? 32 : fnv::kTmaBoxRows, &cp.dst[d]);
+      encode_rows(copies->p[d], n / fnv::kThreadBytes, fnv::kTmaBoxRows, &cp.dst[d]);
       cp.dst_ptr[d] = copies->p[d];
     }
   }
