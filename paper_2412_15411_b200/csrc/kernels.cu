@@ -46,6 +46,72 @@ struct Laps {
   }
 };
 
+// ---- tcgen05 helpers: the chunk-wide dot products of the witness verifier
+// (fnv_witness_tc_kernel).  Per chunk, a 128 x 16 x 512 u8 MMA: A = the
+// chunk's 512 rows in shared memory (M = the 128 byte positions of a row,
+// K = the row: the TMA's 128-byte-swizzled rows are the canonical MN-major
+// SWIZZLE_128B operand), B = the 8-bit limbs of P^-(128 k) (or of
+// -2 P^-(128 k)) for row k, s32 accumulators (< 2^26) in TMEM.
+constexpr int kTcN = 16;  // MMA N (limbs 0-7 used, 8-15 zero)
+__device__ uint8_t g_tcw[2][fnv::kComputeThreads][kTcN];  // B tables (init_constants)
+
+__device__ __forceinline__ bool mbar_try(unsigned long long* m, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(ok)
+               : "r"(fnv::smem_addr(m)), "r"(parity)
+               : "memory");
+  return ok != 0;
+}
+// A bounded wait: a protocol error ends the kernel with the record marked
+// unverified (the caller re-hashes it) instead of hanging the GPU.
+__device__ __forceinline__ bool mbar_wait_tc(unsigned long long* m, uint32_t parity, volatile uint32_t* abort) {
+  for (uint32_t n = 1;; ++n) {
+    if (mbar_try(m, parity)) return true;
+    if ((n & 255u) == 0 && (*abort || n > (1u << 24))) {
+      *abort = 1;
+      return false;
+    }
+  }
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+// shared-memory matrix descriptors (sm_100 layout: start >> 4 @0, LBO >> 4
+// @16, SBO >> 4 @32, version 1 @46, layout type @61)
+__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3fffu) | (static_cast<uint64_t>((lbo >> 4) & 0x3fffu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3fffu) << 32) | (1ull << 46) | (static_cast<uint64_t>(layout) << 61);
+}
+// kind::i8, u8 x u8 -> s32, A and B MN-major, N = 16, M = 128
+constexpr uint32_t kTcIdesc = (2u << 4) | (1u << 15) | (1u << 16) | ((kTcN >> 3) << 17) | ((128 >> 4) << 24);
+// D[tmem] (+)= A[128 x 512 rows at a] . B[512 x 16 at b]: 16 MMAs of K = 32
+// (accumulate = 0: the first overwrites D)
+__device__ __forceinline__ void tc_chunk_mma(uint32_t d_tmem, uint32_t a, uint32_t b, uint32_t accumulate = 0) {
+#pragma unroll
+  for (int k = 0; k < fnv::kComputeThreads / 32; ++k) {
+    // A: SWIZZLE_128B MN-major, 8-row atoms 1 KiB apart, K-step = 32 rows (4 KiB)
+    const uint64_t da = tc_desc(a + 4096u * k, 0, 1024, 2);
+    // B: no swizzle, MN-major, core matrices of 8 rows x 16 B, 128 B apart along K
+    const uint64_t db = tc_desc(b + 512u * k, 128, 0, 0);
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }" ::"r"(d_tmem),
+        "l"(da), "l"(db), "r"(kTcIdesc), "r"(k | accumulate)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tc_commit(unsigned long long* m) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(fnv::smem_addr(m))
+               : "memory");
+}
+// 8 columns of this warp's 32 TMEM lanes
+__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+}
+
+
 // Compute warps: per slot turn, take the look-back result of the round
 // published on the previous turn, then (after round 3) hash the slot's bytes
 // and refill it, else compute and publish the next round.
@@ -653,7 +719,6 @@ __global__ void __launch_bounds__(kWitnessThreads, 1)
 #define MLCK_WITNESS_TC 1
 #endif
 constexpr int kTcThreads = fnv::kComputeThreads + 96;  // + the producer warp + one warp per MMA
-constexpr int kTcN = 16;                              // MMA N (limbs 0-7 used, 8-15 zero)
 constexpr uint32_t kTcCols = 128;                     // TMEM columns: [buffer][2 accumulators][16]
 struct WitnessTcSmem {
   uint4 data[kWitnessBufs][fnv::kComputeThreads * fnv::kGranules];  // 1 KiB-aligned rows (TMA swizzle)
@@ -668,63 +733,6 @@ struct WitnessTcSmem {
   uint32_t abort;
 };
 constexpr size_t kWitnessTcSmem = sizeof(WitnessTcSmem) + 1024;
-__device__ uint8_t g_tcw[2][fnv::kComputeThreads][kTcN];  // B tables (init_constants)
-
-__device__ __forceinline__ bool mbar_try(unsigned long long* m, uint32_t parity) {
-  uint32_t ok;
-  asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-               : "=r"(ok)
-               : "r"(fnv::smem_addr(m)), "r"(parity)
-               : "memory");
-  return ok != 0;
-}
-// A bounded wait: a protocol error ends the kernel with the record marked
-// unverified (the caller re-hashes it) instead of hanging the GPU.
-__device__ __forceinline__ bool mbar_wait_tc(unsigned long long* m, uint32_t parity, volatile uint32_t* abort) {
-  for (uint32_t n = 1;; ++n) {
-    if (mbar_try(m, parity)) return true;
-    if ((n & 255u) == 0 && (*abort || n > (1u << 24))) {
-      *abort = 1;
-      return false;
-    }
-  }
-}
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-// shared-memory matrix descriptors (sm_100 layout: start >> 4 @0, LBO >> 4
-// @16, SBO >> 4 @32, version 1 @46, layout type @61)
-__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
-  return static_cast<uint64_t>((saddr >> 4) & 0x3fffu) | (static_cast<uint64_t>((lbo >> 4) & 0x3fffu) << 16) |
-         (static_cast<uint64_t>((sbo >> 4) & 0x3fffu) << 32) | (1ull << 46) | (static_cast<uint64_t>(layout) << 61);
-}
-// kind::i8, u8 x u8 -> s32, A and B MN-major, N = 16, M = 128
-constexpr uint32_t kTcIdesc = (2u << 4) | (1u << 15) | (1u << 16) | ((kTcN >> 3) << 17) | ((128 >> 4) << 24);
-// D[tmem] (+)= A[128 x 512 rows at a] . B[512 x 16 at b]: 16 MMAs of K = 32
-__device__ __forceinline__ void tc_chunk_mma(uint32_t d_tmem, uint32_t a, uint32_t b) {
-#pragma unroll
-  for (int k = 0; k < fnv::kComputeThreads / 32; ++k) {
-    // A: SWIZZLE_128B MN-major, 8-row atoms 1 KiB apart, K-step = 32 rows (4 KiB)
-    const uint64_t da = tc_desc(a + 4096u * k, 0, 1024, 2);
-    // B: no swizzle, MN-major, core matrices of 8 rows x 16 B, 128 B apart along K
-    const uint64_t db = tc_desc(b + 512u * k, 128, 0, 0);
-    asm volatile(
-        "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }" ::"r"(d_tmem),
-        "l"(da), "l"(db), "r"(kTcIdesc), "r"(k)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void tc_commit(unsigned long long* m) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(fnv::smem_addr(m))
-               : "memory");
-}
-// 8 columns of this warp's 32 TMEM lanes
-__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t (&r)[8]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr)
-               : "memory");
-}
-
 __global__ void __launch_bounds__(kTcThreads, 1)
     fnv_witness_tc_kernel(const uint8_t* data, uint64_t n, uint64_t seed, const uint32_t* witness, fnv::Scratch scr,
                           unsigned long long* bad, int64_t n_chunks, const __grid_constant__ CUtensorMap tmap,
