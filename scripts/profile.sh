@@ -15,7 +15,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $O/launches.csv $CMD > $O/ncu_launches.log 2>&1
 echo "launch list rc=$?"
 # full sections of the hot kernels, one launch each (after warm-up launches)
-for k in fnv_kernel pack_kernel replay_kernel fnv_witness_kernel; do
+for k in fnv_kernel pack_kernel replay_kernel fnv_witness_tc_kernel; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
       -o $O/prof_$k $CMD > $O/ncu_$k.log 2>&1
   echo "$k rc=$?"

@@ -71,7 +71,7 @@ def main():
     if os.path.exists(os.path.join(OUT, "launches.csv")):
         summary["launch_list"] = launch_shares(os.path.join(OUT, "launches.csv"))
     kernels = {}
-    for k in ("fnv_kernel", "pack_kernel", "replay_kernel", "fnv_witness_kernel", "scope_kernel"):
+    for k in ("fnv_kernel", "pack_kernel", "replay_kernel", "fnv_witness_tc_kernel", "fnv_witness_kernel", "scope_kernel"):
         rep = os.path.join(OUT, f"prof_{k}.ncu-rep")
         if os.path.exists(rep):
             m = raw_metrics(rep)
