@@ -31,12 +31,15 @@
 // split between the ALU and FMA pipes.
 //
 // Latency.  Each CTA keeps kSlots chunks in flight (their bytes in shared
-// memory, refilled with cp.async) and its compute warps visit them
-// round-robin; each compute thread owns kSegs consecutive 32-byte segments of
-// a chunk, so the per-round scan and hand-off amortise over 128 bytes.  Every slot has its own look-back warp, which folds the warp
-// maps of the slot's round, publishes it and looks back while the compute
-// warps work on the other slots: a look-back has kSlots-1 slot turns to
-// complete before its result is needed.
+// memory, loaded by TMA -- from the record, or straight from the record's
+// sources in the fused snapshot -- or by cp.async for unaligned inputs) and
+// its compute warps visit them round-robin; each compute thread owns kSegs
+// consecutive 32-byte segments of a chunk, so the per-round scan and
+// hand-off amortise over 128 bytes.  Every slot has its own look-back warp,
+// which folds the warp maps of the slot's round, publishes it and looks back
+// while the compute warps work on the other slots: a look-back has kSlots-1
+// slot turns to complete before its result is needed.  The same warp
+// issues the slot's TMA loads and, for copies, its TMA stores.
 #pragma once
 
 #include <cuda.h>
