@@ -304,6 +304,27 @@ def cpu_convert_sample(threads, scale=256):
             "replay_ms_extrapolated_configs3": 1000 * full_steps / replay_rate}
 
 
+def cpu_fnv_sample(mb=256):
+    """The reference's fnv1a64 (digest.hpp:18-25) on one core over `mb` MiB:
+    the byte-serial trailer of serialize_record and the check of parse_record."""
+    import ctypes as C
+    import numpy as np
+    from oracle.oracle import load_reference
+    ref = load_reference()
+    if ref is None:
+        return None
+    L = ref.lib
+    L.mlr_fnv1a64.restype = C.c_uint64
+    L.mlr_fnv1a64.argtypes = [C.c_void_p, C.c_size_t, C.c_uint64]
+    buf = np.random.default_rng(7).integers(0, 256, mb << 20, dtype=np.uint8)
+    L.mlr_fnv1a64(buf.ctypes.data, 1 << 20, 0xCBF29CE484222325)  # warm
+    t0 = time.perf_counter()
+    L.mlr_fnv1a64(buf.ctypes.data, buf.size, 0xCBF29CE484222325)
+    sec = time.perf_counter() - t0
+    return {"threads": 1, "bytes": int(buf.size), "seconds": sec, "gbs": buf.size / sec / GB,
+            "note": "byte-serial: one core is the reference's rate for any one record (no parallel FNV)"}
+
+
 def host_info():
     model = None
     try:
@@ -332,7 +353,7 @@ def cpu_baseline_full(wl):
                       f"{p_all['full_params']} + {p_all['n_co']} CO x {p_all['co_params']} params, "
                       f"{n} independent engines, {p_all['seconds']:.1f} s"),
            "pack_1core_gbs": p_one["bytes_per_s"] / GB, "pack_all_cores_gbs": p_all["bytes_per_s"] / GB,
-           "conversion_1core": c_one, "conversion_all_cores": c_all}
+           "conversion_1core": c_one, "conversion_all_cores": c_all, "fnv1a64_1core": cpu_fnv_sample()}
     out.update(host_info())
     return out
 
