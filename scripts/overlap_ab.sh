@@ -1,7 +1,7 @@
 #!/bin/bash
 # conversion: witnessed verification beside the replay on N SMs (0 = sequential)
 mkdir -p gpurun_out/r2
-for n in 0 24 37 48 74; do
+for n in ${OVERLAPS:-0 24 37 48 74}; do
   timeout 300 python bench.py --no-cpu --no-log --no-extras --steps 3 --convert-overlap $n > gpurun_out/r2/oab_$n.log 2>&1
   python -c "
 import json; j=json.loads(open('gpurun_out/r2/oab_$n.log').read().strip().splitlines()[-1]); c=j['conversion']; k=c['kernels']
