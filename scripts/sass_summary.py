@@ -13,7 +13,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BUILD = os.path.join(ROOT, "paper_2412_15411_b200", "_build")
-OPS = ["UTMALDG", "UTMASTG", "UTMACMDFLUSH", "SYNCS.ARRIVE", "SYNCS.PHASECHK", "IMMA", "HMMA", "LDGSTS",
+OPS = ["UTMALDG", "UTMASTG", "UBLKCP", "UTCIMMA", "UTCBAR", "UTMACMDFLUSH", "SYNCS.ARRIVE", "SYNCS.PHASECHK", "IMMA", "HMMA", "LDGSTS",
        "LDG", "STG", "LDS", "STS", "MUFU", "SHFL", "BAR"]
 
 
@@ -57,7 +57,7 @@ def main():
             rows.append((obj, cur, counts))
     out = [f"# SASS summary ({rnd})", "",
            "`cuobjdump -sass` of `paper_2412_15411_b200/_build/*.o` (sm_100a), static instruction counts per "
-           "kernel (`scripts/sass_summary.py`). UTMALDG / UTMASTG = TMA tensor loads / stores, SYNCS.* = "
+           "kernel (`scripts/sass_summary.py`). UTMALDG / UTMASTG = TMA tensor loads / stores, UBLKCP = bulk copies, UTCIMMA = tcgen05 integer MMA, UTCBAR = tcgen05.commit, SYNCS.* = "
            "mbarrier arrive / try-wait, IMMA = integer tensor-core MMA (mma.sync u8).", "",
            "| object | kernel | instr | " + " | ".join(OPS) + " |",
            "|---|---|---|" + "---|" * len(OPS)]
