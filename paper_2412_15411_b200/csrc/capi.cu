@@ -907,7 +907,7 @@ void verify_begin(ParseJob& j) {
   for (uint32_t k = 0; k < n; ++k) {
     const mlck_blob* b = j.blobs[k];
     if (b->size < 8) continue;
-    const int side = static_cast<int>(launched++ & 1u);
+    const int side = static_cast<int>(launched++ & 1u);  // (one side stream: 0.1 ms slower)
     cudaStream_t st = ctx->vside[side];
     uint32_t* scratch = ctx->vscratch_for(side, b->size - 8);
     TrailerDsts none{};
