@@ -1276,8 +1276,8 @@ void launch_replay(const adam::ConvOp* ops, int n_ops, const float* const* gptr,
     MLCK_CUDA(cudaGetLastError());
   }
   const uint64_t blocks = total_units;  // total_units counts CTAs (run_replay)
-  adam::replay_kernel<<<static_cast<unsigned>(blocks), adam::kReplayThreads, 0, stream>>>(ops, n_ops, gptr, bc, steps,
-                                                                                        o, cb, total_units);
+  adam::replay_kernel<<<static_cast<unsigned>(blocks), adam::kReplayThreads, 0, stream>>>(ops, n_ops, gptr, bc,
+                                                                                        steps, o, cb, total_units);
   MLCK_CUDA(cudaGetLastError());
 }
 
