@@ -636,6 +636,11 @@ __device__ __forceinline__ void tma_load_rows(void* dst, const CUtensorMap* map,
       : "memory");
 #endif
 }
+#ifndef MLCK_FNV_BOX_ROWS
+#define MLCK_FNV_BOX_ROWS 256
+#endif
+constexpr int kTmaBoxRows = MLCK_FNV_BOX_ROWS;  // rows per TMA box (a divisor of kComputeThreads)
+static_assert(kComputeThreads % kTmaBoxRows == 0, "whole boxes per chunk");
 // Tensor-map store of `rows` x 128 bytes of swizzled rows at src to record
 // row `row` (rows past the tensor are clipped); bulk async-group.
 __device__ __forceinline__ void tma_store_rows(const CUtensorMap* map, int32_t row, const void* src) {
@@ -662,8 +667,8 @@ __device__ __forceinline__ void tma_load_src(Shared& sh, int slot, const Copy& c
   sh.shift[slot] = delta;  // released to the waiters by the arrival below
   fence_async_shared();
   mbar_arrive_expect_tx(mb, (kComputeThreads + (delta ? 8 : 0)) * kThreadBytes);
-  for (int b = 0; b < kComputeThreads / 256; ++b)
-    tma_load_rows(&sh.data[slot][kGranules * 256 * b], &cp.src[r.map][0], row + 256 * b, mb);
+  for (int b = 0; b < kComputeThreads / kTmaBoxRows; ++b)
+    tma_load_rows(&sh.data[slot][kGranules * kTmaBoxRows * b], &cp.src[r.map][0], row + kTmaBoxRows * b, mb);
   if (delta) tma_load_rows(&sh.data[slot][kGranules * kComputeThreads], &cp.src[r.map][1], row + kComputeThreads, mb);
 }
 // The run holding record chunk c (warp-collective: a 32-ary search over the
@@ -686,16 +691,16 @@ __device__ __forceinline__ void tma_store_chunk(const Shared& sh, int slot, cons
                                                 uint64_t rows_full) {
   const uint64_t row0 = static_cast<uint64_t>(chunk) * kComputeThreads;
   for (int d = 0; d < cp.n_dst; ++d)
-    for (int b = 0; b < kComputeThreads / 256; ++b)
-      if (row0 + 256 * b < rows_full)
-        tma_store_rows(&cp.dst[d], static_cast<int32_t>(row0 + 256 * b), &sh.data[slot][kGranules * 256 * b]);
+    for (int b = 0; b < kComputeThreads / kTmaBoxRows; ++b)
+      if (row0 + kTmaBoxRows * b < rows_full)
+        tma_store_rows(&cp.dst[d], static_cast<int32_t>(row0 + kTmaBoxRows * b),
+                       &sh.data[slot][kGranules * kTmaBoxRows * b]);
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
 // The chunk of `slot` by one thread: the 256-row boxes that start inside the
 // map's rows_full full rows (the compute threads write the rest), one
 // mbarrier arrival with their byte count.
-constexpr int kTmaBoxRows = 256;
 __device__ __forceinline__ void tma_load_chunk(Shared& sh, int slot, const CUtensorMap* map, int64_t chunk,
                                                uint64_t rows_full) {
   unsigned long long* mb = &sh.mbar[slot][0];
