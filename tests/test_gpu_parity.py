@@ -264,6 +264,51 @@ def test_fused_snapshot_on_few_sms_and_unaligned_replicas(mk, ctx, oracle, reser
         st.close()
 
 
+@pytest.mark.parametrize("cb", [1, 2, 4])
+def test_fused_snapshot_many_boundaries(mk, ctx, oracle, cb):
+    """Transport 2 on a record of 40 operators of 100K-400K parameters: ~80
+    segment boundaries, each a pre-gathered patch chunk between runs of
+    TMA-loaded chunks at every shift; bytes against the oracle, and the local
+    replica; the fused kernel (not the pack fallback) did it."""
+    rng = np.random.default_rng(40 + cb)
+    pcs = [int(x) for x in rng.integers(100_000, 400_000, 40)]
+    st = mk.DeviceState(ctx, pcs, cb)
+    st.fill_synthetic(seed=5 + cb, step=3)
+    st.set_meta(30, 2)
+    active = sorted(int(x) for x in rng.choice(40, 12, replace=False))
+    co = [i for i in range(40) if i not in active]
+    ents = []
+    for i in range(40):
+        P = pcs[i]
+        master = oracle.synth(5 + cb, 3 * i, -0.25, 0.25, P)
+        if i in active:
+            ents.append(dict(id=i, mode=0, param_count=P, step=3, master=master,
+                             m=oracle.synth(5 + cb, 3 * i + 1, -1e-3, 1e-3, P),
+                             v=oracle.synth(5 + cb, 3 * i + 2, 0.0, 1e-6, P)))
+        else:
+            ents.append(dict(id=i, mode=1, param_count=P, compute=oracle.quantize(master, cb)))
+    ref = oracle.serialize_record(dict(kind=1, iteration=30, window_start=30, wsparse=3, slot=0, data_seed=2),
+                                  ents, cb)
+    cap = len(ref) + 4096
+    ctx.set_replica_mode(2)
+    try:
+        out = mk.Blob(ctx, cap)
+        rep = ctx.alloc(cap)
+        out.add_replica(rep, cap)
+        ctx.set_timing(True)
+        mk.snapshot_record(st, active, co, 0, 1, 30, 3, out)
+        labels = [name for name, _ in ctx.timings()]
+        ctx.set_timing(False)
+        assert "pack_fnv" in labels and "pack" not in labels, labels
+        assert out.to_host() == ref
+        assert ctx.download(rep, len(ref)) == ref
+        out.close()
+        ctx.free(rep)
+    finally:
+        ctx.set_replica_mode(-1)
+        st.close()
+
+
 def test_replay_fast_paths_match_ieee_intrinsics(mk, ctx):
     """The conversion's hoisted-reciprocal division and spelled-out square root
     equal __fdiv_rn / __fsqrt_rn: 2^28 divisions over every exponent pair of
