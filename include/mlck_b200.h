@@ -173,6 +173,24 @@ int mlck_blob_to_host(const mlck_blob* b, uint8_t* host, uint64_t cap);
  * with mlck_ipc_open / peer access).  Up to 3 replicas. */
 int mlck_blob_add_replica(mlck_blob* b, void* device_ptr, uint64_t capacity);
 int mlck_blob_clear_replicas(mlck_blob* b);
+/* A witness buffer beside a replica (same device as the replica, e.g. the
+ * peer's HBM through CUDA IPC): after each record's hash its witness (one u32
+ * per 128-byte row, ~3.1 % of the record) is copied there, behind the record
+ * (it is part of mlck_blob_replication's completion).  `capacity` must be at
+ * least mlck_witness_bytes(record size); cleared by mlck_blob_clear_replicas.
+ * A node recovering from that replica wraps the record and the witness
+ * (mlck_blob_wrap), so parse / conversion / localized recovery verify it on
+ * the witnessed path instead of re-hashing from scratch -- still exact: a
+ * witness that does not match the bytes only costs the from-scratch hash. */
+int mlck_blob_add_replica_witness(mlck_blob* b, void* device_ptr, uint64_t capacity);
+/* Bytes a witness buffer needs for a record of `record_bytes` (the witness
+ * plus the verifier's bulk over-read). */
+uint64_t mlck_witness_bytes(uint64_t record_bytes);
+/* A read-only blob over `n` record bytes the caller owns in device memory (a
+ * replica buffer), with the record's witness if `witness` is not null; no
+ * copy.  Parse, coverage, conversion and localized recovery read it in place;
+ * snapshots into it are refused.  Destroying it frees nothing of the caller's. */
+int mlck_blob_wrap(mlck_ctx* ctx, void* record, uint64_t n, const void* witness, mlck_blob** out);
 
 /* ---- window lifecycle and durability (SparseCheckpoint::replication /
  * persisted(), snapshot.hpp:300-320; "one persisted + one

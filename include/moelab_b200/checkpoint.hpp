@@ -265,6 +265,20 @@ class DeviceBlob {
   void add_replica(void* device_ptr, uint64_t capacity) {
     check(mlck_blob_add_replica(h_, device_ptr, capacity));
   }
+  // each record's witness also goes to this buffer beside a replica
+  // (capacity >= witness_bytes(record size)): a node recovering from the
+  // replica wraps both and verifies on the witnessed path
+  void add_replica_witness(void* device_ptr, uint64_t capacity) {
+    check(mlck_blob_add_replica_witness(h_, device_ptr, capacity));
+  }
+  static uint64_t witness_bytes(uint64_t record_bytes) { return mlck_witness_bytes(record_bytes); }
+  // a read-only view of `n` record bytes the caller owns in device memory (a
+  // replica buffer) and its witness, if any: no copy
+  static DeviceBlob wrap(Context& ctx, void* record, uint64_t n, const void* witness = nullptr) {
+    DeviceBlob b(ctx, nullptr);
+    check(mlck_blob_wrap(ctx.get(), record, n, witness, &b.h_));
+    return b;
+  }
   // replicas holding the complete last record (0 while its push is in flight)
   uint32_t replication() const {
     uint32_t n = 0;

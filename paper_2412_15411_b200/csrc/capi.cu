@@ -303,6 +303,10 @@ struct mlck_state {
   }
 };
 
+// u32 words a record's witness buffer holds: one per 128-byte row of the body,
+// plus the verifier's bulk over-read of a chunk's words (fnv_witness_tc_kernel)
+inline uint64_t witness_alloc_words(uint64_t body) { return fnv_witness_words(body) + 1 + 520; }
+
 struct mlck_blob {
   mlck_ctx* ctx = nullptr;
   uint8_t* dev = nullptr;
@@ -316,8 +320,15 @@ struct mlck_blob {
   // for a body of witness_n bytes when witness_n == size - 8
   uint32_t* witness = nullptr;
   uint64_t witness_cap = 0, witness_n = ~0ull;
+  // witness buffers next to replicas (mlck_blob_add_replica_witness): each
+  // record's witness follows it there, so a blob wrapped over the replica
+  // verifies on the witnessed path
+  std::vector<std::pair<uint8_t*, uint64_t>> witness_dsts;
+  // mlck_blob_wrap: a read-only view of a record (and witness) the caller owns
+  bool external = false, external_witness = false;
 
   void reserve(uint64_t n) {
+    if (external) throw_invalid("a wrapped blob (mlck_blob_wrap) is read-only");
     if (n <= cap) return;
     ctx->join_hash();
     MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -328,8 +339,9 @@ struct mlck_blob {
     if (ctx->witness) reserve_witness(cap);  // with the record buffer: never inside a snapshot
   }
   void reserve_witness(uint64_t body) {
-    const uint64_t words = fnv_witness_words(body) + 1 + 520;  // + the verifier's bulk over-read of a chunk
+    const uint64_t words = witness_alloc_words(body);
     if (words <= witness_cap) return;
+    if (external_witness) throw_invalid("a wrapped blob (mlck_blob_wrap) is read-only");
     ctx->join_hash();
     MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
     if (witness) MLCK_CUDA(cudaFree(witness));
@@ -529,10 +541,19 @@ int resolve_mode(const mlck_ctx* ctx, const mlck_blob* out) {
 // `trailer`): the blob body is [0, builder.pos), the trailer at pos.
 cudaStream_t run_pack_impl(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer);
 void run_pack(mlck_ctx* ctx, SegmentBuilder& b, mlck_blob* out, bool trailer) {
+  if (out->external) throw_invalid("a wrapped blob (mlck_blob_wrap) is read-only");
+  const uint64_t wit_bytes = 4 * fnv_witness_words(b.pos);
+  for (const auto& d : out->witness_dsts)
+    if (trailer && ctx->witness && d.second < 4 * witness_alloc_words(b.pos))
+      throw_invalid("replica witness capacity " + std::to_string(d.second) + " < " +
+                    std::to_string(4 * witness_alloc_words(b.pos)) + " (mlck_witness_bytes)");
   // the blob's previous record may still be read by its asynchronous hash
   if (out->written) MLCK_CUDA(cudaStreamWaitEvent(ctx->stream, out->written, 0));
   out->witness_n = ~0ull;
   const cudaStream_t last = run_pack_impl(ctx, b, out, trailer);
+  if (out->witness_n == b.pos)  // the record's witness to every replica witness buffer (NVLink for peers)
+    for (const auto& d : out->witness_dsts)
+      MLCK_CUDA(cudaMemcpyAsync(d.first, out->witness, wit_bytes, cudaMemcpyDefault, last));
   if (!out->written) MLCK_CUDA(cudaEventCreateWithFlags(&out->written, cudaEventDisableTiming));
   MLCK_CUDA(cudaEventRecord(out->written, last));  // every path ends with the pushes joined
   out->written_replicas = static_cast<uint32_t>(out->replicas.size());
@@ -1411,8 +1432,8 @@ int mlck_blob_destroy(mlck_blob* b) {
     b->ctx->activate();
     if (b->written) cudaEventSynchronize(b->written);
     cudaStreamSynchronize(b->ctx->stream);
-    if (b->dev) cudaFree(b->dev);
-    if (b->witness) cudaFree(b->witness);
+    if (b->dev && !b->external) cudaFree(b->dev);
+    if (b->witness && !b->external_witness) cudaFree(b->witness);
     if (b->written) cudaEventDestroy(b->written);
     auto& v = b->ctx->blobs;
     v.erase(std::remove(v.begin(), v.end(), b), v.end());
@@ -1463,7 +1484,40 @@ int mlck_blob_add_replica(mlck_blob* b, void* ptr, uint64_t capacity) {
   });
 }
 int mlck_blob_clear_replicas(mlck_blob* b) {
-  return api([&] { b->replicas.clear(); });
+  return api([&] {
+    b->replicas.clear();
+    b->witness_dsts.clear();
+  });
+}
+int mlck_blob_add_replica_witness(mlck_blob* b, void* ptr, uint64_t capacity) {
+  return api([&] {
+    if (b->witness_dsts.size() + 1 >= static_cast<size_t>(pack::kMaxDst))
+      throw_invalid("at most " + std::to_string(pack::kMaxDst - 1) + " replica witnesses per blob");
+    if (reinterpret_cast<uintptr_t>(ptr) % 16) throw_invalid("replica witness buffers must be 16-byte aligned");
+    b->witness_dsts.push_back({static_cast<uint8_t*>(ptr), capacity});
+  });
+}
+uint64_t mlck_witness_bytes(uint64_t record_bytes) {
+  return 4 * witness_alloc_words(record_bytes >= 8 ? record_bytes - 8 : 0);
+}
+int mlck_blob_wrap(mlck_ctx* ctx, void* record, uint64_t n, const void* witness, mlck_blob** out) {
+  return api([&] {
+    ctx->activate();
+    if (!record && n) throw_invalid("blob wrap: null record");
+    auto* b = new mlck_blob();
+    b->ctx = ctx;
+    b->external = true;
+    b->dev = static_cast<uint8_t*>(record);
+    b->cap = b->size = n;
+    if (witness && n >= 8) {
+      b->external_witness = true;
+      b->witness = static_cast<uint32_t*>(const_cast<void*>(witness));
+      b->witness_cap = witness_alloc_words(n - 8);
+      b->witness_n = n - 8;
+    }
+    ctx->blobs.push_back(b);
+    *out = b;
+  });
 }
 
 // ---- window lifecycle and durability ----------------------
@@ -2285,15 +2339,14 @@ int mlck_ipc_close(mlck_ctx* ctx, void* ptr) {
     // would be stored to unmapped memory): in-flight writes finish first
     ctx->join_hash();
     MLCK_CUDA(cudaStreamSynchronize(ctx->stream));
-    for (mlck_blob* b : ctx->blobs) {
-      auto& reps = b->replicas;
-      reps.erase(std::remove_if(reps.begin(), reps.end(),
-                                [&](const auto& r) {
-                                  const uint64_t p = reinterpret_cast<uint64_t>(r.first);
-                                  return p >= a && p < end;
-                                }),
-                 reps.end());
-    }
+    for (mlck_blob* b : ctx->blobs)
+      for (auto* reps : {&b->replicas, &b->witness_dsts})
+        reps->erase(std::remove_if(reps->begin(), reps->end(),
+                                   [&](const auto& r) {
+                                     const uint64_t p = reinterpret_cast<uint64_t>(r.first);
+                                     return p >= a && p < end;
+                                   }),
+                    reps->end());
     MLCK_CUDA(cudaIpcCloseMemHandle(ptr));
   });
 }

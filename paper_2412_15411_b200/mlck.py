@@ -126,6 +126,9 @@ def lib():
             "mlck_blob_to_host": (C.c_int, [vp, u8p, C.c_uint64]),
             "mlck_blob_add_replica": (C.c_int, [vp, vp, C.c_uint64]),
             "mlck_blob_clear_replicas": (C.c_int, [vp]),
+            "mlck_blob_add_replica_witness": (C.c_int, [vp, vp, C.c_uint64]),
+            "mlck_witness_bytes": (C.c_uint64, [C.c_uint64]),
+            "mlck_blob_wrap": (C.c_int, [vp, vp, C.c_uint64, vp, C.POINTER(vp)]),
             "mlck_blob_replication": (C.c_int, [vp, C.POINTER(C.c_uint32)]),
             "mlck_fastmath_check": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64)]),
             "mlck_blob_save": (C.c_int, [vp, C.c_char_p, C.POINTER(C.c_uint64)]),
@@ -525,6 +528,11 @@ class DeviceState:
                                              C.byref(opt)))
 
 
+def witness_bytes(record_bytes: int) -> int:
+    """Capacity a replica witness buffer needs for a record of record_bytes."""
+    return int(lib().mlck_witness_bytes(record_bytes))
+
+
 class Blob:
     """A serialized record in device memory (+ replicas)."""
 
@@ -542,6 +550,18 @@ class Blob:
         h = vp()
         check(lib().mlck_blob_from_host(ctx.h, _ptr(a, u8p) if a.size else None, a.size, C.byref(h)))
         return cls(ctx, _h=h)
+
+    @classmethod
+    def wrap(cls, ctx: Context, record_ptr: int, n: int, witness_ptr: int | None = None) -> "Blob":
+        """A read-only blob over n record bytes in device memory the caller owns
+        (a replica buffer), with its witness when given (mlck_blob_wrap)."""
+        h = vp()
+        check(lib().mlck_blob_wrap(ctx.h, record_ptr, n, witness_ptr, C.byref(h)))
+        return cls(ctx, _h=h)
+
+    def add_replica_witness(self, device_ptr: int, capacity: int):
+        """Each record's witness also goes to this buffer beside a replica."""
+        check(lib().mlck_blob_add_replica_witness(self.h, device_ptr, capacity))
 
     def close(self):
         if self.h:

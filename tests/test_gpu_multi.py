@@ -113,7 +113,29 @@ def _worker(rank, world, port, q):
                     ok, msg = False, f"mode {mode}: rank {rank} replica {j} of rank {src} differs"
             dist.barrier()
         ctx.set_replica_mode(-1)
+        # witnesses travel with the replicas (mlck_blob_add_replica_witness): a rank
+        # verifies a peer's record on the witnessed path, straight from its inbound buffer
+        wcap = mlck.witness_bytes(cap)
+        recv_w = [ctx.alloc(wcap) for _ in range(r)]
+        wtargets = pl.exchange_handles(all_gather, [ctx.ipc_export(p) for p in recv_w], rank, world)
+        opened_w = [ctx.ipc_open(h) for h, _peer in wtargets]
+        for p in opened_w:
+            blob.add_replica_witness(p, wcap)
+        mlck.snapshot_record(st, active, compute_only, 1, 1, 36, 4, blob)
+        ctx.synchronize()
+        dist.barrier()
+        sizes = all_gather(blob.size)
+        for j, src in enumerate(pl.ring_sources(rank, world)):
+            view = mlck.Blob.wrap(ctx, recv[j], sizes[src], recv_w[j])
+            used0, fb0 = ctx.witness_stats()
+            mlck.parse_record(view, cb)
+            used, fb = ctx.witness_stats()
+            if not (used > used0 and fb == fb0):
+                ok, msg = False, f"rank {rank}: replica {j} of rank {src} did not verify on its witness"
+            view.close()
         dist.barrier()  # every peer is done reading its inbound buffers
+        for p in opened_w:
+            ctx.ipc_close(p)
         # closing the mappings drops the blob's replicas inside them: the next
         # record stays local instead of storing to unmapped memory
         for p in opened:

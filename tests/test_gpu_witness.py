@@ -115,3 +115,88 @@ def test_host_records_have_no_witness(mk, ctx):
     used0, _ = ctx.witness_stats()
     mk.parse_record(b, c.compute_bytes)
     assert ctx.witness_stats()[0] == used0
+
+
+@pytest.mark.parametrize("mode", [-1, 0, 1, 2, 5])
+def test_witness_travels_with_a_replica(mk, ctx, mode):
+    """mlck_blob_add_replica_witness: each record's witness follows it to a
+    buffer beside its replica; a blob wrapped over the replica (no copy)
+    verifies on the witnessed path, and a corrupted replica is still caught."""
+    pcs = [2_000_003, 700_001, 99]
+    st = mk.DeviceState(ctx, pcs, 2)
+    st.fill_synthetic(seed=8, step=2)
+    st.set_meta(12, 4)
+    cap = 40 << 20
+    out = mk.Blob(ctx, cap)
+    rep, wit = ctx.alloc(cap), ctx.alloc(mk.witness_bytes(cap))
+    out.add_replica(rep, cap)
+    out.add_replica_witness(wit, mk.witness_bytes(cap))
+    ctx.set_replica_mode(mode)
+    try:
+        mk.snapshot_record(st, [0, 2], [1], 0, 1, 12, 2, out)
+        ctx.synchronize()
+        n = out.size
+        view = mk.Blob.wrap(ctx, rep, n, wit)
+        assert view.to_host() == out.to_host()
+        used0, fb0 = ctx.witness_stats()
+        mk.parse_record(view, 2)
+        used, fb = ctx.witness_stats()
+        assert used > used0 and fb == fb0  # the replica's own witness, no from-scratch hash
+        raw = view.to_host()[n // 3]
+        ctx.memset(rep + n // 3, raw ^ 0x40, 1)
+        with pytest.raises(RuntimeError, match="container checksum mismatch"):
+            mk.parse_record(view, 2)
+        with pytest.raises(ValueError, match="read-only"):
+            mk.snapshot_record(st, [0, 2], [1], 0, 1, 12, 2, view)
+        view.close()
+        with pytest.raises(ValueError, match="replica witness capacity"):
+            small = mk.Blob(ctx, cap)
+            small.add_replica_witness(wit, 64)
+            mk.snapshot_record(st, [0, 2], [1], 0, 1, 12, 2, small)
+    finally:
+        ctx.set_replica_mode(-1)
+        out.close()
+        ctx.free(rep)
+        ctx.free(wit)
+        st.close()
+
+
+def test_conversion_from_wrapped_replicas(mk, ctx):
+    """The golden window converted from blobs wrapped over replica buffers and
+    their witnesses: the reference's bytes, every record verified against its
+    travelled witness."""
+    c = load_case("verify_toy")
+    w = 3
+    g = mk.GradLog(ctx, c.meta["param_counts"], c.W)
+    for it in range(w + 1, w + c.W + 1):
+        for i in range(c.n_ops):
+            g.put(it, i, c.grads(it, i))
+    cap = 1 << 16
+    views, keep = [], []
+    for k in range(c.W):
+        s = w + k
+        st = mk.DeviceState(ctx, c.meta["param_counts"], c.compute_bytes)
+        for i in range(c.n_ops):
+            o = c.op(s, i)
+            st.upload_op(i, o["master"], o["m"], o["v"], o["step"])
+        st.set_meta(s, c.data_seed)
+        b = mk.Blob(ctx, cap)
+        rep, wit = ctx.alloc(cap), ctx.alloc(mk.witness_bytes(cap))
+        b.add_replica(rep, cap)
+        b.add_replica_witness(wit, mk.witness_bytes(cap))
+        mk.snapshot_record(st, *c.slot(k), k, 1, w, c.W, b)
+        ctx.synchronize()
+        views.append(mk.Blob.wrap(ctx, rep, b.size, wit))
+        keep.append((st, b, rep, wit))
+    used0, fb0 = ctx.witness_stats()
+    out = mk.DeviceState(ctx, c.meta["param_counts"], c.compute_bytes)
+    mk.sparse_to_dense_convert(out, views, w, c.W, c.data_seed, g)
+    assert out.serialize_state() == c.converted(w)
+    used, fb = ctx.witness_stats()
+    assert used - used0 == c.W and fb == fb0
+    for v in views:
+        v.close()
+    for st, b, rep, wit in keep:
+        b.close()
+        ctx.free(rep)
+        ctx.free(wit)
