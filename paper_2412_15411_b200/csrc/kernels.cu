@@ -773,16 +773,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_after();
   const uint32_t tmem = sh.tmem;
   volatile uint32_t* abort = &sh.abort;
-  const int64_t my_chunks = blockIdx.x < n_chunks ? (n_chunks - 1 - blockIdx.x) / G + 1 : 0;
+  // (32-bit chunk counters: buffer index and phase by multiply, not a 64-bit division)
+  const uint32_t my_chunks = blockIdx.x < n_chunks ? static_cast<uint32_t>((n_chunks - 1 - blockIdx.x) / G + 1) : 0;
   uint64_t acc = 0;
   bool ok = true;
   if (warp == kProducer) {  // ---- rows + witness words of every chunk, kWitnessBufs ahead
     if (lane == 0)
-      for (int64_t i = 0; i < my_chunks; ++i) {
+      for (uint32_t i = 0; i < my_chunks; ++i) {
         const int b = static_cast<int>(i % kWitnessBufs);
         if (i >= kWitnessBufs && !mbar_wait_tc(&sh.empty[b], static_cast<uint32_t>(i / kWitnessBufs - 1) & 1u, abort))
           break;
-        const uint64_t row0 = static_cast<uint64_t>(blockIdx.x + i * G) * kComputeThreads;
+        const uint64_t row0 = (blockIdx.x + static_cast<uint64_t>(i) * G) * kComputeThreads;
         int boxes = 0;
 #pragma unroll
         for (int x = 0; x < kComputeThreads / kTmaBoxRows; ++x) boxes += row0 + kTmaBoxRows * x < rows_full;
@@ -798,12 +799,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
   } else if (warp == kMma) {  // ---- MMA 1 of every chunk, as soon as its bytes land
     if (lane == 0)
-      for (int64_t i = 0; i < my_chunks; ++i) {
+      for (uint32_t i = 0; i < my_chunks; ++i) {
         const int b = static_cast<int>(i % kWitnessBufs);
         const uint32_t ph = static_cast<uint32_t>(i / kWitnessBufs) & 1u;
         if (!mbar_wait_tc(&sh.full[b], ph, abort)) break;
         if (i >= kWitnessBufs && !mbar_wait_tc(&sh.tfree[b], ph ^ 1u, abort)) break;  // chunk i-3 folded
-        const bool last = (static_cast<uint64_t>(blockIdx.x + i * G) + 1) * kComputeThreads > rows_full;
+        const bool last = ((blockIdx.x + static_cast<uint64_t>(i) * G) + 1) * kComputeThreads > rows_full;
         if (last && !mbar_wait_tc(&sh.tail, 0, abort)) break;  // the partial rows, written by their threads
         tc_fence_after();
         tc_chunk_mma(tmem + 2 * kTcN * b, smem_addr(&sh.data[b][0]), smem_addr(&sh.wb[0][0][0]));  // bytes as landed
@@ -811,7 +812,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
   } else if (warp == kMma2) {  // ---- MMA 2 of every chunk, once its u & b rows are written
     if (lane == 0)
-      for (int64_t i = 0; i < my_chunks; ++i) {
+      for (uint32_t i = 0; i < my_chunks; ++i) {
         const int b = static_cast<int>(i % kWitnessBufs);
         const uint32_t ph = static_cast<uint32_t>(i / kWitnessBufs) & 1u;
         // (uab follows mma1 of the same chunk, which followed the fold of chunk i-3)
@@ -825,7 +826,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int m = 32 * (warp & 3) + lane;                                      // this lane's TMEM lane
     const uint64_t w_nat = pow_u64(kPrimeInv, static_cast<uint64_t>(m));       // MMA 1: natural byte m
     const uint64_t w_il = pow_u64(kPrimeInv, static_cast<uint64_t>(32 * (m & 3) + (m >> 2)));  // MMA 2: 4j+s
-    auto fold = [&](int64_t j) {
+    auto fold = [&](uint32_t j) {
       const int b = static_cast<int>(j % kWitnessBufs);
       if (!mbar_wait_tc(&sh.mma2[b], static_cast<uint32_t>(j / kWitnessBufs) & 1u, abort)) return;
       tc_fence_after();
@@ -840,17 +841,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         s0 += static_cast<uint64_t>(r0[q]) << (8 * q);
         s1 += static_cast<uint64_t>(r1[q]) << (8 * q);
       }
-      acc += (s0 * w_nat + s1 * w_il) * chunk_weight(static_cast<int64_t>(blockIdx.x) + j * G);
+      acc += (s0 * w_nat + s1 * w_il) * chunk_weight(static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(j) * G);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.tfree[b]);
     };
-    for (int64_t i = 0; i < my_chunks; ++i) {  // (a timed-out wait breaks the loop)
+    for (uint32_t i = 0; i < my_chunks; ++i) {  // (a timed-out wait breaks the loop)
       const int b = static_cast<int>(i % kWitnessBufs);
       const uint32_t ph = static_cast<uint32_t>(i / kWitnessBufs) & 1u;
       if (warp < 4 && i > 1) fold(i - 2);  // the sums of two chunks back, long done
       if (!mbar_wait_tc(&sh.full[b], ph, abort)) break;
-      const int64_t chunk = blockIdx.x + i * G;
+      const int64_t chunk = blockIdx.x + static_cast<int64_t>(i) * G;
       uint4* rows = sh.data[b];
       const uint64_t row = static_cast<uint64_t>(chunk) * kComputeThreads + tid;
       uint32_t st = 0, expect = 0, check = 0;
@@ -885,7 +886,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.uab[b]);
     }
-    for (int64_t j = my_chunks > 2 ? my_chunks - 2 : 0; warp < 4 && j < my_chunks && !*abort; ++j) fold(j);
+    for (uint32_t j = my_chunks > 2 ? my_chunks - 2 : 0; warp < 4 && j < my_chunks && !*abort; ++j) fold(j);
   }
   if (__any_sync(0xffffffffu, !ok) && lane == 0) atomicExch(bad, 1ull);
 #pragma unroll
