@@ -855,7 +855,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       uint4* rows = sh.data[b];
       const uint64_t row = static_cast<uint64_t>(chunk) * kComputeThreads + tid;
       uint32_t st = 0, expect = 0, check = 0;
-      if (row * kThreadBytes < n) {
+      const bool tail_chunk = (static_cast<uint64_t>(chunk) + 1) * kComputeThreads > rows_full;
+      if (!tail_chunk && (static_cast<uint64_t>(chunk) + 1) * kComputeThreads < rows_full) {
+        // interior chunk: every row full and followed by another (the next
+        // chunk's first witness word rides along)
+        st = sh.wit[b][tid];
+        expect = (st >> 8) | ((sh.wit[b][tid + 1] & 0xffu) << 24);
+        check = ~0u;
+        if (chunk == 0 && tid == 0 && (st & 0xffu) != (seed & 0xffu)) ok = false;
+      } else if (row * kThreadBytes < n) {
         st = sh.wit[b][tid];
         const uint64_t seg0 = 4 * row;
         const uint32_t next = seg0 + 4 < n_seg ? (sh.wit[b][tid + 1] & 0xffu) : 0u;
@@ -869,7 +877,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         if (row == 0 && (st & 0xffu) != (seed & 0xffu)) ok = false;
       }
-      if ((static_cast<uint64_t>(chunk) + 1) * kComputeThreads > rows_full) {  // the partial rows: before MMA 1
+      if (tail_chunk) {  // the partial rows: before MMA 1
         if (row >= rows_full) witness_row_bytes(rows, tid, data, n, row * kThreadBytes);
         fence_async_shared();
         __syncwarp();
