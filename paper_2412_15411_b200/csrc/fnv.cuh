@@ -90,11 +90,13 @@ constexpr int kThreadWords = kThreadBytes / 4;
 constexpr int kChunk = kComputeThreads * kThreadBytes;  // 65,536 bytes by default
 constexpr int kRounds = 4;
 static_assert(kSegs % 2 == 0, "segments are processed in pairs");
-// One 64-bit look-back word per chunk, kStatusStride words apart (256 B) so
-// the in-flight chunks' words land in different L2 slices.  The high half is
-// the launch epoch, so the array is never cleared between launches.
+// One 64-bit look-back word per chunk, kStatusStride words apart (128 B: one
+// L2 line each, the in-flight chunks' words in different lines; 256 B was
+// 2 % slower, 64 B equal, 32 B and 8 B 8 % and 60 % slower on the fused
+// snapshot).  The high half is the launch epoch, so the array is never
+// cleared between launches.
 #ifndef MLCK_FNV_STATUS_STRIDE
-#define MLCK_FNV_STATUS_STRIDE 32
+#define MLCK_FNV_STATUS_STRIDE 16
 #endif
 constexpr int kStatusStride = MLCK_FNV_STATUS_STRIDE;
 constexpr uint32_t kSpinLimit = 1u << 24;  // watchdog: never hang the GPU
