@@ -976,7 +976,7 @@ void init_constants() {
 uint64_t fnv_chunks(uint64_t n) { return div_up(n, fnv::kChunk); }
 // [256 B header: chunk ticket u64 @0, finished u32 @8, accum u64 @16, ulast u32 @24, error u32
 //  @28, sticky watchdog u32 @32 (not cleared per launch)] [status: n_chunks
-//  words of 8 B at a 256 B stride]
+//  words of 8 B at a kStatusStride * 8 B (128 B) stride]
 size_t fnv_scratch_words(uint64_t n) { return (256 + fnv_chunks(n) * fnv::kStatusStride * 8) / 4; }
 
 uint64_t fnv_chunk_bytes() { return fnv::kChunk; }
@@ -987,6 +987,9 @@ uint32_t fnv_sticky_word() { return 8; }
 // kernels' shared-memory rows use.  False when the TMA cannot serve it.
 // `rows` x 128-byte rows at data as a tensor map with `box_rows`-row boxes in
 // the 128-byte swizzle of the FNV kernels' shared-memory rows.
+#ifndef MLCK_TMA_L2_PROMOTION
+#define MLCK_TMA_L2_PROMOTION 3  // CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 void encode_rows(const uint8_t* data, uint64_t rows, uint32_t box_rows, CUtensorMap* tmap) {
   using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1004,7 +1007,7 @@ void encode_rows(const uint8_t* data, uint64_t rows, uint32_t box_rows, CUtensor
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode(tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(data), dims, strides, box,
                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                            static_cast<CUtensorMapL2promotion>(MLCK_TMA_L2_PROMOTION), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(kCuda, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 bool make_row_tmap(const uint8_t* data, uint64_t n, CUtensorMap* tmap) {
