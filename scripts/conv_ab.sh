@@ -3,6 +3,7 @@
 #   bash scripts/conv_ab.sh base minb8 ...   (base = the in-tree build)
 mkdir -p gpurun_out/r2
 for v in "$@"; do
+  if [ "$v" != base ] && [ ! -f variants/$v/libmlck_b200.so ]; then echo "$v: not built (scripts/build_variant.sh $v -D...)"; continue; fi
   if [ "$v" = base ]; then unset MLCK_B200_LIB; else export MLCK_B200_LIB=variants/$v/libmlck_b200.so; fi
   timeout 300 python bench.py --no-cpu --no-log --no-extras --steps 3 > gpurun_out/r2/cab_$v.log 2>&1
   python -c "

@@ -2,6 +2,7 @@
 # Development A/B: FNV register cap (variants/regNN) x async hash, N=1 step
 mkdir -p gpurun_out/r2
 for v in base reg80 reg72; do
+  if [ "$v" != base ] && [ ! -f variants/$v/libmlck_b200.so ]; then echo "$v: not built (scripts/build_variant.sh $v -D...)"; continue; fi
   for a in 0 1; do
     if [ $v = base ]; then unset MLCK_B200_LIB; else export MLCK_B200_LIB=variants/$v/libmlck_b200.so; fi
     L=gpurun_out/r2/rab_${v}_$a.log
