@@ -68,6 +68,12 @@ int main(int argc, char** argv) {
   SparseCheckpoint ckpt;
   ckpt.window_start = ws;
   ckpt.wsparse = W;
+  // the same window recovered from replica buffers: each record's witness
+  // travels beside its replica, the recovering side wraps both in place
+  SparseCheckpoint from_replicas;
+  from_replicas.window_start = ws;
+  from_replicas.wsparse = W;
+  std::vector<void*> rep_buffers;
   std::vector<ScheduleSlot> slots(W);
   for (uint32_t k = 0; k < W; ++k) {
     DeviceState st(ctx, P, static_cast<int>(cb));
@@ -89,6 +95,21 @@ int main(int argc, char** argv) {
     for (auto& id : sl.compute_only) id = r.get<uint32_t>();
     // capture_windows (verify.hpp:75-76)
     ckpt.add_record(take_sparse_snapshot(st, sl, k), plan);
+    {
+      const uint64_t cap = 1 << 20, wcap = DeviceBlob::witness_bytes(cap);
+      void *rep = nullptr, *wit = nullptr;
+      check(mlck_device_alloc(ctx.get(), cap, &rep));
+      check(mlck_device_alloc(ctx.get(), wcap, &wit));
+      rep_buffers.push_back(rep);
+      rep_buffers.push_back(wit);
+      DeviceBlob sender(ctx, cap);
+      sender.add_replica(rep, cap);
+      sender.add_replica_witness(wit, wcap);
+      serialize_record(take_sparse_snapshot(st, sl, k), plan, 1, ws, W, sender);
+      from_replicas.blobs.push_back(DeviceBlob::wrap(ctx, rep, sender.size(), wit));
+      from_replicas.replication.push_back(1);
+      ctx.synchronize();
+    }
     write(out + "/blob_" + std::to_string(k) + ".bin",
           serialize_record(take_sparse_snapshot(st, sl, k), plan, 1, ws, W));
     if (k == 0) {
@@ -144,6 +165,17 @@ int main(int argc, char** argv) {
   DeviceState conv(ctx, P, static_cast<int>(cb));
   sparse_to_dense_convert(conv, ckpt, &g, data_seed, oc);
   write(out + "/conv.bin", conv.serialize_state());
+  {
+    uint64_t used0 = 0, fb0 = 0, used = 0, fb = 0;
+    check(mlck_ctx_witness_stats(ctx.get(), &used0, &fb0));
+    DeviceState conv_rep(ctx, P, static_cast<int>(cb));
+    sparse_to_dense_convert(conv_rep, from_replicas, &g, data_seed, oc);
+    check(mlck_ctx_witness_stats(ctx.get(), &used, &fb));
+    std::cout << "REPLICA_WITNESS same " << (conv_rep.serialize_state() == conv.serialize_state())
+              << " witnessed " << (used - used0) << " fallbacks " << (fb - fb0) << "\n";
+    from_replicas.blobs.clear();
+    for (void* p : rep_buffers) check(mlck_device_free(ctx.get(), p));
+  }
   try {
     SparseCheckpoint partial;
     partial.wsparse = W + 1;

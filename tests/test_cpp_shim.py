@@ -70,6 +70,8 @@ def test_cpp_shim_window_matches_reference(tmp_path, reference, name, w):
     # one durable copy (persisted only at target 1); the ring promotes the window
     assert "SAVED same 1 durable_persisted 0" in out
     assert f"RING before 0 after {w} in_flight 0" in out
+    # recovery from replica buffers: witnesses sent beside the replicas, records wrapped in place
+    assert f"REPLICA_WITNESS same 1 witnessed {c.W} fallbacks 0" in out
     assert (tmp_path / "window" / f"window_{w}_slot_0.mlck").read_bytes() == c.blob(w)
     # conversion_plan, scalar codecs and the log budget through the C++ shim
     plan_line = next(x for x in out.splitlines() if x.startswith("PLAN "))
