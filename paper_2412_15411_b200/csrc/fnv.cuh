@@ -156,9 +156,17 @@ static_assert(kPrime * kPrimeInv == 1ull, "P^-1 mod 2^64");
 constexpr uint64_t kPow32 = pow_p(32);
 
 static_assert(kWarps <= 32, "one look-back warp per slot");
-__host__ __device__ constexpr int lookback_warp(int s) { return kComputeWarps + s; }
+// MLCK_FNV_LB_FIRST: the look-back warps are the CTA's first warps (1) or
+// its last (0); compute thread t is threadIdx.x - kComputeTidBase.
+#ifndef MLCK_FNV_LB_FIRST
+#define MLCK_FNV_LB_FIRST 0
+#endif
+__host__ __device__ constexpr int lookback_warp(int s) { return MLCK_FNV_LB_FIRST ? s : kComputeWarps + s; }
 // index of a compute warp among the compute warps, -1 for a look-back warp
-__host__ __device__ constexpr int compute_warp(int warp) { return warp < kComputeWarps ? warp : -1; }
+__host__ __device__ constexpr int compute_warp(int warp) {
+  return MLCK_FNV_LB_FIRST ? (warp >= kSlots ? warp - kSlots : -1) : (warp < kComputeWarps ? warp : -1);
+}
+constexpr int kComputeTidBase = MLCK_FNV_LB_FIRST ? 32 * kSlots : 0;
 
 // P^-(c * kChunk) as a product of three table entries (init_constants)
 __constant__ unsigned long long c_wchunk[3][1024];

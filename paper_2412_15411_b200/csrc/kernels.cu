@@ -124,7 +124,7 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
   // TMA mode: the slot's look-back warp loads whole chunks through the tensor
   // map; rows at or past the last full 128-byte row are written here
   const uint64_t rows_full = n / kThreadBytes;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = static_cast<int>(threadIdx.x) - kComputeTidBase, warp = tid >> 5, lane = tid & 31;
 #if MLCK_FNV_MMA
   // P^-(end of the warp's span in the chunk)
   const uint64_t pinv_t = pow_u64(kPrimeInv, static_cast<uint64_t>(kThreadBytes) * 32 * (warp + 1));
