@@ -1,7 +1,9 @@
 """Per-kernel SASS evidence of the product library (cuobjdump -sass of the
 sm_100a objects): TMA loads/stores (UTMALDG / UTMASTG), mbarrier operations
 (SYNCS.*), tensor-core MMAs (IMMA), async copies (LDGSTS), and the
-register / spill figures ptxas reported.
+register / spill figures ptxas reported.  YIELD counts the forward-progress
+yields ptxas inserted (in fnv_kernel only the out-of-line mbarrier retry
+stubs should have them: one at a look-back loop head costs ~8 %, DESIGN 3.2).
 
   python scripts/sass_summary.py r02      -> profiles/r02_sass_summary.md
 """
@@ -14,7 +16,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BUILD = os.path.join(ROOT, "paper_2412_15411_b200", "_build")
 OPS = ["UTMALDG", "UTMASTG", "UBLKCP", "UTCIMMA", "UTCBAR", "UTMACMDFLUSH", "SYNCS.ARRIVE", "SYNCS.PHASECHK", "IMMA", "HMMA", "LDGSTS",
-       "LDG", "STG", "LDS", "STS", "MUFU", "SHFL", "BAR"]
+       "LDG", "STG", "LDS", "STS", "MUFU", "SHFL", "BAR", "YIELD"]
 
 
 def demangle(name):
@@ -58,7 +60,7 @@ def main():
     out = [f"# SASS summary ({rnd})", "",
            "`cuobjdump -sass` of `paper_2412_15411_b200/_build/*.o` (sm_100a), static instruction counts per "
            "kernel (`scripts/sass_summary.py`). UTMALDG / UTMASTG = TMA tensor loads / stores, UBLKCP = bulk copies, UTCIMMA = tcgen05 integer MMA, UTCBAR = tcgen05.commit, SYNCS.* = "
-           "mbarrier arrive / try-wait, IMMA = integer tensor-core MMA (mma.sync u8).", "",
+           "mbarrier arrive / try-wait, IMMA = integer tensor-core MMA (mma.sync u8), YIELD = forward-progress yields ptxas inserted.", "",
            "| object | kernel | instr | " + " | ".join(OPS) + " |",
            "|---|---|---|" + "---|" * len(OPS)]
     for obj, k, c in rows:
