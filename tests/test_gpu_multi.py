@@ -7,7 +7,12 @@ equal the oracle's serialize_record of the same shard state, and its trailer
 the CPU oracle's FNV-1a-64 (`digest.hpp:18-25`).
 
 One process per GPU; gloo carries only the IPC handles and the host copies the
-checker compares (the data path itself has no collective)."""
+checker compares (the data path itself has no collective).  The "2rank-1gpu"
+cases put two ranks on one GPU (CUDA IPC between processes on the same
+device): the same handle exchange, ring placement, capacity checks, witness
+travel and mapping teardown, so a single-GPU run exercises the protocol too.
+
+CASES: (world, devices)."""
 import os
 import socket
 
@@ -32,7 +37,11 @@ def _record_bytes(pcs, a, c, cb):
     return 45 + 8 + sum(13 + 8 + 12 * pcs[i] for i in a) + sum(13 + cb * pcs[i] for i in c)
 
 
-def _worker(rank, world, port, q):
+CASES = [(2, 2), (4, 4), (2, 1)]
+IDS = ["2gpu", "4gpu", "2rank-1gpu"]
+
+
+def _worker(rank, world, port, q, ndev):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     ok, msg, cur_mode = True, "", None
@@ -45,7 +54,7 @@ def _worker(rank, world, port, q):
         classes = ["E"] * E + ["NE", "G"]
         pcs = [40_001 + 4_099 * i for i in range(E)] + [70_003, 517]
         owned = pl.shard_operators(classes, E, world, rank)
-        ctx = mlck.Context(rank)
+        ctx = mlck.Context(rank % ndev)
         st = mlck.DeviceState(ctx, pcs, cb)
         st.fill_synthetic(seed=11, step=3)
         st.set_meta(40, 11)
@@ -151,14 +160,14 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_ring_replicas_byte_exact(world):
-    if torch.cuda.device_count() < world:
-        pytest.skip(f"needs {world} GPUs")
+@pytest.mark.parametrize("world,ndev", CASES, ids=IDS)
+def test_ring_replicas_byte_exact(world, ndev):
+    if torch.cuda.device_count() < ndev:
+        pytest.skip(f"needs {ndev} GPUs")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, ndev)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in procs]
@@ -168,7 +177,7 @@ def test_ring_replicas_byte_exact(world):
     assert not bad, bad
 
 
-def _log_worker(rank, world, port, q):
+def _log_worker(rank, world, port, q, ndev):
     """Upstream logging into the ring successor's HBM (kind 2 over an IPC
     mapping, what bench.py's N>1 logging does): the entries read back through
     the log equal the reference's UpstreamLog bit for bit (engine.hpp:55-94)."""
@@ -181,7 +190,7 @@ def _log_worker(rank, world, port, q):
 
         ref = load_case("dp2_pp2").log_entries()
         cap = 1 << 22
-        ctx = mlck.Context(rank)
+        ctx = mlck.Context(rank % ndev)
         mine = ctx.alloc(cap)  # this rank hosts its predecessor's log
         handles = [None] * world
         dist.all_gather_object(handles, ctx.ipc_export(mine))
@@ -211,14 +220,14 @@ def _log_worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_upstream_log_in_peer_hbm(world):
-    if torch.cuda.device_count() < world:
-        pytest.skip(f"needs {world} GPUs")
+@pytest.mark.parametrize("world,ndev", CASES, ids=IDS)
+def test_upstream_log_in_peer_hbm(world, ndev):
+    if torch.cuda.device_count() < ndev:
+        pytest.skip(f"needs {ndev} GPUs")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_log_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_log_worker, args=(r, world, port, q, ndev)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in procs]
