@@ -309,6 +309,65 @@ def test_fused_snapshot_many_boundaries(mk, ctx, oracle, cb):
         st.close()
 
 
+@pytest.mark.parametrize("seed", range(9))
+def test_fused_snapshot_random_layouts(mk, ctx, oracle, seed):
+    """Transport 2 on random record layouts: operators of 1-3000 parameters
+    mixed with 50K-600K ones (runs at every shift; seeds 0-5, the fused
+    kernel), 2000 operators of 1-150 parameters (a record made of patch
+    chunks; seeds 6-7) and a one-parameter record under one row (seed 8) --
+    those two take the pack path; random Full / compute-only split and compute
+    width, a replica 0 or 16 bytes into its buffer; every byte of the record
+    and the replica against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    if seed < 6:
+        n = int(rng.integers(3, 24))
+        pcs = [int(rng.integers(1, 3000)) if rng.random() < 0.5 else int(rng.integers(50_000, 600_000))
+               for _ in range(n)]
+    elif seed < 8:
+        n = 2000
+        pcs = [int(x) for x in rng.integers(1, 150, n)]
+    else:
+        n, pcs = 1, [1]
+    cb = int(rng.choice([1, 2, 4]))
+    st = mk.DeviceState(ctx, pcs, cb)
+    st.fill_synthetic(seed=seed, step=5)
+    st.set_meta(12, 1 + seed)
+    active = sorted(int(x) for x in rng.choice(n, int(rng.integers(1, n + 1)), replace=False))
+    co = [i for i in range(n) if i not in active]
+    ents = []
+    for i in range(n):
+        P = pcs[i]
+        master = oracle.synth(seed, 3 * i, -0.25, 0.25, P)
+        if i in active:
+            ents.append(dict(id=i, mode=0, param_count=P, step=5, master=master,
+                             m=oracle.synth(seed, 3 * i + 1, -1e-3, 1e-3, P),
+                             v=oracle.synth(seed, 3 * i + 2, 0.0, 1e-6, P)))
+        else:
+            ents.append(dict(id=i, mode=1, param_count=P, compute=oracle.quantize(master, cb)))
+    ref = oracle.serialize_record(dict(kind=1, iteration=12, window_start=10, wsparse=3, slot=2, data_seed=1 + seed),
+                                  ents, cb)
+    cap = len(ref) + 4096
+    off = 16 * int(rng.integers(0, 2))
+    ctx.set_replica_mode(2)
+    try:
+        out = mk.Blob(ctx, cap)
+        buf = ctx.alloc(cap + 64)
+        out.add_replica(buf + off, cap)
+        ctx.set_timing(True)
+        mk.snapshot_record(st, active, co, 2, 1, 10, 3, out)
+        path = "fused" if "pack_fnv" in [name for name, _ in ctx.timings()] else "pack"
+        ctx.set_timing(False)
+        print(f"seed {seed}: {n} operators, {len(ref)} bytes, cb {cb}, replica +{off}: {path}")
+        assert path == ("fused" if seed < 6 else "pack")
+        assert out.to_host() == ref, path
+        assert ctx.download(buf + off, len(ref)) == ref, path
+        out.close()
+        ctx.free(buf)
+    finally:
+        ctx.set_replica_mode(-1)
+        st.close()
+
+
 def test_replay_fast_paths_match_ieee_intrinsics(mk, ctx):
     """The conversion's hoisted-reciprocal division and spelled-out square root
     equal __fdiv_rn / __fsqrt_rn: 2^28 divisions over every exponent pair of
