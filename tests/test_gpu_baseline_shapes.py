@@ -174,6 +174,57 @@ def test_full_size_window_conversion_and_localized_recovery(mk, ctx, oracle):
         b.close()
 
 
+@pytest.mark.parametrize("seed", range(8))
+def test_random_windows_conversion_and_recovery(mk, ctx, oracle, seed):
+    """Random windows at small sizes: 2-20 operators of 1 to 200K parameters
+    (odd sizes: the replay's 4-element units end mid-unit), W = 1-8, compute
+    width 1/2/4, 0-3 lost iterations past the window and a random scope;
+    conversion and localized recovery against the oracle's Adam trajectory,
+    bit for bit."""
+    rng = np.random.default_rng(500 + seed)
+    n = int(rng.integers(2, 21))
+    W = int(rng.integers(1, 9))
+    O = -(-n // W)  # every operator Full in exactly one slot
+    pcs = [int(rng.choice([rng.integers(1, 11), rng.integers(100, 5000), rng.integers(100_000, 200_000)]))
+           for _ in range(n)]
+    cb = int(rng.choice([1, 2, 4]))
+    a, sseed, gseed, extra = int(rng.integers(0, 10_000)), 60 + seed, 70 + seed, int(rng.integers(0, 4))
+    order = [int(x) for x in rng.permutation(n)]
+    slots = schedule(order, W, O)
+    st = mk.DeviceState(ctx, pcs, cb)
+    st.fill_synthetic(seed=sseed, step=3)
+    g = mk.GradLog(ctx, pcs, W + extra)
+    g.fill_synthetic(a + 1, W + extra, seed=gseed)
+    blobs = []
+    for k in range(W):
+        st.set_meta(a + k, 5)
+        blobs.append(mk.snapshot_record(st, *slots[k], k, 1, a, W))
+        st.apply_updates(range(n), g, a + k + 1)
+    out = mk.DeviceState(ctx, pcs, cb)
+    mk.sparse_to_dense_convert(out, blobs, a, W, 5, g)
+    assert out.meta() == (a + W, 5)
+    for i in range(n):
+        w, m, v, step = host_trajectory(oracle, pcs[i], i, sseed, gseed, n, a + 1, W, 3)
+        got = out.download_op(i)
+        assert got.step == step, (seed, i)
+        for x, y in ((got.master, w), (got.m, m), (got.v, v)):
+            assert np.array_equal(bits(x), bits(y)), (seed, i)
+        assert np.array_equal(bits(got.compute), bits(oracle.quantize(w, cb))), (seed, i)
+    scope = sorted(int(x) for x in rng.choice(n, int(rng.integers(1, n + 1)), replace=False))
+    rec = mk.DeviceState(ctx, pcs, cb)
+    mk.localized_recover(rec, scope, blobs, a, W, 5, g, a + W + extra)
+    for i in scope:
+        w, m, v, step = host_trajectory(oracle, pcs[i], i, sseed, gseed, n, a + 1, W + extra, 3)
+        got = rec.download_op(i)
+        assert got.step == step, (seed, i)
+        for x, y in ((got.master, w), (got.m, m), (got.v, v)):
+            assert np.array_equal(bits(x), bits(y)), (seed, i)
+    for b in blobs:
+        b.close()
+    for x in (st, out, rec, g):
+        x.close()
+
+
 # ---------------------------------------------------------------- configs[0]
 def test_configs0_window_against_the_reference(mk, ctx, reference):
     """configs[0]: 8 experts + NE + G at 2^21 params each, W=5, O=2, the
