@@ -177,10 +177,10 @@ def test_full_size_window_conversion_and_localized_recovery(mk, ctx, oracle):
 @pytest.mark.parametrize("seed", range(8))
 def test_random_windows_conversion_and_recovery(mk, ctx, oracle, seed):
     """Random windows at small sizes: 2-20 operators of 1 to 200K parameters
-    (odd sizes: the replay's 4-element units end mid-unit), W = 1-8, compute
-    width 1/2/4, 0-3 lost iterations past the window and a random scope;
-    conversion and localized recovery against the oracle's Adam trajectory,
-    bit for bit."""
+    (odd sizes: the replay's 4-element units end mid-unit), W = 1-8 (W = 1 is
+    the reference's degenerate window: no replay), compute width 1/2/4, 0-3
+    lost iterations past the window and a random scope; conversion and
+    localized recovery against the oracle's Adam trajectory, bit for bit."""
     rng = np.random.default_rng(500 + seed)
     n = int(rng.integers(2, 21))
     W = int(rng.integers(1, 9))
@@ -202,9 +202,11 @@ def test_random_windows_conversion_and_recovery(mk, ctx, oracle, seed):
         st.apply_updates(range(n), g, a + k + 1)
     out = mk.DeviceState(ctx, pcs, cb)
     mk.sparse_to_dense_convert(out, blobs, a, W, 5, g)
-    assert out.meta() == (a + W, 5)
+    # W = 1: the single record already is the dense checkpoint (recovery.hpp:192-201)
+    n_conv = 0 if W == 1 else W
+    assert out.meta() == (a + n_conv, 5)
     for i in range(n):
-        w, m, v, step = host_trajectory(oracle, pcs[i], i, sseed, gseed, n, a + 1, W, 3)
+        w, m, v, step = host_trajectory(oracle, pcs[i], i, sseed, gseed, n, a + 1, n_conv, 3)
         got = out.download_op(i)
         assert got.step == step, (seed, i)
         for x, y in ((got.master, w), (got.m, m), (got.v, v)):
