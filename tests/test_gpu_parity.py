@@ -651,3 +651,80 @@ def test_upstream_log_matches_reference(mk, ctx, name, kind):
         log.at(1, 0, 0, 0)
     for p in bufs:
         ctx.free(p)
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("seed", range(3))
+def test_upstream_log_random_puts_and_gc(mk, ctx, kind, seed):
+    """UpstreamLog (engine.hpp:55-94) under random traffic: 300 puts of 1-20K
+    floats on colliding keys (a repeated key overwrites, like the reference's
+    map assignment), gc_logs at rising window starts, reads of present and
+    missing keys -- against a dict model of the reference's std::map after
+    every operation batch (key order, bytes, at(), bytes()); then a 1 MiB
+    ring recycled many times over, collected, and refilled by one entry of its
+    whole capacity (the allocator's holes coalesce)."""
+    rng = np.random.default_rng(300 + seed)
+    log = mk.UpstreamLog(ctx, 1 << 26, kind=kind, device=0)
+    model, bufs, floor = {}, [], 0
+
+    def check():
+        log.sync()
+        got = log.entries()
+        want = sorted(model.items())
+        assert [k for k, _ in got] == [k for k, _ in want]
+        for (_, a), (_, b) in zip(got, want):
+            assert np.array_equal(bits(a), bits(b))
+        assert log.bytes() == sum(v.size * 4 for v in model.values())
+
+    for step in range(300):
+        if rng.random() < 0.05:
+            floor += int(rng.integers(1, 3))
+            log.gc(floor)
+            model = {k: v for k, v in model.items() if k[0] >= floor}
+        key = (int(rng.integers(floor, floor + 5)), int(rng.integers(0, 4)), int(rng.integers(0, 3)),
+               int(rng.integers(0, 2)))
+        data = rng.standard_normal(int(rng.integers(1, 20_000))).astype(np.float32)
+        p = ctx.upload(data)
+        bufs.append(p)
+        log.put(*key, p, data.size)
+        model[key] = data
+        if step % 50 == 49:
+            check()
+            k = list(model)[int(rng.integers(0, len(model)))]
+            assert np.array_equal(bits(log.at(*k)), bits(model[k]))
+    check()
+    with pytest.raises(RuntimeError, match="upstream log missing entry"):
+        log.at(floor + 100, 0, 0, 1)
+    log.close()
+    # a 1 MiB ring recycled many times over (first-fit holes from overwrites and gc):
+    # the same model, then everything collected and one entry of the whole ring
+    cap = 1 << 20
+    log = mk.UpstreamLog(ctx, cap, kind=kind, device=0)
+    model, floor = {}, 0
+    for step in range(600):
+        if step % 10 == 9:
+            floor += 1
+            log.gc(floor)
+            model = {k: v for k, v in model.items() if k[0] >= floor}
+        key = (int(rng.integers(floor, floor + 3)), int(rng.integers(0, 4)), int(rng.integers(0, 3)),
+               int(rng.integers(0, 2)))
+        data = rng.standard_normal(int(rng.integers(1, 4_000))).astype(np.float32)
+        live = sum(-(-v.size * 4 // 256) * 256 for k, v in model.items() if k != key)
+        if live + data.size * 4 > cap // 2:
+            continue
+        p = ctx.upload(data)
+        bufs.append(p)
+        log.put(*key, p, data.size)
+        model[key] = data
+    check()
+    log.gc(floor + 1000)
+    assert len(log) == 0 and log.bytes() == 0
+    whole = rng.standard_normal(cap // 4).astype(np.float32)
+    p = ctx.upload(whole)
+    bufs.append(p)
+    log.put(floor + 1000, 0, 0, 0, p, whole.size)  # the free list coalesced back to one block
+    log.sync()
+    assert np.array_equal(bits(log.at(floor + 1000, 0, 0, 0)), bits(whole))
+    log.close()
+    for p in bufs:
+        ctx.free(p)
