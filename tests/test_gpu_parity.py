@@ -483,6 +483,79 @@ def test_parse_errors(mk, ctx, oracle):
         mk.parse_record(mk.Blob.from_host(ctx, bad), 4)
 
 
+def _ref_parse_verdicts(records, cb, q):
+    """The compiled reference's parse of each record, in a child process whose
+    address space is capped: a mutated count makes the reference allocate
+    (and zero) a vector of that many entries, which must fail as bad_alloc
+    instead of exhausting the host."""
+    import resource
+
+    resource.setrlimit(resource.RLIMIT_AS, (4 << 30, 4 << 30))
+    from oracle.oracle import RefError, load_reference, ref_parse_record
+
+    ref = load_reference()
+    out = []
+    for rec in records:
+        try:
+            out.append(ref_parse_record(ref, rec, cb))
+        except RefError as e:
+            out.append(str(e))
+        except MemoryError:
+            out.append("std::bad_alloc")
+    q.put(out)
+
+
+@pytest.mark.parametrize("name", ["verify_toy", "six_op_cb1", "six_op_cb4", "dp2_pp2"])
+def test_parse_fuzz_matches_reference(mk, ctx, oracle, reference, name):
+    """parse_record (snapshot.hpp:146-197) on 150 mutated copies of a real
+    record -- random byte flips (header, entry table, payloads), truncations
+    and extensions, each re-sealed with a valid FNV trailer so the structural
+    checks run -- against the compiled reference's parse of the same bytes:
+    the same error text, or the same entry count, iteration and slot.  Where
+    a mutated count makes the reference's own vector allocation throw, any
+    error is the same verdict."""
+    import multiprocessing as mproc
+
+    c = load_case(name)
+    cb = c.compute_bytes
+    rng = np.random.default_rng(sum(map(ord, name)))
+    base = c.blob(1)[:-8]
+    records = []
+    for trial in range(150):
+        body = bytearray(base)
+        kind = trial % 3
+        if kind == 0:  # flips, mostly in the header and entry table
+            for _ in range(int(rng.integers(1, 4))):
+                pos = int(rng.integers(0, min(len(body), 160))) if rng.random() < 0.8 else int(rng.integers(0, len(body)))
+                body[pos] ^= 1 << int(rng.integers(0, 8))
+        elif kind == 1:  # truncated
+            body = body[:int(rng.integers(0, len(body)))]
+        else:  # extended
+            body += bytes(rng.integers(0, 256, int(rng.integers(1, 64)), dtype=np.uint8))
+        records.append(bytes(body) + oracle.fnv1a64(bytes(body)).to_bytes(8, "little"))
+    mp = mproc.get_context("spawn")
+    q = mp.Queue()
+    proc = mp.Process(target=_ref_parse_verdicts, args=(records, cb, q))
+    proc.start()
+    wants = q.get(timeout=300)
+    proc.join(timeout=60)
+    outcomes = {"ok": 0, "error": 0}
+    for trial, (rec, want) in enumerate(zip(records, wants)):
+        try:
+            hdr, ents = mk.parse_record(mk.Blob.from_host(ctx, rec), cb)
+            got = (len(ents), hdr["iteration"], hdr["slot"])
+        except (mk.MlckRuntime, mk.MlckInvalid) as e:
+            got = str(e)
+        if isinstance(want, str):
+            alloc = "bad_alloc" in want or "_M_default_append" in want or "length" in want
+            assert isinstance(got, str) and (alloc or want in got), (trial, want, got)
+            outcomes["error"] += 1
+        else:
+            assert got == tuple(want), (trial, want, got)
+            outcomes["ok"] += 1
+    assert outcomes["error"] > 0
+
+
 def test_check_coverage(mk, ctx):
     c = load_case("six_op_cb4")  # test_snapshot.cpp:170-196
     blobs = [mk.Blob.from_host(ctx, c.blob(k)) for k in range(3)]
