@@ -280,7 +280,7 @@ class Context:
         return int(lib().mlck_ctx_kernel_launches(self.h))
 
     def set_replica_mode(self, mode: int):
-        """-1 (default): auto (0 for replicas in local HBM, else 1); 1: pack,
+        """-1 (default): auto (2 for replicas in local HBM, else 1); 1: pack,
         then copy engines overlapped with the hash; 5: pack, then the hash
         kernel stores the replicas; 3: pack, then a push kernel on reserved
         SMs overlapped with the hash; 2: fused gather+store+hash kernel; 0:

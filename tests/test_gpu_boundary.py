@@ -2,8 +2,9 @@
 reference: conversion_plan (recovery.hpp:123-137), the scalar codec forms
 quantize_value / pack_reduced / unpack_reduced (tensor.hpp:99-183) and the
 generic reduced formats, localized_recover with a RecoverySegment
-(recovery.hpp:240-289), the log's ordered / async source contract, and the
-hash kernel on a reserved-SM grid (any grid size is correct)."""
+(recovery.hpp:240-289), the log's ordered / async source contract, the
+hash kernel on a reserved-SM grid (any grid size is correct), and snapshots
+ordered on a caller's stream (mlck_ctx_set_stream, hash_async)."""
 import numpy as np
 import pytest
 
@@ -239,3 +240,69 @@ def test_parse_beyond_the_old_caps(mk, ctx, oracle):
     blob = oracle.serialize_record(hdr, ents, 2)
     info, entries = mk.parse_record(mk.Blob.from_host(ctx, blob), 2)
     assert len(entries) == n and entries[-1]["id"] == n - 1
+
+
+# ---------------------------------------------------------------- stream order
+class _DevArray:
+    """A raw device float32 span as a torch tensor (no copy)."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
+
+
+@pytest.mark.parametrize("mode", [-1, 0, 1, 5])
+@pytest.mark.parametrize("hash_async", [False, True])
+def test_snapshot_follows_the_user_stream(mk, ctx, oracle, mode, hash_async):
+    """mlck_ctx_set_stream: a snapshot is ordered after the work already
+    queued on the caller's stream (here a ~10 ms sleep, then an in-place write
+    to operator 0's master and v), with the trailer hash on the same stream or
+    on the context's side stream (mlck_ctx_set_hash_async); the record and its
+    replica equal the oracle's serialize_record of the written state."""
+    import torch
+
+    pcs = [300_001, 1_000_003, 77]
+    st = mk.DeviceState(ctx, pcs, 2)
+    st.fill_synthetic(seed=4, step=6)
+    st.set_meta(20, 3)
+    ctx.synchronize()
+    master0, _m0, v0, _codes = st.op_ptrs(0)
+    stream = torch.cuda.Stream()
+    ctx.set_stream(stream.cuda_stream)
+    ctx.set_replica_mode(mode)
+    ctx.set_hash_async(hash_async)
+    try:
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(20_000_000)
+            torch.as_tensor(_DevArray(master0, pcs[0]), device="cuda").fill_(0.5)
+            torch.as_tensor(_DevArray(v0, pcs[0]), device="cuda").mul_(2.0)
+        cap = 16 << 20
+        out = mk.Blob(ctx, cap)
+        rep = ctx.alloc(cap)
+        out.add_replica(rep, cap)
+        mk.snapshot_record(st, [0, 2], [1], 1, 1, 19, 2, out)
+        stream.synchronize()
+        ctx.synchronize()
+        ents = []
+        for i, P in enumerate(pcs):
+            master = oracle.synth(4, 3 * i, -0.25, 0.25, P)
+            if i == 1:
+                ents.append(dict(id=i, mode=1, param_count=P, compute=oracle.quantize(master, 2)))
+                continue
+            v = oracle.synth(4, 3 * i + 2, 0.0, 1e-6, P)
+            if i == 0:
+                master = np.full(P, 0.5, dtype=np.float32)
+                v = v * np.float32(2.0)
+            ents.append(dict(id=i, mode=0, param_count=P, step=6, master=master,
+                             m=oracle.synth(4, 3 * i + 1, -1e-3, 1e-3, P), v=v))
+        ref = oracle.serialize_record(dict(kind=1, iteration=20, window_start=19, wsparse=2, slot=1, data_seed=3),
+                                      ents, 2)
+        assert out.to_host() == ref
+        assert ctx.download(rep, len(ref)) == ref
+        assert out.replication() == 1
+        out.close()
+        ctx.free(rep)
+    finally:
+        ctx.set_stream(None)
+        ctx.set_replica_mode(-1)
+        ctx.set_hash_async(False)
+        st.close()
