@@ -98,28 +98,58 @@ def meta_bytes(slot):
 # clocks (nvidia-smi sampled during the timed region)
 # --------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 20 ms; __enter__
-    returns once the sampler is live, so the samples cover the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region: NVML
+    polled every 2 ms in a thread (a 12-step region is ~17 ms), else
+    nvidia-smi every 20 ms; __enter__ returns once the sampler is live, so the
+    samples cover the timed region."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits in the order of FIELDS[3:]
+    NVML_BITS = (0x8, 0x40, 0x20, 0x4)
 
     def __init__(self, index: int):
         self.index, self.samples, self.proc = index, [], None
         self.t_start = self.t_end = None
+        self.stop = threading.Event()
+        self.t = None
+        self.source = None
+
+    def _nvml_loop(self, nv, h):
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                break
+            flags = ["Active" if r & b else "Not Active" for b in self.NVML_BITS]
+            self.samples.append((time.monotonic(), [str(sm), str(mx), hex(r)] + flags))
+            self.stop.wait(0.002)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.t = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
             self.t.start()
-            deadline = time.monotonic() + 10
-            while not self.samples and time.monotonic() < deadline:
-                time.sleep(0.01)
-        except OSError:
-            self.proc = None
+            self.source = "nvml, 2 ms"
+        except Exception:
+            self.t = None
+        if self.t is None:
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                     "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.t = threading.Thread(target=self._read, daemon=True)
+                self.t.start()
+                self.source = "nvidia-smi, 20 ms"
+            except OSError:
+                self.proc = None
+        deadline = time.monotonic() + 10
+        while self.t is not None and not self.samples and time.monotonic() < deadline:
+            time.sleep(0.001)
         self.t_start = time.monotonic()
         return self
 
@@ -131,12 +161,14 @@ class ClockSampler:
 
     def __exit__(self, *a):
         self.t_end = time.monotonic()
-        if self.proc:
+        if self.t is not None:
             # one more sample after the region ends (a region can be shorter than the period)
             n = len(self.samples)
             deadline = time.monotonic() + 0.2
             while len(self.samples) == n and time.monotonic() < deadline:
-                time.sleep(0.005)
+                time.sleep(0.001)
+        self.stop.set()
+        if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -154,7 +186,7 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in inside for i in range(4) if s[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(inside)}
+                "reasons": reasons, "samples": len(inside), "source": self.source}
 
 
 def peaks():
