@@ -189,7 +189,9 @@ uint64_t mlck_witness_bytes(uint64_t record_bytes);
 /* A read-only blob over `n` record bytes the caller owns in device memory (a
  * replica buffer), with the record's witness if `witness` is not null; no
  * copy.  Parse, coverage, conversion and localized recovery read it in place;
- * snapshots into it are refused.  Destroying it frees nothing of the caller's. */
+ * snapshots into it are refused.  Destroying it frees nothing of the caller's.
+ * The witness buffer must span mlck_witness_bytes(n) bytes; a record or
+ * witness running past the allocation it points into is refused. */
 int mlck_blob_wrap(mlck_ctx* ctx, void* record, uint64_t n, const void* witness, mlck_blob** out);
 
 /* ---- window lifecycle and durability (SparseCheckpoint::replication /

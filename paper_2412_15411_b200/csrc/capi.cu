@@ -1504,6 +1504,17 @@ int mlck_blob_wrap(mlck_ctx* ctx, void* record, uint64_t n, const void* witness,
   return api([&] {
     ctx->activate();
     if (!record && n) throw_invalid("blob wrap: null record");
+    // the record and the witness (with the verifier's whole-chunk over-read)
+    // must lie inside the allocations they point into
+    uint64_t base = 0, bytes = 0;
+    const uint64_t r = reinterpret_cast<uint64_t>(record), w = reinterpret_cast<uint64_t>(witness);
+    if (n && alloc_range(record, &base, &bytes) && r + n > base + bytes)
+      throw_invalid("blob wrap: " + std::to_string(n) + " record bytes run past their allocation (" +
+                    std::to_string(base + bytes - r) + " bytes from the record pointer)");
+    const uint64_t wneed = n >= 8 ? 4 * witness_alloc_words(n - 8) : 0;
+    if (witness && n >= 8 && alloc_range(witness, &base, &bytes) && w + wneed > base + bytes)
+      throw_invalid("blob wrap: witness buffer of " + std::to_string(base + bytes - w) + " bytes < " +
+                    std::to_string(wneed) + " (mlck_witness_bytes)");
     auto* b = new mlck_blob();
     b->ctx = ctx;
     b->external = true;

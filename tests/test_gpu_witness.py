@@ -200,3 +200,25 @@ def test_conversion_from_wrapped_replicas(mk, ctx):
         b.close()
         ctx.free(rep)
         ctx.free(wit)
+
+
+def test_wrap_refuses_spans_past_their_allocation(mk, ctx):
+    """mlck_blob_wrap: a record running past its allocation, or a witness
+    buffer smaller than mlck_witness_bytes (the verifier reads whole chunks of
+    it), is refused up front instead of read out of bounds."""
+    c = load_case("verify_toy")
+    rec = c.blob(3)
+    n = len(rec)
+    buf = ctx.alloc(n)
+    wbuf = ctx.alloc(2 << 20)  # (device allocations are whole 2 MiB pages: point 64 B before the end)
+    big_w = ctx.alloc(mk.witness_bytes(n))
+    try:
+        with pytest.raises(ValueError, match="run past their allocation"):
+            mk.Blob.wrap(ctx, buf, n + (4 << 20))
+        with pytest.raises(ValueError, match="mlck_witness_bytes"):
+            mk.Blob.wrap(ctx, buf, n, wbuf + (2 << 20) - 64)
+        view = mk.Blob.wrap(ctx, buf, n, big_w)  # fits: accepted (a stale witness only costs the full hash)
+        view.close()
+    finally:
+        for p in (buf, wbuf, big_w):
+            ctx.free(p)
