@@ -1476,10 +1476,19 @@ int mlck_blob_add_replica(mlck_blob* b, void* ptr, uint64_t capacity) {
     // a replica inside a peer's IPC mapping must fit in it: the pack kernel and
     // the copy engines would otherwise write past the peer's allocation
     const uint64_t a = reinterpret_cast<uint64_t>(ptr);
+    bool ipc = false;
     for (const auto& r : b->ctx->ipc_ranges)
-      if (a >= r.first && a < r.first + r.second && capacity > r.first + r.second - a)
-        throw_invalid("replica capacity " + std::to_string(capacity) + " exceeds its IPC mapping (" +
-                      std::to_string(r.first + r.second - a) + " bytes from the replica pointer)");
+      if (a >= r.first && a < r.first + r.second) {
+        ipc = true;
+        if (capacity > r.first + r.second - a)
+          throw_invalid("replica capacity " + std::to_string(capacity) + " exceeds its IPC mapping (" +
+                        std::to_string(r.first + r.second - a) + " bytes from the replica pointer)");
+      }
+    // any other device pointer (local, peer access): against its allocation
+    uint64_t base = 0, bytes = 0;
+    if (!ipc && alloc_range(ptr, &base, &bytes) && capacity > base + bytes - a)
+      throw_invalid("replica capacity " + std::to_string(capacity) + " exceeds its allocation (" +
+                    std::to_string(base + bytes - a) + " bytes from the replica pointer)");
     b->replicas.push_back({static_cast<uint8_t*>(ptr), capacity});
   });
 }
@@ -1494,6 +1503,11 @@ int mlck_blob_add_replica_witness(mlck_blob* b, void* ptr, uint64_t capacity) {
     if (b->witness_dsts.size() + 1 >= static_cast<size_t>(pack::kMaxDst))
       throw_invalid("at most " + std::to_string(pack::kMaxDst - 1) + " replica witnesses per blob");
     if (reinterpret_cast<uintptr_t>(ptr) % 16) throw_invalid("replica witness buffers must be 16-byte aligned");
+    uint64_t base = 0, bytes = 0;
+    const uint64_t a = reinterpret_cast<uint64_t>(ptr);
+    if (alloc_range(ptr, &base, &bytes) && capacity > base + bytes - a)
+      throw_invalid("replica witness capacity " + std::to_string(capacity) + " exceeds its allocation (" +
+                    std::to_string(base + bytes - a) + " bytes from the pointer)");
     b->witness_dsts.push_back({static_cast<uint8_t*>(ptr), capacity});
   });
 }

@@ -181,6 +181,13 @@ def test_snapshot_replicas_identical(mk, ctx, mode):
         small = mk.Blob(ctx, 1 << 16)
         small.add_replica(r1, 64)
         mk.snapshot_record(st, active, co, 1, 1, 3, 3, small)
+    # a capacity past the replica's own allocation is refused when the replica is added
+    big = ctx.alloc(2 << 20)
+    with pytest.raises(ValueError, match="exceeds its allocation"):
+        mk.Blob(ctx, 1 << 16).add_replica(big + (1 << 20), 2 << 20)
+    with pytest.raises(ValueError, match="exceeds its allocation"):
+        mk.Blob(ctx, 1 << 16).add_replica_witness(big + (1 << 20), 2 << 20)
+    ctx.free(big)
     ctx.free(r1)
     ctx.free(r2)
 
