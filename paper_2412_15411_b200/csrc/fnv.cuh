@@ -167,6 +167,11 @@ __host__ __device__ constexpr int compute_warp(int warp) {
   return MLCK_FNV_LB_FIRST ? (warp >= kSlots ? warp - kSlots : -1) : (warp < kComputeWarps ? warp : -1);
 }
 constexpr int kComputeTidBase = MLCK_FNV_LB_FIRST ? 32 * kSlots : 0;
+// MLCK_FNV_LB_ONE_COPY: the look-back warps share one copy of their code
+// (the slot a run-time value) instead of one inlined copy per slot.
+#ifndef MLCK_FNV_LB_ONE_COPY
+#define MLCK_FNV_LB_ONE_COPY 1
+#endif
 
 // P^-(c * kChunk) as a product of three table entries (init_constants)
 __constant__ unsigned long long c_wchunk[3][1024];

@@ -522,11 +522,23 @@ __global__ void MLCK_FNV_BOUNDS
   if (compute_warp(warp) >= 0) {
     acc = fnv_compute<kProf, kGather>(sh, data, n, scr, n_chunks, first, stride, cp, tma);
   } else {
+#if MLCK_FNV_LB_ONE_COPY
+    // one copy of the look-back code for every slot's warp (the slot is a
+    // run-time value): the kernel's hot code fits the instruction caches
+    const int s = MLCK_FNV_LB_FIRST ? warp : warp - kComputeWarps;
+    int64_t f = first[0];
+#pragma unroll
+    for (int q = 1; q < kSlots; ++q)
+      if (s == q) f = first[q];
+    fnv_lookback<kProf, kGather>(sh, s, seed, scr, f, n_chunks, stride, !kGather && use_tma ? &tmap : nullptr, n,
+                                 cp);
+#else
 #pragma unroll
     for (int s = 0; s < kSlots; ++s)
       if (warp == lookback_warp(s))
         fnv_lookback<kProf, kGather>(sh, s, seed, scr, first[s], n_chunks, stride,
                                      !kGather && use_tma ? &tmap : nullptr, n, cp);
+#endif
   }
   // CTA sum -> global accumulator; the last CTA finishes the hash
 #pragma unroll
