@@ -172,6 +172,11 @@ constexpr int kComputeTidBase = MLCK_FNV_LB_FIRST ? 32 * kSlots : 0;
 #ifndef MLCK_FNV_LB_ONE_COPY
 #define MLCK_FNV_LB_ONE_COPY 1
 #endif
+// MLCK_FNV_COMPUTE_ONE_COPY: the same for the compute warps' turn code
+// (per-slot state in shared memory and packed registers, fnv_compute1).
+#ifndef MLCK_FNV_COMPUTE_ONE_COPY
+#define MLCK_FNV_COMPUTE_ONE_COPY 1
+#endif
 
 // P^-(c * kChunk) as a product of three table entries (init_constants)
 __constant__ unsigned long long c_wchunk[3][1024];
@@ -519,6 +524,11 @@ struct alignas(1024) Shared {
   uint32_t wmap[kSlots][32];    // warp maps of the round (compute -> look-back)
   uint32_t wstart[kSlots][32];  // warp start bits (look-back -> compute)
   unsigned long long red[32];
+#if MLCK_FNV_COMPUTE_ONE_COPY
+  int64_t cw[kSlots][kComputeWarps];        // each compute warp's chunk of the slot
+  uint32_t cst[kSlots][kComputeThreads];    // segment start bits per thread
+  uint32_t ckeep[kSlots][kComputeThreads];  // pending round's maps per thread
+#endif
 #if MLCK_FNV_MMA
   uint2 wfrag[2][4][32];        // mma_pass B fragments: [data | automaton][k-block][lane]
   unsigned long long kpos[32][4];  // mma_pass epilogue weights per lane

@@ -368,6 +368,206 @@ __device__ __forceinline__ uint64_t fnv_compute(fnv::Shared& sh, const uint8_t* 
   return acc;
 }
 
+#if MLCK_FNV_COMPUTE_ONE_COPY
+// fnv_compute with one copy of the turn code for every slot (the slot a
+// run-time value): the per-slot state lives in shared memory (chunk ids per
+// warp, start bits and pending maps per thread) and in packed registers
+// (round and pending flags), so the compute warps' hot code is a third of
+// the unrolled form's and fits the instruction caches.
+template <bool kProf, bool kGather>
+__device__ __forceinline__ uint64_t fnv_compute1(fnv::Shared& sh, const uint8_t* data, uint64_t n,
+                                                 const fnv::Scratch& scr, int64_t n_chunks,
+                                                 const int64_t (&first)[kSlots], int64_t stride,
+                                                 const fnv::Copy& cp, bool tma) {
+  using namespace fnv;
+  static_assert(MLCK_FNV_MMA, "the one-copy compute loop has the tensor-core final pass only");
+  const uint64_t rows_full = n / kThreadBytes;
+  const int tid = static_cast<int>(threadIdx.x) - kComputeTidBase, warp = tid >> 5, lane = tid & 31;
+#if MLCK_FNV_MMA
+  const uint64_t pinv_t = pow_u64(kPrimeInv, static_cast<uint64_t>(kThreadBytes) * 32 * (warp + 1));
+#else
+  const uint64_t pinv_t = pow_u64(kPrimeInv, static_cast<uint64_t>(kThreadBytes) * (tid + 1));
+#endif
+  uint32_t rndp = 0;   // round of slot s: bits 4s .. 4s+3
+  uint32_t pendp = 0;  // bit s: a published round of slot s awaits its result
+  uint32_t par = 0, rpar = 0, spar = 0, rdpar = 0;  // mbarrier phase parities per slot (as fnv_compute)
+  const bool copy = cp.n_dst > 0;
+  uint64_t acc = 0;
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) {
+    sh.cw[s][warp] = first[s];
+    sh.cst[s][tid] = 0;
+    sh.ckeep[s][tid] = 0;
+    if (first[s] >= 0 && !tma) load_thread(sh, s, tid, data, n, first[s]);
+  }
+  (void)stride;
+  (void)n_chunks;
+  Laps<kProf, 7> lap;
+  lap.start();
+  for (bool any = true; any;) {
+    any = false;
+#pragma unroll 1
+    for (int s = 0; s < kSlots; ++s) {
+      int64_t c = sh.cw[s][warp];
+      if (c < 0) continue;
+      any = true;
+      uint32_t r = (rndp >> (4 * s)) & 15u;
+      uint32_t stv = sh.cst[s][tid];
+      if ((pendp >> s) & 1u) {
+        lap.mark(3);
+        fnv::mbar_wait(&sh.res[s], (rpar >> s) & 1u);
+        rpar ^= 1u << s;
+        const uint32_t kp = sh.ckeep[s][tid];
+#if MLCK_FNV_PACKED_MAPS
+        const uint32_t add = starts_lanes(kp, map_apply(kp & 7u, sh.wstart[s][warp]));
+#else
+        uint32_t ss = map_apply(kp & 7u, sh.wstart[s][warp]);
+        uint32_t add = ss;
+#pragma unroll
+        for (int i = 1; i < kSegs; ++i) {
+          ss = map_apply((kp >> (3 * i)) & 7u, ss);
+          add |= ss << (8 * i);
+        }
+#endif
+        stv |= add << (2 * r);
+        lap.mark(1);
+        pendp &= ~(1u << s);
+        if (++r == kRounds) {
+          {
+            int mac[2][4] = {};
+            mma_pass(sh, s, warp, lane, 0, mac);  // the data vector
+            uint32_t w[kThreadWords];
+            read_thread(sh, s, tid, w);
+            automaton_and(w, stv);
+            __syncwarp();
+            write_thread(sh, s, tid, w);
+            __syncwarp();
+            mma_pass(sh, s, warp, lane, 1, mac);  // the u & b vector, weights -2 P^(...)
+            acc += mma_epilogue(sh, lane, mac) * (pinv_t * chunk_weight(c));
+          }
+          {
+            uint32_t* const wp = *reinterpret_cast<uint32_t* volatile*>(&sh.witness);
+            const uint64_t row = static_cast<uint64_t>(c) * kComputeThreads + tid;
+            if (wp && row * kThreadBytes < n) wp[row] = stv;
+          }
+          lap.mark(6);
+          if (kProf && scr.trace && tid == 0) scr.trace[c * 12 + 9] = gtimer();
+          lap.mark(2);
+          c = sh.next[s];  // the ticket the look-back warp took in round 3
+          sh.cw[s][warp] = c;
+          rndp &= ~(15u << (4 * s));
+          sh.cst[s][tid] = 0;
+          par ^= 1u << s;
+          if (tma) {
+            bar_arrive(bar_pub(s), kBarThreads);
+          } else if (c >= 0) {
+            load_thread(sh, s, tid, data, n, c);
+          }
+          lap.mark(4);
+          continue;
+        }
+      }
+      // ---- compute and publish round r
+      if (r == 0) {
+        lap.mark(0);
+        fnv::mbar_wait(&sh.mbar[s][tma ? 0 : warp], (par >> s) & 1u);
+        if (tma && !kGather) {
+          const uint64_t row = static_cast<uint64_t>(c) * kComputeThreads + tid;
+          if (row >= rows_full) {
+            const uint64_t p = row * kThreadBytes;
+            load_thread_bytes(sh, s, tid, [&](int i) -> uint32_t { return p + i < n ? data[p + i] : 0u; }, false);
+          }
+        }
+        lap.mark(5);
+        if (kProf && scr.trace && tid == 0) {
+          scr.trace[c * 12 + 0] = gtimer();
+          scr.trace[c * 12 + 10] = smid();
+        }
+      }
+      uint32_t w[kThreadWords];
+      const uint32_t delta = kGather && r == 0 ? sh.shift[s] : 0u;
+      if (delta)
+        read_thread_shifted(sh, s, tid, delta, w);
+      else
+        read_thread(sh, s, tid, w);
+      const bool store = copy && r == 0;
+      if (r == 0) {
+        if (delta) {
+          __syncwarp();
+          if (lane == 0 && warp + 1 < kComputeWarps) mbar_arrive(&sh.rd[s][warp + 1]);
+          if (warp > 0) fnv::mbar_wait(&sh.rd[s][warp], (rdpar >> s) & 1u);
+          rdpar ^= 1u << s;
+          write_thread(sh, s, tid, w);
+        }
+        if (store) {
+          fence_async_shared();
+          bar_arrive(bar_store(s), kBarThreads);
+          const uint64_t row = static_cast<uint64_t>(c) * kComputeThreads + tid;
+          if (row == rows_full && (n & (kThreadBytes - 1))) {
+            const uint8_t* rb = reinterpret_cast<const uint8_t*>(sh.data[s]);
+            for (uint32_t k = 0; k < (n & (kThreadBytes - 1)); ++k) {
+              const uint8_t b = rb[16 * granule(tid, k >> 4) + (k & 15)];
+              for (int d = 0; d < cp.n_dst; ++d) cp.dst_ptr[d][rows_full * kThreadBytes + k] = b;
+            }
+          }
+        }
+        interleave(w);
+        if (!store) write_thread(sh, s, tid, w);
+      } else if (copy && r == 1) {
+        interleave(w);
+        fnv::mbar_wait(&sh.sres[s], (spar >> s) & 1u);
+        spar ^= 1u << s;
+        write_thread(sh, s, tid, w);
+      }
+#if MLCK_FNV_PACKED_MAPS
+      uint32_t e0, e1, kp;
+      if (MLCK_FNV_ROUND0_LINEAR && r == 0)
+        round0_lanes(w, &e0, &e1);
+      else if (r < 2)
+        round_lanes_low(w, stv, r, &e0, &e1);
+      else
+        round_lanes_high(w, stv, r, &e0, &e1);
+      const uint32_t tm = compose_lanes(e0, e1, &kp);
+#else
+      uint32_t m[kSegs];
+      if (MLCK_FNV_ROUND0_LINEAR && r == 0)
+        round0_maps(w, m);
+      else if (r < 2)
+        round_maps_low(w, stv, r, m);
+      else
+        round_maps_high(w, stv, r, m);
+      uint32_t tm = m[0], kp = 0;
+#pragma unroll
+      for (int i = 1; i < kSegs; ++i) {
+        kp |= m[i - 1] << (3 * i);
+        tm = map_compose(m[i], tm);
+      }
+#endif
+      uint32_t wtot;
+      sh.ckeep[s][tid] = map_scan_warp(tm, &wtot) | kp;
+      if (lane == 0) sh.wmap[s][warp] = wtot;
+      bar_arrive(bar_pub(s), kBarThreads);
+      pendp |= 1u << s;
+      rndp = (rndp & ~(15u << (4 * s))) | (r << (4 * s));
+      sh.cst[s][tid] = stv;
+      lap.mark(0);
+    }
+  }
+  if (copy && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (kProf && tid == 0) {
+    lap.mark(3);
+    atomicAdd(scr.prof + 2, static_cast<unsigned long long>(lap.t[0]));
+    atomicAdd(scr.prof + 3, static_cast<unsigned long long>(lap.t[1]));
+    atomicAdd(scr.prof + 4, static_cast<unsigned long long>(lap.t[2]));
+    atomicAdd(scr.prof + 6, static_cast<unsigned long long>(lap.t[3]));
+    atomicAdd(scr.prof + 16, static_cast<unsigned long long>(lap.t[4]));
+    atomicAdd(scr.prof + 17, static_cast<unsigned long long>(lap.t[5]));
+    atomicAdd(scr.prof + 20, static_cast<unsigned long long>(lap.t[6]));
+  }
+  return acc;
+}
+#endif
+
 // Look-back warp of slot s: for every round the compute warps publish on
 // the slot it folds their warp maps into the chunk's map, publishes it,
 // looks back for the chunk's start bits and hands each warp its start.  Only
@@ -520,7 +720,11 @@ __global__ void MLCK_FNV_BOUNDS
   uint64_t acc = 0;
   const bool tma = kGather || use_tma;  // chunks land by TMA (from the sources under kGather)
   if (compute_warp(warp) >= 0) {
+#if MLCK_FNV_COMPUTE_ONE_COPY
+    acc = fnv_compute1<kProf, kGather>(sh, data, n, scr, n_chunks, first, stride, cp, tma);
+#else
     acc = fnv_compute<kProf, kGather>(sh, data, n, scr, n_chunks, first, stride, cp, tma);
+#endif
   } else {
 #if MLCK_FNV_LB_ONE_COPY
     // one copy of the look-back code for every slot's warp (the slot is a
