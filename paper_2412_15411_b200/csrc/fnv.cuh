@@ -173,9 +173,11 @@ constexpr int kComputeTidBase = MLCK_FNV_LB_FIRST ? 32 * kSlots : 0;
 #define MLCK_FNV_LB_ONE_COPY 1
 #endif
 // MLCK_FNV_COMPUTE_ONE_COPY: the same for the compute warps' turn code
-// (per-slot state in shared memory and packed registers, fnv_compute1).
+// (per-slot state in shared memory and packed registers, fnv_compute1; it
+// has the tensor-core final pass only, so MLCK_FNV_MMA=0 builds keep the
+// unrolled loop).
 #ifndef MLCK_FNV_COMPUTE_ONE_COPY
-#define MLCK_FNV_COMPUTE_ONE_COPY 1
+#define MLCK_FNV_COMPUTE_ONE_COPY MLCK_FNV_MMA
 #endif
 
 // P^-(c * kChunk) as a product of three table entries (init_constants)
